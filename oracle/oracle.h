@@ -1,0 +1,77 @@
+/*
+ * oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * fp64 CPU restatement of the reference's evaluate path plus
+ * brute-force restatements of the tree and the interaction
+ * lists.  It is the parity checker for the GPU library and
+ * the timed CPU baseline ("kind": "port") in bench.py.  The product library
+ * (paper_2303_08394_b200) never links, imports or calls anything in oracle/.
+ *
+ * Parity status: the reference ships no runnable FMM, so this
+ * oracle is pinned by the SPEC's known-answer tests and by direct summation
+ * (tests/golden), not by reference outputs.
+ */
+#ifndef KIFMM_ORACLE_H_
+#define KIFMM_ORACLE_H_
+
+#include <stdint.h>
+
+#include "kifmm.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct oracle_timings {
+  double p2m_ms, m2m_ms, m2l_ms, p2l_ms, l2l_ms, near_ms, l2p_ms, m2p_ms, total_ms;
+} oracle_timings;
+
+/* Full evaluate over reordered charges.  potential: N (reordered);
+ * gradient: N x 3 or NULL.  Only targets of leaves [leaf_begin, leaf_end) are
+ * written (pass 0, n_leaves for all); the upward pass is always complete. */
+int oracle_evaluate(const kifmm_tree_view* tree, const kifmm_operator_view* ops, const double* charges,
+                    double* potential, double* gradient, int32_t threads, int64_t leaf_begin,
+                    int64_t leaf_end, oracle_timings* timings);
+
+/* Partitioned evaluate, split at the exchange point:
+ *  upward_local: P2M + M2M for nodes at level >= cut_level whose leaves all lie
+ *                in [leaf_begin, leaf_end) (plus owned leaves coarser than cut);
+ *                every other multipole slice is left 0.  multipole: n_nodes x n_e.
+ *  upward_top:   M2M for the non-leaf nodes above cut_level from the (gathered)
+ *                complete level-cut multipoles.
+ *  downward:     M2L/P2L/L2L/L2P/M2P/near field for the owned leaves. */
+int oracle_upward_local(const kifmm_tree_view* tree, const kifmm_operator_view* ops, const double* charges,
+                        int64_t leaf_begin, int64_t leaf_end, int32_t cut_level, double* multipole,
+                        int32_t threads);
+int oracle_upward_top(const kifmm_tree_view* tree, const kifmm_operator_view* ops, int32_t cut_level,
+                      double* multipole, int32_t threads);
+int oracle_downward(const kifmm_tree_view* tree, const kifmm_operator_view* ops, const double* charges,
+                    const double* multipole, int64_t leaf_begin, int64_t leaf_end, double* potential,
+                    double* gradient, int32_t threads, oracle_timings* timings);
+
+/* Direct summation at m targets (indices into positions, or
+ * NULL for all n) from all n sources; self-pairs contribute 0. */
+void oracle_direct(const double* positions, const double* charges, int64_t n, const int64_t* targets,
+                   int64_t m, double* potential, double* gradient, int32_t threads);
+
+/* Brute-force lists from the definitions (X on all nodes),
+ * written in the same CSR layout as kifmm_tree_view.  Buffers sized by the
+ * caller from the product's list sizes; returns 0 if every CSR fits and
+ * matches in length, else the 1-based list id (1 U, 2 V, 3 W, 4 X) that differs
+ * in total length.  The caller compares contents. */
+int oracle_lists_bruteforce(const kifmm_tree_view* tree, int64_t* u_ptr, int64_t* u_idx, int64_t u_cap,
+                            int64_t* v_ptr, int64_t* v_idx, int32_t* v_tv, int64_t v_cap, int64_t* w_ptr,
+                            int64_t* w_idx, int64_t w_cap, int64_t* x_ptr, int64_t* x_idx, int64_t x_cap);
+
+/* Brute-force recursive split + pairwise balance.
+ * Writes the sorted leaf keys (capacity cap) and returns their count (or -1). */
+int64_t oracle_tree_leaves(const double* positions, int64_t n, int32_t n_crit, const double domain[4],
+                           int32_t balance, uint64_t* leaves, int64_t cap);
+
+/* Relative L2 error ||a-b|| / ||b||; -1 when ||b|| = 0. */
+double oracle_relative_error(const double* a, const double* b, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,60 @@
+// Device-side helpers shared by the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "common.hpp"
+
+namespace kifmm {
+namespace gpu {
+
+constexpr double kInv4PiD = 0.07957747154594767;  // 1 / (4 pi)
+
+#define KIFMM_CUDA(call)                                                                          \
+  do {                                                                                            \
+    cudaError_t err_ = (call);                                                                    \
+    if (err_ != cudaSuccess)                                                                      \
+      throw ::kifmm::DeviceError(err_ == cudaErrorMemoryAllocation ? KIFMM_E_OUT_OF_MEMORY        \
+                                                                   : KIFMM_E_CUDA,                \
+                                 std::string(#call) + ": " + cudaGetErrorString(err_));          \
+  } while (0)
+
+#define KIFMM_LAUNCH_CHECK() KIFMM_CUDA(cudaGetLastError())
+
+// (x, y, z, w) quadruple of the working precision: positions with charge or
+// half side in w.  16 B (fp32) / 32 B (fp64) aligned for vector loads.
+template <class T>
+struct V4;
+template <>
+struct V4<float> {
+  using type = float4;
+};
+template <>
+struct V4<double> {
+  using type = double4;
+};
+template <class T>
+using v4_t = typename V4<T>::type;
+
+template <class T>
+__device__ __forceinline__ v4_t<T> make4(T x, T y, T z, T w);
+template <>
+__device__ __forceinline__ float4 make4<float>(float x, float y, float z, float w) {
+  return make_float4(x, y, z, w);
+}
+template <>
+__device__ __forceinline__ double4 make4<double>(double x, double y, double z, double w) {
+  return make_double4(x, y, z, w);
+}
+
+// 1/sqrt(r2) with the SPEC self-interaction convention (0 at r = 0).
+__device__ __forceinline__ float rinv_masked(float r2) { return r2 > 0.f ? rsqrtf(r2) : 0.f; }
+__device__ __forceinline__ double rinv_masked(double r2) { return r2 > 0.0 ? rsqrt(r2) : 0.0; }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace gpu
+}  // namespace kifmm

@@ -1,0 +1,1063 @@
+// GPU evaluate plan: upload of tree/lists/operators, work-list construction,
+// the evaluate launch sequence, CUDA-graph capture, the NCCL
+// multipole exchange, and the kifmm_gpu_* C ABI.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "m2l_tc.cuh"
+#include "morton.hpp"
+#include "p2p.cuh"
+
+namespace kifmm {
+namespace gpu {
+
+// ------------------------------------------------------------ device memory
+struct DevMem {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevMem() = default;
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  ~DevMem() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t b, size_t* total) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = b;
+    if (b) KIFMM_CUDA(cudaMalloc(&p, b));
+    if (total) *total += b;
+  }
+  template <class T>
+  void upload(const std::vector<T>& v, size_t* total) {
+    alloc(v.size() * sizeof(T), total);
+    if (!v.empty()) KIFMM_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Segmented gather-GEMM work description (see gemm.cuh).
+struct TileSpec {
+  std::vector<int> out;                                 // BM rows (-1 pad)
+  std::vector<std::pair<int, std::vector<int>>> segs;   // (matrix, BM input rows)
+};
+
+struct GemmTiles {
+  int n_tiles = 0, n_segs = 0, bm = 0;
+  int64_t slots = 0;  // sum over segments of BM (computed rows incl. zero rows)
+  DevMem out, seg_ptr, seg_mat, seg_in;
+  void build(const std::vector<TileSpec>& tiles, int bm_, size_t* total) {
+    bm = bm_;
+    n_tiles = int(tiles.size());
+    std::vector<int> o, sp{0}, sm, si;
+    for (const auto& t : tiles) {
+      o.insert(o.end(), t.out.begin(), t.out.end());
+      for (const auto& s : t.segs) {
+        sm.push_back(s.first);
+        si.insert(si.end(), s.second.begin(), s.second.end());
+      }
+      sp.push_back(int(sm.size()));
+    }
+    n_segs = int(sm.size());
+    slots = int64_t(n_segs) * bm;
+    out.upload(o, total);
+    seg_ptr.upload(sp, total);
+    seg_mat.upload(sm, total);
+    seg_in.upload(si, total);
+  }
+};
+
+template <class T>
+struct KC_;
+template <>
+struct KC_<float> {
+  static constexpr int v = 32;
+};
+template <>
+struct KC_<double> {
+  static constexpr int v = 16;
+};
+
+template <class T, int N, int BM, int TM>
+void launch_gemm_n(const GemmTiles& t, const GemmArgs<T>& a, cudaStream_t s) {
+  constexpr int KC = KC_<T>::v;
+  using S = GemmShape<T, N, BM, TM, 8, KC, 3>;
+  auto kern = gather_gemm_kernel<T, N, BM, TM, 8, KC, 3>;
+  static bool attr = false;
+  if (!attr) {
+    KIFMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM)));
+    attr = true;
+  }
+  kern<<<t.n_tiles, S::NT, S::SMEM, s>>>(a);
+  KIFMM_LAUNCH_CHECK();
+}
+
+template <class T, int BM, int TM>
+void launch_gemm(int np, const GemmTiles& t, GemmArgs<T> a, cudaStream_t s) {
+  if (t.n_tiles == 0) return;
+  a.tile_out = t.out.as<int>();
+  a.tile_seg = t.seg_ptr.as<int>();
+  a.seg_mat = t.seg_mat.as<int>();
+  a.seg_in = t.seg_in.as<int>();
+  switch (np) {
+    case 32: return launch_gemm_n<T, 32, BM, TM>(t, a, s);
+    case 64: return launch_gemm_n<T, 64, BM, TM>(t, a, s);
+    case 128: return launch_gemm_n<T, 128, BM, TM>(t, a, s);
+    case 160: return launch_gemm_n<T, 160, BM, TM>(t, a, s);
+    case 224: return launch_gemm_n<T, 224, BM, TM>(t, a, s);
+    default: throw InvalidArgument("gemm: unsupported padded width " + std::to_string(np));
+  }
+}
+
+// ------------------------------------------------------------------- NCCL
+// libnccl is opened lazily so single-GPU use has no NCCL dependency.
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  static Nccl& get() {
+    static Nccl n;
+    if (!n.h) {
+      n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!n.h) throw DeviceError(KIFMM_E_NCCL, "cannot dlopen libnccl.so.2");
+      n.getUniqueId = reinterpret_cast<decltype(n.getUniqueId)>(dlsym(n.h, "ncclGetUniqueId"));
+      n.commInitRank = reinterpret_cast<decltype(n.commInitRank)>(dlsym(n.h, "ncclCommInitRank"));
+      n.allGather = reinterpret_cast<decltype(n.allGather)>(dlsym(n.h, "ncclAllGather"));
+      n.commDestroy = reinterpret_cast<decltype(n.commDestroy)>(dlsym(n.h, "ncclCommDestroy"));
+      n.getErrorString = reinterpret_cast<decltype(n.getErrorString)>(dlsym(n.h, "ncclGetErrorString"));
+      if (!n.getUniqueId || !n.commInitRank || !n.allGather || !n.commDestroy)
+        throw DeviceError(KIFMM_E_NCCL, "libnccl.so.2 lacks required symbols");
+    }
+    return n;
+  }
+  void check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+      throw DeviceError(KIFMM_E_NCCL, std::string(what) + ": " + (getErrorString ? getErrorString(r) : "nccl error"));
+  }
+};
+
+// Row gather / scatter for the multipole exchange.
+template <class T>
+__global__ void gather_rows_kernel(const T* __restrict__ src, int ld, const int* __restrict__ rows, int n,
+                                   T* __restrict__ dst) {
+  const int r = blockIdx.x;
+  if (r >= n) return;
+  for (int j = threadIdx.x; j < ld; j += blockDim.x) dst[size_t(r) * ld + j] = src[size_t(rows[r]) * ld + j];
+}
+template <class T>
+__global__ void scatter_rows_kernel(const T* __restrict__ src, int ld, const int* __restrict__ rows,
+                                    const int* __restrict__ rank_of, int max_rows, int me, int n, T* __restrict__ dst) {
+  const int r = blockIdx.x;  // flat over all ranks' exported rows
+  if (r >= n || rank_of[r] == me) return;
+  const int rank = rank_of[r];
+  // position of this row inside its rank's slot = r - first row of that rank; stored in rows[n + r]
+  const int pos = rows[n + r];
+  const T* s = src + (size_t(rank) * max_rows + pos) * ld;
+  for (int j = threadIdx.x; j < ld; j += blockDim.x) dst[size_t(rows[r]) * ld + j] = s[j];
+}
+
+}  // namespace gpu
+}  // namespace kifmm
+
+using namespace kifmm;
+using namespace kifmm::gpu;
+
+struct kifmm_gpu_plan {
+  kifmm_gpu_options opt{};
+  int device = 0;
+  int precision = 32;
+  bool grad = false;
+  int64_t N = 0, nl = 0, nn = 0;
+  int depth = 0, ne = 0, nc = 0, np = 0, ref_level = 2, cut = 2;
+  int world = 1, rank = 0;
+  int64_t lb = 0, le = 0, pb = 0, pe = 0;  // owned leaves / particles
+  int m2l_backend = 1;
+  double alpha_in = 1.05, alpha_out = 2.95;
+  size_t dev_bytes = 0;
+  cudaStream_t stream = nullptr;
+  std::array<cudaEvent_t, 16> ev{};
+  kifmm_gpu_plan_info info{};
+  kifmm_gpu_timings last{};
+
+  // static data
+  DevMem pos4, perm, node_geom, node_level, surface;
+  DevMem w_us_u, w_vt_u, w_us_d, w_vt_d, w_m2m, w_l2l, w_m2l;
+  // per-evaluate buffers
+  DevMem q_in, src4, pot, grad_buf, pot_out, grad_out;
+  DevMem M, L, check_up, check_dn, tmp;
+  // work lists
+  DevMem p2m_works, p2m_ranges, p2l_works, p2l_ranges, leaf_works, leaf_items;
+  int n_p2m = 0, n_p2l = 0, n_leafw = 0;
+  GemmTiles solve_up1, solve_up2, solve_dn1, solve_dn2, m2l;
+  std::vector<std::unique_ptr<GemmTiles>> m2m_levels, l2l_levels, m2m_top;
+  M2LTcPlan m2l_tc;
+  // exchange
+  void* comm = nullptr;
+  DevMem x_send, x_recv, x_rows, x_rank, x_my_rows;
+  int x_max = 0, x_total = 0, x_mine = 0;
+  // graphs
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+
+  ~kifmm_gpu_plan() {
+    for (auto& g : graph)
+      if (g) cudaGraphExecDestroy(g);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+    if (comm) Nccl::get().commDestroy(static_cast<ncclComm_t>(comm));
+  }
+
+  size_t esz() const { return precision == 32 ? 4 : 8; }
+  void build(const kifmm_gpu_options& o, const kifmm_tree_view& t, const kifmm_operator_view& ops);
+  template <class T>
+  void upload_static(const kifmm_tree_view& t, const kifmm_operator_view& ops);
+  template <class T>
+  void run(cudaStream_t s, bool input_order, bool timed);
+  void exchange(cudaStream_t s);
+  void evaluate_device(const void* q, void* pot_dst, void* grad_dst, bool input_order, cudaStream_t user, bool timed);
+};
+
+namespace {
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+template <class T>
+std::vector<T> to_t(const std::vector<double>& v) {
+  return std::vector<T>(v.begin(), v.end());
+}
+
+}  // namespace
+
+template <class T>
+void kifmm_gpu_plan::upload_static(const kifmm_tree_view& t, const kifmm_operator_view& ops) {
+  // positions (x, y, z, 0)
+  std::vector<T> p4(size_t(N) * 4, T(0));
+  for (int64_t i = 0; i < N; ++i)
+    for (int d = 0; d < 3; ++d) p4[4 * i + d] = T(t.positions[3 * i + d]);
+  pos4.upload(p4, &dev_bytes);
+  std::vector<int> pm(N);
+  for (int64_t i = 0; i < N; ++i) pm[i] = int(t.original_index[i]);
+  perm.upload(pm, &dev_bytes);
+  // node geometry (center, half side) computed in fp64 then rounded
+  std::vector<T> g(size_t(nn) * 4);
+  std::vector<int> lv(nn);
+  for (int64_t n = 0; n < nn; ++n) {
+    const uint64_t k = t.node_key[n];
+    const auto a = key_anchor(k);
+    const int l = key_level(k);
+    const double w = t.side / double(uint64_t(1) << l);
+    for (int d = 0; d < 3; ++d) g[4 * n + d] = T(t.origin[d] + (double(a[d]) + 0.5) * w);
+    g[4 * n + 3] = T(t.side / double(uint64_t(1) << (l + 1)));
+    lv[n] = l;
+  }
+  node_geom.upload(g, &dev_bytes);
+  node_level.upload(lv, &dev_bytes);
+  surface.upload(to_t<T>(std::vector<double>(ops.surface, ops.surface + 3 * ne)), &dev_bytes);
+
+  // factored pinvs as two GEMM operands: W1 = U diag(1/s) (nc x k), W2 = V^T (k x ne), zero padded to np x np
+  auto factored = [&](const double* U, const double* S, const double* V, int k, DevMem& w1, DevMem& w2) {
+    std::vector<double> a(size_t(np) * np, 0.0), b(size_t(np) * np, 0.0);
+    for (int i = 0; i < nc; ++i)
+      for (int j = 0; j < k; ++j) a[size_t(i) * np + j] = U[size_t(i) * k + j] / S[j];
+    for (int j = 0; j < k; ++j)
+      for (int e = 0; e < ne; ++e) b[size_t(j) * np + e] = V[size_t(e) * k + j];
+    w1.upload(to_t<T>(a), &dev_bytes);
+    w2.upload(to_t<T>(b), &dev_bytes);
+  };
+  factored(ops.uc2e_u, ops.uc2e_s, ops.uc2e_v, ops.uc2e_rank, w_us_u, w_vt_u);
+  factored(ops.dc2e_u, ops.dc2e_s, ops.dc2e_v, ops.dc2e_rank, w_us_d, w_vt_d);
+  // W[k][n] = A[n][k] for m2m / l2l / m2l (out_n = sum_k A[n][k] in_k)
+  auto transposed = [&](const double* A, int count, int rows, int cols, DevMem& w) {
+    std::vector<T> out(size_t(count) * np * np, T(0));
+    for (int c = 0; c < count; ++c)
+      for (int n = 0; n < rows; ++n)
+        for (int k = 0; k < cols; ++k)
+          out[size_t(c) * np * np + size_t(k) * np + n] = T(A[size_t(c) * rows * cols + size_t(n) * cols + k]);
+    w.upload(out, &dev_bytes);
+  };
+  transposed(ops.m2m, 8, ne, ne, w_m2m);
+  transposed(ops.l2l, 8, ne, ne, w_l2l);
+  transposed(ops.m2l, ops.n_m2l, nc, ne, w_m2l);
+}
+
+void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t, const kifmm_operator_view& ops) {
+  opt = o;
+  device = o.device;
+  precision = o.precision;
+  grad = o.gradient != 0;
+  world = std::max(1, o.world_size);
+  rank = o.rank;
+  cut = o.cut_level > 0 ? o.cut_level : 2;
+  if (precision != 32 && precision != 64) throw InvalidArgument("gpu: precision must be 32 or 64");
+  if (rank < 0 || rank >= world) throw InvalidArgument("gpu: rank out of range");
+  if (ops.n_e != ops.n_c) throw InvalidArgument("gpu: n_c != n_e is not supported");
+  if (ops.n_e > 224) throw InvalidArgument("gpu: expansion order above p=7 (n_e > 224) is not supported");
+  if (t.n_particles >= (int64_t(1) << 31)) throw InvalidArgument("gpu: N >= 2^31");
+  if (ops.n_m2l != 316) throw InvalidArgument("gpu: operator cache must hold 316 M2L matrices");
+  KIFMM_CUDA(cudaSetDevice(device));
+  N = t.n_particles;
+  nl = t.n_leaves;
+  nn = t.n_nodes;
+  depth = t.depth;
+  ne = ops.n_e;
+  nc = ops.n_c;
+  np = round_up(ne, 32);
+  if (np == 96 || np == 192) np += 32;  // instantiated widths: 32, 64, 128, 160, 224
+  ref_level = ops.reference_level;
+  alpha_in = ops.alpha_inner;
+  alpha_out = ops.alpha_outer;
+  const double expect_half = t.side / double(1 << (ref_level + 1));
+  if (std::fabs(ops.ref_half_side - expect_half) > 1e-12 * expect_half)
+    throw InvalidArgument("gpu: operator cache was built for another domain side");
+  KIFMM_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  for (auto& e : ev) KIFMM_CUDA(cudaEventCreate(&e));
+
+  // ---- partition
+  std::vector<int64_t> lbeg(world + 1, 0);
+  lbeg[world] = nl;
+  if (world > 1) {
+    const kifmm_status st = kifmm_partition_leaves(&t, ne, grad ? 1 : 0, world, cut, lbeg.data());
+    if (st != KIFMM_OK) throw InvalidArgument(std::string("partition: ") + kifmm_last_error());
+  }
+  lb = lbeg[rank];
+  le = lbeg[rank + 1];
+  pb = t.leaf_ptr[lb];
+  pe = t.leaf_ptr[le];
+
+  // leaf range covered by each node (leaves ascend in raw key = spatial order)
+  std::vector<int64_t> nlo(nn, INT64_MAX), nhi(nn, -1);
+  for (int64_t l = 0; l < nl; ++l)
+    for (int64_t n = t.leaf_node[l]; n >= 0; n = t.node_parent[n]) {
+      nlo[n] = std::min(nlo[n], l);
+      nhi[n] = std::max(nhi[n], l + 1);
+    }
+  auto node_lvl = [&](int64_t n) { return key_level(t.node_key[n]); };
+  auto is_leaf = [&](int64_t n) { return t.node_leaf[n] >= 0; };
+  // owner rank of a node for the upward pass: all leaves in one rank's range and (level >= cut or leaf)
+  auto owner_of_range = [&](int64_t lo, int64_t hi) -> int {
+    const int r = int(std::upper_bound(lbeg.begin(), lbeg.end(), lo) - lbeg.begin()) - 1;
+    return (hi <= lbeg[r + 1]) ? r : -1;
+  };
+  std::vector<int> up_owner(nn, -1);
+  for (int64_t n = 0; n < nn; ++n) {
+    if (world == 1) {
+      up_owner[n] = 0;
+      continue;
+    }
+    if (is_leaf(n) || node_lvl(n) >= cut) up_owner[n] = owner_of_range(nlo[n], nhi[n]);
+  }
+  // downward-active nodes: ancestors-or-self of owned leaves
+  std::vector<char> active(nn, 0);
+  for (int64_t l = lb; l < le; ++l)
+    for (int64_t n = t.leaf_node[l]; n >= 0 && !active[n]; n = t.node_parent[n]) active[n] = 1;
+
+  if (precision == 32)
+    upload_static<float>(t, ops);
+  else
+    upload_static<double>(t, ops);
+
+  const size_t es = esz();
+  q_in.alloc(size_t(N) * es, &dev_bytes);
+  src4.alloc(size_t(N) * 4 * es, &dev_bytes);
+  pot.alloc(size_t(N) * es, &dev_bytes);
+  pot_out.alloc(size_t(N) * es, &dev_bytes);
+  if (grad) {
+    grad_buf.alloc(size_t(N) * 3 * es, &dev_bytes);
+    grad_out.alloc(size_t(N) * 3 * es, &dev_bytes);
+  }
+  M.alloc(size_t(nn) * np * es, &dev_bytes);
+  L.alloc(size_t(nn) * np * es, &dev_bytes);
+  KIFMM_CUDA(cudaMemset(M.p, 0, M.bytes));
+  KIFMM_CUDA(cudaMemset(L.p, 0, L.bytes));
+  check_dn.alloc(size_t(nn) * np * es, &dev_bytes);
+
+  const int bm_big = precision == 32 ? 128 : 64;
+  const int bm_m2l = 64;
+  const int ld_tiles = bm_big;
+
+  // ---- P2M: one check work per owned leaf, solve rows = slots
+  {
+    std::vector<CheckWork> w;
+    std::vector<int2> rg;
+    for (int64_t l = lb; l < le; ++l) {
+      w.push_back({int(t.leaf_node[l]), int(l - lb), int(rg.size()), int(rg.size()) + 1});
+      rg.push_back(make_int2(int(t.leaf_ptr[l]), int(t.leaf_ptr[l + 1] - t.leaf_ptr[l])));
+      info.p2m_pairs += (t.leaf_ptr[l + 1] - t.leaf_ptr[l]) * ne;
+    }
+    n_p2m = int(w.size());
+    p2m_works.upload(w, &dev_bytes);
+    p2m_ranges.upload(rg, &dev_bytes);
+    check_up.alloc(size_t(std::max<int64_t>(1, le - lb)) * np * es, &dev_bytes);
+    std::vector<TileSpec> a, b;
+    for (int64_t s0 = 0; s0 < le - lb; s0 += ld_tiles) {
+      TileSpec x, y;
+      std::vector<int> slots(ld_tiles, -1), nodes(ld_tiles, -1);
+      for (int r = 0; r < ld_tiles && s0 + r < le - lb; ++r) {
+        slots[r] = int(s0 + r);
+        nodes[r] = int(t.leaf_node[lb + s0 + r]);
+      }
+      x.out = slots;
+      x.segs.push_back({0, slots});
+      y.out = nodes;
+      y.segs.push_back({0, slots});
+      a.push_back(x);
+      b.push_back(y);
+    }
+    solve_up1.build(a, ld_tiles, &dev_bytes);
+    solve_up2.build(b, ld_tiles, &dev_bytes);
+  }
+
+  // ---- M2M per level (owned internal nodes), then the redundant top levels
+  auto m2m_tiles = [&](std::vector<int64_t>& parents) {
+    std::vector<TileSpec> tiles;
+    for (size_t s0 = 0; s0 < parents.size(); s0 += ld_tiles) {
+      TileSpec ts;
+      ts.out.assign(ld_tiles, -1);
+      for (int o = 0; o < 8; ++o) ts.segs.push_back({o, std::vector<int>(ld_tiles, -1)});
+      for (int r = 0; r < ld_tiles && s0 + r < parents.size(); ++r) {
+        const int64_t pn = parents[s0 + r];
+        ts.out[r] = int(pn);
+        for (int o = 0; o < 8; ++o) ts.segs[o].second[r] = int(t.node_children[8 * pn + o]);
+      }
+      // drop octants absent in the whole tile
+      std::vector<std::pair<int, std::vector<int>>> keep;
+      for (auto& sg : ts.segs)
+        if (std::any_of(sg.second.begin(), sg.second.end(), [](int v) { return v >= 0; })) keep.push_back(sg);
+      ts.segs.swap(keep);
+      tiles.push_back(std::move(ts));
+    }
+    auto g = std::make_unique<GemmTiles>();
+    g->build(tiles, ld_tiles, &dev_bytes);
+    return g;
+  };
+  const int up_floor = world > 1 ? cut : 0;
+  for (int l = depth - 1; l >= up_floor; --l) {
+    std::vector<int64_t> parents;
+    for (int64_t n = t.level_ptr[l]; n < t.level_ptr[l + 1]; ++n)
+      if (!is_leaf(n) && up_owner[n] == rank) parents.push_back(n);
+    if (!parents.empty()) m2m_levels.push_back(m2m_tiles(parents));
+  }
+  if (world > 1) {
+    for (int l = std::min(cut, depth) - 1; l >= 0; --l) {
+      std::vector<int64_t> parents;
+      for (int64_t n = t.level_ptr[l]; n < t.level_ptr[l + 1]; ++n)
+        if (!is_leaf(n)) parents.push_back(n);
+      if (!parents.empty()) m2m_top.push_back(m2m_tiles(parents));
+    }
+    // exchange tables: every rank exports the multipoles it owns
+    std::vector<std::vector<int>> exp(world);
+    for (int64_t n = 0; n < nn; ++n)
+      if (up_owner[n] >= 0) exp[up_owner[n]].push_back(int(n));
+    x_max = 0;
+    for (auto& e : exp) x_max = std::max<int>(x_max, int(e.size()));
+    x_mine = int(exp[rank].size());
+    std::vector<int> rows, pos, rk;
+    for (int r = 0; r < world; ++r)
+      for (size_t i = 0; i < exp[r].size(); ++i) {
+        rows.push_back(exp[r][i]);
+        pos.push_back(int(i));
+        rk.push_back(r);
+      }
+    x_total = int(rows.size());
+    rows.insert(rows.end(), pos.begin(), pos.end());
+    x_rows.upload(rows, &dev_bytes);
+    x_rank.upload(rk, &dev_bytes);
+    x_my_rows.upload(exp[rank], &dev_bytes);
+    x_send.alloc(size_t(std::max(1, x_max)) * np * es, &dev_bytes);
+    x_recv.alloc(size_t(std::max(1, x_max)) * np * es * world, &dev_bytes);
+    if (!o.nccl_unique_id) throw InvalidArgument("gpu: world_size > 1 needs nccl_unique_id");
+    ncclUniqueId id;
+    std::memcpy(&id, o.nccl_unique_id, sizeof(id));
+    ncclComm_t c;
+    Nccl& nc_ = Nccl::get();
+    nc_.check(nc_.commInitRank(&c, world, id, rank), "ncclCommInitRank");
+    comm = c;
+  }
+
+  // ---- P2L check works: active nodes with X members
+  {
+    std::vector<CheckWork> w;
+    std::vector<int2> rg;
+    for (int64_t n = 0; n < nn; ++n) {
+      if (!active[n] || t.x_ptr[n] == t.x_ptr[n + 1]) continue;
+      const int r0 = int(rg.size());
+      for (int64_t e = t.x_ptr[n]; e < t.x_ptr[n + 1]; ++e) {
+        const int64_t a = t.x_idx[e];
+        rg.push_back(make_int2(int(t.leaf_ptr[a]), int(t.leaf_ptr[a + 1] - t.leaf_ptr[a])));
+        info.p2l_pairs += (t.leaf_ptr[a + 1] - t.leaf_ptr[a]) * ne;
+      }
+      w.push_back({int(n), int(n), r0, int(rg.size())});
+    }
+    n_p2l = int(w.size());
+    p2l_works.upload(w, &dev_bytes);
+    p2l_ranges.upload(rg, &dev_bytes);
+  }
+
+  // ---- M2L tiles: active targets at level >= 2 grouped by (level, octant), Z-order inside
+  std::vector<std::vector<int64_t>> m2l_groups;
+  {
+    std::map<std::pair<int, int>, std::vector<int64_t>> groups;
+    for (int64_t n = 0; n < nn; ++n) {
+      if (!active[n] || node_lvl(n) < 2 || t.v_ptr[n] == t.v_ptr[n + 1]) continue;
+      groups[{node_lvl(n), key_octant(t.node_key[n])}].push_back(n);
+      info.m2l_pairs += t.v_ptr[n + 1] - t.v_ptr[n];
+    }
+    for (auto& kv : groups) m2l_groups.push_back(kv.second);
+    std::vector<TileSpec> tiles;
+    for (auto& grp : m2l_groups) {
+      for (size_t s0 = 0; s0 < grp.size(); s0 += bm_m2l) {
+        TileSpec ts;
+        ts.out.assign(bm_m2l, -1);
+        std::map<int, std::vector<int>> taps;
+        for (int r = 0; r < bm_m2l && s0 + r < grp.size(); ++r) {
+          const int64_t b = grp[s0 + r];
+          ts.out[r] = int(b);
+          for (int64_t e = t.v_ptr[b]; e < t.v_ptr[b + 1]; ++e) {
+            auto& v = taps[t.v_tv[e]];
+            if (v.empty()) v.assign(bm_m2l, -1);
+            v[r] = int(t.v_idx[e]);
+          }
+        }
+        for (auto& kv : taps) ts.segs.push_back({kv.first, kv.second});
+        tiles.push_back(std::move(ts));
+      }
+    }
+    // most expensive tiles first (better tail on the block scheduler)
+    std::stable_sort(tiles.begin(), tiles.end(),
+                     [](const TileSpec& x, const TileSpec& y) { return x.segs.size() > y.segs.size(); });
+    m2l.build(tiles, bm_m2l, &dev_bytes);
+    info.m2l_padded_pairs = m2l.slots;
+  }
+  m2l_backend = 1;
+  if (o.m2l_backend == 2 || (o.m2l_backend == 0 && precision == 32 && m2l_tc_available())) {
+    if (precision != 32) throw InvalidArgument("gpu: tcgen05 3xTF32 M2L is an fp32 path");
+    m2l_tc.build(t, m2l_groups, np, ops, &dev_bytes);
+    m2l_backend = 2;
+  }
+
+  // ---- downward solves over active nodes at level >= 2 (slots -> tmp rows)
+  std::vector<int64_t> dn_nodes;
+  for (int64_t n = 0; n < nn; ++n)
+    if (active[n] && node_lvl(n) >= 2) dn_nodes.push_back(n);
+  {
+    std::vector<TileSpec> a, b;
+    for (size_t s0 = 0; s0 < dn_nodes.size(); s0 += ld_tiles) {
+      TileSpec x, y;
+      std::vector<int> slots(ld_tiles, -1), nodes(ld_tiles, -1);
+      for (int r = 0; r < ld_tiles && s0 + r < dn_nodes.size(); ++r) {
+        slots[r] = int(s0 + r);
+        nodes[r] = int(dn_nodes[s0 + r]);
+      }
+      x.out = slots;
+      x.segs.push_back({0, nodes});
+      y.out = nodes;
+      y.segs.push_back({0, slots});
+      a.push_back(x);
+      b.push_back(y);
+    }
+    solve_dn1.build(a, ld_tiles, &dev_bytes);
+    solve_dn2.build(b, ld_tiles, &dev_bytes);
+  }
+  tmp.alloc(size_t(std::max<int64_t>({int64_t(1), le - lb, int64_t(dn_nodes.size())})) * np * es, &dev_bytes);
+
+  // ---- L2L per level: active children at l+1 (l >= 2), grouped by octant
+  for (int l = 2; l < depth; ++l) {
+    std::vector<TileSpec> tiles;
+    for (int oc = 0; oc < 8; ++oc) {
+      std::vector<int64_t> ch;
+      for (int64_t n = t.level_ptr[l + 1]; n < t.level_ptr[l + 2]; ++n)
+        if (active[n] && key_octant(t.node_key[n]) == oc) ch.push_back(n);
+      for (size_t s0 = 0; s0 < ch.size(); s0 += ld_tiles) {
+        TileSpec ts;
+        ts.out.assign(ld_tiles, -1);
+        std::vector<int> in(ld_tiles, -1);
+        for (int r = 0; r < ld_tiles && s0 + r < ch.size(); ++r) {
+          ts.out[r] = int(ch[s0 + r]);
+          in[r] = int(t.node_parent[ch[s0 + r]]);
+        }
+        ts.segs.push_back({oc, in});
+        tiles.push_back(std::move(ts));
+      }
+    }
+    if (!tiles.empty()) {
+      auto g = std::make_unique<GemmTiles>();
+      g->build(tiles, ld_tiles, &dev_bytes);
+      l2l_levels.push_back(std::move(g));
+    }
+  }
+
+  // ---- leaf works: near field (U) + L2P + M2P (W), <= 128 targets per work
+  {
+    std::vector<LeafWork> w;
+    std::vector<int4> items;
+    for (int64_t l = lb; l < le; ++l) {
+      const int64_t node = t.leaf_node[l];
+      const int ib = int(items.size());
+      int64_t src_cnt = 0;
+      // U ranges, merged when contiguous in the reordered buffer
+      int cur_b = -1, cur_e = -1;
+      for (int64_t e = t.u_ptr[l]; e < t.u_ptr[l + 1]; ++e) {
+        const int64_t s = t.u_idx[e];
+        const int b = int(t.leaf_ptr[s]), en = int(t.leaf_ptr[s + 1]);
+        src_cnt += en - b;
+        if (b == cur_e) {
+          cur_e = en;
+        } else {
+          if (cur_b >= 0) items.push_back(make_int4(kSrcParticles, cur_b, cur_e - cur_b, 0));
+          cur_b = b;
+          cur_e = en;
+        }
+      }
+      if (cur_b >= 0) items.push_back(make_int4(kSrcParticles, cur_b, cur_e - cur_b, 0));
+      const int64_t nt = t.leaf_ptr[l + 1] - t.leaf_ptr[l];
+      info.near_pairs += nt * src_cnt;
+      if (node_lvl(node) >= 2) {
+        items.push_back(make_int4(kSrcL2P, int(node), 0, 0));
+        info.l2p_pairs += nt * ne;
+      }
+      for (int64_t e = t.w_ptr[l]; e < t.w_ptr[l + 1]; ++e) {
+        items.push_back(make_int4(kSrcM2P, int(t.w_idx[e]), 0, 0));
+        info.m2p_pairs += nt * ne;
+      }
+      const int ie = int(items.size());
+      for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += kP2PThreads)
+        w.push_back({int(l), int(t0), int(std::min<int64_t>(kP2PThreads, t.leaf_ptr[l + 1] - t0)), ib, ie});
+    }
+    n_leafw = int(w.size());
+    leaf_works.upload(w, &dev_bytes);
+    leaf_items.upload(items, &dev_bytes);
+  }
+
+  info.n_particles = N;
+  info.n_leaves = nl;
+  info.n_nodes = nn;
+  info.owned_leaf_begin = lb;
+  info.owned_leaf_end = le;
+  info.owned_particle_begin = pb;
+  info.owned_particle_end = pe;
+  info.n_e = ne;
+  info.n_c = nc;
+  info.ne_pad = np;
+  info.m2l_backend = m2l_backend;
+  KIFMM_CUDA(cudaDeviceSynchronize());
+  info.device_bytes = int64_t(dev_bytes);
+}
+
+void kifmm_gpu_plan::exchange(cudaStream_t s) {
+  if (world <= 1) return;
+  const size_t es = esz();
+  if (x_mine > 0) {
+    if (precision == 32)
+      gather_rows_kernel<float><<<x_mine, 128, 0, s>>>(M.as<float>(), np, x_my_rows.as<int>(), x_mine, x_send.as<float>());
+    else
+      gather_rows_kernel<double><<<x_mine, 128, 0, s>>>(M.as<double>(), np, x_my_rows.as<int>(), x_mine, x_send.as<double>());
+    KIFMM_LAUNCH_CHECK();
+  }
+  Nccl& n = Nccl::get();
+  n.check(n.allGather(x_send.p, x_recv.p, size_t(x_max) * np, precision == 32 ? ncclFloat32 : ncclFloat64,
+                      static_cast<ncclComm_t>(comm), s),
+          "ncclAllGather");
+  (void)es;
+  if (x_total > 0) {
+    if (precision == 32)
+      scatter_rows_kernel<float><<<x_total, 128, 0, s>>>(x_recv.as<float>(), np, x_rows.as<int>(), x_rank.as<int>(),
+                                                          x_max, rank, x_total, M.as<float>());
+    else
+      scatter_rows_kernel<double><<<x_total, 128, 0, s>>>(x_recv.as<double>(), np, x_rows.as<int>(), x_rank.as<int>(),
+                                                           x_max, rank, x_total, M.as<double>());
+    KIFMM_LAUNCH_CHECK();
+  }
+}
+
+template <class T>
+void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
+  constexpr int BMB = sizeof(T) == 4 ? 128 : 64;
+  constexpr int TMB = sizeof(T) == 4 ? 8 : 4;
+  int ei = 0;
+  auto mark = [&]() {
+    if (timed) KIFMM_CUDA(cudaEventRecord(ev[ei++], s));
+  };
+  int launches = 0;
+  const P2PParams<T> pp{src4.as<v4_t<T>>(), node_geom.as<v4_t<T>>(), surface.as<T>(), ne, np, T(alpha_in),
+                        T(alpha_out)};
+  auto gemm = [&](const GemmTiles& tl, const T* X, const T* W, T* Y, bool acc, bool m2l_shape) {
+    if (tl.n_tiles == 0) return;
+    GemmArgs<T> a{};
+    a.X = X;
+    a.ldx = np;
+    a.W = W;
+    a.K = np;
+    a.Y = Y;
+    a.ldy = np;
+    a.accumulate = acc ? 1 : 0;
+    if (m2l_shape)
+      launch_gemm<T, 64, 4>(np, tl, a, s);
+    else
+      launch_gemm<T, BMB, TMB>(np, tl, a, s);
+    ++launches;
+  };
+  T* Mp = M.as<T>();
+  T* Lp = L.as<T>();
+
+  mark();  // 0
+  pack_sources_kernel<T><<<int(ceil_div(N, 256)), 256, 0, s>>>(pos4.as<v4_t<T>>(), q_in.as<T>(),
+                                                               input_order ? perm.as<int>() : nullptr, int(N),
+                                                               src4.as<v4_t<T>>());
+  KIFMM_LAUNCH_CHECK();
+  ++launches;
+  // upward: P2M check -> factored solve
+  if (n_p2m) {
+    check_kernel<T><<<n_p2m, kP2PThreads, 0, s>>>(pp, p2m_works.as<CheckWork>(), p2m_ranges.as<int2>(),
+                                                  node_level.as<int>(), ref_level, T(alpha_out), check_up.as<T>(), np);
+    KIFMM_LAUNCH_CHECK();
+    ++launches;
+  }
+  gemm(solve_up1, check_up.as<T>(), w_us_u.as<T>(), tmp.as<T>(), false, false);
+  gemm(solve_up2, tmp.as<T>(), w_vt_u.as<T>(), Mp, false, false);
+  mark();  // 1
+  // M2M, levels d-1 .. floor
+  for (auto& lv : m2m_levels) gemm(*lv, Mp, w_m2m.as<T>(), Mp, false, false);
+  mark();  // 2
+  // multipole exchange (multi-GPU) and the redundant top of the tree
+  if (world > 1) {
+    exchange(s);
+    launches += 2;
+    for (auto& lv : m2m_top) gemm(*lv, Mp, w_m2m.as<T>(), Mp, false, false);
+  }
+  mark();  // 3
+  // downward: P2L check into the down-check buffer
+  KIFMM_CUDA(cudaMemsetAsync(check_dn.p, 0, check_dn.bytes, s));
+  if (n_p2l) {
+    check_kernel<T><<<n_p2l, kP2PThreads, 0, s>>>(pp, p2l_works.as<CheckWork>(), p2l_ranges.as<int2>(),
+                                                  node_level.as<int>(), ref_level, T(alpha_in), check_dn.as<T>(), np);
+    KIFMM_LAUNCH_CHECK();
+    ++launches;
+  }
+  mark();  // 4
+  // M2L over all levels at once, accumulated as reference-level check potentials
+  if (m2l_backend == 2) {
+    if constexpr (sizeof(T) == 4) {
+      m2l_tc.launch(Mp, check_dn.as<float>(), np, s);
+      launches += m2l_tc.launches();
+    }
+  } else {
+    gemm(m2l, Mp, w_m2l.as<T>(), check_dn.as<T>(), true, true);
+  }
+  mark();  // 5
+  // factored downward solve (dc2e at the reference level; M2L/P2L level factors folded)
+  gemm(solve_dn1, check_dn.as<T>(), w_us_d.as<T>(), tmp.as<T>(), false, false);
+  gemm(solve_dn2, tmp.as<T>(), w_vt_d.as<T>(), Lp, false, false);
+  mark();  // 6
+  // L2L top-down
+  for (auto& lv : l2l_levels) gemm(*lv, Lp, w_l2l.as<T>(), Lp, true, false);
+  mark();  // 7
+  // leaves: near field + L2P + M2P
+  if (n_leafw) {
+    if (grad)
+      leaf_eval_kernel<T, true><<<n_leafw, kP2PThreads, 0, s>>>(pp, leaf_works.as<LeafWork>(), leaf_items.as<int4>(),
+                                                                Mp, Lp, pot.as<T>(), grad_buf.as<T>());
+    else
+      leaf_eval_kernel<T, false><<<n_leafw, kP2PThreads, 0, s>>>(pp, leaf_works.as<LeafWork>(), leaf_items.as<int4>(),
+                                                                 Mp, Lp, pot.as<T>(), nullptr);
+    KIFMM_LAUNCH_CHECK();
+    ++launches;
+  }
+  mark();  // 8
+  if (input_order) {
+    if (world > 1) {
+      KIFMM_CUDA(cudaMemsetAsync(pot_out.p, 0, pot_out.bytes, s));
+      if (grad) KIFMM_CUDA(cudaMemsetAsync(grad_out.p, 0, grad_out.bytes, s));
+    }
+    const int cnt = int(pe - pb);
+    if (cnt > 0) {
+      unpermute_kernel<T><<<int(ceil_div(cnt, 256)), 256, 0, s>>>(pot.as<T>(), perm.as<int>(), int(pb), int(pe), 1,
+                                                                  pot_out.as<T>());
+      ++launches;
+      if (grad) {
+        unpermute_kernel<T><<<int(ceil_div(cnt, 256)), 256, 0, s>>>(grad_buf.as<T>(), perm.as<int>(), int(pb),
+                                                                    int(pe), 3, grad_out.as<T>());
+        ++launches;
+      }
+      KIFMM_LAUNCH_CHECK();
+    }
+  }
+  mark();  // 9
+  info.kernel_launches = launches;
+}
+
+void kifmm_gpu_plan::evaluate_device(const void* q, void* pot_dst, void* grad_dst, bool input_order,
+                                     cudaStream_t user, bool timed) {
+  KIFMM_CUDA(cudaSetDevice(device));
+  cudaStream_t s = user ? user : stream;
+  const size_t es = esz();
+  KIFMM_CUDA(cudaMemcpyAsync(q_in.p, q, size_t(N) * es, cudaMemcpyDefault, s));
+  const int gi = input_order ? 1 : 0;
+  if (!timed && opt.use_graph) {
+    if (!graph[gi]) {
+      cudaGraph_t g;
+      KIFMM_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        if (precision == 32)
+          run<float>(stream, input_order, false);
+        else
+          run<double>(stream, input_order, false);
+      } catch (...) {
+        cudaStreamEndCapture(stream, &g);
+        throw;
+      }
+      KIFMM_CUDA(cudaStreamEndCapture(stream, &g));
+      KIFMM_CUDA(cudaGraphInstantiate(&graph[gi], g, 0));
+      cudaGraphDestroy(g);
+    }
+    KIFMM_CUDA(cudaGraphLaunch(graph[gi], s));
+  } else {
+    if (precision == 32)
+      run<float>(s, input_order, timed);
+    else
+      run<double>(s, input_order, timed);
+  }
+  const void* ps = input_order ? pot_out.p : pot.p;
+  const void* gs = input_order ? grad_out.p : grad_buf.p;
+  if (input_order || world == 1) {
+    if (pot_dst) KIFMM_CUDA(cudaMemcpyAsync(pot_dst, ps, size_t(N) * es, cudaMemcpyDefault, s));
+    if (grad && grad_dst) KIFMM_CUDA(cudaMemcpyAsync(grad_dst, gs, size_t(N) * 3 * es, cudaMemcpyDefault, s));
+  } else {
+    const size_t off = size_t(pb) * es, cnt = size_t(pe - pb) * es;
+    if (pot_dst && cnt)
+      KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(pot_dst) + off, static_cast<const char*>(ps) + off, cnt,
+                                 cudaMemcpyDefault, s));
+    if (grad && grad_dst && cnt)
+      KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(grad_dst) + 3 * off, static_cast<const char*>(gs) + 3 * off,
+                                 3 * cnt, cudaMemcpyDefault, s));
+  }
+}
+
+namespace {
+template <class T>
+void direct_impl(int device, const T* pos, const T* q, int64_t n, const int64_t* targets, int64_t m, T* pot, T* grad) {
+  KIFMM_CUDA(cudaSetDevice(device));
+  std::vector<T> s4(size_t(n) * 4);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int d = 0; d < 3; ++d) s4[4 * i + d] = pos[3 * i + d];
+    s4[4 * i + 3] = q[i];
+  }
+  std::vector<int64_t> tg(targets, targets + m);
+  size_t dummy = 0;
+  DevMem d_src, d_tg, d_pot, d_grad;
+  d_src.upload(s4, &dummy);
+  d_tg.upload(tg, &dummy);
+  d_pot.alloc(size_t(m) * sizeof(T), &dummy);
+  if (grad) d_grad.alloc(size_t(m) * 3 * sizeof(T), &dummy);
+  const int blocks = int(ceil_div(m, kP2PThreads));
+  if (grad)
+    direct_kernel<T, true><<<blocks, kP2PThreads>>>(d_src.as<v4_t<T>>(), n, d_tg.as<int64_t>(), m, d_pot.as<T>(),
+                                                    d_grad.as<T>());
+  else
+    direct_kernel<T, false><<<blocks, kP2PThreads>>>(d_src.as<v4_t<T>>(), n, d_tg.as<int64_t>(), m, d_pot.as<T>(),
+                                                     nullptr);
+  KIFMM_LAUNCH_CHECK();
+  KIFMM_CUDA(cudaMemcpy(pot, d_pot.p, size_t(m) * sizeof(T), cudaMemcpyDeviceToHost));
+  if (grad) KIFMM_CUDA(cudaMemcpy(grad, d_grad.p, size_t(m) * 3 * sizeof(T), cudaMemcpyDeviceToHost));
+}
+
+template <class T>
+double fma_peak_impl(int device) {
+  KIFMM_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  KIFMM_CUDA(cudaGetDeviceProperties(&prop, device));
+  DevMem out;
+  size_t dummy = 0;
+  out.alloc(64, &dummy);
+  const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = sizeof(T) == 4 ? 16384 : 2048;
+  cudaEvent_t a, b;
+  KIFMM_CUDA(cudaEventCreate(&a));
+  KIFMM_CUDA(cudaEventCreate(&b));
+  fma_probe_kernel<T><<<blocks, threads>>>(out.as<T>(), iters / 4, T(0.999), T(1e-3));
+  KIFMM_CUDA(cudaEventRecord(a));
+  fma_probe_kernel<T><<<blocks, threads>>>(out.as<T>(), iters, T(0.999), T(1e-3));
+  KIFMM_CUDA(cudaEventRecord(b));
+  KIFMM_CUDA(cudaEventSynchronize(b));
+  float ms = 0;
+  KIFMM_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return double(blocks) * threads * iters * 8 * 2 / (ms * 1e-3);
+}
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+kifmm_status kifmm_gpu_plan_create(const kifmm_gpu_options* options, const kifmm_tree_view* tree,
+                                   const kifmm_operator_view* ops, kifmm_gpu_plan** out) {
+  return guard([&] {
+    if (!options || !tree || !ops || !out) throw InvalidArgument("plan_create: null argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw DeviceError(KIFMM_E_CUDA, "plan_create: no CUDA device available (the library has no CPU fallback)");
+    if (options->device < 0 || options->device >= ndev) throw InvalidArgument("plan_create: bad device ordinal");
+    auto p = std::make_unique<kifmm_gpu_plan>();
+    p->build(*options, *tree, *ops);
+    // one untimed warm-up pass (sets kernel attributes, validates every launch)
+    KIFMM_CUDA(cudaMemsetAsync(p->q_in.p, 0, p->q_in.bytes, p->stream));
+    if (p->precision == 32)
+      p->run<float>(p->stream, false, false);
+    else
+      p->run<double>(p->stream, false, false);
+    KIFMM_CUDA(cudaStreamSynchronize(p->stream));
+    *out = p.release();
+  });
+}
+
+kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* p, const void* charges, void* potential, void* gradient,
+                                int32_t input_order, kifmm_gpu_timings* timings) {
+  return guard([&] {
+    if (!p || !charges || !potential) throw InvalidArgument("evaluate: null argument");
+    KIFMM_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = p->stream;
+    const size_t es = p->esz();
+    auto& ev = p->ev;
+    // events 10..13: H2D, compute, D2H boundaries
+    KIFMM_CUDA(cudaEventRecord(ev[10], s));
+    KIFMM_CUDA(cudaMemcpyAsync(p->q_in.p, charges, size_t(p->N) * es, cudaMemcpyDefault, s));
+    KIFMM_CUDA(cudaEventRecord(ev[11], s));
+    const bool timed = timings != nullptr;
+    const int gi = input_order ? 1 : 0;
+    if (!timed && p->opt.use_graph) {
+      if (!p->graph[gi]) {
+        cudaGraph_t g;
+        KIFMM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        if (p->precision == 32)
+          p->run<float>(s, input_order != 0, false);
+        else
+          p->run<double>(s, input_order != 0, false);
+        KIFMM_CUDA(cudaStreamEndCapture(s, &g));
+        KIFMM_CUDA(cudaGraphInstantiate(&p->graph[gi], g, 0));
+        cudaGraphDestroy(g);
+      }
+      KIFMM_CUDA(cudaGraphLaunch(p->graph[gi], s));
+    } else if (p->precision == 32) {
+      p->run<float>(s, input_order != 0, timed);
+    } else {
+      p->run<double>(s, input_order != 0, timed);
+    }
+    KIFMM_CUDA(cudaEventRecord(ev[12], s));
+    const void* ps = input_order ? p->pot_out.p : p->pot.p;
+    const void* gs = input_order ? p->grad_out.p : p->grad_buf.p;
+    if (input_order || p->world == 1) {
+      KIFMM_CUDA(cudaMemcpyAsync(potential, ps, size_t(p->N) * es, cudaMemcpyDefault, s));
+      if (p->grad && gradient) KIFMM_CUDA(cudaMemcpyAsync(gradient, gs, size_t(p->N) * 3 * es, cudaMemcpyDefault, s));
+    } else {
+      const size_t off = size_t(p->pb) * es, cnt = size_t(p->pe - p->pb) * es;
+      if (cnt) {
+        KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(potential) + off, static_cast<const char*>(ps) + off, cnt,
+                                   cudaMemcpyDefault, s));
+        if (p->grad && gradient)
+          KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(gradient) + 3 * off, static_cast<const char*>(gs) + 3 * off,
+                                     3 * cnt, cudaMemcpyDefault, s));
+      }
+    }
+    KIFMM_CUDA(cudaEventRecord(ev[13], s));
+    KIFMM_CUDA(cudaStreamSynchronize(s));
+    if (timed) {
+      kifmm_gpu_timings t{};
+      auto el = [&](int a, int b) {
+        float ms = 0;
+        KIFMM_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+        return ms;
+      };
+      t.upload_ms = el(10, 11);
+      t.p2m_ms = el(0, 1);
+      t.m2m_ms = el(1, 2);
+      t.exchange_ms = el(2, 3);
+      t.p2l_ms = el(3, 4);
+      t.m2l_ms = el(4, 5);
+      t.down_solve_ms = el(5, 6);
+      t.l2l_ms = el(6, 7);
+      t.leaf_ms = el(7, 8);
+      t.total_ms = el(0, 9);
+      t.download_ms = el(12, 13);
+      p->last = t;
+      *timings = t;
+    }
+  });
+}
+
+kifmm_status kifmm_gpu_evaluate_device(kifmm_gpu_plan* p, const void* d_charges, void* d_potential,
+                                       void* d_gradient, int32_t input_order, void* stream) {
+  return guard([&] {
+    if (!p || !d_charges) throw InvalidArgument("evaluate_device: null argument");
+    p->evaluate_device(d_charges, d_potential, d_gradient, input_order != 0, static_cast<cudaStream_t>(stream), false);
+  });
+}
+
+kifmm_status kifmm_gpu_plan_get_info(const kifmm_gpu_plan* p, kifmm_gpu_plan_info* info) {
+  return guard([&] {
+    if (!p || !info) throw InvalidArgument("plan_get_info: null argument");
+    *info = p->info;
+  });
+}
+
+kifmm_status kifmm_gpu_last_timings(kifmm_gpu_plan* p, kifmm_gpu_timings* t) {
+  return guard([&] {
+    if (!p || !t) throw InvalidArgument("last_timings: null argument");
+    *t = p->last;
+  });
+}
+
+void kifmm_gpu_plan_destroy(kifmm_gpu_plan* p) { delete p; }
+
+kifmm_status kifmm_gpu_nccl_unique_id(void* out128) {
+  return guard([&] {
+    if (!out128) throw InvalidArgument("nccl_unique_id: null out");
+    Nccl& n = Nccl::get();
+    ncclUniqueId id;
+    n.check(n.getUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+kifmm_status kifmm_gpu_direct(int32_t precision, int32_t device, const void* positions, const void* charges,
+                              int64_t n, const int64_t* targets, int64_t m, void* potential, void* gradient) {
+  return guard([&] {
+    if (!positions || !charges || !targets || !potential || n < 1 || m < 0)
+      throw InvalidArgument("gpu_direct: bad argument");
+    if (m == 0) return;
+    if (precision == 32)
+      direct_impl<float>(device, static_cast<const float*>(positions), static_cast<const float*>(charges), n, targets,
+                         m, static_cast<float*>(potential), static_cast<float*>(gradient));
+    else if (precision == 64)
+      direct_impl<double>(device, static_cast<const double*>(positions), static_cast<const double*>(charges), n,
+                          targets, m, static_cast<double*>(potential), static_cast<double*>(gradient));
+    else
+      throw InvalidArgument("gpu_direct: precision must be 32 or 64");
+  });
+}
+
+kifmm_status kifmm_gpu_fma_peak(int32_t device, int32_t precision, double* flops) {
+  return guard([&] {
+    if (!flops) throw InvalidArgument("fma_peak: null out");
+    *flops = precision == 64 ? fma_peak_impl<double>(device) : fma_peak_impl<float>(device);
+  });
+}
+
+}  // extern "C"
