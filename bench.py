@@ -1,0 +1,344 @@
+"""Benchmark of the B200 KIFMM evaluate (BASELINE.json metric).
+
+Workload (N=1 GPU): BASELINE config 2 -- 1,000,000 points uniform in [0,1]^3,
+fp32 charges U[0,1), p=6 (n_e=152), n_crit=150 (uniform depth 5), potential +
+gradient, fp32.  Synthetic seeded data (splitmix64, generators.py).
+
+  value : points/s of the evaluate with charges already resident in HBM
+          (device pointers, CUDA events on the launch stream, L2 flushed with a
+          256 MiB write between timed steps), max over ranks.
+  e2e   : points/s through the public API Fmm.evaluate_ptr with pinned host
+          buffers (H2D charges + evaluate + D2H potential & gradient).
+  roofline: the dominant kernel (M2L) -- useful flops 2*n_e*n_c per V pair over
+          its measured launch time, against the measured peak of the unit it uses.
+  cpu_baseline: the fp64 C++ oracle (restatement of SPEC.md) on the host cores,
+          bounded sample (full upward pass + downward for a Morton range of leaves).
+
+`--impl reference` times that CPU restatement alone (the reference ships no
+runnable FMM) and prints the same JSON schema with "impl": "reference".
+For N > 1 (torchrun) the leaves are Morton-partitioned across ranks (strong
+scaling of the same 1M-point problem) with an NCCL all-gather of multipoles.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = 2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=CONFIG)
+    ap.add_argument("--m2l-backend", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-fraction", type=float, default=0.25)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"),
+                                 f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def ncu_traffic(name):
+    """Per-launch DRAM bytes of a kernel from the committed ncu summary, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get(name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_sample(tree, ops, q_reordered, fraction, steps=1):
+    """Oracle (fp64 C++ restatement) on a bounded sample; returns (points/s, threads, desc, seconds)."""
+    import oracle  # CPU baseline leg only
+
+    nl = tree.n_leaves
+    take = max(1, int(round(nl * fraction)))
+    lb = (nl - take) // 2
+    le = lb + take
+    pts = int(tree.leaf_ptr[le] - tree.leaf_ptr[lb])
+    threads = os.cpu_count() or 1
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        oracle.evaluate(tree, ops, q_reordered, gradient=True, threads=threads, leaf_range=(lb, le))
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    desc = (f"fp64 oracle, full upward pass (P2M+M2M over all {nl} leaves) + downward/near field for a "
+            f"Morton range of {take} leaves ({pts} target points, {fraction:.4f} of the leaves); "
+            f"points/s = target points / wall time, mean of {steps}")
+    return pts / t, threads, desc, t
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2303_08394_b200 import generators, host
+
+    c = generators.CONFIGS[args.config]
+    pos, q = generators.config_sample(args.config)
+    tree = host.Tree(pos, c["n_crit"])
+    ops = host.Operators(c["p"], domain_side=tree.side)
+    qr = q[tree.original_index]
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_sample(tree, ops, qr, args.cpu_fraction / 2, 1)
+    value, threads, desc, t = cpu_sample(tree, ops, qr, args.cpu_fraction / 2, args.steps)
+    line = {
+        "impl": "reference", "metric": "FMM evaluate points/sec at N=1M p=6", "value": value, "unit": "points/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"BASELINE config {args.config}: N={c['n']} {c['kind']}, p={c['p']}, "
+                               f"n_crit={c['n_crit']}, gradient={c['gradient']}", "parallelism": "cpu-openmp"},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2303_08394_b200 import fmm, generators
+
+    c = generators.CONFIGS[args.config]
+    pos, q = generators.config_sample(args.config)
+    n = pos.shape[0]
+    prec = c["precision"]
+    tdt = torch.float32 if prec == 32 else torch.float64
+    ndt = np.float32 if prec == 32 else np.float64
+
+    uid = None
+    if world > 1:
+        from paper_2303_08394_b200._lib import lib
+        import ctypes
+        buf = ctypes.create_string_buffer(128)
+        if rank == 0:
+            lib.kifmm_gpu_nccl_unique_id(buf)
+        obj = [bytes(buf.raw)]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+
+    cfg = fmm.FmmConfig(p=c["p"], n_crit=c["n_crit"], precision=prec, gradient=c["gradient"], device=local,
+                        m2l_backend=args.m2l_backend, rank=rank, world_size=world, nccl_unique_id=uid)
+    f = fmm.Fmm(pos, cfg)
+    info = f.info()
+
+    # ---- device-resident run (value)
+    dq = torch.from_numpy(q.astype(ndt)).to("cuda")
+    dpot = torch.empty(n, dtype=tdt, device="cuda")
+    dgrad = torch.empty((n, 3), dtype=tdt, device="cuda") if c["gradient"] else None
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.Stream()  # explicit non-default stream: plan kernels and timing events share it
+    torch.cuda.set_stream(stream)
+    sp = stream.cuda_stream
+
+    def step():
+        f.evaluate_device(dq.data_ptr(), dpot.data_ptr(), dgrad.data_ptr() if dgrad is not None else None,
+                          input_order=True, stream=sp)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))  # L2 flush between timed steps (256 MiB > 126 MB L2)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = total_ms / args.steps
+    value = n / (ms_per_step * 1e-3)
+
+    # ---- per-phase device times (same kernels, events between phases, not graph-captured)
+    phases = []
+    qh = q.astype(ndt)
+    for _ in range(max(3, min(args.steps, 10))):
+        _, _, tm = f.evaluate(qh, timed=True)
+        phases.append(tm)
+    ph = {k: float(np.mean([p[k] for p in phases])) for k in phases[0]}
+
+    # ---- end-to-end through the public API with pinned host buffers (e2e)
+    hq = torch.from_numpy(qh).pin_memory()
+    hpot = torch.empty(n, dtype=tdt).pin_memory()
+    hgrad = torch.empty((n, 3), dtype=tdt).pin_memory() if c["gradient"] else None
+    for _ in range(args.warmup):
+        f.evaluate_ptr(hq.data_ptr(), hpot.data_ptr(), hgrad.data_ptr() if hgrad is not None else None)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        f.evaluate_ptr(hq.data_ptr(), hpot.data_ptr(), hgrad.data_ptr() if hgrad is not None else None)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = n * args.steps / e2e_s
+    esz = 4 if prec == 32 else 8
+    h2d = n * esz
+    d2h = n * esz * (4 if c["gradient"] else 1)
+
+    if rank != 0:
+        f.close()
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (M2L)
+    peaks = measured_peaks()
+    n_e = info["n_e"]
+    m2l_flops = 2.0 * n_e * info["n_c"] * info["m2l_pairs"]
+    m2l_s = ph["m2l_ms"] * 1e-3
+    achieved = m2l_flops / m2l_s / 1e12 if m2l_s > 0 else 0.0
+    if info["m2l_backend"] == 2:
+        tf32 = peaks.get("bf16_tflops", 1590.0) / 2.0
+        peak, bound, src = tf32 / 3.0, "tensor", ("measured bf16/2 (TF32) / 3 (3xTF32 issues 3 MMAs per "
+                                                  "useful MAC), of measured" if peaks else "of fallback")
+    else:
+        fp32 = fmm.fma_peak(32, local) / 1e12
+        peak, bound, src = fp32, "tensor", ("FP32 SIMT kernel: peak = FFMA throughput measured in this run "
+                                            "(MEASURED_PEAKS.json has no FP32 entry); 'tensor' here means the "
+                                            "compute roof, not tensor cores")
+    roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if peak else None, "traffic": ncu_traffic("m2l"),
+            "kernel": "M2L (gather_gemm_kernel)" if info["m2l_backend"] != 2 else "M2L (m2l_tc_kernel)",
+            "peak_source": src,
+            "work": f"2*n_e*n_c flop per V pair x {info['m2l_pairs']} V pairs per launch",
+            "m2l_ms": ph["m2l_ms"]}
+    p2p_pairs = info["near_pairs"] + info["l2p_pairs"] + info["m2p_pairs"]
+    pair_flops = 19.0 if c["gradient"] else 11.0
+    fp32_peak = fmm.fma_peak(32, local) / 1e12 if prec == 32 else fmm.fma_peak(64, local) / 1e12
+    p2p = {"achieved_tflops": p2p_pairs * pair_flops / (ph["leaf_ms"] * 1e-3) / 1e12 if ph["leaf_ms"] else None,
+           "peak_tflops": fp32_peak, "pairs": p2p_pairs, "flop_per_pair": pair_flops, "leaf_ms": ph["leaf_ms"]}
+    p2p["frac"] = p2p["achieved_tflops"] / fp32_peak if p2p["achieved_tflops"] else None
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        qr = q[f.tree.original_index]
+        v, th, desc, _ = cpu_sample(f.tree, f.operators, qr, args.cpu_fraction, 1)
+        cpu = {"value": v, "unit": "points/s", "cores": th, "kind": "port", "sample": desc}
+
+    line = {
+        "metric": "FMM evaluate points/sec at N=1M p=6", "value": value, "unit": "points/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if prec == 32 else "f64", "data": "synthetic",
+        "config": {"workload": f"BASELINE config {args.config}: N={n} {c['kind']} (seed 0), p={c['p']}, "
+                               f"n_crit={c['n_crit']}, gradient={c['gradient']}, depth {f.tree.depth}, "
+                               f"{f.tree.n_leaves} leaves",
+                   "parallelism": f"morton-range x{world}" if world > 1 else "single-gpu",
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "m2l_backend": {1: "simt", 2: "tcgen05-3xtf32"}.get(info["m2l_backend"])},
+        "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(info["kernel_launches"]) * args.steps,
+        "roofline": roof, "p2p": p2p, "phases_ms": ph, "clocks": clk.summary(), "cpu_baseline": cpu,
+        "plan": {k: info[k] for k in ("n_leaves", "n_nodes", "near_pairs", "m2l_pairs", "m2l_padded_pairs",
+                                      "device_bytes", "kernel_launches")},
+    }
+    print(json.dumps(line), flush=True)
+    f.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

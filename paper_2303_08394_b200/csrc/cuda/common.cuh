@@ -50,9 +50,21 @@ __device__ __forceinline__ double4 make4<double>(double x, double y, double z, d
   return make_double4(x, y, z, w);
 }
 
-// 1/sqrt(r2) with the SPEC self-interaction convention (0 at r = 0).
-__device__ __forceinline__ float rinv_masked(float r2) { return r2 > 0.f ? rsqrtf(r2) : 0.f; }
-__device__ __forceinline__ double rinv_masked(double r2) { return r2 > 0.0 ? rsqrt(r2) : 0.0; }
+// 1/sqrt(r2): one MUFU.RSQ in fp32 (rsqrt.approx.ftz, no denormal fix-up; r2 is
+// either 0 or a squared distance far above FLT_MIN), correctly rounded-ish in fp64.
+__device__ __forceinline__ float rinv(float r2) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(r2));
+  return r;
+}
+__device__ __forceinline__ double rinv(double r2) { return rsqrt(r2); }
+// ... with the SPEC self-interaction convention (0 at r = 0).
+template <class T>
+__device__ __forceinline__ T rinv_masked(T r2) {
+  return r2 > T(0) ? rinv(r2) : T(0);
+}
+// Far-away zero-charge source used to pad staged source rounds (contributes exactly 0).
+constexpr double kFarAway = 1e15;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

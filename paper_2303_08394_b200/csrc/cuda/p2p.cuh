@@ -24,7 +24,9 @@ namespace gpu {
 //   kind 0: particles [a, a + b) of the packed source array
 //   kind 1: down-equivalent surface of node a (alpha_outer), densities L[a]   (L2P)
 //   kind 2: up-equivalent surface of node a (alpha_inner), densities M[a]     (M2P)
-enum : int { kSrcParticles = 0, kSrcL2P = 1, kSrcM2P = 2 };
+//   kind 3: particles [a, a + b) of the target leaf itself (the only sources that can
+//           coincide with a target, so the only ones evaluated with the r = 0 mask)
+enum : int { kSrcParticles = 0, kSrcL2P = 1, kSrcM2P = 2, kSrcSelf = 3 };
 
 struct LeafWork {
   int leaf;
@@ -54,8 +56,40 @@ __device__ __forceinline__ v4_t<T> surface_source(const P2PParams<T>& p, int nod
                   dens[size_t(node) * p.ld + j]);
 }
 
-// One block per work item (leaf, <=128 targets). 4 warps split the staged
-// sources; lane l of each warp owns targets l, l+32, l+64, l+96 of the item.
+// One block per work item (leaf, <=128 targets).  Sources are staged in rounds of
+// up to kP2PCap, padded to a multiple of 32 with far-away zero charges; warp w
+// takes the contiguous quarter [w*n/4, (w+1)*n/4) of a round and lane l owns
+// targets l, l+32, l+64, l+96 of the item.  A round holds either only self-leaf
+// particles (masked r = 0 path) or only other sources (no mask).
+template <class T, bool GRAD, bool MASK>
+__device__ __forceinline__ void p2p_round(const v4_t<T>* sh, int begin, int end, T x, T y, T z, T& ph, T& gx, T& gy,
+                                          T& gz) {
+  T a_ph = 0, a_gx = 0, a_gy = 0, a_gz = 0;
+  for (int j = begin; j < end; j += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const v4_t<T> s = sh[j + u];
+      const T dx = x - s.x, dy = y - s.y, dz = z - s.z;
+      const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const T ri = MASK ? rinv_masked(r2) : rinv(r2);
+      if (GRAD) {
+        const T qr = s.w * ri;
+        a_ph += qr;
+        const T qr3 = qr * (ri * ri);
+        a_gx = fma(qr3, dx, a_gx);
+        a_gy = fma(qr3, dy, a_gy);
+        a_gz = fma(qr3, dz, a_gz);
+      } else {
+        a_ph = fma(s.w, ri, a_ph);
+      }
+    }
+  }
+  ph += a_ph;
+  gx += a_gx;
+  gy += a_gy;
+  gz += a_gz;
+}
+
 template <class T, bool GRAD>
 __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, const LeafWork* __restrict__ works,
                                                                  const int4* __restrict__ items,
@@ -81,11 +115,14 @@ __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, 
   int it = w.item_begin, off = 0;
   while (it < w.item_end) {
     int fill = 0;
+    const bool masked = items[it].x == kSrcSelf;
     while (it < w.item_end && fill < kP2PCap) {
       const int4 item = items[it];
-      const int len = item.x == kSrcParticles ? item.z : p.n_e;
+      if ((item.x == kSrcSelf) != masked) break;
+      const bool particles = item.x == kSrcParticles || item.x == kSrcSelf;
+      const int len = particles ? item.z : p.n_e;
       const int take = min(len - off, kP2PCap - fill);
-      if (item.x == kSrcParticles) {
+      if (particles) {
         for (int i = tid; i < take; i += kP2PThreads) sh[fill + i] = p.src[item.y + off + i];
       } else {
         const bool l2p = item.x == kSrcL2P;
@@ -100,32 +137,19 @@ __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, 
         off = 0;
       }
     }
+    const int padded = (fill + 31) & ~31;
+    for (int i = fill + tid; i < padded; i += kP2PThreads)
+      sh[i] = make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
     __syncthreads();
-    // warp w takes sources w, w+4, w+8, ...
+    const int q4 = padded >> 2;
+    const int jb = warp * q4, je = jb + q4;
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       if (g >= ngroups) break;
-      T a_ph = 0, a_gx = 0, a_gy = 0, a_gz = 0;
-      const T x = tx[g], y = ty[g], z = tz[g];
-#pragma unroll 4
-      for (int j = warp; j < fill; j += 4) {
-        const v4_t<T> s = sh[j];
-        const T dx = x - s.x, dy = y - s.y, dz = z - s.z;
-        const T r2 = dx * dx + dy * dy + dz * dz;
-        const T ri = rinv_masked(r2);
-        const T qr = s.w * ri;
-        a_ph += qr;
-        if (GRAD) {
-          const T qr3 = qr * ri * ri;
-          a_gx += qr3 * dx;
-          a_gy += qr3 * dy;
-          a_gz += qr3 * dz;
-        }
-      }
-      ph[g] += a_ph;
-      gx[g] += a_gx;
-      gy[g] += a_gy;
-      gz[g] += a_gz;
+      if (masked)
+        p2p_round<T, GRAD, true>(sh, jb, je, tx[g], ty[g], tz[g], ph[g], gx[g], gy[g], gz[g]);
+      else
+        p2p_round<T, GRAD, false>(sh, jb, je, tx[g], ty[g], tz[g], ph[g], gx[g], gy[g], gz[g]);
     }
     __syncthreads();
   }
@@ -141,14 +165,14 @@ __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, 
     }
   }
   __syncthreads();
-  if (tid < w.t_count) {
+  for (int t0 = tid; t0 < w.t_count; t0 += kP2PThreads) {
     const T c = T(kInv4PiD);
-    const int t = w.t_begin + tid;
-    pot[t] = c * (((red[0][0][tid] + red[1][0][tid]) + red[2][0][tid]) + red[3][0][tid]);
+    const int t = w.t_begin + t0;
+    pot[t] = c * (((red[0][0][t0] + red[1][0][t0]) + red[2][0][t0]) + red[3][0][t0]);
     if (GRAD) {
 #pragma unroll
       for (int d = 0; d < 3; ++d)
-        grad[3 * size_t(t) + d] = -c * (((red[0][d + 1][tid] + red[1][d + 1][tid]) + red[2][d + 1][tid]) + red[3][d + 1][tid]);
+        grad[3 * size_t(t) + d] = -c * (((red[0][d + 1][t0] + red[1][d + 1][t0]) + red[2][d + 1][t0]) + red[3][d + 1][t0]);
     }
   }
 }
@@ -195,16 +219,22 @@ __global__ void __launch_bounds__(kP2PThreads) check_kernel(P2PParams<T> p, cons
         off = 0;
       }
     }
+    const int padded = (fill + 7) & ~7;
+    for (int i = fill + tid; i < padded; i += kP2PThreads)
+      sh[i] = make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
     __syncthreads();
+    // check surfaces never touch particles (alpha > 1 around the node / X-list separation): no r = 0 mask
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
       if (m * kP2PThreads >= p.n_e) break;
       T a = 0;
-#pragma unroll 4
-      for (int i = 0; i < fill; ++i) {
-        const v4_t<T> q = sh[i];
-        const T dx = yx[m] - q.x, dy = yy[m] - q.y, dz = yz[m] - q.z;
-        a += q.w * rinv_masked(dx * dx + dy * dy + dz * dz);
+      for (int i = 0; i < padded; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const v4_t<T> q = sh[i + u];
+          const T dx = yx[m] - q.x, dy = yy[m] - q.y, dz = yz[m] - q.z;
+          a = fma(q.w, rinv(fma(dz, dz, fma(dy, dy, dx * dx))), a);
+        }
       }
       acc[m] += a;
     }

@@ -175,6 +175,29 @@ __global__ void scatter_rows_kernel(const T* __restrict__ src, int ld, const int
   for (int j = threadIdx.x; j < ld; j += blockDim.x) dst[size_t(rows[r]) * ld + j] = s[j];
 }
 
+// M2M split over octants: partial products land in scratch rows (slot*8 + octant)
+// and are summed here in fixed octant order (deterministic, no atomics).
+template <class T>
+__global__ void m2m_reduce_kernel(const T* __restrict__ scratch, const int* __restrict__ parents,
+                                  const int* __restrict__ masks, int n, int ld, T* __restrict__ M) {
+  const int s = blockIdx.x;
+  if (s >= n) return;
+  const int mask = masks[s];
+  for (int c = threadIdx.x; c < ld; c += blockDim.x) {
+    T acc = T(0);
+#pragma unroll
+    for (int o = 0; o < 8; ++o)
+      if ((mask >> o) & 1) acc += scratch[(size_t(s) * 8 + o) * ld + c];
+    M[size_t(parents[s]) * ld + c] = acc;
+  }
+}
+
+struct M2MLevel {
+  GemmTiles tiles;  // one tile per (64 parents, octant)
+  DevMem parents, masks;
+  int n = 0;
+};
+
 }  // namespace gpu
 }  // namespace kifmm
 
@@ -208,7 +231,10 @@ struct kifmm_gpu_plan {
   DevMem p2m_works, p2m_ranges, p2l_works, p2l_ranges, leaf_works, leaf_items;
   int n_p2m = 0, n_p2l = 0, n_leafw = 0;
   GemmTiles solve_up1, solve_up2, solve_dn1, solve_dn2, m2l;
-  std::vector<std::unique_ptr<GemmTiles>> m2m_levels, l2l_levels, m2m_top;
+  std::vector<std::unique_ptr<M2MLevel>> m2m_levels, m2m_top;
+  std::vector<std::unique_ptr<GemmTiles>> l2l_levels;
+  DevMem m2m_scratch;
+  int64_t m2m_scratch_rows = 0;
   M2LTcPlan m2l_tc;
   // exchange
   void* comm = nullptr;
@@ -428,25 +454,40 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
 
   // ---- M2M per level (owned internal nodes), then the redundant top levels
   auto m2m_tiles = [&](std::vector<int64_t>& parents) {
+    constexpr int BMS = 64;
     std::vector<TileSpec> tiles;
-    for (size_t s0 = 0; s0 < parents.size(); s0 += ld_tiles) {
-      TileSpec ts;
-      ts.out.assign(ld_tiles, -1);
-      for (int o = 0; o < 8; ++o) ts.segs.push_back({o, std::vector<int>(ld_tiles, -1)});
-      for (int r = 0; r < ld_tiles && s0 + r < parents.size(); ++r) {
-        const int64_t pn = parents[s0 + r];
-        ts.out[r] = int(pn);
-        for (int o = 0; o < 8; ++o) ts.segs[o].second[r] = int(t.node_children[8 * pn + o]);
+    std::vector<int> par, msk;
+    for (size_t s0 = 0; s0 < parents.size(); s0 += BMS) {
+      for (int o = 0; o < 8; ++o) {
+        TileSpec ts;
+        ts.out.assign(BMS, -1);
+        std::vector<int> in(BMS, -1);
+        bool any = false;
+        for (int r = 0; r < BMS && s0 + r < parents.size(); ++r) {
+          const int64_t ch = t.node_children[8 * parents[s0 + r] + o];
+          if (ch < 0) continue;
+          ts.out[r] = int((s0 + r) * 8 + o);
+          in[r] = int(ch);
+          any = true;
+        }
+        if (!any) continue;
+        ts.segs.push_back({o, in});
+        tiles.push_back(std::move(ts));
       }
-      // drop octants absent in the whole tile
-      std::vector<std::pair<int, std::vector<int>>> keep;
-      for (auto& sg : ts.segs)
-        if (std::any_of(sg.second.begin(), sg.second.end(), [](int v) { return v >= 0; })) keep.push_back(sg);
-      ts.segs.swap(keep);
-      tiles.push_back(std::move(ts));
     }
-    auto g = std::make_unique<GemmTiles>();
-    g->build(tiles, ld_tiles, &dev_bytes);
+    for (int64_t pn : parents) {
+      int m = 0;
+      for (int o = 0; o < 8; ++o)
+        if (t.node_children[8 * pn + o] >= 0) m |= 1 << o;
+      par.push_back(int(pn));
+      msk.push_back(m);
+    }
+    auto g = std::make_unique<M2MLevel>();
+    g->tiles.build(tiles, BMS, &dev_bytes);
+    g->parents.upload(par, &dev_bytes);
+    g->masks.upload(msk, &dev_bytes);
+    g->n = int(parents.size());
+    m2m_scratch_rows = std::max<int64_t>(m2m_scratch_rows, int64_t(parents.size()) * 8);
     return g;
   };
   const int up_floor = world > 1 ? cut : 0;
@@ -492,6 +533,8 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     nc_.check(nc_.commInitRank(&c, world, id, rank), "ncclCommInitRank");
     comm = c;
   }
+
+  m2m_scratch.alloc(size_t(std::max<int64_t>(1, m2m_scratch_rows)) * np * es, &dev_bytes);
 
   // ---- P2L check works: active nodes with X members
   {
@@ -615,10 +658,12 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       int64_t src_cnt = 0;
       // U ranges, merged when contiguous in the reordered buffer
       int cur_b = -1, cur_e = -1;
+      items.push_back(make_int4(kSrcSelf, int(t.leaf_ptr[l]), int(t.leaf_ptr[l + 1] - t.leaf_ptr[l]), 0));
       for (int64_t e = t.u_ptr[l]; e < t.u_ptr[l + 1]; ++e) {
         const int64_t s = t.u_idx[e];
         const int b = int(t.leaf_ptr[s]), en = int(t.leaf_ptr[s + 1]);
         src_cnt += en - b;
+        if (s == l) continue;
         if (b == cur_e) {
           cur_e = en;
         } else {
@@ -735,13 +780,20 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   gemm(solve_up2, tmp.as<T>(), w_vt_u.as<T>(), Mp, false, false);
   mark();  // 1
   // M2M, levels d-1 .. floor
-  for (auto& lv : m2m_levels) gemm(*lv, Mp, w_m2m.as<T>(), Mp, false, false);
+  auto m2m_level = [&](const M2MLevel& lv) {
+    gemm(lv.tiles, Mp, w_m2m.as<T>(), m2m_scratch.as<T>(), false, true);
+    m2m_reduce_kernel<T><<<lv.n, 128, 0, s>>>(m2m_scratch.as<T>(), lv.parents.as<int>(), lv.masks.as<int>(), lv.n,
+                                             np, Mp);
+    KIFMM_LAUNCH_CHECK();
+    ++launches;
+  };
+  for (auto& lv : m2m_levels) m2m_level(*lv);
   mark();  // 2
   // multipole exchange (multi-GPU) and the redundant top of the tree
   if (world > 1) {
     exchange(s);
     launches += 2;
-    for (auto& lv : m2m_top) gemm(*lv, Mp, w_m2m.as<T>(), Mp, false, false);
+    for (auto& lv : m2m_top) m2m_level(*lv);
   }
   mark();  // 3
   // downward: P2L check into the down-check buffer
