@@ -591,7 +591,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     info.m2l_padded_pairs = m2l.slots;
   }
   m2l_backend = 1;
-  if (o.m2l_backend == 2 || (o.m2l_backend == 0 && precision == 32 && m2l_tc_available())) {
+  if (o.m2l_backend == 2 || (o.m2l_backend == 0 && precision == 32 && np == tc::NP && m2l_tc_available())) {
     if (precision != 32) throw InvalidArgument("gpu: tcgen05 3xTF32 M2L is an fp32 path");
     m2l_tc.build(t, m2l_groups, np, ops, &dev_bytes);
     m2l_backend = 2;
