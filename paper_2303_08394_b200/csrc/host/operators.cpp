@@ -25,15 +25,16 @@ std::vector<double> surface_grid(int p) {
   if (p < 2) throw InvalidArgument("surface_grid: p must be >= 2");
   std::vector<double> pts;
   pts.reserve(3 * size_t(surface_count(p)));
-  const double step = 2.0 / double(p - 1);
+  // (2i - (p-1)) / (p-1): exact at the faces and symmetric under reflection
+  auto coord = [p](int i) { return double(2 * i - (p - 1)) / double(p - 1); };
   for (int i = 0; i < p; ++i)
     for (int j = 0; j < p; ++j)
       for (int k = 0; k < p; ++k) {
         const bool on = i == 0 || i == p - 1 || j == 0 || j == p - 1 || k == 0 || k == p - 1;
         if (!on) continue;
-        pts.push_back(-1.0 + step * i);
-        pts.push_back(-1.0 + step * j);
-        pts.push_back(-1.0 + step * k);
+        pts.push_back(coord(i));
+        pts.push_back(coord(j));
+        pts.push_back(coord(k));
       }
   return pts;
 }

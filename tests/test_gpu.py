@@ -1,0 +1,158 @@
+"""GPU parity tests (run on a B200 with -m gpu): the CUDA evaluate through the
+C ABI against the fp64 oracle on identical inputs.
+
+Tolerances (north star, BASELINE.json): relative L2 <= 1e-12 for fp64 and
+<= 1e-5 for fp32 (potentials); gradients (an extension) use
+1e-11 (fp64) and 5e-5 (fp32).  Both oracle and GPU consume the same fp64
+operator matrices and factored pseudo-inverses (SURVEY 8c parity protocol).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2303_08394_b200 import InvalidArgument, fmm, generators, host
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = {64: (1e-12, 1e-11), 32: (1e-5, 5e-5)}
+
+
+def _inv(t):
+    i = np.empty_like(t.original_index)
+    i[t.original_index] = np.arange(t.n)
+    return i
+
+
+def _ref(f, q, gradient):
+    qr = np.asarray(q, dtype=np.float64)[f.tree.original_index]
+    phi, g, _ = oracle.evaluate(f.tree, f.operators, qr, gradient=gradient)
+    ii = _inv(f.tree)
+    return phi[ii], (g[ii] if g is not None else None)
+
+
+CASES = [("uniform-cube", 6000, 40, 4), ("uniform-cube", 5000, 50, 6), ("sphere-surface", 8000, 40, 6),
+         ("two-cluster", 6000, 20, 5), ("two-cluster", 4000, 8, 7), ("uniform-cube", 3000, 30, 2)]
+
+
+@pytest.mark.parametrize("kind,n,n_crit,p", CASES)
+@pytest.mark.parametrize("precision", [64, 32])
+def test_parity_vs_oracle(require_gpu, kind, n, n_crit, p, precision):
+    pos, q = generators.sample(kind, n, seed=7, charges="signed", fp32=precision == 32)
+    cfg = fmm.FmmConfig(p=p, n_crit=n_crit, precision=precision, gradient=True, m2l_backend=1)
+    with fmm.Fmm(pos, cfg) as f:
+        pot, grad, _ = f.evaluate(q)
+        ref, gref = _ref(f, q, True)
+    tp, tg = TOL[precision]
+    assert fmm.relative_error(pot, ref) <= tp
+    assert fmm.relative_error(grad, gref) <= tg
+
+
+@pytest.mark.parametrize("kind,n,n_crit", [("uniform-cube", 20000, 60), ("sphere-surface", 30000, 50),
+                                           ("two-cluster", 20000, 30)])
+def test_tcgen05_m2l_parity(require_gpu, kind, n, n_crit):
+    pos, q = generators.sample(kind, n, seed=8, charges="signed", fp32=True)
+    cfg = fmm.FmmConfig(p=6, n_crit=n_crit, precision=32, gradient=True, m2l_backend=2)
+    with fmm.Fmm(pos, cfg) as f:
+        assert f.info()["m2l_backend"] == 2
+        pot, grad, _ = f.evaluate(q)
+        ref, gref = _ref(f, q, True)
+    assert fmm.relative_error(pot, ref) <= 1e-5
+    assert fmm.relative_error(grad, gref) <= 5e-5
+
+
+def test_single_leaf_equals_direct(require_gpu):
+    pos, q = generators.sample("uniform-cube", 200, seed=1, charges="uniform")
+    with fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=500, precision=64)) as f:
+        assert f.tree.n_leaves == 1
+        pot, _, _ = f.evaluate(q)
+    assert fmm.relative_error(pot, oracle.direct(pos, q)) <= 1e-13
+
+
+def test_golden_config1(require_gpu):  # BASELINE config 1 (p=5, n_crit=64), fp32
+    g = np.load(os.path.join(GOLD, "config1_direct.npz"))
+    pos, q = g["positions"], g["charges"]
+    with fmm.Fmm(pos, fmm.FmmConfig(p=5, n_crit=64, precision=32, gradient=True)) as f:
+        pot, grad, _ = f.evaluate(q)
+        ref, gref = _ref(f, q, True)
+    assert fmm.relative_error(pot, ref) <= 1e-5
+    assert fmm.relative_error(pot, g["potential"]) <= 1e-4
+
+
+def test_config2_full_size(require_gpu):
+    """BASELINE config 2 at full size (1M points, p=6, fp32, gradient): GPU vs the
+    fp64 oracle on all points, and vs direct summation on the 1,000 committed
+    sampled targets (north star)."""
+    pos, q = generators.config_sample(2)
+    with fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=150, precision=32, gradient=True)) as f:
+        pot, grad, _ = f.evaluate(q.astype(np.float32))
+        pot2, grad2, _ = f.evaluate(q.astype(np.float32))
+        ref, gref = _ref(f, q, True)
+        backend = f.info()["m2l_backend"]
+    assert np.array_equal(pot, pot2) and np.array_equal(grad, grad2)  # deterministic
+    assert fmm.relative_error(pot, ref) <= 1e-5, backend
+    assert fmm.relative_error(grad, gref) <= 5e-5
+    gold = np.load(os.path.join(GOLD, "config2_sampled_direct.npz"))
+    tg = gold["targets"]
+    assert fmm.relative_error(pot[tg], gold["potential"]) <= 1e-5
+    assert fmm.relative_error(grad[tg], gold["gradient"]) <= 1e-4
+    # the GPU direct-sum kernel (K10) agrees with the fp64 numpy fixture
+    d = fmm.direct(pos, q, targets=tg, precision=64)
+    assert fmm.relative_error(d, gold["potential"]) <= 1e-12
+
+
+def test_size_independent_properties(require_gpu):
+    pos, q = generators.sample("sphere-surface", 200000, seed=9, charges="signed", fp32=True)
+    with fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=150, precision=32)) as f:
+        a, _, _ = f.evaluate(q.astype(np.float32))
+        b, _, _ = f.evaluate((2.0 * q).astype(np.float32))  # scaling by 2 is exact
+        z, _, _ = f.evaluate(np.zeros(f.n, np.float32))
+        # reordered-order interface agrees with input order
+        r, _, _ = f.evaluate(q[f.tree.original_index].astype(np.float32), input_order=False)
+    assert np.array_equal(b, 2.0 * a)
+    assert not np.any(z)
+    assert np.array_equal(r, a[f.tree.original_index])
+
+
+def test_direct_kernel(require_gpu):
+    pos, q = generators.sample("two-cluster", 3000, seed=10, charges="signed")
+    tg = np.arange(0, 3000, 7)
+    d64, g64 = fmm.direct(pos, q, targets=tg, precision=64, gradient=True)
+    r, gr = oracle.direct(pos, q, targets=tg, gradient=True)
+    assert fmm.relative_error(d64, r) <= 1e-13 and fmm.relative_error(g64, gr) <= 1e-12
+    d32 = fmm.direct(pos, q, targets=tg, precision=32)
+    assert fmm.relative_error(d32, r) <= 1e-5
+
+
+def test_evaluate_device_and_graph(require_gpu):
+    import torch
+    pos, q = generators.sample("uniform-cube", 50000, seed=12, charges="uniform", fp32=True)
+    with fmm.Fmm(pos, fmm.FmmConfig(p=5, n_crit=64, precision=32, gradient=True, use_graph=True)) as f:
+        host_pot, host_grad, _ = f.evaluate(q)
+        dq = torch.from_numpy(q.astype(np.float32)).cuda()
+        dp = torch.empty(f.n, device="cuda")
+        dg = torch.empty((f.n, 3), device="cuda")
+        s = torch.cuda.Stream()
+        f.evaluate_device(dq.data_ptr(), dp.data_ptr(), dg.data_ptr(), stream=s.cuda_stream)
+        s.synchronize()
+    assert np.array_equal(dp.cpu().numpy(), host_pot)
+    assert np.array_equal(dg.cpu().numpy(), host_grad)
+
+
+def test_invalid_arguments(require_gpu):
+    pos, q = generators.sample("uniform-cube", 1000, seed=0)
+    with fmm.Fmm(pos, fmm.FmmConfig(p=3, n_crit=20)) as f:
+        with pytest.raises(InvalidArgument):
+            f.evaluate(q[:10])
+    with pytest.raises(InvalidArgument):
+        fmm.Fmm(pos, fmm.FmmConfig(p=9, n_crit=20))  # n_e > 224 unsupported on the GPU
+    with pytest.raises(InvalidArgument):
+        fmm.Fmm(pos, fmm.FmmConfig(precision=16))
+
+
+def test_run_api(require_gpu):  # run(particles, config) -> potentials (input order) + timings
+    pos, q = generators.sample("sphere-surface", 20000, seed=13, charges="unit")
+    pot, grad, tm = fmm.run(pos, q, fmm.FmmConfig(p=6, n_crit=50, precision=64))
+    assert grad is None and tm["total_ms"] > 0 and "tree_s" in tm
+    assert fmm.relative_error(pot[:500], oracle.direct(pos, q, targets=np.arange(500))) <= 1e-5

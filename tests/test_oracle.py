@@ -1,0 +1,110 @@
+"""The fp64 oracle (CPU restatement of SPEC.md evaluate) against direct summation,
+the SPEC acceptance criteria and the committed golden fixtures.
+
+These pin the oracle itself before it is used as the GPU parity checker.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2303_08394_b200 import generators, host
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _eval(pos, q, n_crit, p, gradient=False, threads=0, domain=None):
+    t = host.Tree(pos, n_crit, domain=domain)
+    o = host.Operators(p, domain_side=t.side)
+    phi, g, _ = oracle.evaluate(t, o, q[t.original_index], gradient=gradient, threads=threads)
+    inv = np.empty_like(t.original_index)
+    inv[t.original_index] = np.arange(t.n)
+    return phi[inv], (g[inv] if g is not None else None), t
+
+
+def test_acceptance_1_degenerate_tree():
+    pos, q = generators.sample("uniform-cube", 200, seed=1, charges="uniform")
+    phi, _, t = _eval(pos, q, 500, 6)
+    assert t.n_leaves == 1
+    assert oracle.relative_error(phi, oracle.direct(pos, q)) <= 1e-13
+
+
+@pytest.mark.parametrize("kind", ["sphere-surface", "two-cluster"])
+def test_acceptance_2_full_pipeline(kind):
+    pos, q = generators.sample(kind, 5000, seed=2, charges="unit")
+    phi, _, t = _eval(pos, q, 50, 6)
+    err = oracle.relative_error(phi, oracle.direct(pos, q))
+    assert err <= 1e-5
+    if kind == "two-cluster":
+        s = t.list_stats()
+        assert s["W"][2] > 0 and s["X"][2] > 0  # W/X exercised
+
+
+def test_acceptance_3_p_convergence():
+    pos, q = generators.sample("sphere-surface", 5000, seed=3, charges="unit")
+    ref = oracle.direct(pos, q)
+    errs = [oracle.relative_error(_eval(pos, q, 50, p)[0], ref) for p in (2, 3, 4, 5, 6)]
+    for a, b in zip(errs, errs[1:]):
+        assert b < a * 1.1
+    assert errs[-1] / errs[0] <= 1e-2
+
+
+@pytest.mark.parametrize("n_crit", [1, 4, 20])
+def test_small_instance_equivalence(n_crit):
+    pos, q = generators.sample("uniform-cube", 200, seed=4, charges="signed")
+    phi, _, _ = _eval(pos, q, n_crit, 6)
+    assert oracle.relative_error(phi, oracle.direct(pos, q)) <= 1e-5
+
+
+def test_linearity_and_determinism():
+    pos, q = generators.sample("two-cluster", 3000, seed=5, charges="signed")
+    t = host.Tree(pos, 30)
+    o = host.Operators(5, domain_side=t.side)
+    qr = q[t.original_index]
+    a, _, _ = oracle.evaluate(t, o, qr, threads=1)
+    b, _, _ = oracle.evaluate(t, o, 3.0 * qr, threads=4)
+    c, _, _ = oracle.evaluate(t, o, qr, threads=0)
+    assert oracle.relative_error(b, 3.0 * a) <= 1e-13
+    assert np.array_equal(a, c)  # thread-count independent, bit-identical
+
+
+def test_homogeneity_level_scaling():  # SPEC.md:499, 503 (level-scaling identity)
+    pos, q = generators.sample("uniform-cube", 3000, seed=6, charges="uniform")
+    phi1, _, _ = _eval(pos, q, 40, 6)
+    phi2, _, _ = _eval(2.0 * pos, q, 40, 6)
+    assert oracle.relative_error(2.0 * phi2, phi1) <= 1e-12
+
+
+def test_golden_config1():
+    g = np.load(os.path.join(GOLD, "config1_direct.npz"))
+    pos, q = generators.config_sample(1)
+    assert np.array_equal(pos, g["positions"]) and np.array_equal(q, g["charges"])  # generator is pinned
+    d, dg = oracle.direct(pos, q, gradient=True)
+    assert oracle.relative_error(d, g["potential"]) <= 1e-13
+    assert oracle.relative_error(dg, g["gradient"]) <= 1e-12
+    phi, grad, _ = _eval(pos, q, 64, 5, gradient=True)  # BASELINE config 1: p=5, n_crit=64
+    assert oracle.relative_error(phi, g["potential"]) <= 1e-4
+    assert oracle.relative_error(grad, g["gradient"]) <= 1e-3
+
+
+def test_golden_two_cluster():
+    g = np.load(os.path.join(GOLD, "two_cluster_direct.npz"))
+    pos, q = g["positions"], g["charges"]
+    phi, grad, t = _eval(pos, q, 20, 6, gradient=True)
+    assert oracle.relative_error(phi, g["potential"]) <= 1e-5
+    assert oracle.relative_error(grad, g["gradient"]) <= 1e-4
+
+
+def test_direct_examples():
+    pos = np.array([[0.0, 0, 0], [1.0, 0, 0]])
+    phi = oracle.direct(pos, np.array([1.0, 1.0]))
+    assert np.allclose(phi, 1 / (4 * np.pi), rtol=1e-15)
+    assert oracle.direct(np.array([[0.3, 0.3, 0.3]]), np.array([2.0]))[0] == 0.0
+
+
+def test_relative_error_examples():
+    b = np.array([1.0, 2.0, 3.0])
+    assert oracle.relative_error(b, b) == 0.0
+    assert oracle.relative_error(2 * b, b) == pytest.approx(1.0)
+    assert oracle.relative_error(b, np.zeros(3)) == -1.0
