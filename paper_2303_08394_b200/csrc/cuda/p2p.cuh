@@ -32,8 +32,12 @@ struct LeafWork {
   int leaf;
   int t_begin;  // first target (reordered particle index)
   int t_count;  // <= 128
-  int item_begin, item_end;
+  int round_begin, round_end;
 };
+// A staging round: {item_begin, item_end, S | n_self << 16, O | n_other << 16}:
+// shared-memory layout [self section, padded to S][other sources, padded to O],
+// S and O multiples of 8R.  Items: {kind | j0 << 4, a, len, dst} (j0 = first
+// surface point for split surface items, dst = shared-memory slot).
 
 template <class T>
 struct P2PParams {
@@ -46,7 +50,7 @@ struct P2PParams {
 };
 
 constexpr int kP2PThreads = 128;
-constexpr int kP2PCap = 512;  // staged sources per round
+constexpr int kP2PCap = 1024;  // staged sources per round
 
 template <class T>
 __device__ __forceinline__ v4_t<T> surface_source(const P2PParams<T>& p, int node, T alpha, const T* dens, int j) {
@@ -56,11 +60,13 @@ __device__ __forceinline__ v4_t<T> surface_source(const P2PParams<T>& p, int nod
                   dens[size_t(node) * p.ld + j]);
 }
 
-// One block per work item (leaf, <=128 targets).  Sources are staged in rounds of
-// up to kP2PCap, padded to a multiple of 32 with far-away zero charges; warp w
-// takes the contiguous quarter [w*n/4, (w+1)*n/4) of a round and lane l owns
-// targets l, l+32, l+64, l+96 of the item.  A round holds either only self-leaf
-// particles (masked r = 0 path) or only other sources (no mask).
+// One block per work item (leaf, <= 128 targets).  The block's 128 threads are
+// R = min(8, 128 / n_t) source slices x n_t targets (thread -> slice tid / n_t,
+// target tid % n_t), so ~94 % of the lanes carry a target for any n_t >= 16.
+// Sources are staged in rounds of up to kP2PCap, padded to a multiple of 8R
+// with far-away zero charges; slice s takes the contiguous s-th of a round.
+// A round holds either only self-leaf particles (masked r = 0 path) or only
+// other sources (no mask).  Slice partials are summed in fixed order.
 template <class T, bool GRAD, bool MASK>
 __device__ __forceinline__ void p2p_round(const v4_t<T>* sh, int begin, int end, T x, T y, T z, T& ph, T& gx, T& gy,
                                           T& gz) {
@@ -90,164 +96,151 @@ __device__ __forceinline__ void p2p_round(const v4_t<T>* sh, int begin, int end,
   gz += a_gz;
 }
 
+constexpr int kMaxSlices = 8;
+
+__host__ __device__ inline int leaf_slices(int nt) {
+  const int r = 128 / (nt > 0 ? nt : 1);
+  return r < 1 ? 1 : (r > kMaxSlices ? kMaxSlices : r);
+}
+
 template <class T, bool GRAD>
 __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, const LeafWork* __restrict__ works,
+                                                                 const int4* __restrict__ rounds,
                                                                  const int4* __restrict__ items,
                                                                  const T* __restrict__ M, const T* __restrict__ L,
                                                                  T* __restrict__ pot, T* __restrict__ grad) {
   __shared__ v4_t<T> sh[kP2PCap];
-  __shared__ T red[4][4][kP2PThreads];  // [warp][component][target]
   const LeafWork w = works[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ngroups = (w.t_count + 31) >> 5;
+  const int nt = w.t_count;
+  const int R = leaf_slices(nt);
+  const int slice = tid / nt, tgt = tid - slice * nt;
+  const bool active = slice < R;
 
-  T tx[4], ty[4], tz[4], ph[4], gx[4], gy[4], gz[4];
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    const int t = g * 32 + lane;
-    v4_t<T> x = p.src[w.t_begin + (t < w.t_count ? t : 0)];
-    tx[g] = x.x;
-    ty[g] = x.y;
-    tz[g] = x.z;
-    ph[g] = gx[g] = gy[g] = gz[g] = T(0);
-  }
+  const v4_t<T> xt = p.src[w.t_begin + (active ? tgt : 0)];
+  T ph = 0, gx = 0, gy = 0, gz = 0;
+  const v4_t<T> far = make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
 
-  int it = w.item_begin, off = 0;
-  while (it < w.item_end) {
-    int fill = 0;
-    const bool masked = items[it].x == kSrcSelf;
-    while (it < w.item_end && fill < kP2PCap) {
-      const int4 item = items[it];
-      if ((item.x == kSrcSelf) != masked) break;
-      const bool particles = item.x == kSrcParticles || item.x == kSrcSelf;
-      const int len = particles ? item.z : p.n_e;
-      const int take = min(len - off, kP2PCap - fill);
-      if (particles) {
-        for (int i = tid; i < take; i += kP2PThreads) sh[fill + i] = p.src[item.y + off + i];
+  for (int r = w.round_begin; r < w.round_end; ++r) {
+    const int4 rd = rounds[r];
+    const int S = rd.z & 0xFFFF, ns = rd.z >> 16, O = rd.w & 0xFFFF, no = rd.w >> 16;
+    // warp-parallel staging: warp w copies items w, w+4, ...
+    for (int k = rd.x + warp; k < rd.y; k += 4) {
+      const int4 item = items[k];
+      const int kind = item.x & 0xF, j0 = item.x >> 4;
+      if (kind == kSrcParticles || kind == kSrcSelf) {
+        for (int i = lane; i < item.z; i += 32) sh[item.w + i] = p.src[item.y + i];
       } else {
-        const bool l2p = item.x == kSrcL2P;
+        const bool l2p = kind == kSrcL2P;
         const T alpha = l2p ? p.alpha_outer : p.alpha_inner;
         const T* dens = l2p ? L : M;
-        for (int i = tid; i < take; i += kP2PThreads) sh[fill + i] = surface_source(p, item.y, alpha, dens, off + i);
-      }
-      fill += take;
-      off += take;
-      if (off == len) {
-        ++it;
-        off = 0;
+        for (int i = lane; i < item.z; i += 32) sh[item.w + i] = surface_source(p, item.y, alpha, dens, j0 + i);
       }
     }
-    const int padded = (fill + 31) & ~31;
-    for (int i = fill + tid; i < padded; i += kP2PThreads)
-      sh[i] = make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
+    for (int i = ns + tid; i < S; i += kP2PThreads) sh[i] = far;
+    for (int i = S + no + tid; i < S + O; i += kP2PThreads) sh[i] = far;
     __syncthreads();
-    const int q4 = padded >> 2;
-    const int jb = warp * q4, je = jb + q4;
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      if (g >= ngroups) break;
-      if (masked)
-        p2p_round<T, GRAD, true>(sh, jb, je, tx[g], ty[g], tz[g], ph[g], gx[g], gy[g], gz[g]);
-      else
-        p2p_round<T, GRAD, false>(sh, jb, je, tx[g], ty[g], tz[g], ph[g], gx[g], gy[g], gz[g]);
+    if (active) {
+      if (S) {
+        const int per = S / R;
+        p2p_round<T, GRAD, true>(sh, slice * per, slice * per + per, xt.x, xt.y, xt.z, ph, gx, gy, gz);
+      }
+      if (O) {
+        const int per = O / R;
+        p2p_round<T, GRAD, false>(sh, S + slice * per, S + slice * per + per, xt.x, xt.y, xt.z, ph, gx, gy, gz);
+      }
     }
     __syncthreads();
   }
 
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    if (g >= ngroups) break;
-    red[warp][0][g * 32 + lane] = ph[g];
+  // slice partials through shared memory (reuses the staging buffer), fixed order
+  T* red = reinterpret_cast<T*>(sh);  // [slice][component][128]
+  constexpr int NC = GRAD ? 4 : 1;
+  if (active) {
+    red[(slice * NC + 0) * kP2PThreads + tgt] = ph;
     if (GRAD) {
-      red[warp][1][g * 32 + lane] = gx[g];
-      red[warp][2][g * 32 + lane] = gy[g];
-      red[warp][3][g * 32 + lane] = gz[g];
+      red[(slice * NC + 1) * kP2PThreads + tgt] = gx;
+      red[(slice * NC + 2) * kP2PThreads + tgt] = gy;
+      red[(slice * NC + 3) * kP2PThreads + tgt] = gz;
     }
   }
   __syncthreads();
-  for (int t0 = tid; t0 < w.t_count; t0 += kP2PThreads) {
+  if (tid < nt) {
     const T c = T(kInv4PiD);
-    const int t = w.t_begin + t0;
-    pot[t] = c * (((red[0][0][t0] + red[1][0][t0]) + red[2][0][t0]) + red[3][0][t0]);
-    if (GRAD) {
+    T a[NC];
 #pragma unroll
-      for (int d = 0; d < 3; ++d)
-        grad[3 * size_t(t) + d] = -c * (((red[0][d + 1][t0] + red[1][d + 1][t0]) + red[2][d + 1][t0]) + red[3][d + 1][t0]);
+    for (int d = 0; d < NC; ++d) a[d] = 0;
+    for (int sl = 0; sl < R; ++sl)
+#pragma unroll
+      for (int d = 0; d < NC; ++d) a[d] += red[(sl * NC + d) * kP2PThreads + tid];
+    const int t = w.t_begin + tid;
+    pot[t] = c * a[0];
+    if (GRAD) {
+      grad[3 * size_t(t)] = -c * a[NC > 1 ? 1 : 0];
+      grad[3 * size_t(t) + 1] = -c * a[NC > 2 ? 2 : 0];
+      grad[3 * size_t(t) + 2] = -c * a[NC > 3 ? 3 : 0];
     }
   }
 }
 
-// Check potentials on a node's surface (alpha) from particle ranges.
-// work: {node, out_row, range_begin, range_end} where ranges index `ranges`
-// (int2 {first particle, count}).  out[out_row][j] = scale * sum q / (4 pi r),
-// scale = 2^(ref_level - level); padding columns get 0.
+// Check potentials on a node's surface (alpha) from particle ranges: one warp
+// per work item, lane l owns check points l, l+32, ... (KMAX x 32 >= n_c); each
+// lane loads one source and the warp broadcasts it with shuffles.
+// work: {node, out_row, range_begin, range_end}, ranges = int2 {first, count}.
+// out[out_row][j] = scale * sum q / (4 pi r), scale = 2^(ref_level - level)
+// (SPEC.md:503); padding columns get 0.  Check surfaces never touch particles
+// (alpha > 1 around the node; X-list separation), so there is no r = 0 mask.
 struct CheckWork {
   int node, out_row, range_begin, range_end;
 };
 
-template <class T>
-__global__ void __launch_bounds__(kP2PThreads) check_kernel(P2PParams<T> p, const CheckWork* __restrict__ works,
-                                                             const int2* __restrict__ ranges,
-                                                             const int* __restrict__ node_level, int ref_level,
-                                                             T alpha, T* __restrict__ out, int ld_out) {
-  __shared__ v4_t<T> sh[kP2PCap];
-  const CheckWork w = works[blockIdx.x];
-  const int tid = threadIdx.x;
+constexpr int kCheckWarps = 8;
+
+template <class T, int KMAX>
+__global__ void __launch_bounds__(kCheckWarps * 32) check_kernel(P2PParams<T> p, const CheckWork* __restrict__ works,
+                                                                  int n_works, const int2* __restrict__ ranges,
+                                                                  const int* __restrict__ node_level, int ref_level,
+                                                                  T alpha, T* __restrict__ out, int ld_out) {
+  const int wi = blockIdx.x * kCheckWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (wi >= n_works) return;
+  const CheckWork w = works[wi];
   const v4_t<T> g = p.node_geom[w.node];
   const T s = alpha * g.w;
-  T yx[2], yy[2], yz[2], acc[2];
+  T yx[KMAX], yy[KMAX], yz[KMAX], acc[KMAX];
 #pragma unroll
-  for (int m = 0; m < 2; ++m) {
-    const int j = tid + m * kP2PThreads;
+  for (int m = 0; m < KMAX; ++m) {
+    const int j = lane + 32 * m;
     const int jj = j < p.n_e ? j : 0;
     yx[m] = g.x + s * p.surface[3 * jj];
     yy[m] = g.y + s * p.surface[3 * jj + 1];
     yz[m] = g.z + s * p.surface[3 * jj + 2];
     acc[m] = T(0);
   }
-  int r = w.range_begin, off = 0;
-  while (r < w.range_end) {
-    int fill = 0;
-    while (r < w.range_end && fill < kP2PCap) {
-      const int2 rg = ranges[r];
-      const int take = min(rg.y - off, kP2PCap - fill);
-      for (int i = tid; i < take; i += kP2PThreads) sh[fill + i] = p.src[rg.x + off + i];
-      fill += take;
-      off += take;
-      if (off == rg.y) {
-        ++r;
-        off = 0;
-      }
-    }
-    const int padded = (fill + 7) & ~7;
-    for (int i = fill + tid; i < padded; i += kP2PThreads)
-      sh[i] = make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
-    __syncthreads();
-    // check surfaces never touch particles (alpha > 1 around the node / X-list separation): no r = 0 mask
+  for (int r = w.range_begin; r < w.range_end; ++r) {
+    const int2 rg = ranges[r];
+    for (int b = 0; b < rg.y; b += 32) {
+      const int cnt = min(32, rg.y - b);
+      v4_t<T> mine = lane < cnt ? p.src[rg.x + b + lane] : make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
+      for (int k = 0; k < cnt; ++k) {
+        const T sx = __shfl_sync(0xffffffffu, mine.x, k), sy = __shfl_sync(0xffffffffu, mine.y, k);
+        const T sz = __shfl_sync(0xffffffffu, mine.z, k), sq = __shfl_sync(0xffffffffu, mine.w, k);
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      if (m * kP2PThreads >= p.n_e) break;
-      T a = 0;
-      for (int i = 0; i < padded; i += 8) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const v4_t<T> q = sh[i + u];
-          const T dx = yx[m] - q.x, dy = yy[m] - q.y, dz = yz[m] - q.z;
-          a = fma(q.w, rinv(fma(dz, dz, fma(dy, dy, dx * dx))), a);
+        for (int m = 0; m < KMAX; ++m) {
+          const T dx = yx[m] - sx, dy = yy[m] - sy, dz = yz[m] - sz;
+          acc[m] = fma(sq, rinv(fma(dz, dz, fma(dy, dy, dx * dx))), acc[m]);
         }
       }
-      acc[m] += a;
     }
-    __syncthreads();
   }
   const int lvl = node_level[w.node];
-  const T scale = T(kInv4PiD) * T(ldexp(1.0, ref_level - lvl));
+  const int e = ref_level - lvl;  // |e| <= 15: exact power of two
+  const T scale = T(kInv4PiD) * (e >= 0 ? T(1 << e) : T(1) / T(1 << (-e)));
   T* o = out + size_t(w.out_row) * ld_out;
-  for (int j = tid; j < ld_out; j += kP2PThreads) {
-    const int m = j / kP2PThreads;
-    T v = T(0);
-    if (j < p.n_e) v = (m == 0 ? acc[0] : acc[1]) * scale;
-    o[j] = v;
+#pragma unroll
+  for (int m = 0; m < KMAX; ++m) {
+    const int j = lane + 32 * m;
+    if (j < ld_out) o[j] = j < p.n_e ? acc[m] * scale : T(0);
   }
 }
 

@@ -175,6 +175,21 @@ __global__ void scatter_rows_kernel(const T* __restrict__ src, int ld, const int
   for (int j = threadIdx.x; j < ld; j += blockDim.x) dst[size_t(rows[r]) * ld + j] = s[j];
 }
 
+template <class T>
+void launch_check(int np, int n, const P2PParams<T>& pp, const CheckWork* works, const int2* ranges, const int* lvl,
+                  int ref, T alpha, T* out, cudaStream_t s) {
+  const int blocks = int(ceil_div(n, kCheckWarps));
+  switch ((np + 31) / 32) {
+    case 1: check_kernel<T, 1><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
+    case 2: check_kernel<T, 2><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
+    case 4: check_kernel<T, 4><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
+    case 5: check_kernel<T, 5><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
+    case 7: check_kernel<T, 7><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
+    default: throw InvalidArgument("check kernel: unsupported width");
+  }
+  KIFMM_LAUNCH_CHECK();
+}
+
 // M2M split over octants: partial products land in scratch rows (slot*8 + octant)
 // and are summed here in fixed octant order (deterministic, no atomics).
 template <class T>
@@ -228,7 +243,7 @@ struct kifmm_gpu_plan {
   DevMem q_in, src4, pot, grad_buf, pot_out, grad_out;
   DevMem M, L, check_up, check_dn, tmp;
   // work lists
-  DevMem p2m_works, p2m_ranges, p2l_works, p2l_ranges, leaf_works, leaf_items;
+  DevMem p2m_works, p2m_ranges, p2l_works, p2l_ranges, leaf_works, leaf_rounds, leaf_items;
   int n_p2m = 0, n_p2l = 0, n_leafw = 0;
   GemmTiles solve_up1, solve_up2, solve_dn1, solve_dn2, m2l;
   std::vector<std::unique_ptr<M2MLevel>> m2m_levels, m2m_top;
@@ -648,47 +663,88 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     }
   }
 
-  // ---- leaf works: near field (U) + L2P + M2P (W), <= 128 targets per work
+  // ---- leaf works: near field (U) + L2P + M2P (W), <= 128 targets per work, staged in rounds
   {
     std::vector<LeafWork> w;
-    std::vector<int4> items;
+    std::vector<int4> rounds, items;
+    struct Src {
+      int kind, a, len, j0;
+    };
     for (int64_t l = lb; l < le; ++l) {
       const int64_t node = t.leaf_node[l];
-      const int ib = int(items.size());
+      std::vector<Src> self, other;
       int64_t src_cnt = 0;
-      // U ranges, merged when contiguous in the reordered buffer
-      int cur_b = -1, cur_e = -1;
-      items.push_back(make_int4(kSrcSelf, int(t.leaf_ptr[l]), int(t.leaf_ptr[l + 1] - t.leaf_ptr[l]), 0));
+      self.push_back({kSrcSelf, int(t.leaf_ptr[l]), int(t.leaf_ptr[l + 1] - t.leaf_ptr[l]), 0});
+      int cur_b = -1, cur_e = -1;  // U ranges, merged when contiguous in the reordered buffer
       for (int64_t e = t.u_ptr[l]; e < t.u_ptr[l + 1]; ++e) {
-        const int64_t s = t.u_idx[e];
-        const int b = int(t.leaf_ptr[s]), en = int(t.leaf_ptr[s + 1]);
+        const int64_t s2 = t.u_idx[e];
+        const int b = int(t.leaf_ptr[s2]), en = int(t.leaf_ptr[s2 + 1]);
         src_cnt += en - b;
-        if (s == l) continue;
+        if (s2 == l) continue;
         if (b == cur_e) {
           cur_e = en;
         } else {
-          if (cur_b >= 0) items.push_back(make_int4(kSrcParticles, cur_b, cur_e - cur_b, 0));
+          if (cur_b >= 0) other.push_back({kSrcParticles, cur_b, cur_e - cur_b, 0});
           cur_b = b;
           cur_e = en;
         }
       }
-      if (cur_b >= 0) items.push_back(make_int4(kSrcParticles, cur_b, cur_e - cur_b, 0));
-      const int64_t nt = t.leaf_ptr[l + 1] - t.leaf_ptr[l];
-      info.near_pairs += nt * src_cnt;
+      if (cur_b >= 0) other.push_back({kSrcParticles, cur_b, cur_e - cur_b, 0});
+      const int64_t ntl = t.leaf_ptr[l + 1] - t.leaf_ptr[l];
+      info.near_pairs += ntl * src_cnt;
       if (node_lvl(node) >= 2) {
-        items.push_back(make_int4(kSrcL2P, int(node), 0, 0));
-        info.l2p_pairs += nt * ne;
+        other.push_back({kSrcL2P, int(node), ne, 0});
+        info.l2p_pairs += ntl * ne;
       }
       for (int64_t e = t.w_ptr[l]; e < t.w_ptr[l + 1]; ++e) {
-        items.push_back(make_int4(kSrcM2P, int(t.w_idx[e]), 0, 0));
-        info.m2p_pairs += nt * ne;
+        other.push_back({kSrcM2P, int(t.w_idx[e]), ne, 0});
+        info.m2p_pairs += ntl * ne;
       }
-      const int ie = int(items.size());
-      for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += kP2PThreads)
-        w.push_back({int(l), int(t0), int(std::min<int64_t>(kP2PThreads, t.leaf_ptr[l + 1] - t0)), ib, ie});
+      for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += kP2PThreads) {
+        const int nt = int(std::min<int64_t>(kP2PThreads, t.leaf_ptr[l + 1] - t0));
+        const int R = leaf_slices(nt), q = 8 * R;
+        const int cap = kP2PCap - kP2PCap % q;
+        const int rb = int(rounds.size());
+        size_t si = 0, oi = 0;
+        int soff = 0, ooff = 0;  // offsets inside the current self / other source
+        while (si < self.size() || oi < other.size()) {
+          const int ib = int(items.size());
+          int ns = 0, no = 0;
+          while (si < self.size() && ns < cap) {  // self section first
+            const Src& x = self[si];
+            const int take = std::min(x.len - soff, cap - ns);
+            items.push_back(make_int4(x.kind, x.a + soff, take, ns));
+            ns += take;
+            soff += take;
+            if (soff == x.len) {
+              ++si;
+              soff = 0;
+            }
+          }
+          const int S = (ns + q - 1) / q * q;
+          while (oi < other.size() && S + no < cap) {
+            const Src& x = other[oi];
+            const int take = std::min(x.len - ooff, cap - S - no);
+            if (x.kind == kSrcParticles)
+              items.push_back(make_int4(x.kind, x.a + ooff, take, S + no));
+            else
+              items.push_back(make_int4(x.kind | (ooff << 4), x.a, take, S + no));
+            no += take;
+            ooff += take;
+            if (ooff == x.len) {
+              ++oi;
+              ooff = 0;
+            }
+          }
+          const int O = (no + q - 1) / q * q;
+          rounds.push_back(make_int4(ib, int(items.size()), S | (ns << 16), O | (no << 16)));
+        }
+        w.push_back({int(l), int(t0), nt, rb, int(rounds.size())});
+      }
     }
     n_leafw = int(w.size());
     leaf_works.upload(w, &dev_bytes);
+    leaf_rounds.upload(rounds, &dev_bytes);
     leaf_items.upload(items, &dev_bytes);
   }
 
@@ -771,8 +827,8 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   ++launches;
   // upward: P2M check -> factored solve
   if (n_p2m) {
-    check_kernel<T><<<n_p2m, kP2PThreads, 0, s>>>(pp, p2m_works.as<CheckWork>(), p2m_ranges.as<int2>(),
-                                                  node_level.as<int>(), ref_level, T(alpha_out), check_up.as<T>(), np);
+    launch_check<T>(np, n_p2m, pp, p2m_works.as<CheckWork>(), p2m_ranges.as<int2>(), node_level.as<int>(),
+                    ref_level, T(alpha_out), check_up.as<T>(), s);
     KIFMM_LAUNCH_CHECK();
     ++launches;
   }
@@ -799,8 +855,8 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   // downward: P2L check into the down-check buffer
   KIFMM_CUDA(cudaMemsetAsync(check_dn.p, 0, check_dn.bytes, s));
   if (n_p2l) {
-    check_kernel<T><<<n_p2l, kP2PThreads, 0, s>>>(pp, p2l_works.as<CheckWork>(), p2l_ranges.as<int2>(),
-                                                  node_level.as<int>(), ref_level, T(alpha_in), check_dn.as<T>(), np);
+    launch_check<T>(np, n_p2l, pp, p2l_works.as<CheckWork>(), p2l_ranges.as<int2>(), node_level.as<int>(),
+                    ref_level, T(alpha_in), check_dn.as<T>(), s);
     KIFMM_LAUNCH_CHECK();
     ++launches;
   }
@@ -825,10 +881,10 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   // leaves: near field + L2P + M2P
   if (n_leafw) {
     if (grad)
-      leaf_eval_kernel<T, true><<<n_leafw, kP2PThreads, 0, s>>>(pp, leaf_works.as<LeafWork>(), leaf_items.as<int4>(),
+      leaf_eval_kernel<T, true><<<n_leafw, kP2PThreads, 0, s>>>(pp, leaf_works.as<LeafWork>(), leaf_rounds.as<int4>(), leaf_items.as<int4>(),
                                                                 Mp, Lp, pot.as<T>(), grad_buf.as<T>());
     else
-      leaf_eval_kernel<T, false><<<n_leafw, kP2PThreads, 0, s>>>(pp, leaf_works.as<LeafWork>(), leaf_items.as<int4>(),
+      leaf_eval_kernel<T, false><<<n_leafw, kP2PThreads, 0, s>>>(pp, leaf_works.as<LeafWork>(), leaf_rounds.as<int4>(), leaf_items.as<int4>(),
                                                                  Mp, Lp, pot.as<T>(), nullptr);
     KIFMM_LAUNCH_CHECK();
     ++launches;
