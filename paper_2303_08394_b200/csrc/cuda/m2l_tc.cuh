@@ -1,27 +1,34 @@
 // M2L on the 5th-generation tensor cores: tcgen05 kind::tf32 with 3xTF32 error
 // compensation (SURVEY 7.3 "M2L batching").
 //
-// Work: for a tile of 128 same-class target nodes and one transfer vector t,
-//   D[128 x 160] += A_t[128 x 160] . K_t^T,   A_t rows = multipoles of the V-list
-// sources at offset t (zero rows where absent), K_t = reference-level kernel
-// matrix (n_c x n_e, K-major).  fp32 operands are split x = hi + lo with hi the
-// round-to-nearest tf32 value, and D += A_hi B_hi + A_hi B_lo + A_lo B_hi keeps
-// fp32-level accuracy (the dropped A_lo B_lo term is ~2^-22 relative).
+// Work: for a tile of same-octant-class target nodes and one transfer vector t,
+//   D[rows x 160] += A_t[rows x 160] . K_t^T,  A_t rows = multipoles of the
+// V-list sources at offset t (a zero row where absent), K_t = reference-level
+// kernel matrix (n_c x n_e, K-major).  fp32 operands are split x = hi + lo (hi =
+// tf32 round-to-nearest) and D += A_hi B_hi + A_hi B_lo + A_lo B_hi keeps fp32-
+// level accuracy (the dropped A_lo B_lo term is ~2^-22 relative).
 //
-// CTA (6 warps, one work item = tile x tap chunk, accumulator in TMEM):
-//   warp 0   : TMEM alloc/dealloc; lane 0 streams B_hi/B_lo K-blocks with TMA
-//              (SWIZZLE_128B, 160 rows x 128 B per operand per stage)
-//   warp 1   : lane 0 issues tcgen05.mma (M=128, N=160, K=8) and commits stages
-//   warps 2-5: gather A_hi/A_lo rows with cp.async into the SW128 K-major layout
-//   warps 6-13: per-tap promotion -- each tap accumulates in a fresh TMEM buffer
-//              (two alternate), drained with tcgen05.ld into fp32 registers; the
-//              tensor-core accumulator is not IEEE round-to-nearest and its bias
-//              grows with the accumulation length (measured: 1.2e-6 at 1 tap,
-//              1.5e-5 at 16, 1.5e-4 at 189 taps), so only one tap (K = 160) ever
-//              accumulates in TMEM.
-// Stages: (tap, 32-wide K block) pairs, 3-deep mbarrier ring (72 KB each).
-// Partials of the tap chunks of a tile are summed by m2l_tc_reduce_kernel in a
-// fixed order (deterministic; no atomics).
+// K_t hi/lo arrive by TMA (SWIZZLE_128B, mbarrier transaction counts); the
+// gathered A rows (missing sources read an appended zero row) are copied by 128
+// threads with cp.async into the same SW128 K-major layout (TMA tile::gather4
+// was measured 3x slower for these 128-byte rows).  Stages are (tap, 32-wide K
+// block) pairs.
+//
+// Two variants (template PAIR):
+//   PAIR = false: one CTA, M = 128 targets, 3 stages of 72 KB.
+//   PAIR = true : a 2-CTA cluster (cta_group::2), M = 256; each CTA gathers its
+//                 own 128 A rows and half of K_t (80 check rows), 4 stages of
+//                 52 KB; only the leader issues tcgen05.mma, and stage / TMEM
+//                 barriers the MMA waits on live in the leader.
+//
+// Warps: 0 TMEM alloc + B producer, 1 MMA issuer, 2-5 A producers, 6-13
+// epilogue, 14 A-arrival forwarder to the leader (pair).  The tensor-core accumulator is not IEEE round-to-
+// nearest and its error grows with the accumulation length (measured 1.2e-6 at
+// 1 tap, 1.5e-5 at 16, 1.5e-4 at 189 taps), so each transfer vector
+// accumulates in a fresh TMEM buffer (two alternate) that the epilogue warps
+// drain with tcgen05.ld into fp32 registers ("per-tap promotion").  Partials of
+// the tap chunks of a tile are summed by m2l_tc_reduce_kernel in fixed order
+// (deterministic; no atomics).
 #pragma once
 
 #include <cuda.h>
@@ -38,24 +45,31 @@
 
 namespace kifmm {
 namespace gpu {
-
 namespace tc {
 
-constexpr int BM = 128;          // target rows per tile (UMMA M)
-constexpr int NP = 160;          // check points, padded (UMMA N); p = 6 only
-constexpr int KB = 32;           // fp32 elements per 128-byte K block
-constexpr int NKB = NP / KB;     // K blocks per tap (K = n_e padded = 160)
-constexpr int STAGES = 3;
-constexpr int A_BYTES = BM * 128;  // one operand K block: 16 KB
-constexpr int B_BYTES = NP * 128;  // 20 KB
-constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int EPI_WARPS = 8;                 // 2 per TMEM lane quarter, 80 columns each
-constexpr int EPI_COLS = NP / 2;
-constexpr int THREADS = (6 + EPI_WARPS) * 32;  // TMA, MMA, 4 A-producer warps, epilogue
-constexpr uint32_t TMEM_COLS = 512;            // two 160-column accumulators at 0 and 256
-// instruction descriptor: D f32 (bit 4), A/B tf32 (bits 7, 10), K-major, N>>3 at 17, M>>4 at 24
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+constexpr int BM = 128;  // target rows per CTA
+constexpr int NP = 160;  // check points / equivalent points, padded (p = 6)
+constexpr int KB = 32;   // fp32 elements per 128-byte K block
+constexpr int NKB = NP / KB;
+constexpr int EPI_WARPS = 8, EPI_COLS = NP / 2;
+constexpr int EPI_WARP0 = 6;                         // epilogue warps 6..13
+constexpr int FWD_WARP = EPI_WARP0 + EPI_WARPS;      // 14: A-arrival forwarder (pair)
+constexpr int THREADS = (FWD_WARP + 1) * 32;
+constexpr uint32_t TMEM_COLS = 512;  // two 160-column accumulators at 0 and 256
+
+template <bool PAIR>
+struct Cfg {
+  static constexpr int NB = PAIR ? NP / 2 : NP;  // B rows held per CTA
+  static constexpr int STAGES = PAIR ? 4 : 3;
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = NB * 128;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int CTAS = PAIR ? 2 : 1;
+  static constexpr uint32_t TX = uint32_t(CTAS * 2 * B_BYTES);  // TMA bytes landing on the leader per stage
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
+                                    (uint32_t((CTAS * BM) >> 4) << 24);
+};
 
 struct Item {
   int tile, seg_begin, seg_end, slot;
@@ -64,12 +78,14 @@ struct Item {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+__device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -89,104 +105,171 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (spin > (1u << 28)) asm volatile("trap;");
   }
 }
-
-__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // SM100 UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms 1024 B apart.
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
   uint64_t d = 0;
-  d |= uint64_t((saddr >> 4) & 0x3FFF);       // start address
-  d |= uint64_t(1) << 16;                      // LBO (unused for swizzled K-major) = 16 B
-  d |= uint64_t(1024 >> 4) << 32;              // SBO = 1024 B
-  d |= uint64_t(1) << 46;                      // version (sm100)
-  d |= uint64_t(2) << 61;                      // SWIZZLE_128B
+  d |= uint64_t((saddr >> 4) & 0x3FFF);  // start address
+  d |= uint64_t(1) << 16;                 // LBO (unused for swizzled K-major) = 16 B
+  d |= uint64_t(1024 >> 4) << 32;         // SBO = 1024 B
+  d |= uint64_t(1) << 46;                 // version (sm100)
+  d |= uint64_t(2) << 61;                 // SWIZZLE_128B
   return d;
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
+template <bool PAIR>
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  if constexpr (PAIR)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(Cfg<PAIR>::IDESC), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(Cfg<PAIR>::IDESC), "r"(accumulate));
+}
+// tcgen05.commit: arrive on `bar` (in both CTAs of the pair when PAIR) once prior MMAs complete
+template <bool PAIR>
+__device__ __forceinline__ void commit(uint32_t bar) {
+  if constexpr (PAIR)
+    asm volatile(
+        "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}" ::"r"(
+            bar)
+        : "memory");
+  else
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+template <bool PAIR>
+__device__ __forceinline__ void tma_tile(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  if constexpr (PAIR)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            dst),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+template <bool PAIR>
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, uint32_t bar, int col, int r0,
+                                            int r1, int r2, int r3) {
+  if constexpr (PAIR)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes.cta_group::2 [%0], "
+        "[%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+        "%5, %6, %7}], [%2];" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+        : "memory");
 }
 
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-
+template <bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
-    m2l_tc_kernel(const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_bhi_lo,
-                  const Item* __restrict__ items, const int* __restrict__ seg_mat, const int* __restrict__ seg_in,
-                  const float* __restrict__ m_hi, const float* __restrict__ m_lo, float* __restrict__ partial) {
+    m2l_tc_kernel(const __grid_constant__ CUtensorMap tm_khi, const __grid_constant__ CUtensorMap tm_klo,
+                  const float* __restrict__ m_hi, const float* __restrict__ m_lo, const Item* __restrict__ items,
+                  const int* __restrict__ seg_mat, const int* __restrict__ seg_in, int zero_row,
+                  float* __restrict__ partial) {
+  using C = Cfg<PAIR>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  // bars: [0,S) full, [S,2S) empty, [2S,2S+2) tmem_full[b], [2S+2,2S+4) tmem_empty[b]; then the TMEM address
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  // bars: [0,S) full, [S,2S) empty, [2S,2S+2) tmem_full[b], [2S+2,2S+4) tmem_empty[b],
+  //       [2S+4,3S+4) a_full (this CTA's A rows landed; PAIR only); then the TMEM address
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::STAGES + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Item it = items[blockIdx.x];
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const Item it = items[PAIR ? (blockIdx.x >> 1) : blockIdx.x];
   const int ntap = it.seg_end - it.seg_begin;
   const int nstage = ntap * NKB;
+  const int rows = C::CTAS * BM;  // rows per tile in seg_in / partial
   const uint32_t sbase = smem_u32(smem);
-  auto a_hi = [&](int s) { return sbase + s * STAGE_BYTES; };
-  auto a_lo = [&](int s) { return sbase + s * STAGE_BYTES + A_BYTES; };
-  auto b_hi = [&](int s) { return sbase + s * STAGE_BYTES + 2 * A_BYTES; };
-  auto b_lo = [&](int s) { return sbase + s * STAGE_BYTES + 2 * A_BYTES + B_BYTES; };
+  auto a_hi = [&](int s) { return sbase + s * C::STAGE_BYTES; };
+  auto a_lo = [&](int s) { return sbase + s * C::STAGE_BYTES + C::A_BYTES; };
+  auto b_hi = [&](int s) { return sbase + s * C::STAGE_BYTES + 2 * C::A_BYTES; };
+  auto b_lo = [&](int s) { return sbase + s * C::STAGE_BYTES + 2 * C::A_BYTES + C::B_BYTES; };
   auto full = [&](int s) { return smem_u32(&bars[s]); };
-  auto empty = [&](int s) { return smem_u32(&bars[STAGES + s]); };
-  auto tfull = [&](int b) { return smem_u32(&bars[2 * STAGES + b]); };
-  auto tempty = [&](int b) { return smem_u32(&bars[2 * STAGES + 2 + b]); };
+  auto empty = [&](int s) { return smem_u32(&bars[C::STAGES + s]); };
+  auto tfull = [&](int b) { return smem_u32(&bars[2 * C::STAGES + b]); };
+  auto tempty = [&](int b) { return smem_u32(&bars[2 * C::STAGES + 2 + b]); };
+  auto afull = [&](int s) { return smem_u32(&bars[2 * C::STAGES + 4 + s]); };
+  // barriers the MMA waits on live in the leader; their cluster addresses
+  auto leader = [&](uint32_t a) { return PAIR ? mapa(a, 0) : a; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full(s), 128 + 1);  // 128 A-producer threads + the TMA arrive (with tx bytes)
-      mbar_init(empty(s), 1);       // one tcgen05.commit per stage
+    for (int s = 0; s < C::STAGES; ++s) {
+      // full: the leader's arrive.expect_tx (B bytes of every CTA) + A arrivals: 128 producer threads
+      // (single CTA) or one forwarder per CTA (pair)
+      mbar_init(full(s), PAIR ? 1 + 2 * 128 : 1 + 128);
+      mbar_init(empty(s), 1);  // one tcgen05.commit per stage (multicast to both CTAs when PAIR)
+      mbar_init(afull(s), 128);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(tfull(b), 1);                  // tcgen05.commit after the tap's last MMA
-      mbar_init(tempty(b), EPI_WARPS * 32);    // every epilogue thread after draining
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), C::CTAS * EPI_WARPS);  // one elected lane per epilogue warp per CTA
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_bhi) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_bhi_lo) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_khi) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_klo) : "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (PAIR) cluster_sync();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- B producer (TMA)
+    // ---------------- B producer: this CTA's rows of K_t hi/lo (TMA tile, SWIZZLE_128B)
     if (lane == 0) {
       for (int i = 0; i < nstage; ++i) {
-        const int s = i % STAGES, round = i / STAGES;
+        const int s = i % C::STAGES, round = i / C::STAGES;
         mbar_wait(empty(s), (round & 1) ^ 1);
         const int seg = it.seg_begin + i / NKB, kb = i % NKB;
-        const int row = seg_mat[seg] * NP;
-        mbar_expect_tx(full(s), 2 * B_BYTES);
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
-                "r"(b_hi(s)),
-            "l"(&tm_bhi), "r"(full(s)), "r"(kb * KB), "r"(row)
-            : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
-                "r"(b_lo(s)),
-            "l"(&tm_bhi_lo), "r"(full(s)), "r"(kb * KB), "r"(row)
-            : "memory");
+        const int row = seg_mat[seg] * NP + int(rank) * C::NB;
+        if (rank == 0) mbar_expect_tx(full(s), C::TX);
+        const uint32_t fb = leader(full(s));
+        tma_tile<PAIR>(b_hi(s), &tm_khi, fb, kb * KB, row);
+        tma_tile<PAIR>(b_lo(s), &tm_klo, fb, kb * KB, row);
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer: one fresh TMEM accumulator per tap (buffers alternate)
-    if (lane == 0) {
+    // ---------------- MMA issuer (leader only): a fresh accumulator per tap
+    if (rank == 0 && lane == 0) {
       for (int j = 0; j < ntap; ++j) {
         const int b = j & 1;
         mbar_wait(tempty(b), ((j >> 1) & 1) ^ 1);
@@ -194,62 +277,80 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t d = tmem_base + uint32_t(b * 256);
         for (int kb = 0; kb < NKB; ++kb) {
           const int i = j * NKB + kb;
-          const int s = i % STAGES, round = i / STAGES;
+          const int s = i % C::STAGES, round = i / C::STAGES;
           mbar_wait(full(s), round & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
           for (int k = 0; k < KB / 8; ++k) {  // 4 x (K = 8 tf32 = 32 bytes) per 128-byte block
             const uint64_t dah = make_desc(a_hi(s) + 32 * k), dal = make_desc(a_lo(s) + 32 * k);
             const uint64_t dbh = make_desc(b_hi(s) + 32 * k), dbl = make_desc(b_lo(s) + 32 * k);
-            mma_tf32(d, dah, dbh, (kb > 0 || k > 0) ? 1u : 0u);
-            mma_tf32(d, dah, dbl, 1u);
-            mma_tf32(d, dal, dbh, 1u);
+            mma<PAIR>(d, dah, dbh, (kb > 0 || k > 0) ? 1u : 0u);
+            mma<PAIR>(d, dah, dbl, 1u);
+            mma<PAIR>(d, dal, dbh, 1u);
           }
-          mma_commit(empty(s));
+          commit<PAIR>(empty(s));
         }
-        mma_commit(tfull(b));
+        commit<PAIR>(tfull(b));
       }
     }
-  } else if (warp < 6) {
-    // ---------------- A producers: thread -> (16-byte chunk c, rows r0 + 16 j)
+  } else if (warp >= 2 && warp < 6) {
+    // ---------------- A producers: thread -> (16-byte chunk c, rows r0 + 16 j) of this CTA, cp.async
+    //                  into the SW128 K-major layout; fence.proxy.async before publishing to the MMA
     const int t = threadIdx.x - 64;  // 0..127
     const int c = t & 7, r0 = t >> 3;
     int src[8];
     int cur_seg = -1;
+    auto publish = [&](int st) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (PAIR)
+        mbar_arrive_cluster(leader(full(st)));
+      else
+        mbar_arrive_local(full(st));
+    };
     for (int i = 0; i < nstage; ++i) {
-      const int s = i % STAGES, round = i / STAGES;
+      const int s = i % C::STAGES, round = i / C::STAGES;
       const int seg = it.seg_begin + i / NKB, kb = i % NKB;
       if (seg != cur_seg) {
         cur_seg = seg;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) src[j] = seg_in[size_t(seg) * BM + r0 + 16 * j];
+        for (int j = 0; j < 8; ++j) src[j] = seg_in[size_t(seg) * rows + rank * BM + r0 + 16 * j];
       }
       mbar_wait(empty(s), (round & 1) ^ 1);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int r = r0 + 16 * j;
         const uint32_t off = uint32_t((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
-        const size_t g = size_t(src[j] < 0 ? 0 : src[j]) * NP + kb * KB + c * 4;
-        cp_async16_zfill(a_hi(s) + off, m_hi + g, src[j] >= 0);
-        cp_async16_zfill(a_lo(s) + off, m_lo + g, src[j] >= 0);
+        const bool ok = src[j] >= 0;  // absent source: zero-fill, no global read
+        const size_t g = size_t(ok ? src[j] : zero_row) * NP + kb * KB + c * 4;
+        const int sz = ok ? 16 : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_hi(s) + off), "l"(m_hi + g), "r"(sz)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_lo(s) + off), "l"(m_lo + g), "r"(sz)
+                     : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
-      // publish the previous stage: its copies are complete once <= 1 group is pending
-      if (i > 0) {
+      if (i > 0) {  // the previous stage's copies are complete once <= 1 group is pending
         asm volatile("cp.async.wait_group 1;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(full((i - 1) % STAGES));
+        publish((i - 1) % C::STAGES);
       }
     }
     if (nstage > 0) {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(full((nstage - 1) % STAGES));
+      publish((nstage - 1) % C::STAGES);
     }
-  } else {
-    // ---------------- epilogue: drain each tap's accumulator into fp32 registers (IEEE RN adds)
-    // warp w reads TMEM lanes 32*(w%4).. (rows) and columns [h*80, h*80+80), h = (w-6)/4
-    const int q = warp & 3, h = (warp - 6) >> 2;
+  } else if (warp == FWD_WARP) {
+    // ---------------- forwarder (pair): this CTA's A rows landed -> one arrive on the leader's stage barrier
+    if (false && PAIR && lane == 0) {
+      for (int i = 0; i < nstage; ++i) {
+        const int s = i % C::STAGES, round = i / C::STAGES;
+        mbar_wait(afull(s), round & 1);
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader(full(s))) : "memory");
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ---------------- epilogue: per-tap promotion; warp w reads TMEM lanes 32*(w%4).. (its rows)
+    //                  and columns [h*80, h*80+80), h = (w-6)/4
+    const int q = warp & 3, h = (warp - EPI_WARP0) >> 2;
     const int row = q * 32 + lane;
     float acc[EPI_COLS];
 #pragma unroll
@@ -273,23 +374,36 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int k = 0; k < 16; ++k) acc[cb * 16 + k] += __uint_as_float(v[k]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(tempty(b));
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR)
+          mbar_arrive_cluster(leader(tempty(b)));
+        else
+          mbar_arrive_local(tempty(b));
+      }
     }
-    float4* o4 = reinterpret_cast<float4*>(partial + (size_t(it.slot) * BM + row) * NP + h * EPI_COLS);
+    float4* o4 =
+        reinterpret_cast<float4*>(partial + (size_t(it.slot) * rows + rank * BM + row) * NP + h * EPI_COLS);
 #pragma unroll
-    for (int k = 0; k < EPI_COLS / 4; ++k) o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+    for (int k = 0; k < EPI_COLS / 4; ++k)
+      o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (PAIR) cluster_sync();
   if (warp == 0) {
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
   }
 }
 
 // x = hi + lo with hi = tf32(x) (round to nearest, ties away), lo exact in fp32.
-__global__ void split_tf32_kernel(const float* __restrict__ x, size_t n, float* __restrict__ hi, float* __restrict__ lo) {
+__global__ void split_tf32_kernel(const float* __restrict__ x, size_t n, float* __restrict__ hi,
+                                  float* __restrict__ lo) {
   const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float v = x[i];
@@ -302,15 +416,15 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, size_t n, float* 
 
 // check[out(r)] += sum over the tile's items (fixed order) of partial[slot][r]
 __global__ void m2l_tc_reduce_kernel(const float* __restrict__ partial, const int* __restrict__ tile_out,
-                                     const int* __restrict__ tile_slot, float* __restrict__ check) {
+                                     const int* __restrict__ tile_slot, int rows, float* __restrict__ check) {
   const int tile = blockIdx.x;
   const int s0 = tile_slot[tile], s1 = tile_slot[tile + 1];
-  for (int idx = threadIdx.x; idx < BM * NP; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < rows * NP; idx += blockDim.x) {
     const int r = idx / NP, col = idx % NP;
-    const int out = tile_out[size_t(tile) * BM + r];
+    const int out = tile_out[size_t(tile) * rows + r];
     if (out < 0) continue;
     float acc = check[size_t(out) * NP + col];
-    for (int s = s0; s < s1; ++s) acc += partial[(size_t(s) * BM + r) * NP + col];
+    for (int s = s0; s < s1; ++s) acc += partial[(size_t(s) * rows + r) * NP + col];
     check[size_t(out) * NP + col] = acc;
   }
 }
@@ -327,12 +441,14 @@ inline bool m2l_tc_available() {
 
 // Host side: tiles/items, split operators, TMA descriptors.
 struct M2LTcPlan {
+  bool pair = true;  // 2-CTA (cta_group::2) kernel; KIFMM_TC_PAIR=0 selects the 1-CTA kernel
+  int rows = 256;    // output rows per tile
   int n_items = 0, n_tiles = 0, n_segs = 0;
   size_t nn = 0;
   float *d_khi = nullptr, *d_klo = nullptr, *d_mhi = nullptr, *d_mlo = nullptr, *d_partial = nullptr;
   int *d_tile_out = nullptr, *d_tile_slot = nullptr, *d_seg_mat = nullptr, *d_seg_in = nullptr;
   tc::Item* d_items = nullptr;
-  CUtensorMap tm_hi{}, tm_lo{};
+  CUtensorMap tm_khi{}, tm_klo{};
   int64_t slots = 0;
 
   ~M2LTcPlan() {
@@ -358,23 +474,40 @@ struct M2LTcPlan {
     return r;
   }
 
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+  static void encode(EncodeFn fn, CUtensorMap* m, float* base, uint64_t rows_total, uint32_t box_rows) {
+    const cuuint64_t dims[2] = {cuuint64_t(tc::NP), cuuint64_t(rows_total)};
+    const cuuint64_t strides[1] = {cuuint64_t(tc::NP) * sizeof(float)};
+    const cuuint32_t box[2] = {cuuint32_t(tc::KB), box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw DeviceError(KIFMM_E_CUDA, "cuTensorMapEncodeTiled failed");
+  }
+
   template <class TreeView, class OpsView>
   void build(const TreeView& t, const std::vector<std::vector<int64_t>>& groups, int np, const OpsView& ops,
              size_t* total) {
     if (np != tc::NP) throw InvalidArgument("tcgen05 M2L: only p = 6 (n_e padded to 160) is instantiated");
     nn = size_t(t.n_nodes);
-    // ---- tiles (128 same-class targets) and their tap segments
+    if (const char* e = std::getenv("KIFMM_TC_PAIR")) pair = std::atoi(e) != 0;
+    rows = pair ? 2 * tc::BM : tc::BM;
+    // ---- tiles (rows same-class targets) and their tap segments
     std::vector<int> tile_out, seg_mat, seg_in, tile_seg{0};
     for (const auto& grp : groups) {
-      for (size_t s0 = 0; s0 < grp.size(); s0 += tc::BM) {
-        std::vector<int> out(tc::BM, -1);
+      for (size_t s0 = 0; s0 < grp.size(); s0 += size_t(rows)) {
+        std::vector<int> out(rows, -1);
         std::map<int, std::vector<int>> taps;
-        for (int r = 0; r < tc::BM && s0 + r < grp.size(); ++r) {
+        for (int r = 0; r < rows && s0 + r < grp.size(); ++r) {
           const int64_t b = grp[s0 + r];
           out[r] = int(b);
           for (int64_t e = t.v_ptr[b]; e < t.v_ptr[b + 1]; ++e) {
             auto& v = taps[t.v_tv[e]];
-            if (v.empty()) v.assign(tc::BM, -1);
+            if (v.empty()) v.assign(rows, -1);
             v[r] = int(t.v_idx[e]);
           }
         }
@@ -388,11 +521,11 @@ struct M2LTcPlan {
     }
     n_tiles = int(tile_seg.size()) - 1;
     n_segs = int(seg_mat.size());
-    slots = int64_t(n_segs) * tc::BM;
-    // ---- items: split each tile's taps into balanced chunks (~4 items per SM in total)
+    slots = int64_t(n_segs) * rows;
+    // ---- items: split each tile's taps into balanced chunks (~4 per SM or SM pair)
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int64_t target_items = int64_t(4) * sms;
+    const int64_t target_items = int64_t(4) * (pair ? sms / 2 : sms);
     int chunk = int(std::max<int64_t>(16, (n_segs + target_items - 1) / std::max<int64_t>(1, target_items)));
     if (const char* e = std::getenv("KIFMM_TC_CHUNK")) chunk = std::max(1, std::atoi(e));
     std::vector<tc::Item> items;
@@ -430,31 +563,25 @@ struct M2LTcPlan {
         }
     up(&d_khi, khi, total);
     up(&d_klo, klo, total);
-    KIFMM_CUDA(cudaMalloc(&d_mhi, nn * tc::NP * sizeof(float)));
-    KIFMM_CUDA(cudaMalloc(&d_mlo, nn * tc::NP * sizeof(float)));
-    KIFMM_CUDA(cudaMalloc(&d_partial, std::max(1, n_items) * size_t(tc::BM) * tc::NP * sizeof(float)));
-    *total += 2 * nn * tc::NP * sizeof(float) + size_t(n_items) * tc::BM * tc::NP * sizeof(float);
-    // ---- TMA descriptors over [nt * 160 rows][160 cols] fp32, box 32 x 160, SWIZZLE_128B
-    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    // multipole hi/lo with one appended zero row (gather target of absent sources)
+    KIFMM_CUDA(cudaMalloc(&d_mhi, (nn + 1) * tc::NP * sizeof(float)));
+    KIFMM_CUDA(cudaMalloc(&d_mlo, (nn + 1) * tc::NP * sizeof(float)));
+    KIFMM_CUDA(cudaMemset(d_mhi + nn * tc::NP, 0, tc::NP * sizeof(float)));
+    KIFMM_CUDA(cudaMemset(d_mlo + nn * tc::NP, 0, tc::NP * sizeof(float)));
+    KIFMM_CUDA(cudaMalloc(&d_partial, std::max(1, n_items) * size_t(rows) * tc::NP * sizeof(float)));
+    *total += 2 * (nn + 1) * tc::NP * sizeof(float) + size_t(n_items) * rows * tc::NP * sizeof(float);
+    // ---- TMA descriptors (SWIZZLE_128B, 32-float boxes): K_t tiles of this CTA's rows, gather4 rows of M
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     KIFMM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
     if (!fn) throw DeviceError(KIFMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-    const cuuint64_t dims[2] = {cuuint64_t(tc::NP), cuuint64_t(nt) * tc::NP};
-    const cuuint64_t strides[1] = {cuuint64_t(tc::NP) * sizeof(float)};
-    const cuuint32_t box[2] = {cuuint32_t(tc::KB), cuuint32_t(tc::NP)};
-    const cuuint32_t estr[2] = {1, 1};
-    for (int which = 0; which < 2; ++which) {
-      CUresult r = reinterpret_cast<EncodeFn>(fn)(which ? &tm_lo : &tm_hi, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                                                  which ? d_klo : d_khi, dims, strides, box, estr,
-                                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) throw DeviceError(KIFMM_E_CUDA, "cuTensorMapEncodeTiled failed");
-    }
-    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES));
+    const uint32_t brow = uint32_t(pair ? tc::Cfg<true>::NB : tc::Cfg<false>::NB);
+    encode(reinterpret_cast<EncodeFn>(fn), &tm_khi, d_khi, uint64_t(nt) * tc::NP, brow);
+    encode(reinterpret_cast<EncodeFn>(fn), &tm_klo, d_klo, uint64_t(nt) * tc::NP, brow);
+    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::Cfg<false>::SMEM_BYTES));
+    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::Cfg<true>::SMEM_BYTES));
   }
 
   // check += M2L(M): split M, run the tcgen05 items, reduce partials.
@@ -463,10 +590,28 @@ struct M2LTcPlan {
     const size_t n = nn * size_t(np);
     tc::split_tf32_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(M, n, d_mhi, d_mlo);
     KIFMM_LAUNCH_CHECK();
-    tc::m2l_tc_kernel<<<n_items, tc::THREADS, tc::SMEM_BYTES, s>>>(tm_hi, tm_lo, d_items, d_seg_mat, d_seg_in, d_mhi,
-                                                                   d_mlo, d_partial);
+    if (pair) {
+      cudaLaunchConfig_t cfg{};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(2 * n_items);
+      cfg.blockDim = dim3(tc::THREADS);
+      cfg.dynamicSmemBytes = tc::Cfg<true>::SMEM_BYTES;
+      cfg.stream = s;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<true>, tm_khi, tm_klo, (const float*)d_mhi,
+                                    (const float*)d_mlo, (const tc::Item*)d_items, (const int*)d_seg_mat,
+                                    (const int*)d_seg_in, int(nn), d_partial));
+    } else {
+      tc::m2l_tc_kernel<false><<<n_items, tc::THREADS, tc::Cfg<false>::SMEM_BYTES, s>>>(
+          tm_khi, tm_klo, d_mhi, d_mlo, d_items, d_seg_mat, d_seg_in, int(nn), d_partial);
+    }
     KIFMM_LAUNCH_CHECK();
-    tc::m2l_tc_reduce_kernel<<<n_tiles, 256, 0, s>>>(d_partial, d_tile_out, d_tile_slot, check);
+    tc::m2l_tc_reduce_kernel<<<n_tiles, 256, 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
     KIFMM_LAUNCH_CHECK();
   }
 };

@@ -103,7 +103,7 @@ __host__ __device__ inline int leaf_slices(int nt) {
   return r < 1 ? 1 : (r > kMaxSlices ? kMaxSlices : r);
 }
 
-template <class T, bool GRAD>
+template <class T, bool GRAD, bool ACC>
 __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, const LeafWork* __restrict__ works,
                                                                  const int4* __restrict__ rounds,
                                                                  const int4* __restrict__ items,
@@ -174,11 +174,12 @@ __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, 
 #pragma unroll
       for (int d = 0; d < NC; ++d) a[d] += red[(sl * NC + d) * kP2PThreads + tid];
     const int t = w.t_begin + tid;
-    pot[t] = c * a[0];
+    pot[t] = (ACC ? pot[t] : T(0)) + c * a[0];
     if (GRAD) {
-      grad[3 * size_t(t)] = -c * a[NC > 1 ? 1 : 0];
-      grad[3 * size_t(t) + 1] = -c * a[NC > 2 ? 2 : 0];
-      grad[3 * size_t(t) + 2] = -c * a[NC > 3 ? 3 : 0];
+      T* gp = grad + 3 * size_t(t);
+      gp[0] = (ACC ? gp[0] : T(0)) - c * a[NC > 1 ? 1 : 0];
+      gp[1] = (ACC ? gp[1] : T(0)) - c * a[NC > 2 ? 2 : 0];
+      gp[2] = (ACC ? gp[2] : T(0)) - c * a[NC > 3 ? 3 : 0];
     }
   }
 }

@@ -207,6 +207,11 @@ __global__ void m2m_reduce_kernel(const T* __restrict__ scratch, const int* __re
   }
 }
 
+struct LeafPlan {
+  DevMem works, rounds, items;
+  int n = 0;
+};
+
 struct M2MLevel {
   GemmTiles tiles;  // one tile per (64 parents, octant)
   DevMem parents, masks;
@@ -231,7 +236,8 @@ struct kifmm_gpu_plan {
   int m2l_backend = 1;
   double alpha_in = 1.05, alpha_out = 2.95;
   size_t dev_bytes = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr, side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::array<cudaEvent_t, 16> ev{};
   kifmm_gpu_plan_info info{};
   kifmm_gpu_timings last{};
@@ -243,8 +249,9 @@ struct kifmm_gpu_plan {
   DevMem q_in, src4, pot, grad_buf, pot_out, grad_out;
   DevMem M, L, check_up, check_dn, tmp;
   // work lists
-  DevMem p2m_works, p2m_ranges, p2l_works, p2l_ranges, leaf_works, leaf_rounds, leaf_items;
-  int n_p2m = 0, n_p2l = 0, n_leafw = 0;
+  DevMem p2m_works, p2m_ranges, p2l_works, p2l_ranges;
+  LeafPlan leaf_near, leaf_far;
+  int n_p2m = 0, n_p2l = 0;
   GemmTiles solve_up1, solve_up2, solve_dn1, solve_dn2, m2l;
   std::vector<std::unique_ptr<M2MLevel>> m2m_levels, m2m_top;
   std::vector<std::unique_ptr<GemmTiles>> l2l_levels;
@@ -264,6 +271,9 @@ struct kifmm_gpu_plan {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (comm) Nccl::get().commDestroy(static_cast<ncclComm_t>(comm));
   }
 
@@ -369,7 +379,14 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   const double expect_half = t.side / double(1 << (ref_level + 1));
   if (std::fabs(ops.ref_half_side - expect_half) > 1e-12 * expect_half)
     throw InvalidArgument("gpu: operator cache was built for another domain side");
-  KIFMM_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;  // numerically lower = higher priority
+    KIFMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    KIFMM_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, hi));
+    KIFMM_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+    KIFMM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    KIFMM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
   for (auto& e : ev) KIFMM_CUDA(cudaEventCreate(&e));
 
   // ---- partition
@@ -663,42 +680,48 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     }
   }
 
-  // ---- leaf works: near field (U) + L2P + M2P (W), <= 128 targets per work, staged in rounds
-  {
+  // ---- leaf works, <= 128 targets per work, staged in rounds:
+  //      near plan = self + U-list particles (runs on the side stream from the start),
+  //      far plan  = L2P + M2P surfaces (after L2L; accumulates into the near result)
+  auto build_leaf_plan = [&](bool near_part, LeafPlan& lp) {
     std::vector<LeafWork> w;
     std::vector<int4> rounds, items;
     struct Src {
-      int kind, a, len, j0;
+      int kind, a, len;
     };
     for (int64_t l = lb; l < le; ++l) {
       const int64_t node = t.leaf_node[l];
       std::vector<Src> self, other;
-      int64_t src_cnt = 0;
-      self.push_back({kSrcSelf, int(t.leaf_ptr[l]), int(t.leaf_ptr[l + 1] - t.leaf_ptr[l]), 0});
-      int cur_b = -1, cur_e = -1;  // U ranges, merged when contiguous in the reordered buffer
-      for (int64_t e = t.u_ptr[l]; e < t.u_ptr[l + 1]; ++e) {
-        const int64_t s2 = t.u_idx[e];
-        const int b = int(t.leaf_ptr[s2]), en = int(t.leaf_ptr[s2 + 1]);
-        src_cnt += en - b;
-        if (s2 == l) continue;
-        if (b == cur_e) {
-          cur_e = en;
-        } else {
-          if (cur_b >= 0) other.push_back({kSrcParticles, cur_b, cur_e - cur_b, 0});
-          cur_b = b;
-          cur_e = en;
-        }
-      }
-      if (cur_b >= 0) other.push_back({kSrcParticles, cur_b, cur_e - cur_b, 0});
       const int64_t ntl = t.leaf_ptr[l + 1] - t.leaf_ptr[l];
-      info.near_pairs += ntl * src_cnt;
-      if (node_lvl(node) >= 2) {
-        other.push_back({kSrcL2P, int(node), ne, 0});
-        info.l2p_pairs += ntl * ne;
-      }
-      for (int64_t e = t.w_ptr[l]; e < t.w_ptr[l + 1]; ++e) {
-        other.push_back({kSrcM2P, int(t.w_idx[e]), ne, 0});
-        info.m2p_pairs += ntl * ne;
+      if (near_part) {
+        int64_t src_cnt = 0;
+        self.push_back({kSrcSelf, int(t.leaf_ptr[l]), int(ntl)});
+        int cur_b = -1, cur_e = -1;  // U ranges, merged when contiguous in the reordered buffer
+        for (int64_t e = t.u_ptr[l]; e < t.u_ptr[l + 1]; ++e) {
+          const int64_t s2 = t.u_idx[e];
+          const int b = int(t.leaf_ptr[s2]), en = int(t.leaf_ptr[s2 + 1]);
+          src_cnt += en - b;
+          if (s2 == l) continue;
+          if (b == cur_e) {
+            cur_e = en;
+          } else {
+            if (cur_b >= 0) other.push_back({kSrcParticles, cur_b, cur_e - cur_b});
+            cur_b = b;
+            cur_e = en;
+          }
+        }
+        if (cur_b >= 0) other.push_back({kSrcParticles, cur_b, cur_e - cur_b});
+        info.near_pairs += ntl * src_cnt;
+      } else {
+        if (node_lvl(node) >= 2) {
+          other.push_back({kSrcL2P, int(node), ne});
+          info.l2p_pairs += ntl * ne;
+        }
+        for (int64_t e = t.w_ptr[l]; e < t.w_ptr[l + 1]; ++e) {
+          other.push_back({kSrcM2P, int(t.w_idx[e]), ne});
+          info.m2p_pairs += ntl * ne;
+        }
+        if (other.empty()) continue;
       }
       for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += kP2PThreads) {
         const int nt = int(std::min<int64_t>(kP2PThreads, t.leaf_ptr[l + 1] - t0));
@@ -742,11 +765,13 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
         w.push_back({int(l), int(t0), nt, rb, int(rounds.size())});
       }
     }
-    n_leafw = int(w.size());
-    leaf_works.upload(w, &dev_bytes);
-    leaf_rounds.upload(rounds, &dev_bytes);
-    leaf_items.upload(items, &dev_bytes);
-  }
+    lp.n = int(w.size());
+    lp.works.upload(w, &dev_bytes);
+    lp.rounds.upload(rounds, &dev_bytes);
+    lp.items.upload(items, &dev_bytes);
+  };
+  build_leaf_plan(true, leaf_near);
+  build_leaf_plan(false, leaf_far);
 
   info.n_particles = N;
   info.n_leaves = nl;
@@ -818,6 +843,23 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   };
   T* Mp = M.as<T>();
   T* Lp = L.as<T>();
+  auto leaf = [&](const LeafPlan& lp, bool acc, cudaStream_t st) {
+    if (!lp.n) return;
+    const LeafWork* w = lp.works.as<LeafWork>();
+    const int4* r = lp.rounds.as<int4>();
+    const int4* it = lp.items.as<int4>();
+    T* g = grad ? grad_buf.as<T>() : nullptr;
+    if (grad && acc)
+      leaf_eval_kernel<T, true, true><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<T>(), g);
+    else if (grad)
+      leaf_eval_kernel<T, true, false><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<T>(), g);
+    else if (acc)
+      leaf_eval_kernel<T, false, true><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<T>(), g);
+    else
+      leaf_eval_kernel<T, false, false><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<T>(), g);
+    KIFMM_LAUNCH_CHECK();
+    ++launches;
+  };
 
   mark();  // 0
   pack_sources_kernel<T><<<int(ceil_div(N, 256)), 256, 0, s>>>(pos4.as<v4_t<T>>(), q_in.as<T>(),
@@ -825,6 +867,13 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
                                                                src4.as<v4_t<T>>());
   KIFMM_LAUNCH_CHECK();
   ++launches;
+  // near field has no dependency on the tree passes: fork it onto the low-priority side stream
+  if (!timed && leaf_near.n) {
+    KIFMM_CUDA(cudaEventRecord(ev_fork, s));
+    KIFMM_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    leaf(leaf_near, false, side);
+    KIFMM_CUDA(cudaEventRecord(ev_join, side));
+  }
   // upward: P2M check -> factored solve
   if (n_p2m) {
     launch_check<T>(np, n_p2m, pp, p2m_works.as<CheckWork>(), p2m_ranges.as<int2>(), node_level.as<int>(),
@@ -878,17 +927,10 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   // L2L top-down
   for (auto& lv : l2l_levels) gemm(*lv, Lp, w_l2l.as<T>(), Lp, true, false);
   mark();  // 7
-  // leaves: near field + L2P + M2P
-  if (n_leafw) {
-    if (grad)
-      leaf_eval_kernel<T, true><<<n_leafw, kP2PThreads, 0, s>>>(pp, leaf_works.as<LeafWork>(), leaf_rounds.as<int4>(), leaf_items.as<int4>(),
-                                                                Mp, Lp, pot.as<T>(), grad_buf.as<T>());
-    else
-      leaf_eval_kernel<T, false><<<n_leafw, kP2PThreads, 0, s>>>(pp, leaf_works.as<LeafWork>(), leaf_rounds.as<int4>(), leaf_items.as<int4>(),
-                                                                 Mp, Lp, pot.as<T>(), nullptr);
-    KIFMM_LAUNCH_CHECK();
-    ++launches;
-  }
+  // leaves: near field (side stream, or here when timed) then L2P + M2P
+  if (timed) leaf(leaf_near, false, s);
+  else if (leaf_near.n) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+  leaf(leaf_far, true, s);
   mark();  // 8
   if (input_order) {
     if (world > 1) {
@@ -933,7 +975,7 @@ void kifmm_gpu_plan::evaluate_device(const void* q, void* pot_dst, void* grad_ds
         throw;
       }
       KIFMM_CUDA(cudaStreamEndCapture(stream, &g));
-      KIFMM_CUDA(cudaGraphInstantiate(&graph[gi], g, 0));
+      KIFMM_CUDA(cudaGraphInstantiateWithFlags(&graph[gi], g, cudaGraphInstantiateFlagUseNodePriority));
       cudaGraphDestroy(g);
     }
     KIFMM_CUDA(cudaGraphLaunch(graph[gi], s));
@@ -1059,7 +1101,7 @@ kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* p, const void* charges, void* po
         else
           p->run<double>(s, input_order != 0, false);
         KIFMM_CUDA(cudaStreamEndCapture(s, &g));
-        KIFMM_CUDA(cudaGraphInstantiate(&p->graph[gi], g, 0));
+        KIFMM_CUDA(cudaGraphInstantiateWithFlags(&p->graph[gi], g, cudaGraphInstantiateFlagUseNodePriority));
         cudaGraphDestroy(g);
       }
       KIFMM_CUDA(cudaGraphLaunch(p->graph[gi], s));
