@@ -39,6 +39,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -49,22 +50,26 @@ namespace tc {
 
 constexpr int BM = 128;  // target rows per CTA
 constexpr int NP = 160;  // check points / equivalent points, padded (p = 6)
-constexpr int KB = 32;   // fp32 elements per 128-byte K block
-constexpr int NKB = NP / KB;
 constexpr int EPI_WARPS = 8, EPI_COLS = NP / 2;
 constexpr int EPI_WARP0 = 6;                         // epilogue warps 6..13
 constexpr int FWD_WARP = EPI_WARP0 + EPI_WARPS;      // 14: A-arrival forwarder (pair)
 constexpr int THREADS = (FWD_WARP + 1) * 32;
 constexpr uint32_t TMEM_COLS = 512;  // two 160-column accumulators at 0 and 256
 
-template <bool PAIR>
+// ROWB: bytes of one operand row per stage (K block of ROWB/4 fp32): 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B,
+// twice the stages for the same shared memory => deeper latency hiding).
+template <bool PAIR, int ROWB>
 struct Cfg {
+  static constexpr int KB = ROWB / 4;            // fp32 per K block
+  static constexpr int NKB = NP / KB;            // K blocks per tap
   static constexpr int NB = PAIR ? NP / 2 : NP;  // B rows held per CTA
-  static constexpr int STAGES = PAIR ? 4 : 3;
-  static constexpr int A_BYTES = BM * 128;
-  static constexpr int B_BYTES = NB * 128;
+  static constexpr int A_BYTES = BM * ROWB;
+  static constexpr int B_BYTES = NB * ROWB;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int STAGES = (216 * 1024) / STAGE_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512;
+  static constexpr int ATOM = 8 * ROWB;           // bytes of an 8-row swizzle atom (= SBO)
+  static constexpr uint64_t LAYOUT = ROWB == 128 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B
   static constexpr int CTAS = PAIR ? 2 : 1;
   static constexpr uint32_t TX = uint32_t(CTAS * 2 * B_BYTES);  // TMA bytes landing on the leader per stage
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
@@ -119,14 +124,15 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// SM100 UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms 1024 B apart.
+// SM100 UMMA shared-memory descriptor: K-major, swizzled, 8-row atoms SBO bytes apart.
+template <int ROWB>
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
   uint64_t d = 0;
-  d |= uint64_t((saddr >> 4) & 0x3FFF);  // start address
-  d |= uint64_t(1) << 16;                 // LBO (unused for swizzled K-major) = 16 B
-  d |= uint64_t(1024 >> 4) << 32;         // SBO = 1024 B
-  d |= uint64_t(1) << 46;                 // version (sm100)
-  d |= uint64_t(2) << 61;                 // SWIZZLE_128B
+  d |= uint64_t((saddr >> 4) & 0x3FFF);          // start address
+  d |= uint64_t(1) << 16;                         // LBO (unused for swizzled K-major) = 16 B
+  d |= uint64_t((8 * ROWB) >> 4) << 32;           // SBO = one 8-row atom
+  d |= uint64_t(1) << 46;                         // version (sm100)
+  d |= uint64_t(ROWB == 128 ? 2 : 4) << 61;       // SWIZZLE_128B / SWIZZLE_64B
   return d;
 }
 
@@ -136,12 +142,12 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uin
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(Cfg<PAIR>::IDESC), "r"(accumulate));
+        "l"(a), "l"(b), "r"(Cfg<PAIR, 128>::IDESC), "r"(accumulate));
   else
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(Cfg<PAIR>::IDESC), "r"(accumulate));
+        "l"(a), "l"(b), "r"(Cfg<PAIR, 128>::IDESC), "r"(accumulate));
 }
 // tcgen05.commit: arrive on `bar` (in both CTAs of the pair when PAIR) once prior MMAs complete
 template <bool PAIR>
@@ -187,13 +193,14 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
-template <bool PAIR>
+template <bool PAIR, int ROWB>
 __global__ void __launch_bounds__(THREADS, 1)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tm_khi, const __grid_constant__ CUtensorMap tm_klo,
                   const float* __restrict__ m_hi, const float* __restrict__ m_lo, const Item* __restrict__ items,
                   const int* __restrict__ seg_mat, const int* __restrict__ seg_in, int zero_row,
                   float* __restrict__ partial) {
-  using C = Cfg<PAIR>;
+  using C = Cfg<PAIR, ROWB>;
+  constexpr int KB = C::KB, NKB = C::NKB;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -281,9 +288,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(full(s), round & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-          for (int k = 0; k < KB / 8; ++k) {  // 4 x (K = 8 tf32 = 32 bytes) per 128-byte block
-            const uint64_t dah = make_desc(a_hi(s) + 32 * k), dal = make_desc(a_lo(s) + 32 * k);
-            const uint64_t dbh = make_desc(b_hi(s) + 32 * k), dbl = make_desc(b_lo(s) + 32 * k);
+          for (int k = 0; k < KB / 8; ++k) {  // K = 8 tf32 = 32 bytes per MMA
+            const uint64_t dah = make_desc<ROWB>(a_hi(s) + 32 * k), dal = make_desc<ROWB>(a_lo(s) + 32 * k);
+            const uint64_t dbh = make_desc<ROWB>(b_hi(s) + 32 * k), dbl = make_desc<ROWB>(b_lo(s) + 32 * k);
             mma<PAIR>(d, dah, dbh, (kb > 0 || k > 0) ? 1u : 0u);
             mma<PAIR>(d, dah, dbl, 1u);
             mma<PAIR>(d, dal, dbh, 1u);
@@ -296,9 +303,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp >= 2 && warp < 6) {
     // ---------------- A producers: thread -> (16-byte chunk c, rows r0 + 16 j) of this CTA, cp.async
     //                  into the SW128 K-major layout; fence.proxy.async before publishing to the MMA
+    constexpr int CH = ROWB / 16;     // 16-byte chunks per row
+    constexpr int RPI = 128 / CH;     // rows covered by the 128 producer threads per pass
+    constexpr int J = BM / RPI;       // passes (rows per thread)
     const int t = threadIdx.x - 64;  // 0..127
-    const int c = t & 7, r0 = t >> 3;
-    int src[8];
+    const int c = t % CH, r0 = t / CH;
+    int src[J];
     int cur_seg = -1;
     auto publish = [&](int st) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -313,13 +323,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (seg != cur_seg) {
         cur_seg = seg;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) src[j] = seg_in[size_t(seg) * rows + rank * BM + r0 + 16 * j];
+        for (int j = 0; j < J; ++j) src[j] = seg_in[size_t(seg) * rows + rank * BM + r0 + RPI * j];
       }
       mbar_wait(empty(s), (round & 1) ^ 1);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int r = r0 + 16 * j;
-        const uint32_t off = uint32_t((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+      for (int j = 0; j < J; ++j) {
+        const int r = r0 + RPI * j;
+        const int sw = ROWB == 128 ? (r & 7) : ((r & 7) >> 1);  // Swizzle<3,4,3> / Swizzle<2,4,3>
+        const uint32_t off = uint32_t((r >> 3) * C::ATOM + (r & 7) * ROWB + ((c ^ sw) << 4));
         const bool ok = src[j] >= 0;  // absent source: zero-fill, no global read
         const size_t g = size_t(ok ? src[j] : zero_row) * NP + kb * KB + c * 4;
         const int sz = ok ? 16 : 0;
@@ -401,6 +412,273 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// A-in-TMEM variant (default).  With both operands in shared memory the three
+// MMAs per K step re-read A_hi twice and B_hi twice from SMEM (~115 B/clk at
+// the MMA rate, plus ~75 B/clk of incoming copies) -- over the ~128 B/clk SMEM
+// port -- which capped the tensor pipe near 60 %.  Here the producers load the
+// gathered fp32 rows with plain loads, split them into tf32 hi/lo in registers
+// and write both into TMEM with tcgen05.st (lane = target row, column = K), so
+// SMEM only carries K_t (TMA, SWIZZLE_64B) and A is read from L2 once, in fp32.
+// TMEM columns: accumulators [0,160) and [256,416); six A stages of 32 columns
+// (hi 16 + lo 16) at 160,192,224,416,448,480.
+namespace ta {
+constexpr int KB = 16;              // K values per stage
+constexpr int NKB = NP / KB;        // 10 stages per tap
+constexpr int STAGES = 6;
+constexpr int ROWB = KB * 4;        // 64-byte B rows, SWIZZLE_64B
+__host__ __device__ constexpr int a_col(int s) { return s < 3 ? 160 + 32 * s : 416 + 32 * (s - 3); }
+
+template <bool PAIR>
+struct Cfg {
+  static constexpr int CTAS = PAIR ? 2 : 1;
+  static constexpr int NB = PAIR ? NP / 2 : NP;
+  static constexpr int B_BYTES = NB * ROWB;  // per operand (hi or lo)
+  static constexpr int STAGE_BYTES = 2 * B_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512;
+  static constexpr uint32_t TX = uint32_t(CTAS * STAGE_BYTES);
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
+                                    (uint32_t((CTAS * BM) >> 4) << 24);
+};
+
+template <bool PAIR>
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t accumulate) {
+  if constexpr (PAIR)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(Cfg<PAIR>::IDESC), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(Cfg<PAIR>::IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+template <bool PAIR>
+__global__ void __launch_bounds__(THREADS, 1)
+    m2l_ta_kernel(const __grid_constant__ CUtensorMap tm_khi, const __grid_constant__ CUtensorMap tm_klo,
+                  const float* __restrict__ M, const Item* __restrict__ items, const int* __restrict__ seg_mat,
+                  const int* __restrict__ seg_in, float* __restrict__ partial) {
+  using C = Cfg<PAIR>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  // bars: [0,S) b_full, [S,2S) empty (stage consumed), [2S,3S) a_full, [3S,3S+2) tfull, [3S+2,3S+4) tempty
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const Item it = items[PAIR ? (blockIdx.x >> 1) : blockIdx.x];
+  const int ntap = it.seg_end - it.seg_begin;
+  const int nstage = ntap * NKB;
+  const int rows = C::CTAS * BM;
+  const uint32_t sbase = smem_u32(smem);
+  auto b_hi = [&](int s) { return sbase + s * C::STAGE_BYTES; };
+  auto b_lo = [&](int s) { return sbase + s * C::STAGE_BYTES + C::B_BYTES; };
+  auto bfull = [&](int s) { return smem_u32(&bars[s]); };
+  auto empty = [&](int s) { return smem_u32(&bars[STAGES + s]); };
+  auto afull = [&](int s) { return smem_u32(&bars[2 * STAGES + s]); };
+  auto tfull = [&](int b) { return smem_u32(&bars[3 * STAGES + b]); };
+  auto tempty = [&](int b) { return smem_u32(&bars[3 * STAGES + 2 + b]); };
+  auto leader = [&](uint32_t a) { return PAIR ? mapa(a, 0) : a; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(bfull(s), 1);                // leader's expect_tx; B bytes of every CTA
+      mbar_init(empty(s), 1);                // tcgen05.commit (multicast when PAIR)
+      mbar_init(afull(s), C::CTAS * 4);      // one elected lane per A-producer warp per CTA
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), C::CTAS * EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_khi) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_klo) : "memory");
+  }
+  if (warp == 0) {
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (PAIR) cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- B producer (TMA, SWIZZLE_64B, this CTA's check rows of K_t hi/lo)
+    if (lane == 0) {
+      for (int i = 0; i < nstage; ++i) {
+        const int s = i % STAGES, round = i / STAGES;
+        mbar_wait(empty(s), (round & 1) ^ 1);
+        const int seg = it.seg_begin + i / NKB, kb = i % NKB;
+        const int row = seg_mat[seg] * NP + int(rank) * C::NB;
+        if (rank == 0) mbar_expect_tx(bfull(s), C::TX);
+        const uint32_t fb = leader(bfull(s));
+        tma_tile<PAIR>(b_hi(s), &tm_khi, fb, kb * KB, row);
+        tma_tile<PAIR>(b_lo(s), &tm_klo, fb, kb * KB, row);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader): A from TMEM, B from SMEM, fresh accumulator per tap
+    if (rank == 0 && lane == 0) {
+      for (int j = 0; j < ntap; ++j) {
+        const int b = j & 1;
+        mbar_wait(tempty(b), ((j >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem_base + uint32_t(b * 256);
+        for (int kb = 0; kb < NKB; ++kb) {
+          const int i = j * NKB + kb;
+          const int s = i % STAGES, round = i / STAGES;
+          mbar_wait(bfull(s), round & 1);
+          mbar_wait(afull(s), round & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t ah = tmem_base + uint32_t(a_col(s)), al = ah + KB;
+#pragma unroll
+          for (int k = 0; k < KB / 8; ++k) {
+            const uint64_t dbh = make_desc<ROWB>(b_hi(s) + 32 * k), dbl = make_desc<ROWB>(b_lo(s) + 32 * k);
+            mma_ts<PAIR>(d, ah + 8 * k, dbh, (kb > 0 || k > 0) ? 1u : 0u);
+            mma_ts<PAIR>(d, ah + 8 * k, dbl, 1u);
+            mma_ts<PAIR>(d, al + 8 * k, dbh, 1u);
+          }
+          commit<PAIR>(empty(s));
+        }
+        commit<PAIR>(tfull(b));
+      }
+    }
+  } else if (warp < 6) {
+    // ---------------- A producers: thread = target row (TMEM lane); 16 fp32 per stage, loaded
+    //                  two stages ahead, split to tf32 hi/lo and stored into the stage's TMEM columns
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t lane_addr = uint32_t(q * 32) << 16;
+    float4 buf[3][4];
+    auto load = [&](int i, float4 (&v)[4]) {
+      const int seg = it.seg_begin + i / NKB, kb = i % NKB;
+      const int src = seg_in[size_t(seg) * rows + rank * BM + row];
+      if (src < 0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        const float4* g = reinterpret_cast<const float4*>(M + size_t(src) * NP + kb * KB);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(g + u);
+      }
+    };
+    auto store = [&](int i, const float4 (&v)[4]) {
+      const int s = i % STAGES, round = i / STAGES;
+      mbar_wait(empty(s), (round & 1) ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float x[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint32_t h;
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x[e]));
+          hi[4 * u + e] = h;
+          lo[4 * u + e] = __float_as_uint(x[e] - __uint_as_float(h));
+        }
+      }
+      const uint32_t col = tmem_base + lane_addr + uint32_t(a_col(s));
+      tmem_st16(col, hi);
+      tmem_st16(col + KB, lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR)
+          mbar_arrive_cluster(leader(afull(s)));
+        else
+          mbar_arrive_local(afull(s));
+      }
+    };
+    if (nstage > 0) load(0, buf[0]);
+    if (nstage > 1) load(1, buf[1]);
+    int i = 0;
+    for (; i + 2 < nstage; i += 3) {
+      load(i + 2, buf[2]);
+      store(i, buf[0]);
+      if (i + 3 < nstage) load(i + 3, buf[0]);
+      store(i + 1, buf[1]);
+      if (i + 4 < nstage) load(i + 4, buf[1]);
+      store(i + 2, buf[2]);
+    }
+    if (i < nstage) store(i, buf[0]);
+    if (i + 1 < nstage) store(i + 1, buf[1]);
+  } else if (warp < EPI_WARP0 + EPI_WARPS) {
+    // ---------------- epilogue (warps 6-13): per-tap promotion into fp32 registers
+    const int q = warp & 3, h = (warp - EPI_WARP0) >> 2;
+    const int row = q * 32 + lane;
+    float acc[EPI_COLS];
+#pragma unroll
+    for (int k = 0; k < EPI_COLS; ++k) acc[k] = 0.f;
+    for (int j = 0; j < ntap; ++j) {
+      const int b = j & 1;
+      mbar_wait(tfull(b), (j >> 1) & 1);
+      __syncwarp();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * 256 + h * EPI_COLS);
+#pragma unroll
+      for (int cb = 0; cb < EPI_COLS / 16; ++cb) {
+        uint32_t v[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr + uint32_t(cb * 16)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[cb * 16 + k] += __uint_as_float(v[k]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR)
+          mbar_arrive_cluster(leader(tempty(b)));
+        else
+          mbar_arrive_local(tempty(b));
+      }
+    }
+    float4* o4 =
+        reinterpret_cast<float4*>(partial + (size_t(it.slot) * rows + rank * BM + row) * NP + h * EPI_COLS);
+#pragma unroll
+    for (int k = 0; k < EPI_COLS / 4; ++k)
+      o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (PAIR) cluster_sync();
+  if (warp == 0) {
+    __syncwarp();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+}  // namespace ta
+
 // x = hi + lo with hi = tf32(x) (round to nearest, ties away), lo exact in fp32.
 __global__ void split_tf32_kernel(const float* __restrict__ x, size_t n, float* __restrict__ hi,
                                   float* __restrict__ lo) {
@@ -441,8 +719,11 @@ inline bool m2l_tc_available() {
 
 // Host side: tiles/items, split operators, TMA descriptors.
 struct M2LTcPlan {
-  bool pair = true;  // 2-CTA (cta_group::2) kernel; KIFMM_TC_PAIR=0 selects the 1-CTA kernel
+  bool pair = false;  // 1-CTA kernel by default; KIFMM_TC_PAIR=1 selects the 2-CTA (cta_group::2) kernel
   int rows = 256;    // output rows per tile
+  int rowb = 128;    // bytes per operand row per stage (128: SWIZZLE_128B, 64: SWIZZLE_64B)
+  bool a_tmem = false;  // A operand in SMEM (default) or TMEM (KIFMM_TC_AMODE=tmem; measured slower)
+  CUtensorMap tm_bhi64{}, tm_blo64{};
   int n_items = 0, n_tiles = 0, n_segs = 0;
   size_t nn = 0;
   float *d_khi = nullptr, *d_klo = nullptr, *d_mhi = nullptr, *d_mlo = nullptr, *d_partial = nullptr;
@@ -478,13 +759,14 @@ struct M2LTcPlan {
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-  static void encode(EncodeFn fn, CUtensorMap* m, float* base, uint64_t rows_total, uint32_t box_rows) {
+  static void encode(EncodeFn fn, CUtensorMap* m, float* base, uint64_t rows_total, uint32_t box_rows, int rowb) {
     const cuuint64_t dims[2] = {cuuint64_t(tc::NP), cuuint64_t(rows_total)};
     const cuuint64_t strides[1] = {cuuint64_t(tc::NP) * sizeof(float)};
-    const cuuint32_t box[2] = {cuuint32_t(tc::KB), box_rows};
+    const cuuint32_t box[2] = {cuuint32_t(rowb / 4), box_rows};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          rowb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw DeviceError(KIFMM_E_CUDA, "cuTensorMapEncodeTiled failed");
   }
@@ -522,11 +804,12 @@ struct M2LTcPlan {
     n_tiles = int(tile_seg.size()) - 1;
     n_segs = int(seg_mat.size());
     slots = int64_t(n_segs) * rows;
-    // ---- items: split each tile's taps into balanced chunks (~4 per SM or SM pair)
+    // ---- items: split each tile's taps into balanced chunks (~8 per SM or SM pair; measured best at
+    //      config 2 among 2/4/8/16 per SM)
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int64_t target_items = int64_t(4) * (pair ? sms / 2 : sms);
-    int chunk = int(std::max<int64_t>(16, (n_segs + target_items - 1) / std::max<int64_t>(1, target_items)));
+    const int64_t target_items = int64_t(8) * (pair ? sms / 2 : sms);
+    int chunk = int(std::max<int64_t>(8, (n_segs + target_items - 1) / std::max<int64_t>(1, target_items)));
     if (const char* e = std::getenv("KIFMM_TC_CHUNK")) chunk = std::max(1, std::atoi(e));
     std::vector<tc::Item> items;
     std::vector<int> tile_slot{0};
@@ -575,22 +858,31 @@ struct M2LTcPlan {
     cudaDriverEntryPointQueryResult q;
     KIFMM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
     if (!fn) throw DeviceError(KIFMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-    const uint32_t brow = uint32_t(pair ? tc::Cfg<true>::NB : tc::Cfg<false>::NB);
-    encode(reinterpret_cast<EncodeFn>(fn), &tm_khi, d_khi, uint64_t(nt) * tc::NP, brow);
-    encode(reinterpret_cast<EncodeFn>(fn), &tm_klo, d_klo, uint64_t(nt) * tc::NP, brow);
-    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::Cfg<false>::SMEM_BYTES));
-    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::Cfg<true>::SMEM_BYTES));
+    if (const char* e = std::getenv("KIFMM_TC_ROWB")) rowb = std::atoi(e) == 64 ? 64 : 128;
+    const uint32_t brow = uint32_t(pair ? tc::NP / 2 : tc::NP);
+    encode(reinterpret_cast<EncodeFn>(fn), &tm_khi, d_khi, uint64_t(nt) * tc::NP, brow, rowb);
+    encode(reinterpret_cast<EncodeFn>(fn), &tm_klo, d_klo, uint64_t(nt) * tc::NP, brow, rowb);
+    set_smem<false, 128>();
+    set_smem<true, 128>();
+    set_smem<false, 64>();
+    set_smem<true, 64>();
+    if (const char* e = std::getenv("KIFMM_TC_AMODE")) a_tmem = std::string(e) == "tmem";
+    encode(reinterpret_cast<EncodeFn>(fn), &tm_bhi64, d_khi, uint64_t(nt) * tc::NP, brow, 64);
+    encode(reinterpret_cast<EncodeFn>(fn), &tm_blo64, d_klo, uint64_t(nt) * tc::NP, brow, 64);
+    KIFMM_CUDA(cudaFuncSetAttribute(tc::ta::m2l_ta_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::ta::Cfg<false>::SMEM_BYTES));
+    KIFMM_CUDA(cudaFuncSetAttribute(tc::ta::m2l_ta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::ta::Cfg<true>::SMEM_BYTES));
   }
 
-  // check += M2L(M): split M, run the tcgen05 items, reduce partials.
-  void launch(const float* M, float* check, int np, cudaStream_t s) {
-    if (!n_items) return;
-    const size_t n = nn * size_t(np);
-    tc::split_tf32_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(M, n, d_mhi, d_mlo);
-    KIFMM_LAUNCH_CHECK();
-    if (pair) {
+  template <bool P, int R>
+  static void set_smem() {
+    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<P, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::Cfg<P, R>::SMEM_BYTES));
+  }
+  template <bool P, int R>
+  void run_kernel(cudaStream_t s) {
+    if (P) {
       cudaLaunchConfig_t cfg{};
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -599,18 +891,58 @@ struct M2LTcPlan {
       attr[0].val.clusterDim.z = 1;
       cfg.gridDim = dim3(2 * n_items);
       cfg.blockDim = dim3(tc::THREADS);
-      cfg.dynamicSmemBytes = tc::Cfg<true>::SMEM_BYTES;
+      cfg.dynamicSmemBytes = tc::Cfg<P, R>::SMEM_BYTES;
       cfg.stream = s;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<true>, tm_khi, tm_klo, (const float*)d_mhi,
+      KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<P, R>, tm_khi, tm_klo, (const float*)d_mhi,
                                     (const float*)d_mlo, (const tc::Item*)d_items, (const int*)d_seg_mat,
                                     (const int*)d_seg_in, int(nn), d_partial));
     } else {
-      tc::m2l_tc_kernel<false><<<n_items, tc::THREADS, tc::Cfg<false>::SMEM_BYTES, s>>>(
+      tc::m2l_tc_kernel<P, R><<<n_items, tc::THREADS, tc::Cfg<P, R>::SMEM_BYTES, s>>>(
           tm_khi, tm_klo, d_mhi, d_mlo, d_items, d_seg_mat, d_seg_in, int(nn), d_partial);
     }
     KIFMM_LAUNCH_CHECK();
+  }
+
+  template <bool P>
+  void run_ta(const float* M, cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((P ? 2 : 1) * n_items);
+    cfg.blockDim = dim3(tc::THREADS);
+    cfg.dynamicSmemBytes = tc::ta::Cfg<P>::SMEM_BYTES;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::ta::m2l_ta_kernel<P>, tm_bhi64, tm_blo64, M, (const tc::Item*)d_items,
+                                  (const int*)d_seg_mat, (const int*)d_seg_in, d_partial));
+  }
+
+  // check += M2L(M): run the tcgen05 items, reduce partials.
+  void launch(const float* M, float* check, int np, cudaStream_t s) {
+    if (!n_items) return;
+    if (a_tmem) {
+      if (pair)
+        run_ta<true>(M, s);
+      else
+        run_ta<false>(M, s);
+      KIFMM_LAUNCH_CHECK();
+      tc::m2l_tc_reduce_kernel<<<n_tiles, 256, 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
+      KIFMM_LAUNCH_CHECK();
+      return;
+    }
+    const size_t n = nn * size_t(np);
+    tc::split_tf32_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(M, n, d_mhi, d_mlo);
+    KIFMM_LAUNCH_CHECK();
+    if (pair && rowb == 64) run_kernel<true, 64>(s);
+    else if (pair) run_kernel<true, 128>(s);
+    else if (rowb == 64) run_kernel<false, 64>(s);
+    else run_kernel<false, 128>(s);
     tc::m2l_tc_reduce_kernel<<<n_tiles, 256, 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
     KIFMM_LAUNCH_CHECK();
   }

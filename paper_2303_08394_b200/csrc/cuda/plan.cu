@@ -207,6 +207,22 @@ __global__ void m2m_reduce_kernel(const T* __restrict__ scratch, const int* __re
   }
 }
 
+// Y[out(r)] += sum over a tile's pieces (fixed order) of partial[slot][r]   (rows x ld per piece)
+template <class T>
+__global__ void reduce_partials_kernel(const T* __restrict__ partial, const int* __restrict__ tile_out,
+                                       const int* __restrict__ tile_slot, int rows, int ld, T* __restrict__ Y) {
+  const int tile = blockIdx.x;
+  const int s0 = tile_slot[tile], s1 = tile_slot[tile + 1];
+  for (int idx = threadIdx.x; idx < rows * ld; idx += blockDim.x) {
+    const int r = idx / ld, col = idx % ld;
+    const int out = tile_out[size_t(tile) * rows + r];
+    if (out < 0) continue;
+    T acc = Y[size_t(out) * ld + col];
+    for (int sl = s0; sl < s1; ++sl) acc += partial[(size_t(sl) * rows + r) * ld + col];
+    Y[size_t(out) * ld + col] = acc;
+  }
+}
+
 struct LeafPlan {
   DevMem works, rounds, items;
   int n = 0;
@@ -256,6 +272,8 @@ struct kifmm_gpu_plan {
   std::vector<std::unique_ptr<M2MLevel>> m2m_levels, m2m_top;
   std::vector<std::unique_ptr<GemmTiles>> l2l_levels;
   DevMem m2m_scratch;
+  DevMem m2l_red_out, m2l_red_slot, m2l_partial;
+  int m2l_red_tiles = 0;
   int64_t m2m_scratch_rows = 0;
   M2LTcPlan m2l_tc;
   // exchange
@@ -597,6 +615,15 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       info.m2l_pairs += t.v_ptr[n + 1] - t.v_ptr[n];
     }
     for (auto& kv : groups) m2l_groups.push_back(kv.second);
+  }
+  m2l_backend = 1;
+  if (o.m2l_backend == 2 || (o.m2l_backend == 0 && precision == 32 && np == tc::NP && m2l_tc_available())) {
+    if (precision != 32) throw InvalidArgument("gpu: tcgen05 3xTF32 M2L is an fp32 path");
+    m2l_tc.build(t, m2l_groups, np, ops, &dev_bytes);
+    m2l_backend = 2;
+    info.m2l_padded_pairs = m2l_tc.slots;
+  }
+  if (m2l_backend == 1) {
     std::vector<TileSpec> tiles;
     for (auto& grp : m2l_groups) {
       for (size_t s0 = 0; s0 < grp.size(); s0 += bm_m2l) {
@@ -616,17 +643,39 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
         tiles.push_back(std::move(ts));
       }
     }
-    // most expensive tiles first (better tail on the block scheduler)
-    std::stable_sort(tiles.begin(), tiles.end(),
+    // split each tile's taps into pieces (~8 per SM-slot in total) so small trees still fill the GPU;
+    // piece partials land in scratch rows and are summed per tile in fixed order (m2l_reduce)
+    int64_t total_segs = 0;
+    for (auto& ts : tiles) total_segs += int64_t(ts.segs.size());
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int64_t chunk = std::max<int64_t>(8, (total_segs + 16 * sms - 1) / (16 * sms));
+    std::vector<TileSpec> pieces;
+    std::vector<int> red_out, red_slot{0};
+    for (auto& ts : tiles) {
+      const int64_t ns = int64_t(ts.segs.size());
+      const int64_t np_ = std::max<int64_t>(1, (ns + chunk - 1) / chunk);
+      for (int64_t pc = 0; pc < np_; ++pc) {
+        TileSpec piece;
+        const int64_t a = ns * pc / np_, b = ns * (pc + 1) / np_;
+        const int slot = int(pieces.size());
+        piece.out.resize(bm_m2l);
+        for (int r = 0; r < bm_m2l; ++r) piece.out[r] = slot * bm_m2l + r;
+        piece.segs.assign(ts.segs.begin() + a, ts.segs.begin() + b);
+        pieces.push_back(std::move(piece));
+      }
+      red_out.insert(red_out.end(), ts.out.begin(), ts.out.end());
+      red_slot.push_back(int(pieces.size()));
+    }
+    // most expensive pieces first (better tail on the block scheduler); slots keep the reduction order
+    std::stable_sort(pieces.begin(), pieces.end(),
                      [](const TileSpec& x, const TileSpec& y) { return x.segs.size() > y.segs.size(); });
-    m2l.build(tiles, bm_m2l, &dev_bytes);
+    m2l.build(pieces, bm_m2l, &dev_bytes);
+    m2l_red_tiles = int(tiles.size());
+    m2l_red_out.upload(red_out, &dev_bytes);
+    m2l_red_slot.upload(red_slot, &dev_bytes);
+    m2l_partial.alloc(std::max<size_t>(1, pieces.size()) * bm_m2l * np * esz(), &dev_bytes);
     info.m2l_padded_pairs = m2l.slots;
-  }
-  m2l_backend = 1;
-  if (o.m2l_backend == 2 || (o.m2l_backend == 0 && precision == 32 && np == tc::NP && m2l_tc_available())) {
-    if (precision != 32) throw InvalidArgument("gpu: tcgen05 3xTF32 M2L is an fp32 path");
-    m2l_tc.build(t, m2l_groups, np, ops, &dev_bytes);
-    m2l_backend = 2;
   }
 
   // ---- downward solves over active nodes at level >= 2 (slots -> tmp rows)
@@ -917,7 +966,13 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
       launches += m2l_tc.launches();
     }
   } else {
-    gemm(m2l, Mp, w_m2l.as<T>(), check_dn.as<T>(), true, true);
+    gemm(m2l, Mp, w_m2l.as<T>(), m2l_partial.as<T>(), false, true);
+    if (m2l_red_tiles) {
+      reduce_partials_kernel<T><<<m2l_red_tiles, 256, 0, s>>>(m2l_partial.as<T>(), m2l_red_out.as<int>(),
+                                                             m2l_red_slot.as<int>(), 64, np, check_dn.as<T>());
+      KIFMM_LAUNCH_CHECK();
+      ++launches;
+    }
   }
   mark();  // 5
   // factored downward solve (dc2e at the reference level; M2L/P2L level factors folded)
