@@ -466,9 +466,8 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   KIFMM_CUDA(cudaMemset(L.p, 0, L.bytes));
   check_dn.alloc(size_t(nn) * np * es, &dev_bytes);
 
-  const int bm_big = precision == 32 ? 128 : 64;
   const int bm_m2l = 64;
-  const int ld_tiles = bm_big;
+  const int ld_tiles = 64;  // solves / L2L: 64-row tiles (2 CTAs per SM; these GEMMs have K = 160 only)
 
   // ---- P2M: one check work per owned leaf, solve rows = slots
   {
@@ -885,7 +884,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     a.ldy = np;
     a.accumulate = acc ? 1 : 0;
     if (m2l_shape)
-      launch_gemm<T, 64, 4>(np, tl, a, s);
+      launch_gemm<T, 64, (sizeof(T) == 8 ? 8 : 4)>(np, tl, a, s);
     else
       launch_gemm<T, BMB, TMB>(np, tl, a, s);
     ++launches;
@@ -930,8 +929,8 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     KIFMM_LAUNCH_CHECK();
     ++launches;
   }
-  gemm(solve_up1, check_up.as<T>(), w_us_u.as<T>(), tmp.as<T>(), false, false);
-  gemm(solve_up2, tmp.as<T>(), w_vt_u.as<T>(), Mp, false, false);
+  gemm(solve_up1, check_up.as<T>(), w_us_u.as<T>(), tmp.as<T>(), false, true);
+  gemm(solve_up2, tmp.as<T>(), w_vt_u.as<T>(), Mp, false, true);
   mark();  // 1
   // M2M, levels d-1 .. floor
   auto m2m_level = [&](const M2MLevel& lv) {
@@ -976,11 +975,11 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   }
   mark();  // 5
   // factored downward solve (dc2e at the reference level; M2L/P2L level factors folded)
-  gemm(solve_dn1, check_dn.as<T>(), w_us_d.as<T>(), tmp.as<T>(), false, false);
-  gemm(solve_dn2, tmp.as<T>(), w_vt_d.as<T>(), Lp, false, false);
+  gemm(solve_dn1, check_dn.as<T>(), w_us_d.as<T>(), tmp.as<T>(), false, true);
+  gemm(solve_dn2, tmp.as<T>(), w_vt_d.as<T>(), Lp, false, true);
   mark();  // 6
   // L2L top-down
-  for (auto& lv : l2l_levels) gemm(*lv, Lp, w_l2l.as<T>(), Lp, true, false);
+  for (auto& lv : l2l_levels) gemm(*lv, Lp, w_l2l.as<T>(), Lp, true, true);
   mark();  // 7
   // leaves: near field (side stream, or here when timed) then L2P + M2P
   if (timed) leaf(leaf_near, false, s);
