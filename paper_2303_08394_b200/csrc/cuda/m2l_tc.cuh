@@ -32,6 +32,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -58,9 +59,9 @@ constexpr uint32_t TMEM_COLS = 512;  // two 160-column accumulators at 0 and 256
 
 // ROWB: bytes of one operand row per stage (K block of ROWB/4 fp32): 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B,
 // twice the stages for the same shared memory => deeper latency hiding).
-template <bool PAIR, int ROWB>
+template <bool PAIR, int ROWB, int ES = 4>
 struct Cfg {
-  static constexpr int KB = ROWB / 4;            // fp32 per K block
+  static constexpr int KB = ROWB / ES;           // operand elements per K block (tf32: 4 B, f16: 2 B)
   static constexpr int NKB = NP / KB;            // K blocks per tap
   static constexpr int NB = PAIR ? NP / 2 : NP;  // B rows held per CTA
   static constexpr int A_BYTES = BM * ROWB;
@@ -72,7 +73,8 @@ struct Cfg {
   static constexpr uint64_t LAYOUT = ROWB == 128 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B
   static constexpr int CTAS = PAIR ? 2 : 1;
   static constexpr uint32_t TX = uint32_t(CTAS * 2 * B_BYTES);  // TMA bytes landing on the leader per stage
-  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
+  static constexpr uint32_t FMT = ES == 4 ? 2u : 0u;  // tf32 / f16
+  static constexpr uint32_t IDESC = (1u << 4) | (FMT << 7) | (FMT << 10) | (uint32_t(NP >> 3) << 17) |
                                     (uint32_t((CTAS * BM) >> 4) << 24);
 };
 
@@ -136,18 +138,29 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
   return d;
 }
 
-template <bool PAIR>
+template <bool PAIR, int ES = 4>
 __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
-  if constexpr (PAIR)
+  constexpr uint32_t idesc = Cfg<PAIR, 128, ES>::IDESC;
+  if constexpr (PAIR && ES == 4)
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(Cfg<PAIR, 128>::IDESC), "r"(accumulate));
-  else
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  else if constexpr (ES == 4)
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(Cfg<PAIR, 128>::IDESC), "r"(accumulate));
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  else if constexpr (PAIR)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 // tcgen05.commit: arrive on `bar` (in both CTAs of the pair when PAIR) once prior MMAs complete
 template <bool PAIR>
@@ -193,13 +206,13 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
-template <bool PAIR, int ROWB>
+template <bool PAIR, int ROWB, int ES>
 __global__ void __launch_bounds__(THREADS, 1)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tm_khi, const __grid_constant__ CUtensorMap tm_klo,
-                  const float* __restrict__ m_hi, const float* __restrict__ m_lo, const Item* __restrict__ items,
+                  const void* __restrict__ m_hi, const void* __restrict__ m_lo, const Item* __restrict__ items,
                   const int* __restrict__ seg_mat, const int* __restrict__ seg_in, int zero_row,
-                  float* __restrict__ partial) {
-  using C = Cfg<PAIR, ROWB>;
+                  const float* __restrict__ row_unscale, float k_unscale, float* __restrict__ partial) {
+  using C = Cfg<PAIR, ROWB, ES>;
   constexpr int KB = C::KB, NKB = C::NKB;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem =
@@ -288,12 +301,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(full(s), round & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-          for (int k = 0; k < KB / 8; ++k) {  // K = 8 tf32 = 32 bytes per MMA
+          for (int k = 0; k < ROWB / 32; ++k) {  // 32 bytes of K per MMA (8 tf32 / 16 f16)
             const uint64_t dah = make_desc<ROWB>(a_hi(s) + 32 * k), dal = make_desc<ROWB>(a_lo(s) + 32 * k);
             const uint64_t dbh = make_desc<ROWB>(b_hi(s) + 32 * k), dbl = make_desc<ROWB>(b_lo(s) + 32 * k);
-            mma<PAIR>(d, dah, dbh, (kb > 0 || k > 0) ? 1u : 0u);
-            mma<PAIR>(d, dah, dbl, 1u);
-            mma<PAIR>(d, dal, dbh, 1u);
+            mma<PAIR, ES>(d, dah, dbh, (kb > 0 || k > 0) ? 1u : 0u);
+            mma<PAIR, ES>(d, dah, dbl, 1u);
+            mma<PAIR, ES>(d, dal, dbh, 1u);
           }
           commit<PAIR>(empty(s));
         }
@@ -332,11 +345,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int sw = ROWB == 128 ? (r & 7) : ((r & 7) >> 1);  // Swizzle<3,4,3> / Swizzle<2,4,3>
         const uint32_t off = uint32_t((r >> 3) * C::ATOM + (r & 7) * ROWB + ((c ^ sw) << 4));
         const bool ok = src[j] >= 0;  // absent source: zero-fill, no global read
-        const size_t g = size_t(ok ? src[j] : zero_row) * NP + kb * KB + c * 4;
+        const size_t g = size_t(ok ? src[j] : zero_row) * NP * ES + kb * ROWB + c * 16;  // bytes
         const int sz = ok ? 16 : 0;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_hi(s) + off), "l"(m_hi + g), "r"(sz)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_hi(s) + off),
+                     "l"(static_cast<const char*>(m_hi) + g), "r"(sz)
                      : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_lo(s) + off), "l"(m_lo + g), "r"(sz)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_lo(s) + off),
+                     "l"(static_cast<const char*>(m_lo) + g), "r"(sz)
                      : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -368,6 +383,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int k = 0; k < EPI_COLS; ++k) acc[k] = 0.f;
     for (int j = 0; j < ntap; ++j) {
       const int b = j & 1;
+      float f = 1.f;  // f16 kind: undo the per-row (source) and K_t power-of-two scalings
+      if constexpr (ES == 2) {
+        const int sr = seg_in[size_t(it.seg_begin + j) * rows + rank * BM + row];
+        f = sr < 0 ? 0.f : row_unscale[sr] * k_unscale;
+      }
       mbar_wait(tfull(b), (j >> 1) & 1);
       __syncwarp();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -382,7 +402,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             : "r"(taddr + uint32_t(cb * 16)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int k = 0; k < 16; ++k) acc[cb * 16 + k] += __uint_as_float(v[k]);
+        for (int k = 0; k < 16; ++k) acc[cb * 16 + k] = fmaf(__uint_as_float(v[k]), f, acc[cb * 16 + k]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -692,6 +712,38 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, size_t n, float* 
   lo[i] = v - hv;
 }
 
+// Per multipole row: scale by 2^e so max|row| lands in [2^9, 2^10) (far inside the fp16 range), split
+// x*2^e = hi + lo in fp16 (round to nearest), and record 2^-e.  One warp per row; row nn (zero) included.
+__global__ void split_f16_rows_kernel(const float* __restrict__ M, int nn, __half* __restrict__ hi,
+                                      __half* __restrict__ lo, float* __restrict__ unscale) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row > nn) return;
+  float v[NP / 32];
+  float mx = 0.f;
+#pragma unroll
+  for (int k = 0; k < NP / 32; ++k) {
+    v[k] = row < nn ? M[size_t(row) * NP + lane + 32 * k] : 0.f;
+    mx = fmaxf(mx, fabsf(v[k]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int e = 0;
+  if (mx > 0.f) {
+    int ex;
+    frexpf(mx, &ex);  // mx in [2^(ex-1), 2^ex)
+    e = 10 - ex;
+  }
+  const float sc = ldexpf(1.f, e);
+#pragma unroll
+  for (int k = 0; k < NP / 32; ++k) {
+    const float x = v[k] * sc;
+    const __half h = __float2half_rn(x);
+    hi[size_t(row) * NP + lane + 32 * k] = h;
+    lo[size_t(row) * NP + lane + 32 * k] = __float2half_rn(x - __half2float(h));
+  }
+  if (lane == 0) unscale[row] = ldexpf(1.f, -e);
+}
+
 // check[out(r)] += sum over the tile's items (fixed order) of partial[slot][r]
 __global__ void m2l_tc_reduce_kernel(const float* __restrict__ partial, const int* __restrict__ tile_out,
                                      const int* __restrict__ tile_slot, int rows, float* __restrict__ check) {
@@ -724,6 +776,11 @@ struct M2LTcPlan {
   int rowb = 128;    // bytes per operand row per stage (128: SWIZZLE_128B, 64: SWIZZLE_64B)
   bool a_tmem = false;  // A operand in SMEM (default) or TMEM (KIFMM_TC_AMODE=tmem; measured slower)
   CUtensorMap tm_bhi64{}, tm_blo64{};
+  bool f16 = true;  // 3-term fp16 split (kind::f16) with power-of-two row scaling; KIFMM_TC_KIND=tf32 for 3xTF32
+  static constexpr float kKScale = 256.f;
+  __half *d_khi16 = nullptr, *d_klo16 = nullptr, *d_mhi16 = nullptr, *d_mlo16 = nullptr;
+  float* d_unscale = nullptr;
+  CUtensorMap tm_khi16{}, tm_klo16{};
   int n_items = 0, n_tiles = 0, n_segs = 0;
   size_t nn = 0;
   float *d_khi = nullptr, *d_klo = nullptr, *d_mhi = nullptr, *d_mlo = nullptr, *d_partial = nullptr;
@@ -734,7 +791,8 @@ struct M2LTcPlan {
 
   ~M2LTcPlan() {
     for (void* p : {(void*)d_khi, (void*)d_klo, (void*)d_mhi, (void*)d_mlo, (void*)d_partial, (void*)d_tile_out,
-                    (void*)d_tile_slot, (void*)d_seg_mat, (void*)d_seg_in, (void*)d_items})
+                    (void*)d_tile_slot, (void*)d_seg_mat, (void*)d_seg_in, (void*)d_items, (void*)d_khi16,
+                    (void*)d_klo16, (void*)d_mhi16, (void*)d_mlo16, (void*)d_unscale})
       if (p) cudaFree(p);
   }
   int launches() const { return n_items ? 3 : 0; }
@@ -759,12 +817,14 @@ struct M2LTcPlan {
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-  static void encode(EncodeFn fn, CUtensorMap* m, float* base, uint64_t rows_total, uint32_t box_rows, int rowb) {
+  static void encode(EncodeFn fn, CUtensorMap* m, void* base, uint64_t rows_total, uint32_t box_rows, int rowb,
+                     int es = 4) {
     const cuuint64_t dims[2] = {cuuint64_t(tc::NP), cuuint64_t(rows_total)};
-    const cuuint64_t strides[1] = {cuuint64_t(tc::NP) * sizeof(float)};
-    const cuuint32_t box[2] = {cuuint32_t(rowb / 4), box_rows};
+    const cuuint64_t strides[1] = {cuuint64_t(tc::NP) * es};
+    const cuuint32_t box[2] = {cuuint32_t(rowb / es), box_rows};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+    const CUresult r = fn(m, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base,
+                          dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE,
                           rowb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -873,15 +933,44 @@ struct M2LTcPlan {
                                     tc::ta::Cfg<false>::SMEM_BYTES));
     KIFMM_CUDA(cudaFuncSetAttribute(tc::ta::m2l_ta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     tc::ta::Cfg<true>::SMEM_BYTES));
+    // ---- f16 kind: K_t * 2^8 split into fp16 hi/lo; multipoles split per row with a power-of-two scale
+    if (const char* e = std::getenv("KIFMM_TC_KIND")) f16 = std::string(e) != "tf32";
+    if (f16) {
+      std::vector<__half> h16(khi.size()), l16(khi.size());
+      for (size_t i = 0; i < khi.size(); ++i) {
+        const float x = (khi[i] + klo[i]) * kKScale;  // (hi + lo) == the fp32 K_t value exactly
+        const __half h = __float2half_rn(x);
+        h16[i] = h;
+        l16[i] = __float2half_rn(x - __half2float(h));
+      }
+      up(&d_khi16, h16, total);
+      up(&d_klo16, l16, total);
+      KIFMM_CUDA(cudaMalloc(&d_mhi16, (nn + 1) * tc::NP * sizeof(__half)));
+      KIFMM_CUDA(cudaMalloc(&d_mlo16, (nn + 1) * tc::NP * sizeof(__half)));
+      KIFMM_CUDA(cudaMalloc(&d_unscale, (nn + 1) * sizeof(float)));
+      *total += 2 * (nn + 1) * tc::NP * sizeof(__half) + (nn + 1) * sizeof(float);
+      encode(reinterpret_cast<EncodeFn>(fn), &tm_khi16, d_khi16, uint64_t(nt) * tc::NP, brow, 64, 2);
+      encode(reinterpret_cast<EncodeFn>(fn), &tm_klo16, d_klo16, uint64_t(nt) * tc::NP, brow, 64, 2);
+      KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<false, 64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      tc::Cfg<false, 64, 2>::SMEM_BYTES));
+      KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<true, 64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      tc::Cfg<true, 64, 2>::SMEM_BYTES));
+    }
   }
 
   template <bool P, int R>
   static void set_smem() {
-    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<P, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::Cfg<P, R>::SMEM_BYTES));
+    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<P, R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::Cfg<P, R, 4>::SMEM_BYTES));
   }
-  template <bool P, int R>
+  template <bool P, int R, int ES = 4>
   void run_kernel(cudaStream_t s) {
+    const CUtensorMap& mh = ES == 4 ? tm_khi : tm_khi16;
+    const CUtensorMap& ml = ES == 4 ? tm_klo : tm_klo16;
+    const void* ah = ES == 4 ? static_cast<const void*>(d_mhi) : static_cast<const void*>(d_mhi16);
+    const void* al = ES == 4 ? static_cast<const void*>(d_mlo) : static_cast<const void*>(d_mlo16);
+    const float* un = ES == 4 ? nullptr : d_unscale;
+    const float ku = ES == 4 ? 1.f : 1.f / kKScale;
     if (P) {
       cudaLaunchConfig_t cfg{};
       cudaLaunchAttribute attr[1];
@@ -891,16 +980,15 @@ struct M2LTcPlan {
       attr[0].val.clusterDim.z = 1;
       cfg.gridDim = dim3(2 * n_items);
       cfg.blockDim = dim3(tc::THREADS);
-      cfg.dynamicSmemBytes = tc::Cfg<P, R>::SMEM_BYTES;
+      cfg.dynamicSmemBytes = tc::Cfg<P, R, ES>::SMEM_BYTES;
       cfg.stream = s;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<P, R>, tm_khi, tm_klo, (const float*)d_mhi,
-                                    (const float*)d_mlo, (const tc::Item*)d_items, (const int*)d_seg_mat,
-                                    (const int*)d_seg_in, int(nn), d_partial));
+      KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<P, R, ES>, mh, ml, ah, al, (const tc::Item*)d_items,
+                                    (const int*)d_seg_mat, (const int*)d_seg_in, int(nn), un, ku, d_partial));
     } else {
-      tc::m2l_tc_kernel<P, R><<<n_items, tc::THREADS, tc::Cfg<P, R>::SMEM_BYTES, s>>>(
-          tm_khi, tm_klo, d_mhi, d_mlo, d_items, d_seg_mat, d_seg_in, int(nn), d_partial);
+      tc::m2l_tc_kernel<P, R, ES><<<n_items, tc::THREADS, tc::Cfg<P, R, ES>::SMEM_BYTES, s>>>(
+          mh, ml, ah, al, d_items, d_seg_mat, d_seg_in, int(nn), un, ku, d_partial);
     }
     KIFMM_LAUNCH_CHECK();
   }
@@ -932,6 +1020,17 @@ struct M2LTcPlan {
       else
         run_ta<false>(M, s);
       KIFMM_LAUNCH_CHECK();
+      tc::m2l_tc_reduce_kernel<<<n_tiles, 256, 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
+      KIFMM_LAUNCH_CHECK();
+      return;
+    }
+    if (f16) {
+      tc::split_f16_rows_kernel<<<unsigned((nn + 7) / 8), 256, 0, s>>>(M, int(nn), d_mhi16, d_mlo16, d_unscale);
+      KIFMM_LAUNCH_CHECK();
+      if (pair)
+        run_kernel<true, 64, 2>(s);
+      else
+        run_kernel<false, 64, 2>(s);
       tc::m2l_tc_reduce_kernel<<<n_tiles, 256, 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
       KIFMM_LAUNCH_CHECK();
       return;
