@@ -310,9 +310,14 @@ def main():
     m2l_s = ph["m2l_ms"] * 1e-3
     achieved = m2l_flops / m2l_s / 1e12 if m2l_s > 0 else 0.0
     if info["m2l_backend"] == 2:
+        bf16 = peaks.get("bf16_tflops", 1590.0)
+        peak, bound, src = bf16 / 3.0, "tensor", ("measured dense bf16 (= fp16 kind::f16 rate) / 3: the 3-term "
+                                                  "fp16 split issues 3 MMAs per useful MAC; " +
+                                                  ("of measured" if peaks else "of fallback"))
+    elif info["m2l_backend"] == 3:
         tf32 = peaks.get("bf16_tflops", 1590.0) / 2.0
         peak, bound, src = tf32 / 3.0, "tensor", ("measured bf16/2 (TF32) / 3 (3xTF32 issues 3 MMAs per "
-                                                  "useful MAC), of measured" if peaks else "of fallback")
+                                                  "useful MAC), " + ("of measured" if peaks else "of fallback"))
     else:
         fp32 = fmm.fma_peak(32, local) / 1e12
         peak, bound, src = fp32, "tensor", ("FP32 SIMT kernel: peak = FFMA throughput measured in this run "
@@ -320,7 +325,7 @@ def main():
                                             "compute roof, not tensor cores")
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak if peak else None, "traffic": ncu_traffic("m2l"),
-            "kernel": "M2L (gather_gemm_kernel)" if info["m2l_backend"] != 2 else "M2L (m2l_tc_kernel)",
+            "kernel": "M2L (gather_gemm_kernel)" if info["m2l_backend"] == 1 else "M2L (m2l_tc_kernel)",
             "peak_source": src,
             "work": f"2*n_e*n_c flop per V pair x {info['m2l_pairs']} V pairs per launch",
             "m2l_ms": ph["m2l_ms"]}
@@ -346,7 +351,7 @@ def main():
                                f"{f.tree.n_leaves} leaves",
                    "parallelism": f"morton-range x{world}" if world > 1 else "single-gpu",
                    "l2": "flushed (256 MiB write) between timed steps",
-                   "m2l_backend": {1: "simt", 2: "tcgen05-3xtf32"}.get(info["m2l_backend"])},
+                   "m2l_backend": {1: "simt", 2: "tcgen05-f16x3", 3: "tcgen05-3xtf32"}.get(info["m2l_backend"])},
         "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(info["kernel_launches"]) * args.steps,
         "roofline": roof, "p2p": p2p, "phases_ms": ph, "clocks": clk.summary(), "cpu_baseline": cpu,

@@ -745,18 +745,26 @@ __global__ void split_f16_rows_kernel(const float* __restrict__ M, int nn, __hal
 }
 
 // check[out(r)] += sum over the tile's items (fixed order) of partial[slot][r]
+// grid (tiles, rows / 16); thread = (row, float4 column group), 640 threads
 __global__ void m2l_tc_reduce_kernel(const float* __restrict__ partial, const int* __restrict__ tile_out,
                                      const int* __restrict__ tile_slot, int rows, float* __restrict__ check) {
   const int tile = blockIdx.x;
+  const int r = blockIdx.y * 16 + threadIdx.x / (NP / 4);
+  const int c4 = threadIdx.x % (NP / 4);
+  if (r >= rows) return;
+  const int out = tile_out[size_t(tile) * rows + r];
+  if (out < 0) return;
   const int s0 = tile_slot[tile], s1 = tile_slot[tile + 1];
-  for (int idx = threadIdx.x; idx < rows * NP; idx += blockDim.x) {
-    const int r = idx / NP, col = idx % NP;
-    const int out = tile_out[size_t(tile) * rows + r];
-    if (out < 0) continue;
-    float acc = check[size_t(out) * NP + col];
-    for (int s = s0; s < s1; ++s) acc += partial[(size_t(s) * rows + r) * NP + col];
-    check[size_t(out) * NP + col] = acc;
+  float4* dst = reinterpret_cast<float4*>(check + size_t(out) * NP) + c4;
+  float4 acc = *dst;
+  for (int s = s0; s < s1; ++s) {
+    const float4 v = reinterpret_cast<const float4*>(partial + (size_t(s) * rows + r) * NP)[c4];
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
   }
+  *dst = acc;
 }
 
 }  // namespace tc
@@ -1020,7 +1028,7 @@ struct M2LTcPlan {
       else
         run_ta<false>(M, s);
       KIFMM_LAUNCH_CHECK();
-      tc::m2l_tc_reduce_kernel<<<n_tiles, 256, 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
+      tc::m2l_tc_reduce_kernel<<<dim3(n_tiles, rows / 16), 16 * (tc::NP / 4), 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
       KIFMM_LAUNCH_CHECK();
       return;
     }
@@ -1031,7 +1039,7 @@ struct M2LTcPlan {
         run_kernel<true, 64, 2>(s);
       else
         run_kernel<false, 64, 2>(s);
-      tc::m2l_tc_reduce_kernel<<<n_tiles, 256, 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
+      tc::m2l_tc_reduce_kernel<<<dim3(n_tiles, rows / 16), 16 * (tc::NP / 4), 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
       KIFMM_LAUNCH_CHECK();
       return;
     }
@@ -1042,7 +1050,7 @@ struct M2LTcPlan {
     else if (pair) run_kernel<true, 128>(s);
     else if (rowb == 64) run_kernel<false, 64>(s);
     else run_kernel<false, 128>(s);
-    tc::m2l_tc_reduce_kernel<<<n_tiles, 256, 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
+    tc::m2l_tc_reduce_kernel<<<dim3(n_tiles, rows / 16), 16 * (tc::NP / 4), 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
     KIFMM_LAUNCH_CHECK();
   }
 };

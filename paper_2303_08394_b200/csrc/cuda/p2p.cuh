@@ -184,6 +184,59 @@ __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, 
   }
 }
 
+// Far field at the leaves: L2P (down-equivalent surface of the leaf, densities L)
+// and M2P (up-equivalent surfaces of the W-list nodes, densities M) -- SPEC.md:467-479.
+// One warp per leaf: lanes own targets (groups of 32), the warp stages one
+// surface (n_e points, padded to a multiple of 8 with far-away zero sources) in
+// its own shared-memory slot and every lane reads it back as broadcasts; no
+// block-wide barriers.  Adds into the potentials/gradients of the near field.
+// works: {first target, surface_begin, surface_end, target count <= 32}; surfaces: {node, kind}.
+constexpr int kFarWarps = 6;
+constexpr int kFarMaxNe = 224;
+
+template <class T, bool GRAD>
+__global__ void __launch_bounds__(kFarWarps * 32) far_kernel(P2PParams<T> p, const int4* __restrict__ works,
+                                                              int n_works, const int2* __restrict__ surfaces,
+                                                              const int64_t* __restrict__ leaf_ptr,
+                                                              const T* __restrict__ M, const T* __restrict__ L,
+                                                              T* __restrict__ pot, T* __restrict__ grad) {
+  __shared__ v4_t<T> sh[kFarWarps][kFarMaxNe];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wi = blockIdx.x * kFarWarps + warp;
+  if (wi >= n_works) return;
+  const int4 w = works[wi];
+  const int t0 = w.x, t1 = w.x + w.w;
+  const int ne8 = (p.n_e + 7) & ~7;
+  v4_t<T>* my = sh[warp];
+  {
+    const int t = t0 + lane;
+    const bool act = t < t1;
+    const v4_t<T> x = p.src[act ? t : t0];
+    T ph = 0, gx = 0, gy = 0, gz = 0;
+    for (int si = w.y; si < w.z; ++si) {
+      const int2 sf = surfaces[si];
+      const bool l2p = sf.y == kSrcL2P;
+      const T alpha = l2p ? p.alpha_outer : p.alpha_inner;
+      const T* dens = l2p ? L : M;
+      __syncwarp();
+      for (int j = lane; j < ne8; j += 32)
+        my[j] = j < p.n_e ? surface_source(p, sf.x, alpha, dens, j)
+                          : make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
+      __syncwarp();
+      p2p_round<T, GRAD, false>(my, 0, ne8, x.x, x.y, x.z, ph, gx, gy, gz);
+    }
+    if (act) {
+      const T c = T(kInv4PiD);
+      pot[t] += c * ph;
+      if (GRAD) {
+        grad[3 * size_t(t)] -= c * gx;
+        grad[3 * size_t(t) + 1] -= c * gy;
+        grad[3 * size_t(t) + 2] -= c * gz;
+      }
+    }
+  }
+}
+
 // Check potentials on a node's surface (alpha) from particle ranges: one warp
 // per work item, lane l owns check points l, l+32, ... (KMAX x 32 >= n_c); each
 // lane loads one source and the warp broadcasts it with shuffles.

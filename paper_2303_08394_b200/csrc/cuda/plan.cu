@@ -267,6 +267,8 @@ struct kifmm_gpu_plan {
   // work lists
   DevMem p2m_works, p2m_ranges, p2l_works, p2l_ranges;
   LeafPlan leaf_near, leaf_far;
+  DevMem far_works, far_surfaces, leaf_ptr_dev;
+  int n_far = 0;
   int n_p2m = 0, n_p2l = 0;
   GemmTiles solve_up1, solve_up2, solve_dn1, solve_dn2, m2l;
   std::vector<std::unique_ptr<M2MLevel>> m2m_levels, m2m_top;
@@ -619,7 +621,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   if (o.m2l_backend == 2 || (o.m2l_backend == 0 && precision == 32 && np == tc::NP && m2l_tc_available())) {
     if (precision != 32) throw InvalidArgument("gpu: tcgen05 3xTF32 M2L is an fp32 path");
     m2l_tc.build(t, m2l_groups, np, ops, &dev_bytes);
-    m2l_backend = 2;
+    m2l_backend = m2l_tc.f16 ? 2 : 3;  // 2: kind::f16 3-term split, 3: kind::tf32 3xTF32
     info.m2l_padded_pairs = m2l_tc.slots;
   }
   if (m2l_backend == 1) {
@@ -819,7 +821,32 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     lp.items.upload(items, &dev_bytes);
   };
   build_leaf_plan(true, leaf_near);
-  build_leaf_plan(false, leaf_far);
+  // far field: one warp-work per owned leaf with any L2P / M2P surface
+  {
+    std::vector<int4> fw;
+    std::vector<int2> sf;
+    for (int64_t l = lb; l < le; ++l) {
+      const int64_t node = t.leaf_node[l];
+      const int b = int(sf.size());
+      const int64_t ntl = t.leaf_ptr[l + 1] - t.leaf_ptr[l];
+      if (node_lvl(node) >= 2) {
+        sf.push_back(make_int2(int(node), kSrcL2P));
+        info.l2p_pairs += ntl * ne;
+      }
+      for (int64_t e = t.w_ptr[l]; e < t.w_ptr[l + 1]; ++e) {
+        sf.push_back(make_int2(int(t.w_idx[e]), kSrcM2P));
+        info.m2p_pairs += ntl * ne;
+      }
+      if (int(sf.size()) > b)
+        for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += 32)
+          fw.push_back(make_int4(int(t0), b, int(sf.size()), int(std::min<int64_t>(32, t.leaf_ptr[l + 1] - t0))));
+    }
+    n_far = int(fw.size());
+    far_works.upload(fw, &dev_bytes);
+    far_surfaces.upload(sf, &dev_bytes);
+    std::vector<int64_t> lp(t.leaf_ptr, t.leaf_ptr + nl + 1);
+    leaf_ptr_dev.upload(lp, &dev_bytes);
+  }
 
   info.n_particles = N;
   info.n_leaves = nl;
@@ -959,7 +986,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   }
   mark();  // 4
   // M2L over all levels at once, accumulated as reference-level check potentials
-  if (m2l_backend == 2) {
+  if (m2l_backend >= 2) {
     if constexpr (sizeof(T) == 4) {
       m2l_tc.launch(Mp, check_dn.as<float>(), np, s);
       launches += m2l_tc.launches();
@@ -984,7 +1011,18 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   // leaves: near field (side stream, or here when timed) then L2P + M2P
   if (timed) leaf(leaf_near, false, s);
   else if (leaf_near.n) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
-  leaf(leaf_far, true, s);
+  if (n_far) {
+    const int blocks = int(ceil_div(n_far, kFarWarps));
+    T* g = grad ? grad_buf.as<T>() : nullptr;
+    if (grad)
+      far_kernel<T, true><<<blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<int4>(), n_far, far_surfaces.as<int2>(),
+                                                           leaf_ptr_dev.as<int64_t>(), Mp, Lp, pot.as<T>(), g);
+    else
+      far_kernel<T, false><<<blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<int4>(), n_far, far_surfaces.as<int2>(),
+                                                            leaf_ptr_dev.as<int64_t>(), Mp, Lp, pot.as<T>(), g);
+    KIFMM_LAUNCH_CHECK();
+    ++launches;
+  }
   mark();  // 8
   if (input_order) {
     if (world > 1) {

@@ -62,13 +62,18 @@ def test_fp32_p7_accuracy_bound(require_gpu):
     assert fmm.relative_error(pot, ref) <= 5e-4
 
 
+@pytest.mark.parametrize("variant", [("f16", "0", 2), ("f16", "1", 2), ("tf32", "0", 3), ("tf32", "1", 3)],
+                         ids=["f16x3", "f16x3-2cta", "tf32x3", "tf32x3-2cta"])
 @pytest.mark.parametrize("kind,n,n_crit", [("uniform-cube", 20000, 60), ("sphere-surface", 30000, 50),
                                            ("two-cluster", 20000, 30)])
-def test_tcgen05_m2l_parity(require_gpu, kind, n, n_crit):
+def test_tcgen05_m2l_parity(require_gpu, monkeypatch, kind, n, n_crit, variant):
+    """Every tensor-core M2L variant (kind::f16 3-term split / kind::tf32 3xTF32, 1-CTA / 2-CTA pair)."""
+    monkeypatch.setenv("KIFMM_TC_KIND", variant[0])
+    monkeypatch.setenv("KIFMM_TC_PAIR", variant[1])
     pos, q = generators.sample(kind, n, seed=8, charges="signed", fp32=True)
     cfg = fmm.FmmConfig(p=6, n_crit=n_crit, precision=32, gradient=True, m2l_backend=2)
     with fmm.Fmm(pos, cfg) as f:
-        assert f.info()["m2l_backend"] == 2
+        assert f.info()["m2l_backend"] == variant[2]
         pot, grad, _ = f.evaluate(q)
         ref, gref = _ref(f, q, True)
     assert fmm.relative_error(pot, ref) <= 1e-5
