@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp >= 2 && warp < 6) {
     // ---------------- A producers: thread -> (16-byte chunk c, rows r0 + 16 j) of this CTA, cp.async
     //                  into the SW128 K-major layout; fence.proxy.async before publishing to the MMA
+    constexpr int LAG = C::STAGES - 2 > 1 ? C::STAGES - 2 : 1;  // stages in flight beyond the newest
     constexpr int CH = ROWB / 16;     // 16-byte chunks per row
     constexpr int RPI = 128 / CH;     // rows covered by the 128 producer threads per pass
     constexpr int J = BM / RPI;       // passes (rows per thread)
@@ -355,15 +356,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                      : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
-      if (i > 0) {  // the previous stage's copies are complete once <= 1 group is pending
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        publish((i - 1) % C::STAGES);
+      // keep LAG stages of gathers in flight per thread (latency hiding); publish the stage LAG behind
+      if (i >= LAG) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(LAG) : "memory");
+        publish((i - LAG) % C::STAGES);
       }
     }
-    if (nstage > 0) {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      publish((nstage - 1) % C::STAGES);
-    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    for (int i = (nstage > LAG ? nstage - LAG : 0); i < nstage; ++i) publish(i % C::STAGES);
   } else if (warp == FWD_WARP) {
     // ---------------- forwarder (pair): this CTA's A rows landed -> one arrive on the leader's stage barrier
     if (false && PAIR && lane == 0) {
