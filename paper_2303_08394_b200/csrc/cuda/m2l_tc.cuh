@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int s = 0; s < C::STAGES; ++s) {
       // full: the leader's arrive.expect_tx (B bytes of every CTA) + A arrivals: 128 producer threads
       // (single CTA) or one forwarder per CTA (pair)
-      mbar_init(full(s), PAIR ? 1 + 2 * 128 : 1 + 128);
+      mbar_init(full(s), PAIR ? 1 + 2 : 1 + 128);
       mbar_init(empty(s), 1);  // one tcgen05.commit per stage (multicast to both CTAs when PAIR)
       mbar_init(afull(s), 128);
     }
@@ -315,8 +315,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp >= 2 && warp < 6) {
     // ---------------- A producers: thread -> (16-byte chunk c, rows r0 + 16 j) of this CTA, cp.async
-    //                  into the SW128 K-major layout; fence.proxy.async before publishing to the MMA
-    constexpr int LAG = C::STAGES - 2 > 1 ? C::STAGES - 2 : 1;  // stages in flight beyond the newest
+    //                  into the swizzled K-major layout; up to STAGES stages in flight per thread
     constexpr int CH = ROWB / 16;     // 16-byte chunks per row
     constexpr int RPI = 128 / CH;     // rows covered by the 128 producer threads per pass
     constexpr int J = BM / RPI;       // passes (rows per thread)
@@ -324,13 +323,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int c = t % CH, r0 = t / CH;
     int src[J];
     int cur_seg = -1;
-    auto publish = [&](int st) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (PAIR)
-        mbar_arrive_cluster(leader(full(st)));
-      else
-        mbar_arrive_local(full(st));
-    };
     for (int i = 0; i < nstage; ++i) {
       const int s = i % C::STAGES, round = i / C::STAGES;
       const int seg = it.seg_begin + i / NKB, kb = i % NKB;
@@ -355,22 +347,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                      "l"(static_cast<const char*>(m_lo) + g), "r"(sz)
                      : "memory");
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      // keep LAG stages of gathers in flight per thread (latency hiding); publish the stage LAG behind
-      if (i >= LAG) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(LAG) : "memory");
-        publish((i - LAG) % C::STAGES);
-      }
+      // non-blocking: the barrier receives this thread's arrival when its copies have landed
+      // (as CUTLASS's cp.async UMMA mainloops do; the full barrier's count includes these arrivals)
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(PAIR ? afull(s) : full(s))
+                   : "memory");
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    for (int i = (nstage > LAG ? nstage - LAG : 0); i < nstage; ++i) publish(i % C::STAGES);
   } else if (warp == FWD_WARP) {
     // ---------------- forwarder (pair): this CTA's A rows landed -> one arrive on the leader's stage barrier
-    if (false && PAIR && lane == 0) {
+    if (PAIR && lane == 0) {
       for (int i = 0; i < nstage; ++i) {
         const int s = i % C::STAGES, round = i / C::STAGES;
         mbar_wait(afull(s), round & 1);
-        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader(full(s))) : "memory");
+        mbar_arrive_cluster(leader(full(s)));
       }
     }
   } else if (warp >= EPI_WARP0) {
@@ -779,7 +767,7 @@ inline bool m2l_tc_available() {
 
 // Host side: tiles/items, split operators, TMA descriptors.
 struct M2LTcPlan {
-  bool pair = false;  // 1-CTA kernel by default; KIFMM_TC_PAIR=1 selects the 2-CTA (cta_group::2) kernel
+  bool pair = false;  // 2-CTA (cta_group::2) kernel on large trees; KIFMM_TC_PAIR=0/1 forces the choice
   int rows = 256;    // output rows per tile
   int rowb = 128;    // bytes per operand row per stage (128: SWIZZLE_128B, 64: SWIZZLE_64B)
   bool a_tmem = false;  // A operand in SMEM (default) or TMEM (KIFMM_TC_AMODE=tmem; measured slower)
@@ -844,6 +832,7 @@ struct M2LTcPlan {
              size_t* total) {
     if (np != tc::NP) throw InvalidArgument("tcgen05 M2L: only p = 6 (n_e padded to 160) is instantiated");
     nn = size_t(t.n_nodes);
+    pair = nn >= 20000;  // 2-CTA pays off once there are enough 256-row tiles (measured at 1e5 / 1e6 points)
     if (const char* e = std::getenv("KIFMM_TC_PAIR")) pair = std::atoi(e) != 0;
     rows = pair ? 2 * tc::BM : tc::BM;
     // ---- tiles (rows same-class targets) and their tap segments
