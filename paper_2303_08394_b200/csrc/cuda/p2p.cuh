@@ -96,11 +96,149 @@ __device__ __forceinline__ void p2p_round(const v4_t<T>* sh, int begin, int end,
   gz += a_gz;
 }
 
-constexpr int kMaxSlices = 8;
+// Thread geometry of a leaf work: the scalar kernel (fp64) gives every thread
+// one target and unrolls sources by 8; the packed fp32 kernel gives every
+// thread two targets (one FP32x2 lane pair) and unrolls by 4.  Sections are
+// padded to a multiple of leaf_unroll * R so every slice gets whole unroll groups.
+__host__ __device__ inline int leaf_slices(int nt, bool packed) {
+  const int tt = packed ? (nt + 1) / 2 : nt;
+  const int mx = packed ? 16 : 8;
+  const int r = 128 / (tt > 0 ? tt : 1);
+  return r < 1 ? 1 : (r > mx ? mx : r);
+}
+__host__ __device__ inline int leaf_unroll(bool packed) { return packed ? 4 : 8; }
 
-__host__ __device__ inline int leaf_slices(int nt) {
-  const int r = 128 / (nt > 0 ? nt : 1);
-  return r < 1 ? 1 : (r > kMaxSlices ? kMaxSlices : r);
+// Packed fp32 pair-of-targets round: FP32x2 instructions whose source operand
+// is a scalar register broadcast to both lanes (ptxas folds mov.b64 {s, s}
+// into the ".F32" operand form), so the staged source stays one float4.  Per
+// source and thread: 3 FADD2 + 3 FMUL2/FFMA2 (r^2) + 2 MUFU.RSQ + 2 (potential)
+// + 5 (gradient) instructions for TWO target-source pairs.
+__device__ __forceinline__ f2_t f2_bcast(float a) { return f2_pack(a, a); }
+
+template <bool GRAD, bool MASK>
+__device__ __forceinline__ void p2p_round_f2(const float4* sh, int begin, int end, f2_t x, f2_t y, f2_t z, f2_t& ph,
+                                             f2_t& gx, f2_t& gy, f2_t& gz) {
+  f2_t a_ph = 0, a_gx = 0, a_gy = 0, a_gz = 0;  // all-zero bits == (0.f, 0.f)
+#pragma unroll 2
+  for (int j = begin; j < end; j += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4 s = sh[j + u];
+      const f2_t dx = f2_sub(x, f2_bcast(s.x)), dy = f2_sub(y, f2_bcast(s.y)), dz = f2_sub(z, f2_bcast(s.z));
+      const f2_t r2 = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+      float ra, rb;
+      f2_unpack(r2, ra, rb);
+      const f2_t ri = MASK ? f2_pack(rinv_masked(ra), rinv_masked(rb)) : f2_pack(rinv(ra), rinv(rb));
+      if (GRAD) {
+        const f2_t qr = f2_mul(f2_bcast(s.w), ri);
+        a_ph = f2_add(a_ph, qr);
+        const f2_t qr3 = f2_mul(qr, f2_mul(ri, ri));
+        a_gx = f2_fma(qr3, dx, a_gx);
+        a_gy = f2_fma(qr3, dy, a_gy);
+        a_gz = f2_fma(qr3, dz, a_gz);
+      } else {
+        a_ph = f2_fma(f2_bcast(s.w), ri, a_ph);
+      }
+    }
+  }
+  ph = f2_add(ph, a_ph);
+  if (GRAD) {
+    gx = f2_add(gx, a_gx);
+    gy = f2_add(gy, a_gy);
+    gz = f2_add(gz, a_gz);
+  }
+}
+
+// fp32 leaf_eval with two targets per thread: thread -> (slice tid / T2, target
+// pair tid % T2) with T2 = ceil(n_t / 2); the pair is (tt, tt + T2).  Same
+// staging rounds / items as leaf_eval_kernel (geometry leaf_slices(nt, true)).
+template <bool GRAD, bool ACC>
+__global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<float> p,
+                                                                       const LeafWork* __restrict__ works,
+                                                                       const int4* __restrict__ rounds,
+                                                                       const int4* __restrict__ items,
+                                                                       const float* __restrict__ M,
+                                                                       const float* __restrict__ L,
+                                                                       float* __restrict__ pot,
+                                                                       float* __restrict__ grad) {
+  __shared__ float4 sh[kP2PCap];
+  const LeafWork w = works[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nt = w.t_count, T2 = (nt + 1) >> 1;
+  const int R = leaf_slices(nt, true);
+  const int slice = tid / T2, ta = tid - slice * T2, tb = ta + T2;
+  const bool active = slice < R, has_b = active && tb < nt;
+
+  const float4 xa = p.src[w.t_begin + (active ? ta : 0)];
+  const float4 xb = p.src[w.t_begin + (has_b ? tb : 0)];
+  const f2_t x = f2_pack(xa.x, xb.x), y = f2_pack(xa.y, xb.y), z = f2_pack(xa.z, xb.z);
+  f2_t ph = 0, gx = 0, gy = 0, gz = 0;
+  const float fa = float(kFarAway);
+  auto put = [&](int i, float4 v) { sh[i] = v; };
+
+  for (int r = w.round_begin; r < w.round_end; ++r) {
+    const int4 rd = rounds[r];
+    const int S = rd.z & 0xFFFF, ns = rd.z >> 16, O = rd.w & 0xFFFF, no = rd.w >> 16;
+    for (int k = rd.x + warp; k < rd.y; k += 4) {
+      const int4 item = items[k];
+      const int kind = item.x & 0xF, j0 = item.x >> 4;
+      if (kind == kSrcParticles || kind == kSrcSelf) {
+        for (int i = lane; i < item.z; i += 32) put(item.w + i, p.src[item.y + i]);
+      } else {
+        const bool l2p = kind == kSrcL2P;
+        const float alpha = l2p ? p.alpha_outer : p.alpha_inner;
+        const float* dens = l2p ? L : M;
+        for (int i = lane; i < item.z; i += 32) put(item.w + i, surface_source(p, item.y, alpha, dens, j0 + i));
+      }
+    }
+    for (int i = ns + tid; i < S; i += kP2PThreads) put(i, make_float4(fa, fa, fa, 0.f));
+    for (int i = S + no + tid; i < S + O; i += kP2PThreads) put(i, make_float4(fa, fa, fa, 0.f));
+    __syncthreads();
+    if (active) {
+      if (S) {
+        const int per = S / R;
+        p2p_round_f2<GRAD, true>(sh, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
+      }
+      if (O) {
+        const int per = O / R;
+        p2p_round_f2<GRAD, false>(sh, S + slice * per, S + slice * per + per, x, y, z, ph, gx, gy, gz);
+      }
+    }
+    __syncthreads();
+  }
+
+  float* red = reinterpret_cast<float*>(sh);  // [slice][component][n_t]: R * n_t <= 256
+  constexpr int NC = GRAD ? 4 : 1;
+  if (active) {
+    float a[4], b[4];
+    f2_unpack(ph, a[0], b[0]);
+    f2_unpack(gx, a[1], b[1]);
+    f2_unpack(gy, a[2], b[2]);
+    f2_unpack(gz, a[3], b[3]);
+#pragma unroll
+    for (int d = 0; d < NC; ++d) {
+      red[(slice * NC + d) * nt + ta] = a[d];
+      if (has_b) red[(slice * NC + d) * nt + tb] = b[d];
+    }
+  }
+  __syncthreads();
+  if (tid < nt) {
+    const float c = float(kInv4PiD);
+    float a[NC];
+#pragma unroll
+    for (int d = 0; d < NC; ++d) a[d] = 0;
+    for (int sl = 0; sl < R; ++sl)
+#pragma unroll
+      for (int d = 0; d < NC; ++d) a[d] += red[(sl * NC + d) * nt + tid];
+    const int t = w.t_begin + tid;
+    pot[t] = (ACC ? pot[t] : 0.f) + c * a[0];
+    if (GRAD) {
+      float* gp = grad + 3 * size_t(t);
+      gp[0] = (ACC ? gp[0] : 0.f) - c * a[NC > 1 ? 1 : 0];
+      gp[1] = (ACC ? gp[1] : 0.f) - c * a[NC > 2 ? 2 : 0];
+      gp[2] = (ACC ? gp[2] : 0.f) - c * a[NC > 3 ? 3 : 0];
+    }
+  }
 }
 
 template <class T, bool GRAD, bool ACC>
@@ -113,7 +251,7 @@ __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, 
   const LeafWork w = works[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nt = w.t_count;
-  const int R = leaf_slices(nt);
+  const int R = leaf_slices(nt, false);
   const int slice = tid / nt, tgt = tid - slice * nt;
   const bool active = slice < R;
 

@@ -244,6 +244,7 @@ struct kifmm_gpu_plan {
   kifmm_gpu_options opt{};
   int device = 0;
   int precision = 32;
+  bool leaf_packed = false;
   bool grad = false;
   int64_t N = 0, nl = 0, nn = 0;
   int depth = 0, ne = 0, nc = 0, np = 0, ref_level = 2, cut = 2;
@@ -733,6 +734,12 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   // ---- leaf works, <= 128 targets per work, staged in rounds:
   //      near plan = self + U-list particles (runs on the side stream from the start),
   //      far plan  = L2P + M2P surfaces (after L2L; accumulates into the near result)
+  // fp32: packed two-targets-per-thread kernel (KIFMM_P2P=scalar selects the scalar one)
+  {
+    const char* e = std::getenv("KIFMM_P2P");
+    leaf_packed = precision == 32 && !(e && std::string(e) == "scalar");
+  }
+  const bool packed = leaf_packed;
   auto build_leaf_plan = [&](bool near_part, LeafPlan& lp) {
     std::vector<LeafWork> w;
     std::vector<int4> rounds, items;
@@ -775,7 +782,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       }
       for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += kP2PThreads) {
         const int nt = int(std::min<int64_t>(kP2PThreads, t.leaf_ptr[l + 1] - t0));
-        const int R = leaf_slices(nt), q = 8 * R;
+        const int R = leaf_slices(nt, packed), q = leaf_unroll(packed) * R;
         const int cap = kP2PCap - kP2PCap % q;
         const int rb = int(rounds.size());
         size_t si = 0, oi = 0;
@@ -924,6 +931,21 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     const int4* r = lp.rounds.as<int4>();
     const int4* it = lp.items.as<int4>();
     T* g = grad ? grad_buf.as<T>() : nullptr;
+    if constexpr (sizeof(T) == 4) {
+      if (leaf_packed) {
+        if (grad && acc)
+          leaf_eval_f2_kernel<true, true><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<T>(), g);
+        else if (grad)
+          leaf_eval_f2_kernel<true, false><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<T>(), g);
+        else if (acc)
+          leaf_eval_f2_kernel<false, true><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<T>(), g);
+        else
+          leaf_eval_f2_kernel<false, false><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<T>(), g);
+        KIFMM_LAUNCH_CHECK();
+        ++launches;
+        return;
+      }
+    }
     if (grad && acc)
       leaf_eval_kernel<T, true, true><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<T>(), g);
     else if (grad)
