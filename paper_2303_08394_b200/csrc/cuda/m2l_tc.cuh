@@ -36,6 +36,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -80,6 +81,17 @@ struct Cfg {
 
 struct Item {
   int tile, seg_begin, seg_end, slot;
+};
+
+// Epilogue destination: per-item partial rows (summed later by m2l_tc_reduce_kernel), or -- when
+// direct_out is set and every tile is one item -- the output rows themselves:
+//   dst[direct_out[tile][r]][c] = (accumulate ? dst[..][c] : 0) + acc[r][c] * col_unscale[c]
+struct Epi {
+  float* partial;
+  const int* direct_out;
+  const float* col_unscale;
+  float* dst;
+  int accumulate;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -211,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tm_khi, const __grid_constant__ CUtensorMap tm_klo,
                   const void* __restrict__ m_hi, const void* __restrict__ m_lo, const Item* __restrict__ items,
                   const int* __restrict__ seg_mat, const int* __restrict__ seg_in, int zero_row,
-                  const float* __restrict__ row_unscale, float k_unscale, float* __restrict__ partial) {
+                  const float* __restrict__ row_unscale, float k_unscale, Epi epi) {
   using C = Cfg<PAIR, ROWB, ES>;
   constexpr int KB = C::KB, NKB = C::NKB;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -401,11 +413,41 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_arrive_local(tempty(b));
       }
     }
-    float4* o4 =
-        reinterpret_cast<float4*>(partial + (size_t(it.slot) * rows + rank * BM + row) * NP + h * EPI_COLS);
+    if (epi.direct_out) {
+      const int out = epi.direct_out[size_t(it.tile) * rows + rank * BM + row];
+      if (out >= 0) {
+        // loads first (column unscale, then the old output row), stores last: no load waits behind a store
+        float4* o4 = reinterpret_cast<float4*>(epi.dst + size_t(out) * NP + h * EPI_COLS);
+        const float4* u4 = reinterpret_cast<const float4*>(epi.col_unscale + h * EPI_COLS);
 #pragma unroll
-    for (int k = 0; k < EPI_COLS / 4; ++k)
-      o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+        for (int k = 0; k < EPI_COLS / 4; ++k) {
+          const float4 u = __ldg(u4 + k);
+          acc[4 * k] *= u.x;
+          acc[4 * k + 1] *= u.y;
+          acc[4 * k + 2] *= u.z;
+          acc[4 * k + 3] *= u.w;
+        }
+        if (epi.accumulate) {
+#pragma unroll
+          for (int k = 0; k < EPI_COLS / 4; ++k) {
+            const float4 o = o4[k];
+            acc[4 * k] += o.x;
+            acc[4 * k + 1] += o.y;
+            acc[4 * k + 2] += o.z;
+            acc[4 * k + 3] += o.w;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < EPI_COLS / 4; ++k)
+          o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+      }
+    } else {
+      float4* o4 =
+          reinterpret_cast<float4*>(epi.partial + (size_t(it.slot) * rows + rank * BM + row) * NP + h * EPI_COLS);
+#pragma unroll
+      for (int k = 0; k < EPI_COLS / 4; ++k)
+        o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -700,12 +742,13 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, size_t n, float* 
   lo[i] = v - hv;
 }
 
-// Per multipole row: scale by 2^e so max|row| lands in [2^9, 2^10) (far inside the fp16 range), split
-// x*2^e = hi + lo in fp16 (round to nearest), and record 2^-e.  One warp per row; row nn (zero) included.
-__global__ void split_f16_rows_kernel(const float* __restrict__ M, int nn, __half* __restrict__ hi,
+// Per operand row r in [r0, r1): scale by 2^e so max|row| lands in [2^9, 2^10) (far inside the fp16
+// range), split x*2^e = hi + lo in fp16 (round to nearest), and record 2^-e.  Rows >= nn are zero rows
+// (the appended gather target of absent sources).  One warp per row.
+__global__ void split_f16_rows_kernel(const float* __restrict__ M, int r0, int r1, int nn, __half* __restrict__ hi,
                                       __half* __restrict__ lo, float* __restrict__ unscale) {
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (row > nn) return;
+  const int row = r0 + blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= r1) return;
   float v[NP / 32];
   float mx = 0.f;
 #pragma unroll
@@ -982,10 +1025,11 @@ struct M2LTcPlan {
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<P, R, ES>, mh, ml, ah, al, (const tc::Item*)d_items,
-                                    (const int*)d_seg_mat, (const int*)d_seg_in, int(nn), un, ku, d_partial));
+                                    (const int*)d_seg_mat, (const int*)d_seg_in, int(nn), un, ku,
+                                    tc::Epi{d_partial, nullptr, nullptr, nullptr, 0}));
     } else {
       tc::m2l_tc_kernel<P, R, ES><<<n_items, tc::THREADS, tc::Cfg<P, R, ES>::SMEM_BYTES, s>>>(
-          mh, ml, ah, al, d_items, d_seg_mat, d_seg_in, int(nn), un, ku, d_partial);
+          mh, ml, ah, al, d_items, d_seg_mat, d_seg_in, int(nn), un, ku, tc::Epi{d_partial, nullptr, nullptr, nullptr, 0});
     }
     KIFMM_LAUNCH_CHECK();
   }
@@ -1022,7 +1066,8 @@ struct M2LTcPlan {
       return;
     }
     if (f16) {
-      tc::split_f16_rows_kernel<<<unsigned((nn + 7) / 8), 256, 0, s>>>(M, int(nn), d_mhi16, d_mlo16, d_unscale);
+      tc::split_f16_rows_kernel<<<unsigned((nn + 8) / 8), 256, 0, s>>>(M, 0, int(nn) + 1, int(nn), d_mhi16, d_mlo16,
+                                                                      d_unscale);
       KIFMM_LAUNCH_CHECK();
       if (pair)
         run_kernel<true, 64, 2>(s);
@@ -1040,6 +1085,129 @@ struct M2LTcPlan {
     else if (rowb == 64) run_kernel<false, 64>(s);
     else run_kernel<false, 128>(s);
     tc::m2l_tc_reduce_kernel<<<dim3(n_tiles, rows / 16), 16 * (tc::NP / 4), 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
+    KIFMM_LAUNCH_CHECK();
+  }
+};
+
+
+// fp32 operand rows split for the kind::f16 GEMMs: rows+1 rows (the last one zero) of hi / lo fp16 and
+// the per-row power-of-two unscale.
+struct TcSplit {
+  __half *hi = nullptr, *lo = nullptr;
+  float* un = nullptr;
+  int rows = 0;
+  TcSplit() = default;
+  TcSplit(const TcSplit&) = delete;
+  TcSplit& operator=(const TcSplit&) = delete;
+  ~TcSplit() {
+    for (void* p : {(void*)hi, (void*)lo, (void*)un})
+      if (p) cudaFree(p);
+  }
+  void alloc(int r, size_t* total) {
+    rows = r;
+    const size_t n = size_t(r + 1) * tc::NP;
+    KIFMM_CUDA(cudaMalloc(&hi, n * sizeof(__half)));
+    KIFMM_CUDA(cudaMalloc(&lo, n * sizeof(__half)));
+    KIFMM_CUDA(cudaMalloc(&un, size_t(r + 1) * sizeof(float)));
+    KIFMM_CUDA(cudaMemset(hi + size_t(r) * tc::NP, 0, tc::NP * sizeof(__half)));
+    KIFMM_CUDA(cudaMemset(lo + size_t(r) * tc::NP, 0, tc::NP * sizeof(__half)));
+    KIFMM_CUDA(cudaMemset(un + r, 0, sizeof(float)));
+    *total += 2 * n * sizeof(__half) + size_t(r + 1) * sizeof(float);
+  }
+  // split rows [r0, r1) of the fp32 buffer X (row stride NP)
+  void split(const float* X, int r0, int r1, cudaStream_t s) const {
+    if (r1 <= r0) return;
+    tc::split_f16_rows_kernel<<<unsigned((r1 - r0 + 7) / 8), 256, 0, s>>>(X, r0, r1, rows, hi, lo, un);
+    KIFMM_LAUNCH_CHECK();
+  }
+};
+
+// The dense (gathered) fp32 GEMMs of the upward / downward passes -- factored check->equivalent solves,
+// M2M and L2L -- on the same tcgen05 kernel as M2L: 128-row tiles, one item per tile
+// carrying all of the tile's segments, direct epilogue into the output rows.  B = n_mats matrices
+// B[m][j][k] (output column j, reduction index k) in fp64, split into fp16 hi / lo after a power-of-two
+// scale per output column common to all matrices (so 1/sigma factors of the pseudo-inverse stay in
+// range); the epilogue multiplies the column unscale back.
+struct TcGemm {
+  int n_tiles = 0;
+  int *d_out = nullptr, *d_seg_mat = nullptr, *d_seg_in = nullptr;
+  tc::Item* d_items = nullptr;
+  __half *d_bhi = nullptr, *d_blo = nullptr;
+  float* d_cu = nullptr;
+  CUtensorMap tm_hi{}, tm_lo{};
+  TcGemm() = default;
+  TcGemm(const TcGemm&) = delete;
+  TcGemm& operator=(const TcGemm&) = delete;
+  ~TcGemm() {
+    for (void* p : {(void*)d_out, (void*)d_seg_mat, (void*)d_seg_in, (void*)d_items, (void*)d_bhi, (void*)d_blo,
+                    (void*)d_cu})
+      if (p) cudaFree(p);
+  }
+
+  // tiles: out (128 rows, -1 pad) + segs (matrix, 128 input rows or -1)
+  template <class Tile>
+  void build(const std::vector<Tile>& tiles, const std::vector<double>& B, int n_mats, size_t* total) {
+    constexpr int NP = tc::NP;
+    if (B.size() != size_t(n_mats) * NP * NP) throw InvalidArgument("TcGemm: B size");
+    std::vector<int> out, seg_mat, seg_in;
+    std::vector<tc::Item> items;
+    for (const auto& t : tiles) {
+      if (t.out.size() != size_t(tc::BM)) throw InvalidArgument("TcGemm: tiles must have 128 rows");
+      const int sb = int(seg_mat.size());
+      out.insert(out.end(), t.out.begin(), t.out.end());
+      for (const auto& sg : t.segs) {
+        seg_mat.push_back(sg.first);
+        seg_in.insert(seg_in.end(), sg.second.begin(), sg.second.end());
+      }
+      items.push_back({int(items.size()), sb, int(seg_mat.size()), int(items.size())});
+    }
+    n_tiles = int(items.size());
+    M2LTcPlan::up(&d_out, out, total);
+    M2LTcPlan::up(&d_seg_mat, seg_mat, total);
+    M2LTcPlan::up(&d_seg_in, seg_in, total);
+    M2LTcPlan::up(&d_items, items, total);
+    std::vector<float> cu(NP, 1.f);
+    std::vector<__half> hi(B.size()), lo(B.size());
+    for (int j = 0; j < NP; ++j) {
+      double mx = 0;
+      for (int m = 0; m < n_mats; ++m)
+        for (int k = 0; k < NP; ++k) mx = std::max(mx, std::fabs(B[(size_t(m) * NP + j) * NP + k]));
+      int e = 0;
+      if (mx > 0) {
+        int ex;
+        std::frexp(mx, &ex);
+        e = 10 - ex;
+      }
+      cu[j] = float(std::ldexp(1.0, -e));
+      for (int m = 0; m < n_mats; ++m)
+        for (int k = 0; k < NP; ++k) {
+          const size_t i = (size_t(m) * NP + j) * NP + k;
+          const double x = std::ldexp(B[i], e);
+          const __half h = __float2half_rn(float(x));
+          hi[i] = h;
+          lo[i] = __float2half_rn(float(x - double(__half2float(h))));
+        }
+    }
+    M2LTcPlan::up(&d_bhi, hi, total);
+    M2LTcPlan::up(&d_blo, lo, total);
+    M2LTcPlan::up(&d_cu, cu, total);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    KIFMM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn) throw DeviceError(KIFMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    auto enc = reinterpret_cast<M2LTcPlan::EncodeFn>(fn);
+    M2LTcPlan::encode(enc, &tm_hi, d_bhi, uint64_t(n_mats) * NP, NP, 64, 2);
+    M2LTcPlan::encode(enc, &tm_lo, d_blo, uint64_t(n_mats) * NP, NP, 64, 2);
+    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<false, 64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::Cfg<false, 64, 2>::SMEM_BYTES));
+  }
+
+  // dst[out rows] (=, or += when accumulate) A(split rows) . B^T
+  void run(const TcSplit& a, float* dst, bool accumulate, cudaStream_t s) const {
+    if (!n_tiles) return;
+    tc::m2l_tc_kernel<false, 64, 2><<<n_tiles, tc::THREADS, tc::Cfg<false, 64, 2>::SMEM_BYTES, s>>>(
+        tm_hi, tm_lo, a.hi, a.lo, d_items, d_seg_mat, d_seg_in, a.rows, a.un, 1.f,
+        tc::Epi{nullptr, d_out, d_cu, dst, accumulate ? 1 : 0});
     KIFMM_LAUNCH_CHECK();
   }
 };

@@ -229,9 +229,17 @@ struct LeafPlan {
 };
 
 struct M2MLevel {
-  GemmTiles tiles;  // one tile per (64 parents, octant)
+  GemmTiles tiles;  // one tile per (64 parents, octant)   [SIMT]
+  TcGemm tc;        // one tile per (128 parents, octant)  [tcgen05]
+  int r0 = 0, r1 = 0;  // child rows to split before the tcgen05 GEMM
   DevMem parents, masks;
   int n = 0;
+};
+
+struct L2LLevel {
+  GemmTiles tiles;
+  TcGemm tc;
+  int r0 = 0, r1 = 0;  // parent rows (level l) to split
 };
 
 }  // namespace gpu
@@ -273,7 +281,11 @@ struct kifmm_gpu_plan {
   int n_p2m = 0, n_p2l = 0;
   GemmTiles solve_up1, solve_up2, solve_dn1, solve_dn2, m2l;
   std::vector<std::unique_ptr<M2MLevel>> m2m_levels, m2m_top;
-  std::vector<std::unique_ptr<GemmTiles>> l2l_levels;
+  std::vector<std::unique_ptr<L2LLevel>> l2l_levels;
+  // fp32 solves / M2M / L2L on tcgen05 (kind::f16 3-term split) -- see TcGemm
+  bool gemm_tc = false;
+  TcSplit sp_cu, sp_tmp, sp_M, sp_cd, sp_L;
+  TcGemm tg_up1, tg_up2, tg_dn1, tg_dn2;
   DevMem m2m_scratch;
   DevMem m2l_red_out, m2l_red_slot, m2l_partial;
   int m2l_red_tiles = 0;
@@ -470,7 +482,30 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   check_dn.alloc(size_t(nn) * np * es, &dev_bytes);
 
   const int bm_m2l = 64;
-  const int ld_tiles = 64;  // solves / L2L: 64-row tiles (2 CTAs per SM; these GEMMs have K = 160 only)
+  {
+    const char* e = std::getenv("KIFMM_TC_GEMM");
+    gemm_tc = precision == 32 && np == tc::NP && o.m2l_backend != 1 && m2l_tc_available() &&
+              !(e && std::string(e) == "0");
+  }
+  // solves / L2L: 64-row tiles on the SIMT path (2 CTAs per SM; K = 160 only), 128 on tcgen05
+  const int ld_tiles = gemm_tc ? tc::BM : 64;
+  // fp64 B operands of the tcgen05 GEMMs: B[m][j][k], j = output column, k = reduction index
+  auto factored_b = [&](const double* U, const double* S, const double* V, int k, std::vector<double>& b1,
+                        std::vector<double>& b2) {
+    b1.assign(size_t(np) * np, 0.0);
+    b2.assign(size_t(np) * np, 0.0);
+    for (int i = 0; i < nc; ++i)
+      for (int j = 0; j < k; ++j) b1[size_t(j) * np + i] = U[size_t(i) * k + j] / S[j];
+    for (int j = 0; j < k; ++j)
+      for (int e = 0; e < ne; ++e) b2[size_t(e) * np + j] = V[size_t(e) * k + j];
+  };
+  auto octant_b = [&](const double* A) {  // 8 x (ne x ne) -> 8 x np x np
+    std::vector<double> b(size_t(8) * np * np, 0.0);
+    for (int m = 0; m < 8; ++m)
+      for (int j = 0; j < ne; ++j)
+        for (int k = 0; k < ne; ++k) b[(size_t(m) * np + j) * np + k] = A[(size_t(m) * ne + j) * ne + k];
+    return b;
+  };
 
   // ---- P2M: one check work per owned leaf, solve rows = slots
   {
@@ -500,13 +535,22 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       a.push_back(x);
       b.push_back(y);
     }
-    solve_up1.build(a, ld_tiles, &dev_bytes);
-    solve_up2.build(b, ld_tiles, &dev_bytes);
+    if (gemm_tc) {
+      std::vector<double> b1, b2;
+      factored_b(ops.uc2e_u, ops.uc2e_s, ops.uc2e_v, ops.uc2e_rank, b1, b2);
+      tg_up1.build(a, b1, 1, &dev_bytes);
+      tg_up2.build(b, b2, 1, &dev_bytes);
+      sp_cu.alloc(int(std::max<int64_t>(1, le - lb)), &dev_bytes);
+    } else {
+      solve_up1.build(a, ld_tiles, &dev_bytes);
+      solve_up2.build(b, ld_tiles, &dev_bytes);
+    }
   }
 
   // ---- M2M per level (owned internal nodes), then the redundant top levels
+  const std::vector<double> b_m2m = gemm_tc ? octant_b(ops.m2m) : std::vector<double>();
   auto m2m_tiles = [&](std::vector<int64_t>& parents) {
-    constexpr int BMS = 64;
+    const int BMS = gemm_tc ? tc::BM : 64;
     std::vector<TileSpec> tiles;
     std::vector<int> par, msk;
     for (size_t s0 = 0; s0 < parents.size(); s0 += BMS) {
@@ -535,7 +579,22 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       msk.push_back(m);
     }
     auto g = std::make_unique<M2MLevel>();
-    g->tiles.build(tiles, BMS, &dev_bytes);
+    if (gemm_tc) {
+      g->tc.build(tiles, b_m2m, 8, &dev_bytes);
+      int64_t lo = INT64_MAX, hi = -1;  // child rows (one level: contiguous node range)
+      for (int64_t pn : parents)
+        for (int o = 0; o < 8; ++o) {
+          const int64_t ch = t.node_children[8 * pn + o];
+          if (ch >= 0) {
+            lo = std::min(lo, ch);
+            hi = std::max(hi, ch + 1);
+          }
+        }
+      g->r0 = int(lo == INT64_MAX ? 0 : lo);
+      g->r1 = int(std::max<int64_t>(hi, g->r0));
+    } else {
+      g->tiles.build(tiles, BMS, &dev_bytes);
+    }
     g->parents.upload(par, &dev_bytes);
     g->masks.upload(msk, &dev_bytes);
     g->n = int(parents.size());
@@ -700,10 +759,25 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       a.push_back(x);
       b.push_back(y);
     }
-    solve_dn1.build(a, ld_tiles, &dev_bytes);
-    solve_dn2.build(b, ld_tiles, &dev_bytes);
+    if (gemm_tc) {
+      std::vector<double> b1, b2;
+      factored_b(ops.dc2e_u, ops.dc2e_s, ops.dc2e_v, ops.dc2e_rank, b1, b2);
+      tg_dn1.build(a, b1, 1, &dev_bytes);
+      tg_dn2.build(b, b2, 1, &dev_bytes);
+    } else {
+      solve_dn1.build(a, ld_tiles, &dev_bytes);
+      solve_dn2.build(b, ld_tiles, &dev_bytes);
+    }
   }
-  tmp.alloc(size_t(std::max<int64_t>({int64_t(1), le - lb, int64_t(dn_nodes.size())})) * np * es, &dev_bytes);
+  const int64_t tmp_rows = std::max<int64_t>({int64_t(1), le - lb, int64_t(dn_nodes.size())});
+  tmp.alloc(size_t(tmp_rows) * np * es, &dev_bytes);
+  if (gemm_tc) {
+    sp_tmp.alloc(int(tmp_rows), &dev_bytes);
+    sp_M.alloc(int(nn), &dev_bytes);
+    sp_cd.alloc(int(nn), &dev_bytes);
+    sp_L.alloc(int(nn), &dev_bytes);
+  }
+  const std::vector<double> b_l2l = gemm_tc ? octant_b(ops.l2l) : std::vector<double>();
 
   // ---- L2L per level: active children at l+1 (l >= 2), grouped by octant
   for (int l = 2; l < depth; ++l) {
@@ -725,8 +799,14 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       }
     }
     if (!tiles.empty()) {
-      auto g = std::make_unique<GemmTiles>();
-      g->build(tiles, ld_tiles, &dev_bytes);
+      auto g = std::make_unique<L2LLevel>();
+      if (gemm_tc) {
+        g->tc.build(tiles, b_l2l, 8, &dev_bytes);
+        g->r0 = int(t.level_ptr[l]);
+        g->r1 = int(t.level_ptr[l + 1]);
+      } else {
+        g->tiles.build(tiles, ld_tiles, &dev_bytes);
+      }
       l2l_levels.push_back(std::move(g));
     }
   }
@@ -978,12 +1058,29 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     KIFMM_LAUNCH_CHECK();
     ++launches;
   }
-  gemm(solve_up1, check_up.as<T>(), w_us_u.as<T>(), tmp.as<T>(), false, true);
-  gemm(solve_up2, tmp.as<T>(), w_vt_u.as<T>(), Mp, false, true);
+  // tcgen05 GEMM: split the fp32 source rows, then dst (=/+=) A . B^T
+  auto tgemm = [&](const TcGemm& g, const TcSplit& sp, const T* X, int r0, int r1, T* Y, bool acc) {
+    if constexpr (sizeof(T) == 4) {
+      if (!g.n_tiles) return;
+      sp.split(X, r0, r1, s);
+      g.run(sp, Y, acc, s);
+      launches += 2;
+    }
+  };
+  if (gemm_tc) {
+    tgemm(tg_up1, sp_cu, check_up.as<T>(), 0, int(le - lb), tmp.as<T>(), false);
+    tgemm(tg_up2, sp_tmp, tmp.as<T>(), 0, int(le - lb), Mp, false);
+  } else {
+    gemm(solve_up1, check_up.as<T>(), w_us_u.as<T>(), tmp.as<T>(), false, true);
+    gemm(solve_up2, tmp.as<T>(), w_vt_u.as<T>(), Mp, false, true);
+  }
   mark();  // 1
   // M2M, levels d-1 .. floor
   auto m2m_level = [&](const M2MLevel& lv) {
-    gemm(lv.tiles, Mp, w_m2m.as<T>(), m2m_scratch.as<T>(), false, true);
+    if (gemm_tc)
+      tgemm(lv.tc, sp_M, Mp, lv.r0, lv.r1, m2m_scratch.as<T>(), false);
+    else
+      gemm(lv.tiles, Mp, w_m2m.as<T>(), m2m_scratch.as<T>(), false, true);
     m2m_reduce_kernel<T><<<lv.n, 128, 0, s>>>(m2m_scratch.as<T>(), lv.parents.as<int>(), lv.masks.as<int>(), lv.n,
                                              np, Mp);
     KIFMM_LAUNCH_CHECK();
@@ -1024,11 +1121,21 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   }
   mark();  // 5
   // factored downward solve (dc2e at the reference level; M2L/P2L level factors folded)
-  gemm(solve_dn1, check_dn.as<T>(), w_us_d.as<T>(), tmp.as<T>(), false, true);
-  gemm(solve_dn2, tmp.as<T>(), w_vt_d.as<T>(), Lp, false, true);
+  if (gemm_tc) {
+    tgemm(tg_dn1, sp_cd, check_dn.as<T>(), 0, int(nn), tmp.as<T>(), false);
+    tgemm(tg_dn2, sp_tmp, tmp.as<T>(), 0, sp_tmp.rows, Lp, false);
+  } else {
+    gemm(solve_dn1, check_dn.as<T>(), w_us_d.as<T>(), tmp.as<T>(), false, true);
+    gemm(solve_dn2, tmp.as<T>(), w_vt_d.as<T>(), Lp, false, true);
+  }
   mark();  // 6
   // L2L top-down
-  for (auto& lv : l2l_levels) gemm(*lv, Lp, w_l2l.as<T>(), Lp, true, true);
+  for (auto& lv : l2l_levels) {
+    if (gemm_tc)
+      tgemm(lv->tc, sp_L, Lp, lv->r0, lv->r1, Lp, true);
+    else
+      gemm(lv->tiles, Lp, w_l2l.as<T>(), Lp, true, true);
+  }
   mark();  // 7
   // leaves: near field (side stream, or here when timed) then L2P + M2P
   if (timed) leaf(leaf_near, false, s);
