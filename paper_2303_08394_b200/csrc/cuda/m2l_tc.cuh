@@ -41,6 +41,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -92,6 +93,7 @@ struct Epi {
   const float* col_unscale;
   float* dst;
   int accumulate;
+  int debug;  // experiments only (KIFMM_TC_DBG): bit 0 skips the A gathers, bit 1 the B TMA loads
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -222,7 +224,7 @@ template <bool PAIR, int ROWB, int ES>
 __global__ void __launch_bounds__(THREADS, 1)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tm_khi, const __grid_constant__ CUtensorMap tm_klo,
                   const void* __restrict__ m_hi, const void* __restrict__ m_lo, const Item* __restrict__ items,
-                  const int* __restrict__ seg_mat, const int* __restrict__ seg_in, int zero_row,
+                  const int* __restrict__ sched, const int* __restrict__ seg_mat, const int* __restrict__ seg_in, int zero_row,
                   const float* __restrict__ row_unscale, float k_unscale, Epi epi) {
   using C = Cfg<PAIR, ROWB, ES>;
   constexpr int KB = C::KB, NKB = C::NKB;
@@ -235,9 +237,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::STAGES + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
-  const Item it = items[PAIR ? (blockIdx.x >> 1) : blockIdx.x];
-  const int ntap = it.seg_end - it.seg_begin;
-  const int nstage = ntap * NKB;
+  // persistent: this CTA (pair) g0 runs the items sched[gs + 1 + k], k in [sched[g0], sched[g0 + 1]) -- a
+  // longest-processing-time-first assignment made on the host; every role walks the same item sequence
+  // with running stage (gi) and tap (gj) counters, so the pipeline runs on across item boundaries
+  const int g0 = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int gs = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
+  const int k_begin = sched[g0], k_end = sched[g0 + 1];
+  const int* sched_list = sched + gs + 1;
   const int rows = C::CTAS * BM;  // rows per tile in seg_in / partial
   const uint32_t sbase = smem_u32(smem);
   auto a_hi = [&](int s) { return sbase + s * C::STAGE_BYTES; };
@@ -286,44 +292,66 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- B producer: this CTA's rows of K_t hi/lo (TMA tile, SWIZZLE_128B)
+    // ---------------- B producer: this CTA's rows of K_t hi/lo (TMA tile, swizzled)
     if (lane == 0) {
-      for (int i = 0; i < nstage; ++i) {
-        const int s = i % C::STAGES, round = i / C::STAGES;
-        mbar_wait(empty(s), (round & 1) ^ 1);
-        const int seg = it.seg_begin + i / NKB, kb = i % NKB;
-        const int row = seg_mat[seg] * NP + int(rank) * C::NB;
-        if (rank == 0) mbar_expect_tx(full(s), C::TX);
-        const uint32_t fb = leader(full(s));
-        tma_tile<PAIR>(b_hi(s), &tm_khi, fb, kb * KB, row);
-        tma_tile<PAIR>(b_lo(s), &tm_klo, fb, kb * KB, row);
+      int gi = 0;
+      for (int kk = k_begin; kk < k_end; ++kk) {
+        const Item it = items[sched_list[kk]];
+        const int nstage = (it.seg_end - it.seg_begin) * NKB;
+        for (int i = 0; i < nstage; ++i, ++gi) {
+          const int s = gi % C::STAGES, round = gi / C::STAGES;
+          mbar_wait(empty(s), (round & 1) ^ 1);
+          const int seg = it.seg_begin + i / NKB, kb = i % NKB;
+          const int row = seg_mat[seg] * NP + int(rank) * C::NB;
+          if (epi.debug & 2) {
+            if (rank == 0) mbar_expect_tx(full(s), 0);
+            continue;
+          }
+          if (rank == 0) mbar_expect_tx(full(s), C::TX);
+          const uint32_t fb = leader(full(s));
+          tma_tile<PAIR>(b_hi(s), &tm_khi, fb, kb * KB, row);
+          tma_tile<PAIR>(b_lo(s), &tm_klo, fb, kb * KB, row);
+        }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only): a fresh accumulator per tap
     if (rank == 0 && lane == 0) {
-      for (int j = 0; j < ntap; ++j) {
-        const int b = j & 1;
-        mbar_wait(tempty(b), ((j >> 1) & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem_base + uint32_t(b * 256);
-        for (int kb = 0; kb < NKB; ++kb) {
-          const int i = j * NKB + kb;
-          const int s = i % C::STAGES, round = i / C::STAGES;
-          mbar_wait(full(s), round & 1);
+      int gi = 0, gj = 0;
+      const bool prof = (epi.debug & 8) != 0;
+      unsigned long long t_all = clock64(), t_te = 0, t_fu = 0;
+      for (int kk = k_begin; kk < k_end; ++kk) {
+        const Item it = items[sched_list[kk]];
+        const int ntap = it.seg_end - it.seg_begin;
+        for (int j = 0; j < ntap; ++j, ++gj) {
+          const int b = gj & 1;
+          unsigned long long c0 = prof ? clock64() : 0;
+          mbar_wait(tempty(b), ((gj >> 1) & 1) ^ 1);
+          if (prof) t_te += clock64() - c0;
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t d = tmem_base + uint32_t(b * 256);
+          for (int kb = 0; kb < NKB; ++kb, ++gi) {
+            const int s = gi % C::STAGES, round = gi / C::STAGES;
+            c0 = prof ? clock64() : 0;
+            mbar_wait(full(s), round & 1);
+            if (prof) t_fu += clock64() - c0;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-          for (int k = 0; k < ROWB / 32; ++k) {  // 32 bytes of K per MMA (8 tf32 / 16 f16)
-            const uint64_t dah = make_desc<ROWB>(a_hi(s) + 32 * k), dal = make_desc<ROWB>(a_lo(s) + 32 * k);
-            const uint64_t dbh = make_desc<ROWB>(b_hi(s) + 32 * k), dbl = make_desc<ROWB>(b_lo(s) + 32 * k);
-            mma<PAIR, ES>(d, dah, dbh, (kb > 0 || k > 0) ? 1u : 0u);
-            mma<PAIR, ES>(d, dah, dbl, 1u);
-            mma<PAIR, ES>(d, dal, dbh, 1u);
+            for (int k = 0; k < ROWB / 32; ++k) {  // 32 bytes of K per MMA (8 tf32 / 16 f16)
+              const uint64_t dah = make_desc<ROWB>(a_hi(s) + 32 * k), dal = make_desc<ROWB>(a_lo(s) + 32 * k);
+              const uint64_t dbh = make_desc<ROWB>(b_hi(s) + 32 * k), dbl = make_desc<ROWB>(b_lo(s) + 32 * k);
+              mma<PAIR, ES>(d, dah, dbh, (kb > 0 || k > 0) ? 1u : 0u);
+              mma<PAIR, ES>(d, dah, dbl, 1u);
+              mma<PAIR, ES>(d, dal, dbh, 1u);
+            }
+            commit<PAIR>(empty(s));
           }
-          commit<PAIR>(empty(s));
+          commit<PAIR>(tfull(b));
         }
-        commit<PAIR>(tfull(b));
       }
+      if (prof && (blockIdx.x == 0 || blockIdx.x == 64))
+        printf("cta %d: total %llu wait_tempty %llu wait_full %llu taps %d stages %d\n", int(blockIdx.x),
+               clock64() - t_all, t_te, t_fu, gj, gi);
     }
   } else if (warp >= 2 && warp < 6) {
     // ---------------- A producers: thread -> (16-byte chunk c, rows r0 + 16 j) of this CTA, cp.async
@@ -334,43 +362,54 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int t = threadIdx.x - 64;  // 0..127
     const int c = t % CH, r0 = t / CH;
     int src[J];
-    int cur_seg = -1;
-    for (int i = 0; i < nstage; ++i) {
-      const int s = i % C::STAGES, round = i / C::STAGES;
-      const int seg = it.seg_begin + i / NKB, kb = i % NKB;
-      if (seg != cur_seg) {
-        cur_seg = seg;
+    int gi = 0;
+    for (int kk = k_begin; kk < k_end; ++kk) {
+      const Item it = items[sched_list[kk]];
+      const int nstage = (it.seg_end - it.seg_begin) * NKB;
+      int cur_seg = -1;
+      for (int i = 0; i < nstage; ++i, ++gi) {
+        const int s = gi % C::STAGES, round = gi / C::STAGES;
+        const int seg = it.seg_begin + i / NKB, kb = i % NKB;
+        if (seg != cur_seg) {
+          cur_seg = seg;
 #pragma unroll
-        for (int j = 0; j < J; ++j) src[j] = seg_in[size_t(seg) * rows + rank * BM + r0 + RPI * j];
-      }
-      mbar_wait(empty(s), (round & 1) ^ 1);
+          for (int j = 0; j < J; ++j) src[j] = seg_in[size_t(seg) * rows + rank * BM + r0 + RPI * j];
+        }
+        mbar_wait(empty(s), (round & 1) ^ 1);
 #pragma unroll
-      for (int j = 0; j < J; ++j) {
-        const int r = r0 + RPI * j;
-        const int sw = ROWB == 128 ? (r & 7) : ((r & 7) >> 1);  // Swizzle<3,4,3> / Swizzle<2,4,3>
-        const uint32_t off = uint32_t((r >> 3) * C::ATOM + (r & 7) * ROWB + ((c ^ sw) << 4));
-        const bool ok = src[j] >= 0;  // absent source: zero-fill, no global read
-        const size_t g = size_t(ok ? src[j] : zero_row) * NP * ES + kb * ROWB + c * 16;  // bytes
-        const int sz = ok ? 16 : 0;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_hi(s) + off),
-                     "l"(static_cast<const char*>(m_hi) + g), "r"(sz)
-                     : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_lo(s) + off),
-                     "l"(static_cast<const char*>(m_lo) + g), "r"(sz)
+        for (int j = 0; j < J; ++j) {
+          const int r = r0 + RPI * j;
+          const int sw = ROWB == 128 ? (r & 7) : ((r & 7) >> 1);  // Swizzle<3,4,3> / Swizzle<2,4,3>
+          const uint32_t off = uint32_t((r >> 3) * C::ATOM + (r & 7) * ROWB + ((c ^ sw) << 4));
+          const bool ok = src[j] >= 0;  // absent source: zero-fill, no global read
+          const size_t g = size_t(ok ? src[j] : zero_row) * NP * ES + kb * ROWB + c * 16;  // bytes
+          const int sz = ok ? 16 : 0;
+          if (epi.debug & 1) continue;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_hi(s) + off),
+                       "l"(static_cast<const char*>(m_hi) + g), "r"(sz)
+                       : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_lo(s) + off),
+                       "l"(static_cast<const char*>(m_lo) + g), "r"(sz)
+                       : "memory");
+        }
+        // non-blocking: the barrier receives this thread's arrival when its copies have landed
+        // (as CUTLASS's cp.async UMMA mainloops do; the full barrier's count includes these arrivals)
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(PAIR ? afull(s) : full(s))
                      : "memory");
       }
-      // non-blocking: the barrier receives this thread's arrival when its copies have landed
-      // (as CUTLASS's cp.async UMMA mainloops do; the full barrier's count includes these arrivals)
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(PAIR ? afull(s) : full(s))
-                   : "memory");
     }
   } else if (warp == FWD_WARP) {
     // ---------------- forwarder (pair): this CTA's A rows landed -> one arrive on the leader's stage barrier
     if (PAIR && lane == 0) {
-      for (int i = 0; i < nstage; ++i) {
-        const int s = i % C::STAGES, round = i / C::STAGES;
-        mbar_wait(afull(s), round & 1);
-        mbar_arrive_cluster(leader(full(s)));
+      int gi = 0;
+      for (int kk = k_begin; kk < k_end; ++kk) {
+        const Item it = items[sched_list[kk]];
+        const int nstage = (it.seg_end - it.seg_begin) * NKB;
+        for (int i = 0; i < nstage; ++i, ++gi) {
+          const int s = gi % C::STAGES, round = gi / C::STAGES;
+          mbar_wait(afull(s), round & 1);
+          mbar_arrive_cluster(leader(full(s)));
+        }
       }
     }
   } else if (warp >= EPI_WARP0) {
@@ -378,75 +417,80 @@ __global__ void __launch_bounds__(THREADS, 1)
     //                  and columns [h*80, h*80+80), h = (w-6)/4
     const int q = warp & 3, h = (warp - EPI_WARP0) >> 2;
     const int row = q * 32 + lane;
-    float acc[EPI_COLS];
+    int gj = 0;
+    for (int kk = k_begin; kk < k_end; ++kk) {
+      const Item it = items[sched_list[kk]];
+      const int ntap = it.seg_end - it.seg_begin;
+      float acc[EPI_COLS];
 #pragma unroll
-    for (int k = 0; k < EPI_COLS; ++k) acc[k] = 0.f;
-    for (int j = 0; j < ntap; ++j) {
-      const int b = j & 1;
-      float f = 1.f;  // f16 kind: undo the per-row (source) and K_t power-of-two scalings
-      if constexpr (ES == 2) {
-        const int sr = seg_in[size_t(it.seg_begin + j) * rows + rank * BM + row];
-        f = sr < 0 ? 0.f : row_unscale[sr] * k_unscale;
-      }
-      mbar_wait(tfull(b), (j >> 1) & 1);
-      __syncwarp();
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * 256 + h * EPI_COLS);
-#pragma unroll
-      for (int cb = 0; cb < EPI_COLS / 16; ++cb) {
-        uint32_t v[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(taddr + uint32_t(cb * 16)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int k = 0; k < 16; ++k) acc[cb * 16 + k] = fmaf(__uint_as_float(v[k]), f, acc[cb * 16 + k]);
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-        if (PAIR)
-          mbar_arrive_cluster(leader(tempty(b)));
-        else
-          mbar_arrive_local(tempty(b));
-      }
-    }
-    if (epi.direct_out) {
-      const int out = epi.direct_out[size_t(it.tile) * rows + rank * BM + row];
-      if (out >= 0) {
-        // loads first (column unscale, then the old output row), stores last: no load waits behind a store
-        float4* o4 = reinterpret_cast<float4*>(epi.dst + size_t(out) * NP + h * EPI_COLS);
-        const float4* u4 = reinterpret_cast<const float4*>(epi.col_unscale + h * EPI_COLS);
-#pragma unroll
-        for (int k = 0; k < EPI_COLS / 4; ++k) {
-          const float4 u = __ldg(u4 + k);
-          acc[4 * k] *= u.x;
-          acc[4 * k + 1] *= u.y;
-          acc[4 * k + 2] *= u.z;
-          acc[4 * k + 3] *= u.w;
+      for (int k = 0; k < EPI_COLS; ++k) acc[k] = 0.f;
+      for (int j = 0; j < ntap; ++j, ++gj) {
+        const int b = gj & 1;
+        float f = 1.f;  // f16 kind: undo the per-row (source) and K_t power-of-two scalings
+        if constexpr (ES == 2) {
+          const int sr = seg_in[size_t(it.seg_begin + j) * rows + rank * BM + row];
+          f = sr < 0 ? 0.f : row_unscale[sr] * k_unscale;
         }
-        if (epi.accumulate) {
+        mbar_wait(tfull(b), (gj >> 1) & 1);
+        __syncwarp();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * 256 + h * EPI_COLS);
+#pragma unroll
+        for (int cb = 0; cb < ((epi.debug & 4) ? 0 : EPI_COLS / 16); ++cb) {
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(taddr + uint32_t(cb * 16)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int k = 0; k < 16; ++k) acc[cb * 16 + k] = fmaf(__uint_as_float(v[k]), f, acc[cb * 16 + k]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR)
+            mbar_arrive_cluster(leader(tempty(b)));
+          else
+            mbar_arrive_local(tempty(b));
+        }
+      }
+      if (epi.direct_out) {
+        const int out = epi.direct_out[size_t(it.tile) * rows + rank * BM + row];
+        if (out >= 0) {
+          // loads first (column unscale, then the old output row), stores last: no load waits behind a store
+          float4* o4 = reinterpret_cast<float4*>(epi.dst + size_t(out) * NP + h * EPI_COLS);
+          const float4* u4 = reinterpret_cast<const float4*>(epi.col_unscale + h * EPI_COLS);
 #pragma unroll
           for (int k = 0; k < EPI_COLS / 4; ++k) {
-            const float4 o = o4[k];
-            acc[4 * k] += o.x;
-            acc[4 * k + 1] += o.y;
-            acc[4 * k + 2] += o.z;
-            acc[4 * k + 3] += o.w;
+            const float4 u = __ldg(u4 + k);
+            acc[4 * k] *= u.x;
+            acc[4 * k + 1] *= u.y;
+            acc[4 * k + 2] *= u.z;
+            acc[4 * k + 3] *= u.w;
           }
+          if (epi.accumulate) {
+#pragma unroll
+            for (int k = 0; k < EPI_COLS / 4; ++k) {
+              const float4 o = o4[k];
+              acc[4 * k] += o.x;
+              acc[4 * k + 1] += o.y;
+              acc[4 * k + 2] += o.z;
+              acc[4 * k + 3] += o.w;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < EPI_COLS / 4; ++k)
+            o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
         }
+      } else {
+        float4* o4 =
+            reinterpret_cast<float4*>(epi.partial + (size_t(it.slot) * rows + rank * BM + row) * NP + h * EPI_COLS);
 #pragma unroll
         for (int k = 0; k < EPI_COLS / 4; ++k)
           o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
       }
-    } else {
-      float4* o4 =
-          reinterpret_cast<float4*>(epi.partial + (size_t(it.slot) * rows + rank * BM + row) * NP + h * EPI_COLS);
-#pragma unroll
-      for (int k = 0; k < EPI_COLS / 4; ++k)
-        o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -800,6 +844,48 @@ __global__ void m2l_tc_reduce_kernel(const float* __restrict__ partial, const in
 
 }  // namespace tc
 
+// Longest-processing-time-first assignment of items (cost = taps + 1) to g persistent CTAs (pairs):
+// returns [ptr (g + 1)][item lists], each list in decreasing cost.
+inline std::vector<int> lpt_schedule(const std::vector<tc::Item>& items, int g) {
+  std::vector<int> order(items.size());
+  for (size_t i = 0; i < items.size(); ++i) order[i] = int(i);
+  auto cost = [&](int i) { return int64_t(items[i].seg_end - items[i].seg_begin) + 1; };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost(a) > cost(b); });
+  std::vector<std::vector<int>> lists(g);
+  using E = std::pair<int64_t, int>;  // (load, cta)
+  std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
+  for (int c = 0; c < g; ++c) pq.push({0, c});
+  for (int i : order) {
+    E e = pq.top();
+    pq.pop();
+    lists[e.second].push_back(i);
+    pq.push({e.first + cost(i), e.second});
+  }
+  std::vector<int> out{0};
+  for (int c = 0; c < g; ++c) out.push_back(out.back() + int(lists[c].size()));
+  for (int c = 0; c < g; ++c) out.insert(out.end(), lists[c].begin(), lists[c].end());
+  return out;
+}
+
+inline int tc_debug() {
+  static const int d = [] {
+    const char* e = std::getenv("KIFMM_TC_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return d;
+}
+
+inline int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 inline bool m2l_tc_available() {
   int dev = 0, major = 0, minor = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
@@ -821,6 +907,8 @@ struct M2LTcPlan {
   float* d_unscale = nullptr;
   CUtensorMap tm_khi16{}, tm_klo16{};
   int n_items = 0, n_tiles = 0, n_segs = 0;
+  int sched_g = 0;         // persistent CTAs (pairs) of the tcgen05 kernel
+  int* d_sched = nullptr;  // lpt_schedule(items, sched_g)
   size_t nn = 0;
   float *d_khi = nullptr, *d_klo = nullptr, *d_mhi = nullptr, *d_mlo = nullptr, *d_partial = nullptr;
   int *d_tile_out = nullptr, *d_tile_slot = nullptr, *d_seg_mat = nullptr, *d_seg_in = nullptr;
@@ -831,7 +919,7 @@ struct M2LTcPlan {
   ~M2LTcPlan() {
     for (void* p : {(void*)d_khi, (void*)d_klo, (void*)d_mhi, (void*)d_mlo, (void*)d_partial, (void*)d_tile_out,
                     (void*)d_tile_slot, (void*)d_seg_mat, (void*)d_seg_in, (void*)d_items, (void*)d_khi16,
-                    (void*)d_klo16, (void*)d_mhi16, (void*)d_mlo16, (void*)d_unscale})
+                    (void*)d_klo16, (void*)d_mhi16, (void*)d_mlo16, (void*)d_unscale, (void*)d_sched})
       if (p) cudaFree(p);
   }
   int launches() const { return n_items ? 3 : 0; }
@@ -880,7 +968,30 @@ struct M2LTcPlan {
     rows = pair ? 2 * tc::BM : tc::BM;
     // ---- tiles (rows same-class targets) and their tap segments
     std::vector<int> tile_out, seg_mat, seg_in, tile_seg{0};
-    for (const auto& grp : groups) {
+    // Inside a (level, octant) group, targets with the same transfer-vector set are made contiguous
+    // (signature = hash of the sorted tap list; ties keep Z-order), so a tile's taps are present for
+    // (nearly) all of its rows: boundary targets no longer pad interior tiles with zero rows.
+    bool by_sig = true;
+    if (const char* e = std::getenv("KIFMM_TC_SIG")) by_sig = std::atoi(e) != 0;
+    std::vector<std::vector<int64_t>> sorted_groups;
+    for (const auto& g0 : groups) {
+      std::vector<int64_t> grp(g0.begin(), g0.end());
+      if (by_sig) {
+        std::vector<std::pair<uint64_t, int64_t>> key;
+        for (int64_t b : grp) {
+          std::vector<int> tv(t.v_tv + t.v_ptr[b], t.v_tv + t.v_ptr[b + 1]);
+          std::sort(tv.begin(), tv.end());
+          uint64_t h = 1469598103934665603ull ^ uint64_t(tv.size());
+          for (int x : tv) h = (h ^ uint64_t(x)) * 1099511628211ull;
+          key.push_back({h, b});
+        }
+        std::stable_sort(key.begin(), key.end(),
+                         [](const auto& x, const auto& y) { return x.first < y.first; });
+        for (size_t i = 0; i < grp.size(); ++i) grp[i] = key[i].second;
+      }
+      sorted_groups.push_back(std::move(grp));
+    }
+    for (const auto& grp : sorted_groups) {
       for (size_t s0 = 0; s0 < grp.size(); s0 += size_t(rows)) {
         std::vector<int> out(rows, -1);
         std::map<int, std::vector<int>> taps;
@@ -932,6 +1043,8 @@ struct M2LTcPlan {
     up(&d_seg_mat, seg_mat, total);
     up(&d_seg_in, seg_in, total);
     up(&d_items, items, total);
+    sched_g = std::max(1, std::min(n_items, pair ? sm_count() / 2 : sm_count()));
+    up(&d_sched, lpt_schedule(items, sched_g), total);
     // ---- K_t split into tf32 hi / lo, padded to 160 x 160 per transfer vector
     const int ne = ops.n_e, nc = ops.n_c, nt = ops.n_m2l;
     std::vector<float> khi(size_t(nt) * tc::NP * tc::NP, 0.f), klo(khi.size(), 0.f);
@@ -1018,18 +1131,18 @@ struct M2LTcPlan {
       attr[0].val.clusterDim.x = 2;
       attr[0].val.clusterDim.y = 1;
       attr[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3(2 * n_items);
+      cfg.gridDim = dim3(2 * sched_g);
       cfg.blockDim = dim3(tc::THREADS);
       cfg.dynamicSmemBytes = tc::Cfg<P, R, ES>::SMEM_BYTES;
       cfg.stream = s;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<P, R, ES>, mh, ml, ah, al, (const tc::Item*)d_items,
+      KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<P, R, ES>, mh, ml, ah, al, (const tc::Item*)d_items, (const int*)d_sched,
                                     (const int*)d_seg_mat, (const int*)d_seg_in, int(nn), un, ku,
-                                    tc::Epi{d_partial, nullptr, nullptr, nullptr, 0}));
+                                    tc::Epi{d_partial, nullptr, nullptr, nullptr, 0, tc_debug()}));
     } else {
-      tc::m2l_tc_kernel<P, R, ES><<<n_items, tc::THREADS, tc::Cfg<P, R, ES>::SMEM_BYTES, s>>>(
-          mh, ml, ah, al, d_items, d_seg_mat, d_seg_in, int(nn), un, ku, tc::Epi{d_partial, nullptr, nullptr, nullptr, 0});
+      tc::m2l_tc_kernel<P, R, ES><<<sched_g, tc::THREADS, tc::Cfg<P, R, ES>::SMEM_BYTES, s>>>(
+          mh, ml, ah, al, d_items, d_sched, d_seg_mat, d_seg_in, int(nn), un, ku, tc::Epi{d_partial, nullptr, nullptr, nullptr, 0, tc_debug()});
     }
     KIFMM_LAUNCH_CHECK();
   }
@@ -1129,8 +1242,8 @@ struct TcSplit {
 // scale per output column common to all matrices (so 1/sigma factors of the pseudo-inverse stay in
 // range); the epilogue multiplies the column unscale back.
 struct TcGemm {
-  int n_tiles = 0;
-  int *d_out = nullptr, *d_seg_mat = nullptr, *d_seg_in = nullptr;
+  int n_tiles = 0, sched_g = 0;
+  int *d_out = nullptr, *d_seg_mat = nullptr, *d_seg_in = nullptr, *d_sched = nullptr;
   tc::Item* d_items = nullptr;
   __half *d_bhi = nullptr, *d_blo = nullptr;
   float* d_cu = nullptr;
@@ -1140,7 +1253,7 @@ struct TcGemm {
   TcGemm& operator=(const TcGemm&) = delete;
   ~TcGemm() {
     for (void* p : {(void*)d_out, (void*)d_seg_mat, (void*)d_seg_in, (void*)d_items, (void*)d_bhi, (void*)d_blo,
-                    (void*)d_cu})
+                    (void*)d_cu, (void*)d_sched})
       if (p) cudaFree(p);
   }
 
@@ -1166,6 +1279,8 @@ struct TcGemm {
     M2LTcPlan::up(&d_seg_mat, seg_mat, total);
     M2LTcPlan::up(&d_seg_in, seg_in, total);
     M2LTcPlan::up(&d_items, items, total);
+    sched_g = std::max(1, std::min(n_tiles, sm_count()));
+    M2LTcPlan::up(&d_sched, lpt_schedule(items, sched_g), total);
     std::vector<float> cu(NP, 1.f);
     std::vector<__half> hi(B.size()), lo(B.size());
     for (int j = 0; j < NP; ++j) {
@@ -1205,9 +1320,9 @@ struct TcGemm {
   // dst[out rows] (=, or += when accumulate) A(split rows) . B^T
   void run(const TcSplit& a, float* dst, bool accumulate, cudaStream_t s) const {
     if (!n_tiles) return;
-    tc::m2l_tc_kernel<false, 64, 2><<<n_tiles, tc::THREADS, tc::Cfg<false, 64, 2>::SMEM_BYTES, s>>>(
-        tm_hi, tm_lo, a.hi, a.lo, d_items, d_seg_mat, d_seg_in, a.rows, a.un, 1.f,
-        tc::Epi{nullptr, d_out, d_cu, dst, accumulate ? 1 : 0});
+    tc::m2l_tc_kernel<false, 64, 2><<<sched_g, tc::THREADS, tc::Cfg<false, 64, 2>::SMEM_BYTES, s>>>(
+        tm_hi, tm_lo, a.hi, a.lo, d_items, d_sched, d_seg_mat, d_seg_in, a.rows, a.un, 1.f,
+        tc::Epi{nullptr, d_out, d_cu, dst, accumulate ? 1 : 0, 0});
     KIFMM_LAUNCH_CHECK();
   }
 };

@@ -329,6 +329,11 @@ __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, 
 // its own shared-memory slot and every lane reads it back as broadcasts; no
 // block-wide barriers.  Adds into the potentials/gradients of the near field.
 // works: {first target, surface_begin, surface_end, target count <= 32}; surfaces: {node, kind}.
+// Packed kernel works also embed the first surface (no dependent load before staging).
+struct FarWork {
+  int t0, count, surf_begin, surf_end;
+  int node0, kind0, pad0, pad1;
+};
 constexpr int kFarWarps = 6;
 constexpr int kFarMaxNe = 224;
 
@@ -375,6 +380,94 @@ __global__ void __launch_bounds__(kFarWarps * 32) far_kernel(P2PParams<T> p, con
   }
 }
 
+// fp32 far field with packed FP32x2 arithmetic and the final output write fused
+// in.  One warp per leaf chunk of <= 64 targets: lane -> (slice lane / T2,
+// target pair (ta, ta + T2)), T2 = ceil(n / 2), R = min(8, 32 / T2) slices that
+// split every staged surface; slice partials are combined with shuffles in a
+// fixed order.  The result pot[t] + far (grad[t] - far) is written to
+// pot_out[perm[t]] (input order) or back to pot[t] when perm is null.  Every
+// owned leaf has a work item (surf_begin == surf_end: output write only).
+template <bool GRAD>
+__global__ void __launch_bounds__(kFarWarps * 32) far_f2_kernel(P2PParams<float> p,
+                                                                 const FarWork* __restrict__ works, int n_works,
+                                                                 const int2* __restrict__ surfaces,
+                                                                 const float* __restrict__ M,
+                                                                 const float* __restrict__ L, float* pot, float* grad,
+                                                                 const int* __restrict__ perm, float* pot_out,
+                                                                 float* grad_out) {
+  __shared__ float4 sh[kFarWarps][kFarMaxNe + 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wi = blockIdx.x * kFarWarps + warp;
+  if (wi >= n_works) return;
+  const FarWork w = works[wi];
+  const int t0 = w.t0, nt = w.count, T2 = (nt + 1) >> 1;
+  int R = 32 / T2;
+  R = R > 8 ? 8 : R;
+  const int slice = lane / T2, ta = lane - slice * T2, tb = ta + T2;
+  const bool active = slice < R, has_b = active && tb < nt;
+  const int q = 4 * R, pad = (p.n_e + q - 1) / q * q, per = pad / R;
+  float4* my = sh[warp];
+  // everything below depends on the work only: issue all of it before any use
+  const float4 xa = p.src[t0 + (active ? ta : 0)], xb = p.src[t0 + (has_b ? tb : 0)];
+  const bool out_a = slice == 0, out_b = slice == 0 && tb < nt;
+  float pv[2] = {0.f, 0.f}, gv[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+  int ov[2] = {0, 0};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = t0 + (h ? tb : ta);
+    if (h ? out_b : out_a) {
+      pv[h] = pot[t];
+      if (GRAD)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) gv[h][d] = grad[3 * size_t(t) + d];
+      ov[h] = perm ? perm[t] : t;
+    }
+  }
+  const f2_t x = f2_pack(xa.x, xb.x), y = f2_pack(xa.y, xb.y), z = f2_pack(xa.z, xb.z);
+  f2_t ph = 0, gx = 0, gy = 0, gz = 0;
+  const float fa = float(kFarAway);
+  for (int si = w.surf_begin; si < w.surf_end; ++si) {
+    const int2 sf = si == w.surf_begin ? make_int2(w.node0, w.kind0) : surfaces[si];
+    const bool l2p = sf.y == kSrcL2P;
+    const float alpha = l2p ? p.alpha_outer : p.alpha_inner;
+    const float* dens = l2p ? L : M;
+    __syncwarp();
+    for (int j = lane; j < pad; j += 32)
+      my[j] = j < p.n_e ? surface_source(p, sf.x, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
+    __syncwarp();
+    if (active) p2p_round_f2<GRAD, false>(my, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
+  }
+  // fixed-order slice reduction into slice 0
+  float v[8];
+  f2_unpack(ph, v[0], v[4]);
+  f2_unpack(gx, v[1], v[5]);
+  f2_unpack(gy, v[2], v[6]);
+  f2_unpack(gz, v[3], v[7]);
+  for (int k = 1; k < R; ++k) {
+    const int src = lane + k * T2 < 32 ? lane + k * T2 : lane;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+      const float o = __shfl_sync(0xffffffffu, v[d], src);
+      if (GRAD || (d & 3) == 0) v[d] += (slice == 0 && lane + k * T2 < 32) ? o : 0.f;
+    }
+  }
+  if (slice != 0) return;
+  const float c = float(kInv4PiD);
+  float* po = perm ? pot_out : pot;
+  float* go = perm ? grad_out : grad;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (!(h ? out_b : out_a)) continue;
+    const int o = ov[h];
+    po[o] = pv[h] + c * v[4 * h];
+    if (GRAD) {
+      go[3 * size_t(o)] = gv[h][0] - c * v[4 * h + 1];
+      go[3 * size_t(o) + 1] = gv[h][1] - c * v[4 * h + 2];
+      go[3 * size_t(o) + 2] = gv[h][2] - c * v[4 * h + 3];
+    }
+  }
+}
+
 // Check potentials on a node's surface (alpha) from particle ranges: one warp
 // per work item, lane l owns check points l, l+32, ... (KMAX x 32 >= n_c); each
 // lane loads one source and the warp broadcasts it with shuffles.
@@ -384,6 +477,7 @@ __global__ void __launch_bounds__(kFarWarps * 32) far_kernel(P2PParams<T> p, con
 // (alpha > 1 around the node; X-list separation), so there is no r = 0 mask.
 struct CheckWork {
   int node, out_row, range_begin, range_end;
+  int first, count, level, pad;  // the first range and the node level, embedded (no dependent loads)
 };
 
 constexpr int kCheckWarps = 8;
@@ -433,6 +527,99 @@ __global__ void __launch_bounds__(kCheckWarps * 32) check_kernel(P2PParams<T> p,
   for (int m = 0; m < KMAX; ++m) {
     const int j = lane + 32 * m;
     if (j < ld_out) o[j] = j < p.n_e ? acc[m] * scale : T(0);
+  }
+}
+
+// fp32 check potentials with packed FP32x2 arithmetic: lane l owns check points
+// l + 32 m (m < KMAX) as KMAX / 2 lane pairs (+ one scalar point when KMAX is
+// odd); sources go through a warp-private shared-memory window of 32 (one
+// LDS.128 broadcast per source instead of four shuffles).  MUFU.RSQ-bound (one
+// per pair, no gradient), so no padded points beyond KMAX x 32.  Same work /
+// output contract as check_kernel.
+template <int KMAX>
+__global__ void __launch_bounds__(kCheckWarps * 32) check_f2_kernel(P2PParams<float> p,
+                                                                     const CheckWork* __restrict__ works, int n_works,
+                                                                     const int2* __restrict__ ranges, int ref_level,
+                                                                     float alpha, float* __restrict__ out, int ld_out) {
+  constexpr int KP = KMAX / 2;
+  constexpr bool ODD = (KMAX & 1) != 0;
+  __shared__ float4 sh[kCheckWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wi = blockIdx.x * kCheckWarps + warp;
+  if (wi >= n_works) return;
+  const CheckWork w = works[wi];
+  const float fa = float(kFarAway);
+  // first source window issued together with the node geometry (both depend on the work only)
+  const float4 pre = lane < w.count ? p.src[w.first + lane] : make_float4(fa, fa, fa, 0.f);
+  const float4 g = p.node_geom[w.node];
+  const float s = alpha * g.w;
+  auto coord = [&](int m, int d) {
+    const int j = lane + 32 * m;
+    const int jj = j < p.n_e ? j : 0;
+    return (d == 0 ? g.x : d == 1 ? g.y : g.z) + s * p.surface[3 * jj + d];
+  };
+  f2_t yx[KP > 0 ? KP : 1], yy[KP > 0 ? KP : 1], yz[KP > 0 ? KP : 1], acc[KP > 0 ? KP : 1];
+#pragma unroll
+  for (int m = 0; m < KP; ++m) {
+    yx[m] = f2_pack(coord(2 * m, 0), coord(2 * m + 1, 0));
+    yy[m] = f2_pack(coord(2 * m, 1), coord(2 * m + 1, 1));
+    yz[m] = f2_pack(coord(2 * m, 2), coord(2 * m + 1, 2));
+    acc[m] = 0;
+  }
+  float ox = 0.f, oy = 0.f, oz = 0.f, oacc = 0.f;
+  if (ODD) {
+    ox = coord(KMAX - 1, 0);
+    oy = coord(KMAX - 1, 1);
+    oz = coord(KMAX - 1, 2);
+  }
+  float4* my = sh[warp];
+  for (int r = w.range_begin; r < w.range_end; ++r) {
+    const int2 rg = r == w.range_begin ? make_int2(w.first, w.count) : ranges[r];
+    for (int b = 0; b < rg.y; b += 32) {
+      const int cnt = min(32, rg.y - b);
+      __syncwarp();
+      my[lane] = (r == w.range_begin && b == 0) ? pre
+                 : lane < cnt                   ? p.src[rg.x + b + lane]
+                                                : make_float4(fa, fa, fa, 0.f);
+      __syncwarp();
+      const int cnt4 = (cnt + 3) & ~3;
+      for (int k = 0; k < cnt4; k += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 sv = my[k + u];
+          const f2_t sx = f2_pack(sv.x, sv.x), sy = f2_pack(sv.y, sv.y), sz = f2_pack(sv.z, sv.z);
+          const f2_t sq = f2_pack(sv.w, sv.w);
+#pragma unroll
+          for (int m = 0; m < KP; ++m) {
+            const f2_t dx = f2_sub(yx[m], sx), dy = f2_sub(yy[m], sy), dz = f2_sub(yz[m], sz);
+            const f2_t r2 = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+            float ra, rb;
+            f2_unpack(r2, ra, rb);
+            acc[m] = f2_fma(sq, f2_pack(rinv(ra), rinv(rb)), acc[m]);
+          }
+          if (ODD) {
+            const float dx = ox - sv.x, dy = oy - sv.y, dz = oz - sv.z;
+            oacc = fmaf(sv.w, rinv(fmaf(dz, dz, fmaf(dy, dy, dx * dx))), oacc);
+          }
+        }
+      }
+    }
+  }
+  const int e = ref_level - w.level;  // |e| <= 15: exact power of two
+  const float scale = float(kInv4PiD) * (e >= 0 ? float(1 << e) : 1.f / float(1 << (-e)));
+  float* o = out + size_t(w.out_row) * ld_out;
+#pragma unroll
+  for (int m = 0; m < KMAX; ++m) {
+    float a;
+    if (ODD && m == KMAX - 1) {
+      a = oacc;
+    } else {
+      float a0, a1;
+      f2_unpack(acc[m / 2], a0, a1);
+      a = (m & 1) ? a1 : a0;
+    }
+    const int j = lane + 32 * m;
+    if (j < ld_out) o[j] = j < p.n_e ? a * scale : 0.f;
   }
 }
 

@@ -179,6 +179,13 @@ template <class T>
 void launch_check(int np, int n, const P2PParams<T>& pp, const CheckWork* works, const int2* ranges, const int* lvl,
                   int ref, T alpha, T* out, cudaStream_t s) {
   const int blocks = int(ceil_div(n, kCheckWarps));
+  if constexpr (sizeof(T) == 4) {
+    if (np == 160) {  // p = 6: packed fp32 kernel
+      check_f2_kernel<5><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, ref, alpha, out, np);
+      KIFMM_LAUNCH_CHECK();
+      return;
+    }
+  }
   switch ((np + 31) / 32) {
     case 1: check_kernel<T, 1><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
     case 2: check_kernel<T, 2><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
@@ -276,7 +283,7 @@ struct kifmm_gpu_plan {
   // work lists
   DevMem p2m_works, p2m_ranges, p2l_works, p2l_ranges;
   LeafPlan leaf_near, leaf_far;
-  DevMem far_works, far_surfaces, leaf_ptr_dev;
+  DevMem far_works, far_surfaces, leaf_ptr_dev;  // far_works: int4 (scalar kernel) or FarWork (packed)
   int n_far = 0;
   int n_p2m = 0, n_p2l = 0;
   GemmTiles solve_up1, solve_up2, solve_dn1, solve_dn2, m2l;
@@ -512,7 +519,9 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     std::vector<CheckWork> w;
     std::vector<int2> rg;
     for (int64_t l = lb; l < le; ++l) {
-      w.push_back({int(t.leaf_node[l]), int(l - lb), int(rg.size()), int(rg.size()) + 1});
+      const int64_t ln = t.leaf_node[l];
+      w.push_back({int(ln), int(l - lb), int(rg.size()), int(rg.size()) + 1, int(t.leaf_ptr[l]),
+                   int(t.leaf_ptr[l + 1] - t.leaf_ptr[l]), node_lvl(ln), 0});
       rg.push_back(make_int2(int(t.leaf_ptr[l]), int(t.leaf_ptr[l + 1] - t.leaf_ptr[l])));
       info.p2m_pairs += (t.leaf_ptr[l + 1] - t.leaf_ptr[l]) * ne;
     }
@@ -659,7 +668,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
         rg.push_back(make_int2(int(t.leaf_ptr[a]), int(t.leaf_ptr[a + 1] - t.leaf_ptr[a])));
         info.p2l_pairs += (t.leaf_ptr[a + 1] - t.leaf_ptr[a]) * ne;
       }
-      w.push_back({int(n), int(n), r0, int(rg.size())});
+      w.push_back({int(n), int(n), r0, int(rg.size()), rg[r0].x, rg[r0].y, node_lvl(n), 0});
     }
     n_p2l = int(w.size());
     p2l_works.upload(w, &dev_bytes);
@@ -670,9 +679,15 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   std::vector<std::vector<int64_t>> m2l_groups;
   {
     std::map<std::pair<int, int>, std::vector<int64_t>> groups;
+    // levels with few targets are one group (octant classes would each fill a fraction of a tile with
+    // zero rows); larger levels are split by octant (shared transfer-vector sets)
+    std::map<int, int64_t> per_level;
+    for (int64_t n = 0; n < nn; ++n)
+      if (active[n] && node_lvl(n) >= 2 && t.v_ptr[n] != t.v_ptr[n + 1]) ++per_level[node_lvl(n)];
     for (int64_t n = 0; n < nn; ++n) {
       if (!active[n] || node_lvl(n) < 2 || t.v_ptr[n] == t.v_ptr[n + 1]) continue;
-      groups[{node_lvl(n), key_octant(t.node_key[n])}].push_back(n);
+      const int lvl = node_lvl(n);
+      groups[{lvl, per_level[lvl] <= 2048 ? 0 : key_octant(t.node_key[n])}].push_back(n);
       info.m2l_pairs += t.v_ptr[n + 1] - t.v_ptr[n];
     }
     for (auto& kv : groups) m2l_groups.push_back(kv.second);
@@ -911,6 +926,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   // far field: one warp-work per owned leaf with any L2P / M2P surface
   {
     std::vector<int4> fw;
+    std::vector<FarWork> fw2;
     std::vector<int2> sf;
     for (int64_t l = lb; l < le; ++l) {
       const int64_t node = t.leaf_node[l];
@@ -924,12 +940,23 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
         sf.push_back(make_int2(int(t.w_idx[e]), kSrcM2P));
         info.m2p_pairs += ntl * ne;
       }
-      if (int(sf.size()) > b)
-        for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += 32)
-          fw.push_back(make_int4(int(t0), b, int(sf.size()), int(std::min<int64_t>(32, t.leaf_ptr[l + 1] - t0))));
+      // <= 32 targets per warp; the packed fp32 kernel has a work for every owned leaf (it also
+      // writes the final output), the scalar kernel only for leaves with far sources
+      const int chunk = 32;  // packed: 16 target pairs x 2 slices fill the warp
+      const int e = int(sf.size());
+      for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += chunk) {
+        const int cnt = int(std::min<int64_t>(chunk, t.leaf_ptr[l + 1] - t0));
+        if (packed)
+          fw2.push_back({int(t0), cnt, b, e, e > b ? sf[b].x : 0, e > b ? sf[b].y : 0, 0, 0});
+        else if (e > b)
+          fw.push_back(make_int4(int(t0), b, e, cnt));
+      }
     }
-    n_far = int(fw.size());
-    far_works.upload(fw, &dev_bytes);
+    n_far = int(packed ? fw2.size() : fw.size());
+    if (packed)
+      far_works.upload(fw2, &dev_bytes);
+    else
+      far_works.upload(fw, &dev_bytes);
     far_surfaces.upload(sf, &dev_bytes);
     std::vector<int64_t> lp(t.leaf_ptr, t.leaf_ptr + nl + 1);
     leaf_ptr_dev.upload(lp, &dev_bytes);
@@ -1140,7 +1167,30 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   // leaves: near field (side stream, or here when timed) then L2P + M2P
   if (timed) leaf(leaf_near, false, s);
   else if (leaf_near.n) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
-  if (n_far) {
+  bool fused_out = false;  // the packed far kernel wrote the final (input-order) output
+  if constexpr (sizeof(T) == 4) {
+    if (leaf_packed && n_far) {
+      if (input_order && world > 1) {
+        KIFMM_CUDA(cudaMemsetAsync(pot_out.p, 0, pot_out.bytes, s));
+        if (grad) KIFMM_CUDA(cudaMemsetAsync(grad_out.p, 0, grad_out.bytes, s));
+      }
+      const int blocks = int(ceil_div(n_far, kFarWarps));
+      float* g = grad ? grad_buf.as<float>() : nullptr;
+      const int* pm = input_order ? perm.as<int>() : nullptr;
+      float* go = grad ? grad_out.as<float>() : nullptr;
+      if (grad)
+        far_f2_kernel<true><<<blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far, far_surfaces.as<int2>(),
+                                                              Mp, Lp, pot.as<float>(), g, pm, pot_out.as<float>(), go);
+      else
+        far_f2_kernel<false><<<blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far,
+                                                               far_surfaces.as<int2>(), Mp, Lp, pot.as<float>(), g, pm,
+                                                               pot_out.as<float>(), go);
+      KIFMM_LAUNCH_CHECK();
+      ++launches;
+      fused_out = true;
+    }
+  }
+  if (!fused_out && n_far) {
     const int blocks = int(ceil_div(n_far, kFarWarps));
     T* g = grad ? grad_buf.as<T>() : nullptr;
     if (grad)
@@ -1153,7 +1203,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     ++launches;
   }
   mark();  // 8
-  if (input_order) {
+  if (input_order && !fused_out) {
     if (world > 1) {
       KIFMM_CUDA(cudaMemsetAsync(pot_out.p, 0, pot_out.bytes, s));
       if (grad) KIFMM_CUDA(cudaMemsetAsync(grad_out.p, 0, grad_out.bytes, s));
