@@ -53,7 +53,7 @@ namespace tc {
 
 constexpr int BM = 128;  // target rows per CTA
 constexpr int NP = 160;  // check points / equivalent points, padded (p = 6)
-constexpr int EPI_WARPS = 8, EPI_COLS = NP / 2;
+constexpr int EPI_WARPS = 8, EPI_COLS = NP / 2;   // 2 warps per TMEM lane quarter, 80 columns each
 constexpr int EPI_WARP0 = 6;                         // epilogue warps 6..13
 constexpr int FWD_WARP = EPI_WARP0 + EPI_WARPS;      // 14: A-arrival forwarder (pair)
 constexpr int THREADS = (FWD_WARP + 1) * 32;
@@ -506,272 +506,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-// ---------------------------------------------------------------------------
-// A-in-TMEM variant (default).  With both operands in shared memory the three
-// MMAs per K step re-read A_hi twice and B_hi twice from SMEM (~115 B/clk at
-// the MMA rate, plus ~75 B/clk of incoming copies) -- over the ~128 B/clk SMEM
-// port -- which capped the tensor pipe near 60 %.  Here the producers load the
-// gathered fp32 rows with plain loads, split them into tf32 hi/lo in registers
-// and write both into TMEM with tcgen05.st (lane = target row, column = K), so
-// SMEM only carries K_t (TMA, SWIZZLE_64B) and A is read from L2 once, in fp32.
-// TMEM columns: accumulators [0,160) and [256,416); six A stages of 32 columns
-// (hi 16 + lo 16) at 160,192,224,416,448,480.
-namespace ta {
-constexpr int KB = 16;              // K values per stage
-constexpr int NKB = NP / KB;        // 10 stages per tap
-constexpr int STAGES = 6;
-constexpr int ROWB = KB * 4;        // 64-byte B rows, SWIZZLE_64B
-__host__ __device__ constexpr int a_col(int s) { return s < 3 ? 160 + 32 * s : 416 + 32 * (s - 3); }
-
-template <bool PAIR>
-struct Cfg {
-  static constexpr int CTAS = PAIR ? 2 : 1;
-  static constexpr int NB = PAIR ? NP / 2 : NP;
-  static constexpr int B_BYTES = NB * ROWB;  // per operand (hi or lo)
-  static constexpr int STAGE_BYTES = 2 * B_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512;
-  static constexpr uint32_t TX = uint32_t(CTAS * STAGE_BYTES);
-  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(NP >> 3) << 17) |
-                                    (uint32_t((CTAS * BM) >> 4) << 24);
-};
-
-template <bool PAIR>
-__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t accumulate) {
-  if constexpr (PAIR)
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(b), "r"(Cfg<PAIR>::IDESC), "r"(accumulate));
-  else
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(b), "r"(Cfg<PAIR>::IDESC), "r"(accumulate));
-}
-
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-          taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-      : "memory");
-}
-
-template <bool PAIR>
-__global__ void __launch_bounds__(THREADS, 1)
-    m2l_ta_kernel(const __grid_constant__ CUtensorMap tm_khi, const __grid_constant__ CUtensorMap tm_klo,
-                  const float* __restrict__ M, const Item* __restrict__ items, const int* __restrict__ seg_mat,
-                  const int* __restrict__ seg_in, float* __restrict__ partial) {
-  using C = Cfg<PAIR>;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
-  // bars: [0,S) b_full, [S,2S) empty (stage consumed), [2S,3S) a_full, [3S,3S+2) tfull, [3S+2,3S+4) tempty
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = PAIR ? cluster_rank() : 0u;
-  const Item it = items[PAIR ? (blockIdx.x >> 1) : blockIdx.x];
-  const int ntap = it.seg_end - it.seg_begin;
-  const int nstage = ntap * NKB;
-  const int rows = C::CTAS * BM;
-  const uint32_t sbase = smem_u32(smem);
-  auto b_hi = [&](int s) { return sbase + s * C::STAGE_BYTES; };
-  auto b_lo = [&](int s) { return sbase + s * C::STAGE_BYTES + C::B_BYTES; };
-  auto bfull = [&](int s) { return smem_u32(&bars[s]); };
-  auto empty = [&](int s) { return smem_u32(&bars[STAGES + s]); };
-  auto afull = [&](int s) { return smem_u32(&bars[2 * STAGES + s]); };
-  auto tfull = [&](int b) { return smem_u32(&bars[3 * STAGES + b]); };
-  auto tempty = [&](int b) { return smem_u32(&bars[3 * STAGES + 2 + b]); };
-  auto leader = [&](uint32_t a) { return PAIR ? mapa(a, 0) : a; };
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(bfull(s), 1);                // leader's expect_tx; B bytes of every CTA
-      mbar_init(empty(s), 1);                // tcgen05.commit (multicast when PAIR)
-      mbar_init(afull(s), C::CTAS * 4);      // one elected lane per A-producer warp per CTA
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(tfull(b), 1);
-      mbar_init(tempty(b), C::CTAS * EPI_WARPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_khi) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_klo) : "memory");
-  }
-  if (warp == 0) {
-    if constexpr (PAIR) {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                   "r"(TMEM_COLS));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-    } else {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                   "r"(TMEM_COLS));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (PAIR) cluster_sync();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    // ---------------- B producer (TMA, SWIZZLE_64B, this CTA's check rows of K_t hi/lo)
-    if (lane == 0) {
-      for (int i = 0; i < nstage; ++i) {
-        const int s = i % STAGES, round = i / STAGES;
-        mbar_wait(empty(s), (round & 1) ^ 1);
-        const int seg = it.seg_begin + i / NKB, kb = i % NKB;
-        const int row = seg_mat[seg] * NP + int(rank) * C::NB;
-        if (rank == 0) mbar_expect_tx(bfull(s), C::TX);
-        const uint32_t fb = leader(bfull(s));
-        tma_tile<PAIR>(b_hi(s), &tm_khi, fb, kb * KB, row);
-        tma_tile<PAIR>(b_lo(s), &tm_klo, fb, kb * KB, row);
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (leader): A from TMEM, B from SMEM, fresh accumulator per tap
-    if (rank == 0 && lane == 0) {
-      for (int j = 0; j < ntap; ++j) {
-        const int b = j & 1;
-        mbar_wait(tempty(b), ((j >> 1) & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem_base + uint32_t(b * 256);
-        for (int kb = 0; kb < NKB; ++kb) {
-          const int i = j * NKB + kb;
-          const int s = i % STAGES, round = i / STAGES;
-          mbar_wait(bfull(s), round & 1);
-          mbar_wait(afull(s), round & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t ah = tmem_base + uint32_t(a_col(s)), al = ah + KB;
-#pragma unroll
-          for (int k = 0; k < KB / 8; ++k) {
-            const uint64_t dbh = make_desc<ROWB>(b_hi(s) + 32 * k), dbl = make_desc<ROWB>(b_lo(s) + 32 * k);
-            mma_ts<PAIR>(d, ah + 8 * k, dbh, (kb > 0 || k > 0) ? 1u : 0u);
-            mma_ts<PAIR>(d, ah + 8 * k, dbl, 1u);
-            mma_ts<PAIR>(d, al + 8 * k, dbh, 1u);
-          }
-          commit<PAIR>(empty(s));
-        }
-        commit<PAIR>(tfull(b));
-      }
-    }
-  } else if (warp < 6) {
-    // ---------------- A producers: thread = target row (TMEM lane); 16 fp32 per stage, loaded
-    //                  two stages ahead, split to tf32 hi/lo and stored into the stage's TMEM columns
-    const int q = warp & 3;
-    const int row = q * 32 + lane;
-    const uint32_t lane_addr = uint32_t(q * 32) << 16;
-    float4 buf[3][4];
-    auto load = [&](int i, float4 (&v)[4]) {
-      const int seg = it.seg_begin + i / NKB, kb = i % NKB;
-      const int src = seg_in[size_t(seg) * rows + rank * BM + row];
-      if (src < 0) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      } else {
-        const float4* g = reinterpret_cast<const float4*>(M + size_t(src) * NP + kb * KB);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldg(g + u);
-      }
-    };
-    auto store = [&](int i, const float4 (&v)[4]) {
-      const int s = i % STAGES, round = i / STAGES;
-      mbar_wait(empty(s), (round & 1) ^ 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t hi[16], lo[16];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float x[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          uint32_t h;
-          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x[e]));
-          hi[4 * u + e] = h;
-          lo[4 * u + e] = __float_as_uint(x[e] - __uint_as_float(h));
-        }
-      }
-      const uint32_t col = tmem_base + lane_addr + uint32_t(a_col(s));
-      tmem_st16(col, hi);
-      tmem_st16(col + KB, lo);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-        if (PAIR)
-          mbar_arrive_cluster(leader(afull(s)));
-        else
-          mbar_arrive_local(afull(s));
-      }
-    };
-    if (nstage > 0) load(0, buf[0]);
-    if (nstage > 1) load(1, buf[1]);
-    int i = 0;
-    for (; i + 2 < nstage; i += 3) {
-      load(i + 2, buf[2]);
-      store(i, buf[0]);
-      if (i + 3 < nstage) load(i + 3, buf[0]);
-      store(i + 1, buf[1]);
-      if (i + 4 < nstage) load(i + 4, buf[1]);
-      store(i + 2, buf[2]);
-    }
-    if (i < nstage) store(i, buf[0]);
-    if (i + 1 < nstage) store(i + 1, buf[1]);
-  } else if (warp < EPI_WARP0 + EPI_WARPS) {
-    // ---------------- epilogue (warps 6-13): per-tap promotion into fp32 registers
-    const int q = warp & 3, h = (warp - EPI_WARP0) >> 2;
-    const int row = q * 32 + lane;
-    float acc[EPI_COLS];
-#pragma unroll
-    for (int k = 0; k < EPI_COLS; ++k) acc[k] = 0.f;
-    for (int j = 0; j < ntap; ++j) {
-      const int b = j & 1;
-      mbar_wait(tfull(b), (j >> 1) & 1);
-      __syncwarp();
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * 256 + h * EPI_COLS);
-#pragma unroll
-      for (int cb = 0; cb < EPI_COLS / 16; ++cb) {
-        uint32_t v[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(taddr + uint32_t(cb * 16)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int k = 0; k < 16; ++k) acc[cb * 16 + k] += __uint_as_float(v[k]);
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-        if (PAIR)
-          mbar_arrive_cluster(leader(tempty(b)));
-        else
-          mbar_arrive_local(tempty(b));
-      }
-    }
-    float4* o4 =
-        reinterpret_cast<float4*>(partial + (size_t(it.slot) * rows + rank * BM + row) * NP + h * EPI_COLS);
-#pragma unroll
-    for (int k = 0; k < EPI_COLS / 4; ++k)
-      o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (PAIR) cluster_sync();
-  if (warp == 0) {
-    __syncwarp();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if constexpr (PAIR)
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
-    else
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
-  }
-}
-}  // namespace ta
 
 // x = hi + lo with hi = tf32(x) (round to nearest, ties away), lo exact in fp32.
 __global__ void split_tf32_kernel(const float* __restrict__ x, size_t n, float* __restrict__ hi,
@@ -899,8 +633,6 @@ struct M2LTcPlan {
   bool pair = false;  // 2-CTA (cta_group::2) kernel on large trees; KIFMM_TC_PAIR=0/1 forces the choice
   int rows = 256;    // output rows per tile
   int rowb = 128;    // bytes per operand row per stage (128: SWIZZLE_128B, 64: SWIZZLE_64B)
-  bool a_tmem = false;  // A operand in SMEM (default) or TMEM (KIFMM_TC_AMODE=tmem; measured slower)
-  CUtensorMap tm_bhi64{}, tm_blo64{};
   bool f16 = true;  // 3-term fp16 split (kind::f16) with power-of-two row scaling; KIFMM_TC_KIND=tf32 for 3xTF32
   static constexpr float kKScale = 256.f;
   __half *d_khi16 = nullptr, *d_klo16 = nullptr, *d_mhi16 = nullptr, *d_mlo16 = nullptr;
@@ -1044,6 +776,7 @@ struct M2LTcPlan {
     up(&d_seg_in, seg_in, total);
     up(&d_items, items, total);
     sched_g = std::max(1, std::min(n_items, pair ? sm_count() / 2 : sm_count()));
+    if (const char* e = std::getenv("KIFMM_TC_GRID")) sched_g = std::max(1, std::min(n_items, std::atoi(e)));
     up(&d_sched, lpt_schedule(items, sched_g), total);
     // ---- K_t split into tf32 hi / lo, padded to 160 x 160 per transfer vector
     const int ne = ops.n_e, nc = ops.n_c, nt = ops.n_m2l;
@@ -1079,13 +812,7 @@ struct M2LTcPlan {
     set_smem<true, 128>();
     set_smem<false, 64>();
     set_smem<true, 64>();
-    if (const char* e = std::getenv("KIFMM_TC_AMODE")) a_tmem = std::string(e) == "tmem";
-    encode(reinterpret_cast<EncodeFn>(fn), &tm_bhi64, d_khi, uint64_t(nt) * tc::NP, brow, 64);
-    encode(reinterpret_cast<EncodeFn>(fn), &tm_blo64, d_klo, uint64_t(nt) * tc::NP, brow, 64);
-    KIFMM_CUDA(cudaFuncSetAttribute(tc::ta::m2l_ta_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::ta::Cfg<false>::SMEM_BYTES));
-    KIFMM_CUDA(cudaFuncSetAttribute(tc::ta::m2l_ta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::ta::Cfg<true>::SMEM_BYTES));
+
     // ---- f16 kind: K_t * 2^8 split into fp16 hi/lo; multipoles split per row with a power-of-two scale
     if (const char* e = std::getenv("KIFMM_TC_KIND")) f16 = std::string(e) != "tf32";
     if (f16) {
@@ -1147,37 +874,9 @@ struct M2LTcPlan {
     KIFMM_LAUNCH_CHECK();
   }
 
-  template <bool P>
-  void run_ta(const float* M, cudaStream_t s) {
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = P ? 2 : 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3((P ? 2 : 1) * n_items);
-    cfg.blockDim = dim3(tc::THREADS);
-    cfg.dynamicSmemBytes = tc::ta::Cfg<P>::SMEM_BYTES;
-    cfg.stream = s;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::ta::m2l_ta_kernel<P>, tm_bhi64, tm_blo64, M, (const tc::Item*)d_items,
-                                  (const int*)d_seg_mat, (const int*)d_seg_in, d_partial));
-  }
-
   // check += M2L(M): run the tcgen05 items, reduce partials.
   void launch(const float* M, float* check, int np, cudaStream_t s) {
     if (!n_items) return;
-    if (a_tmem) {
-      if (pair)
-        run_ta<true>(M, s);
-      else
-        run_ta<false>(M, s);
-      KIFMM_LAUNCH_CHECK();
-      tc::m2l_tc_reduce_kernel<<<dim3(n_tiles, rows / 16), 16 * (tc::NP / 4), 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
-      KIFMM_LAUNCH_CHECK();
-      return;
-    }
     if (f16) {
       tc::split_f16_rows_kernel<<<unsigned((nn + 8) / 8), 256, 0, s>>>(M, 0, int(nn) + 1, int(nn), d_mhi16, d_mlo16,
                                                                       d_unscale);
