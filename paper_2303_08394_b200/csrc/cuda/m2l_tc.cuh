@@ -53,10 +53,17 @@ namespace tc {
 
 constexpr int BM = 128;  // target rows per CTA
 constexpr int NP = 160;  // check points / equivalent points, padded (p = 6)
+// Warpgroups: 0 = {TMA + TMEM alloc, MMA issuer, A-arrival forwarder (pair), idle}, 1 = A producers,
+// 2-3 = epilogue.  The kernel launches with 96 registers per thread (__maxnreg__) and rebalances with
+// setmaxnreg (warpgroups 0-1 down to 56, epilogue up to 136): a CTA holds 48 K registers instead of
+// 60 K, leaving registers on the SM for small blocks of other kernels next to it.
 constexpr int EPI_WARPS = 8, EPI_COLS = NP / 2;   // 2 warps per TMEM lane quarter, 80 columns each
-constexpr int EPI_WARP0 = 6;                         // epilogue warps 6..13
-constexpr int FWD_WARP = EPI_WARP0 + EPI_WARPS;      // 14: A-arrival forwarder (pair)
-constexpr int THREADS = (FWD_WARP + 1) * 32;
+constexpr int EPI_WARP0 = 8;                      // epilogue warps 8..15
+constexpr int PROD_WARP0 = 4;                     // A producer warps 4..7
+constexpr int FWD_WARP = 2;                       // A-arrival forwarder (pair)
+constexpr int THREADS = 512;
+constexpr int LAUNCH_REGS = 96, LOW_REGS = 56, EPI_REGS = 136;
+static_assert(4 * 32 * LOW_REGS * 2 + 8 * 32 * EPI_REGS <= THREADS * LAUNCH_REGS, "setmaxnreg budget");
 constexpr uint32_t TMEM_COLS = 512;  // two 160-column accumulators at 0 and 256
 
 // ROWB: bytes of one operand row per stage (K block of ROWB/4 fp32): 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B,
@@ -221,7 +228,7 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map
 }
 
 template <bool PAIR, int ROWB, int ES>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __maxnreg__(LAUNCH_REGS)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tm_khi, const __grid_constant__ CUtensorMap tm_klo,
                   const void* __restrict__ m_hi, const void* __restrict__ m_lo, const Item* __restrict__ items,
                   const int* __restrict__ sched, const int* __restrict__ seg_mat, const int* __restrict__ seg_in, int zero_row,
@@ -290,129 +297,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (PAIR) cluster_sync();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  if (warp >= EPI_WARP0) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
 
-  if (warp == 0) {
-    // ---------------- B producer: this CTA's rows of K_t hi/lo (TMA tile, swizzled)
-    if (lane == 0) {
-      int gi = 0;
-      for (int kk = k_begin; kk < k_end; ++kk) {
-        const Item it = items[sched_list[kk]];
-        const int nstage = (it.seg_end - it.seg_begin) * NKB;
-        for (int i = 0; i < nstage; ++i, ++gi) {
-          const int s = gi % C::STAGES, round = gi / C::STAGES;
-          mbar_wait(empty(s), (round & 1) ^ 1);
-          const int seg = it.seg_begin + i / NKB, kb = i % NKB;
-          const int row = seg_mat[seg] * NP + int(rank) * C::NB;
-          if (epi.debug & 2) {
-            if (rank == 0) mbar_expect_tx(full(s), 0);
-            continue;
-          }
-          if (rank == 0) mbar_expect_tx(full(s), C::TX);
-          const uint32_t fb = leader(full(s));
-          tma_tile<PAIR>(b_hi(s), &tm_khi, fb, kb * KB, row);
-          tma_tile<PAIR>(b_lo(s), &tm_klo, fb, kb * KB, row);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (leader only): a fresh accumulator per tap
-    if (rank == 0 && lane == 0) {
-      int gi = 0, gj = 0;
-      const bool prof = (epi.debug & 8) != 0;
-      unsigned long long t_all = clock64(), t_te = 0, t_fu = 0;
-      for (int kk = k_begin; kk < k_end; ++kk) {
-        const Item it = items[sched_list[kk]];
-        const int ntap = it.seg_end - it.seg_begin;
-        for (int j = 0; j < ntap; ++j, ++gj) {
-          const int b = gj & 1;
-          unsigned long long c0 = prof ? clock64() : 0;
-          mbar_wait(tempty(b), ((gj >> 1) & 1) ^ 1);
-          if (prof) t_te += clock64() - c0;
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t d = tmem_base + uint32_t(b * 256);
-          for (int kb = 0; kb < NKB; ++kb, ++gi) {
-            const int s = gi % C::STAGES, round = gi / C::STAGES;
-            c0 = prof ? clock64() : 0;
-            mbar_wait(full(s), round & 1);
-            if (prof) t_fu += clock64() - c0;
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-            for (int k = 0; k < ROWB / 32; ++k) {  // 32 bytes of K per MMA (8 tf32 / 16 f16)
-              const uint64_t dah = make_desc<ROWB>(a_hi(s) + 32 * k), dal = make_desc<ROWB>(a_lo(s) + 32 * k);
-              const uint64_t dbh = make_desc<ROWB>(b_hi(s) + 32 * k), dbl = make_desc<ROWB>(b_lo(s) + 32 * k);
-              mma<PAIR, ES>(d, dah, dbh, (kb > 0 || k > 0) ? 1u : 0u);
-              mma<PAIR, ES>(d, dah, dbl, 1u);
-              mma<PAIR, ES>(d, dal, dbh, 1u);
-            }
-            commit<PAIR>(empty(s));
-          }
-          commit<PAIR>(tfull(b));
-        }
-      }
-      if (prof && (blockIdx.x == 0 || blockIdx.x == 64))
-        printf("cta %d: total %llu wait_tempty %llu wait_full %llu taps %d stages %d\n", int(blockIdx.x),
-               clock64() - t_all, t_te, t_fu, gj, gi);
-    }
-  } else if (warp >= 2 && warp < 6) {
-    // ---------------- A producers: thread -> (16-byte chunk c, rows r0 + 16 j) of this CTA, cp.async
-    //                  into the swizzled K-major layout; up to STAGES stages in flight per thread
-    constexpr int CH = ROWB / 16;     // 16-byte chunks per row
-    constexpr int RPI = 128 / CH;     // rows covered by the 128 producer threads per pass
-    constexpr int J = BM / RPI;       // passes (rows per thread)
-    const int t = threadIdx.x - 64;  // 0..127
-    const int c = t % CH, r0 = t / CH;
-    int src[J];
-    int gi = 0;
-    for (int kk = k_begin; kk < k_end; ++kk) {
-      const Item it = items[sched_list[kk]];
-      const int nstage = (it.seg_end - it.seg_begin) * NKB;
-      int cur_seg = -1;
-      for (int i = 0; i < nstage; ++i, ++gi) {
-        const int s = gi % C::STAGES, round = gi / C::STAGES;
-        const int seg = it.seg_begin + i / NKB, kb = i % NKB;
-        if (seg != cur_seg) {
-          cur_seg = seg;
-#pragma unroll
-          for (int j = 0; j < J; ++j) src[j] = seg_in[size_t(seg) * rows + rank * BM + r0 + RPI * j];
-        }
-        mbar_wait(empty(s), (round & 1) ^ 1);
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          const int r = r0 + RPI * j;
-          const int sw = ROWB == 128 ? (r & 7) : ((r & 7) >> 1);  // Swizzle<3,4,3> / Swizzle<2,4,3>
-          const uint32_t off = uint32_t((r >> 3) * C::ATOM + (r & 7) * ROWB + ((c ^ sw) << 4));
-          const bool ok = src[j] >= 0;  // absent source: zero-fill, no global read
-          const size_t g = size_t(ok ? src[j] : zero_row) * NP * ES + kb * ROWB + c * 16;  // bytes
-          const int sz = ok ? 16 : 0;
-          if (epi.debug & 1) continue;
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_hi(s) + off),
-                       "l"(static_cast<const char*>(m_hi) + g), "r"(sz)
-                       : "memory");
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_lo(s) + off),
-                       "l"(static_cast<const char*>(m_lo) + g), "r"(sz)
-                       : "memory");
-        }
-        // non-blocking: the barrier receives this thread's arrival when its copies have landed
-        // (as CUTLASS's cp.async UMMA mainloops do; the full barrier's count includes these arrivals)
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(PAIR ? afull(s) : full(s))
-                     : "memory");
-      }
-    }
-  } else if (warp == FWD_WARP) {
-    // ---------------- forwarder (pair): this CTA's A rows landed -> one arrive on the leader's stage barrier
-    if (PAIR && lane == 0) {
-      int gi = 0;
-      for (int kk = k_begin; kk < k_end; ++kk) {
-        const Item it = items[sched_list[kk]];
-        const int nstage = (it.seg_end - it.seg_begin) * NKB;
-        for (int i = 0; i < nstage; ++i, ++gi) {
-          const int s = gi % C::STAGES, round = gi / C::STAGES;
-          mbar_wait(afull(s), round & 1);
-          mbar_arrive_cluster(leader(full(s)));
-        }
-      }
-    }
-  } else if (warp >= EPI_WARP0) {
     // ---------------- epilogue: per-tap promotion; warp w reads TMEM lanes 32*(w%4).. (its rows)
     //                  and columns [h*80, h*80+80), h = (w-6)/4
     const int q = warp & 3, h = (warp - EPI_WARP0) >> 2;
@@ -490,6 +377,130 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int k = 0; k < EPI_COLS / 4; ++k)
           o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(LOW_REGS));
+    if (warp == 0) {
+      // ---------------- B producer: this CTA's rows of K_t hi/lo (TMA tile, swizzled)
+      if (lane == 0) {
+        int gi = 0;
+        for (int kk = k_begin; kk < k_end; ++kk) {
+          const Item it = items[sched_list[kk]];
+          const int nstage = (it.seg_end - it.seg_begin) * NKB;
+          for (int i = 0; i < nstage; ++i, ++gi) {
+            const int s = gi % C::STAGES, round = gi / C::STAGES;
+            mbar_wait(empty(s), (round & 1) ^ 1);
+            const int seg = it.seg_begin + i / NKB, kb = i % NKB;
+            const int row = seg_mat[seg] * NP + int(rank) * C::NB;
+            if (epi.debug & 2) {
+              if (rank == 0) mbar_expect_tx(full(s), 0);
+              continue;
+            }
+            if (rank == 0) mbar_expect_tx(full(s), C::TX);
+            const uint32_t fb = leader(full(s));
+            tma_tile<PAIR>(b_hi(s), &tm_khi, fb, kb * KB, row);
+            tma_tile<PAIR>(b_lo(s), &tm_klo, fb, kb * KB, row);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ---------------- MMA issuer (leader only): a fresh accumulator per tap
+      if (rank == 0 && lane == 0) {
+        int gi = 0, gj = 0;
+        const bool prof = (epi.debug & 8) != 0;
+        unsigned long long t_all = clock64(), t_te = 0, t_fu = 0;
+        for (int kk = k_begin; kk < k_end; ++kk) {
+          const Item it = items[sched_list[kk]];
+          const int ntap = it.seg_end - it.seg_begin;
+          for (int j = 0; j < ntap; ++j, ++gj) {
+            const int b = gj & 1;
+            unsigned long long c0 = prof ? clock64() : 0;
+            mbar_wait(tempty(b), ((gj >> 1) & 1) ^ 1);
+            if (prof) t_te += clock64() - c0;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t d = tmem_base + uint32_t(b * 256);
+            for (int kb = 0; kb < NKB; ++kb, ++gi) {
+              const int s = gi % C::STAGES, round = gi / C::STAGES;
+              c0 = prof ? clock64() : 0;
+              mbar_wait(full(s), round & 1);
+              if (prof) t_fu += clock64() - c0;
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  #pragma unroll
+              for (int k = 0; k < ROWB / 32; ++k) {  // 32 bytes of K per MMA (8 tf32 / 16 f16)
+                const uint64_t dah = make_desc<ROWB>(a_hi(s) + 32 * k), dal = make_desc<ROWB>(a_lo(s) + 32 * k);
+                const uint64_t dbh = make_desc<ROWB>(b_hi(s) + 32 * k), dbl = make_desc<ROWB>(b_lo(s) + 32 * k);
+                mma<PAIR, ES>(d, dah, dbh, (kb > 0 || k > 0) ? 1u : 0u);
+                mma<PAIR, ES>(d, dah, dbl, 1u);
+                mma<PAIR, ES>(d, dal, dbh, 1u);
+              }
+              commit<PAIR>(empty(s));
+            }
+            commit<PAIR>(tfull(b));
+          }
+        }
+        if (prof && (blockIdx.x == 0 || blockIdx.x == 64))
+          printf("cta %d: total %llu wait_tempty %llu wait_full %llu taps %d stages %d\n", int(blockIdx.x),
+                 clock64() - t_all, t_te, t_fu, gj, gi);
+      }
+    } else if (warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
+      // ---------------- A producers: thread -> (16-byte chunk c, rows r0 + 16 j) of this CTA, cp.async
+      //                  into the swizzled K-major layout; up to STAGES stages in flight per thread
+      constexpr int CH = ROWB / 16;     // 16-byte chunks per row
+      constexpr int RPI = 128 / CH;     // rows covered by the 128 producer threads per pass
+      constexpr int J = BM / RPI;       // passes (rows per thread)
+      const int t = threadIdx.x - 32 * PROD_WARP0;  // 0..127
+      const int c = t % CH, r0 = t / CH;
+      int src[J];
+      int gi = 0;
+      for (int kk = k_begin; kk < k_end; ++kk) {
+        const Item it = items[sched_list[kk]];
+        const int nstage = (it.seg_end - it.seg_begin) * NKB;
+        int cur_seg = -1;
+        for (int i = 0; i < nstage; ++i, ++gi) {
+          const int s = gi % C::STAGES, round = gi / C::STAGES;
+          const int seg = it.seg_begin + i / NKB, kb = i % NKB;
+          if (seg != cur_seg) {
+            cur_seg = seg;
+  #pragma unroll
+            for (int j = 0; j < J; ++j) src[j] = seg_in[size_t(seg) * rows + rank * BM + r0 + RPI * j];
+          }
+          mbar_wait(empty(s), (round & 1) ^ 1);
+  #pragma unroll
+          for (int j = 0; j < J; ++j) {
+            const int r = r0 + RPI * j;
+            const int sw = ROWB == 128 ? (r & 7) : ((r & 7) >> 1);  // Swizzle<3,4,3> / Swizzle<2,4,3>
+            const uint32_t off = uint32_t((r >> 3) * C::ATOM + (r & 7) * ROWB + ((c ^ sw) << 4));
+            const bool ok = src[j] >= 0;  // absent source: zero-fill, no global read
+            const size_t g = size_t(ok ? src[j] : zero_row) * NP * ES + kb * ROWB + c * 16;  // bytes
+            const int sz = ok ? 16 : 0;
+            if (epi.debug & 1) continue;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_hi(s) + off),
+                         "l"(static_cast<const char*>(m_hi) + g), "r"(sz)
+                         : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_lo(s) + off),
+                         "l"(static_cast<const char*>(m_lo) + g), "r"(sz)
+                         : "memory");
+          }
+          // non-blocking: the barrier receives this thread's arrival when its copies have landed
+          // (as CUTLASS's cp.async UMMA mainloops do; the full barrier's count includes these arrivals)
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(PAIR ? afull(s) : full(s))
+                       : "memory");
+        }
+      }
+    } else if (warp == FWD_WARP) {
+      // ---------------- forwarder (pair): this CTA's A rows landed -> one arrive on the leader's stage barrier
+      if (PAIR && lane == 0) {
+        int gi = 0;
+        for (int kk = k_begin; kk < k_end; ++kk) {
+          const Item it = items[sched_list[kk]];
+          const int nstage = (it.seg_end - it.seg_begin) * NKB;
+          for (int i = 0; i < nstage; ++i, ++gi) {
+            const int s = gi % C::STAGES, round = gi / C::STAGES;
+            mbar_wait(afull(s), round & 1);
+            mbar_arrive_cluster(leader(full(s)));
+          }
+        }
       }
     }
   }
