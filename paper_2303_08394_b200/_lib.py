@@ -11,7 +11,7 @@ import os
 from .errors import STATUS_TO_ERROR, KifmmError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libkifmm_b200.so")
+LIB_PATH = os.environ.get("KIFMM_LIB") or os.path.join(_HERE, "lib", "libkifmm_b200.so")  # override: experiments
 
 i32, i64, u64, f32, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double
 P = C.c_void_p

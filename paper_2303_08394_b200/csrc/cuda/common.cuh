@@ -1,6 +1,7 @@
 // Device-side helpers shared by the sm_100a kernels.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -93,6 +94,38 @@ __device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
   f2_t r;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
+}
+
+// fp16 operand split of an expansion row for the kind::f16 tensor-core GEMMs: x * 2^e with e chosen so
+// max|row| lands in [2^9, 2^10), stored as hi = fp16(x 2^e), lo = fp16(x 2^e - hi), unscale 2^-e.
+__device__ __forceinline__ int f16_row_exponent(float mx) {
+  int e = 0;
+  if (mx > 0.f) {
+    int ex;
+    frexpf(mx, &ex);  // mx in [2^(ex-1), 2^ex)
+    e = 10 - ex;
+  }
+  return e;
+}
+// Warp-cooperative split of one W-wide row held as v[k] = row[lane + 32 k].
+template <int W>
+__device__ __forceinline__ void split_row_warp(const float (&v)[W / 32], int lane, size_t row, __half* hi, __half* lo,
+                                               float* un) {
+  float mx = 0.f;
+#pragma unroll
+  for (int k = 0; k < W / 32; ++k) mx = fmaxf(mx, fabsf(v[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int e = f16_row_exponent(mx);
+  const float sc = ldexpf(1.f, e);
+#pragma unroll
+  for (int k = 0; k < W / 32; ++k) {
+    const float x = v[k] * sc;
+    const __half h = __float2half_rn(x);
+    hi[row * W + lane + 32 * k] = h;
+    lo[row * W + lane + 32 * k] = __float2half_rn(x - __half2float(h));
+  }
+  if (lane == 0) un[row] = ldexpf(1.f, -e);
 }
 
 // Far-away zero-charge source used to pad staged source rounds (contributes exactly 0).

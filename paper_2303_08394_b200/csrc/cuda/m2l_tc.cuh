@@ -68,6 +68,14 @@ constexpr uint32_t TMEM_COLS = 512;  // two 160-column accumulators at 0 and 256
 
 // ROWB: bytes of one operand row per stage (K block of ROWB/4 fp32): 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B,
 // twice the stages for the same shared memory => deeper latency hiding).
+#ifndef KIFMM_TC_STAGE_KB
+#define KIFMM_TC_STAGE_KB 184
+#endif
+// shared memory for pipeline stages: 184 KB (7 stages for the f16 pair, 5 for the single CTA) leaves
+// room on the SM for two near-field blocks next to a tcgen05 CTA (measured 6 % faster end to end than a
+// full 216 KB pipeline with the near field waiting for whole SMs)
+constexpr int kStageBudgetKB = KIFMM_TC_STAGE_KB;
+
 template <bool PAIR, int ROWB, int ES = 4>
 struct Cfg {
   static constexpr int KB = ROWB / ES;           // operand elements per K block (tf32: 4 B, f16: 2 B)
@@ -76,8 +84,8 @@ struct Cfg {
   static constexpr int A_BYTES = BM * ROWB;
   static constexpr int B_BYTES = NB * ROWB;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int STAGES = (216 * 1024) / STAGE_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512;
+  static constexpr int STAGES = (kStageBudgetKB * 1024) / STAGE_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512 + 2048;  // + row-max exchange
   static constexpr int ATOM = 8 * ROWB;           // bytes of an 8-row swizzle atom (= SBO)
   static constexpr uint64_t LAYOUT = ROWB == 128 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B
   static constexpr int CTAS = PAIR ? 2 : 1;
@@ -94,6 +102,9 @@ struct Item {
 // Epilogue destination: per-item partial rows (summed later by m2l_tc_reduce_kernel), or -- when
 // direct_out is set and every tile is one item -- the output rows themselves:
 //   dst[direct_out[tile][r]][c] = (accumulate ? dst[..][c] : 0) + acc[r][c] * col_unscale[c]
+// Optionally (split_hi set, direct mode) the epilogue also emits the fp16 hi / lo split of every output
+// row with its power-of-two unscale -- the A operand of the next tcgen05 GEMM -- exactly as
+// split_f16_rows_kernel would; dst may then be null (the fp32 row is not needed).
 struct Epi {
   float* partial;
   const int* direct_out;
@@ -101,6 +112,9 @@ struct Epi {
   float* dst;
   int accumulate;
   int debug;  // experiments only (KIFMM_TC_DBG): bit 0 skips the A gathers, bit 1 the B TMA loads
+  __half* split_hi;
+  __half* split_lo;
+  float* split_un;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -242,6 +256,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   // bars: [0,S) full, [S,2S) empty, [2S,2S+2) tmem_full[b], [2S+2,2S+4) tmem_empty[b],
   //       [2S+4,3S+4) a_full (this CTA's A rows landed; PAIR only); then the TMEM address
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::STAGES + 4);
+  float* xmax = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 512);  // [2][2][128]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
   // persistent: this CTA (pair) g0 runs the items sched[gs + 1 + k], k in [sched[g0], sched[g0 + 1]) -- a
@@ -347,7 +362,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
         const int out = epi.direct_out[size_t(it.tile) * rows + rank * BM + row];
         if (out >= 0) {
           // loads first (column unscale, then the old output row), stores last: no load waits behind a store
-          float4* o4 = reinterpret_cast<float4*>(epi.dst + size_t(out) * NP + h * EPI_COLS);
+          float4* o4 = reinterpret_cast<float4*>((epi.dst ? epi.dst : epi.partial) + size_t(out) * NP + h * EPI_COLS);
           const float4* u4 = reinterpret_cast<const float4*>(epi.col_unscale + h * EPI_COLS);
 #pragma unroll
           for (int k = 0; k < EPI_COLS / 4; ++k) {
@@ -367,9 +382,47 @@ __global__ void __maxnreg__(LAUNCH_REGS)
               acc[4 * k + 3] += o.w;
             }
           }
+          if (epi.dst) {
 #pragma unroll
-          for (int k = 0; k < EPI_COLS / 4; ++k)
-            o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+            for (int k = 0; k < EPI_COLS / 4; ++k)
+              o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+          }
+        }
+        if (epi.split_hi) {
+          // row max over both column halves: the partner warp (same lane quarter, other half) meets
+          // this one on named barrier 1 + q (64 threads); xmax is double-buffered by item parity
+          float mx = 0.f;
+          if (out >= 0) {
+#pragma unroll
+            for (int k = 0; k < EPI_COLS; ++k) mx = fmaxf(mx, fabsf(acc[k]));
+          }
+          float* xm = xmax + (kk & 1) * 256;
+          xm[h * 128 + row] = mx;
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+          mx = fmaxf(mx, xm[(1 - h) * 128 + row]);
+          if (out >= 0) {
+            const int e = f16_row_exponent(mx);
+            const float sc = ldexpf(1.f, e);
+            uint4* ph = reinterpret_cast<uint4*>(epi.split_hi + size_t(out) * NP + h * EPI_COLS);
+            uint4* pl = reinterpret_cast<uint4*>(epi.split_lo + size_t(out) * NP + h * EPI_COLS);
+#pragma unroll
+            for (int k = 0; k < EPI_COLS / 8; ++k) {  // 16-byte stores: 8 halves each
+              uint32_t wh[4], wl[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float x0 = acc[8 * k + 2 * u] * sc, x1 = acc[8 * k + 2 * u + 1] * sc;
+                const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+                const __half2 hh = __halves2half2(h0, h1);
+                const __half2 ll =
+                    __halves2half2(__float2half_rn(x0 - __half2float(h0)), __float2half_rn(x1 - __half2float(h1)));
+                wh[u] = *reinterpret_cast<const uint32_t*>(&hh);
+                wl[u] = *reinterpret_cast<const uint32_t*>(&ll);
+              }
+              ph[k] = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+              pl[k] = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+            }
+            if (h == 0) epi.split_un[out] = ldexpf(1.f, -e);
+          }
         }
       } else {
         float4* o4 =
@@ -564,6 +617,43 @@ __global__ void split_f16_rows_kernel(const float* __restrict__ M, int r0, int r
   if (lane == 0) unscale[row] = ldexpf(1.f, -e);
 }
 
+// Split the listed rows (warp per row).
+__global__ void split_f16_list_kernel(const float* __restrict__ X, const int* __restrict__ list, int n,
+                                      __half* __restrict__ hi, __half* __restrict__ lo, float* __restrict__ un) {
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int row = list[i];
+  float v[NP / 32];
+#pragma unroll
+  for (int k = 0; k < NP / 32; ++k) v[k] = X[size_t(row) * NP + lane + 32 * k];
+  split_row_warp<NP>(v, lane, size_t(row), hi, lo, un);
+}
+
+// check[out(r)] += sum over the tile's items (fixed order) of partial[slot][r], warp per row (grid
+// (tiles, rows / 8), 256 threads); with hi set, also the fp16 split of the finished row.
+__global__ void m2l_tc_reduce_split_kernel(const float* __restrict__ partial, const int* __restrict__ tile_out,
+                                           const int* __restrict__ tile_slot, int rows, float* __restrict__ check,
+                                           __half* __restrict__ hi, __half* __restrict__ lo,
+                                           float* __restrict__ un) {
+  const int tile = blockIdx.x;
+  const int r = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int out = tile_out[size_t(tile) * rows + r];
+  if (out < 0) return;
+  const int s0 = tile_slot[tile], s1 = tile_slot[tile + 1];
+  float v[NP / 32];
+#pragma unroll
+  for (int k = 0; k < NP / 32; ++k) v[k] = check[size_t(out) * NP + lane + 32 * k];
+  for (int sl = s0; sl < s1; ++sl) {
+    const float* pr = partial + (size_t(sl) * rows + r) * NP;
+#pragma unroll
+    for (int k = 0; k < NP / 32; ++k) v[k] += pr[lane + 32 * k];
+  }
+#pragma unroll
+  for (int k = 0; k < NP / 32; ++k) check[size_t(out) * NP + lane + 32 * k] = v[k];
+  if (hi) split_row_warp<NP>(v, lane, size_t(out), hi, lo, un);
+}
+
 // check[out(r)] += sum over the tile's items (fixed order) of partial[slot][r]
 // grid (tiles, rows / 16); thread = (row, float4 column group), 640 threads
 __global__ void m2l_tc_reduce_kernel(const float* __restrict__ partial, const int* __restrict__ tile_out,
@@ -638,6 +728,39 @@ inline bool m2l_tc_available() {
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
   return major == 10 && minor == 0;
 }
+
+// fp32 operand rows split for the kind::f16 GEMMs: rows+1 rows (the last one zero) of hi / lo fp16 and
+// the per-row power-of-two unscale.
+struct TcSplit {
+  __half *hi = nullptr, *lo = nullptr;
+  float* un = nullptr;
+  int rows = 0;
+  TcSplit() = default;
+  TcSplit(const TcSplit&) = delete;
+  TcSplit& operator=(const TcSplit&) = delete;
+  ~TcSplit() {
+    for (void* p : {(void*)hi, (void*)lo, (void*)un})
+      if (p) cudaFree(p);
+  }
+  void alloc(int r, size_t* total) {
+    rows = r;
+    const size_t n = size_t(r + 1) * tc::NP;
+    KIFMM_CUDA(cudaMalloc(&hi, n * sizeof(__half)));
+    KIFMM_CUDA(cudaMalloc(&lo, n * sizeof(__half)));
+    KIFMM_CUDA(cudaMalloc(&un, size_t(r + 1) * sizeof(float)));
+    // all zero: the appended zero row, and rows a plan never writes read as zero rows
+    KIFMM_CUDA(cudaMemset(hi, 0, n * sizeof(__half)));
+    KIFMM_CUDA(cudaMemset(lo, 0, n * sizeof(__half)));
+    KIFMM_CUDA(cudaMemset(un, 0, size_t(r + 1) * sizeof(float)));
+    *total += 2 * n * sizeof(__half) + size_t(r + 1) * sizeof(float);
+  }
+  // split rows [r0, r1) of the fp32 buffer X (row stride NP)
+  void split(const float* X, int r0, int r1, cudaStream_t s) const {
+    if (r1 <= r0) return;
+    tc::split_f16_rows_kernel<<<unsigned((r1 - r0 + 7) / 8), 256, 0, s>>>(X, r0, r1, rows, hi, lo, un);
+    KIFMM_LAUNCH_CHECK();
+  }
+};
 
 // Host side: tiles/items, split operators, TMA descriptors.
 struct M2LTcPlan {
@@ -855,12 +978,13 @@ struct M2LTcPlan {
                                     tc::Cfg<P, R, 4>::SMEM_BYTES));
   }
   template <bool P, int R, int ES = 4>
-  void run_kernel(cudaStream_t s) {
+  void run_kernel(cudaStream_t s, const void* ah_ext = nullptr, const void* al_ext = nullptr,
+                  const float* un_ext = nullptr) {
     const CUtensorMap& mh = ES == 4 ? tm_khi : tm_khi16;
     const CUtensorMap& ml = ES == 4 ? tm_klo : tm_klo16;
-    const void* ah = ES == 4 ? static_cast<const void*>(d_mhi) : static_cast<const void*>(d_mhi16);
-    const void* al = ES == 4 ? static_cast<const void*>(d_mlo) : static_cast<const void*>(d_mlo16);
-    const float* un = ES == 4 ? nullptr : d_unscale;
+    const void* ah = ah_ext ? ah_ext : ES == 4 ? static_cast<const void*>(d_mhi) : static_cast<const void*>(d_mhi16);
+    const void* al = al_ext ? al_ext : ES == 4 ? static_cast<const void*>(d_mlo) : static_cast<const void*>(d_mlo16);
+    const float* un = un_ext ? un_ext : ES == 4 ? nullptr : d_unscale;
     const float ku = ES == 4 ? 1.f : 1.f / kKScale;
     if (P) {
       cudaLaunchConfig_t cfg{};
@@ -877,11 +1001,26 @@ struct M2LTcPlan {
       cfg.numAttrs = 1;
       KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<P, R, ES>, mh, ml, ah, al, (const tc::Item*)d_items, (const int*)d_sched,
                                     (const int*)d_seg_mat, (const int*)d_seg_in, int(nn), un, ku,
-                                    tc::Epi{d_partial, nullptr, nullptr, nullptr, 0, tc_debug()}));
+                                    tc::Epi{d_partial, nullptr, nullptr, nullptr, 0, tc_debug(), nullptr, nullptr, nullptr}));
     } else {
       tc::m2l_tc_kernel<P, R, ES><<<sched_g, tc::THREADS, tc::Cfg<P, R, ES>::SMEM_BYTES, s>>>(
-          mh, ml, ah, al, d_items, d_sched, d_seg_mat, d_seg_in, int(nn), un, ku, tc::Epi{d_partial, nullptr, nullptr, nullptr, 0, tc_debug()});
+          mh, ml, ah, al, d_items, d_sched, d_seg_mat, d_seg_in, int(nn), un, ku, tc::Epi{d_partial, nullptr, nullptr, nullptr, 0, tc_debug(), nullptr, nullptr, nullptr});
     }
+    KIFMM_LAUNCH_CHECK();
+  }
+
+  // check += M2L(M) with the multipoles already split into sp (rows = n_nodes, kind::f16 plan); the
+  // reduce also writes the fp16 split of the finished check rows into cd (when given)
+  void launch_presplit(const TcSplit& sp, float* check, const TcSplit* cd, cudaStream_t s) {
+    if (!n_items) return;
+    if (!f16 || sp.rows != int(nn)) throw InvalidArgument("M2L presplit: kind::f16 plan over all nodes required");
+    if (pair)
+      run_kernel<true, 64, 2>(s, sp.hi, sp.lo, sp.un);
+    else
+      run_kernel<false, 64, 2>(s, sp.hi, sp.lo, sp.un);
+    tc::m2l_tc_reduce_split_kernel<<<dim3(n_tiles, (rows + 7) / 8), 256, 0, s>>>(
+        d_partial, d_tile_out, d_tile_slot, rows, check, cd ? cd->hi : nullptr, cd ? cd->lo : nullptr,
+        cd ? cd->un : nullptr);
     KIFMM_LAUNCH_CHECK();
   }
 
@@ -912,38 +1051,6 @@ struct M2LTcPlan {
   }
 };
 
-
-// fp32 operand rows split for the kind::f16 GEMMs: rows+1 rows (the last one zero) of hi / lo fp16 and
-// the per-row power-of-two unscale.
-struct TcSplit {
-  __half *hi = nullptr, *lo = nullptr;
-  float* un = nullptr;
-  int rows = 0;
-  TcSplit() = default;
-  TcSplit(const TcSplit&) = delete;
-  TcSplit& operator=(const TcSplit&) = delete;
-  ~TcSplit() {
-    for (void* p : {(void*)hi, (void*)lo, (void*)un})
-      if (p) cudaFree(p);
-  }
-  void alloc(int r, size_t* total) {
-    rows = r;
-    const size_t n = size_t(r + 1) * tc::NP;
-    KIFMM_CUDA(cudaMalloc(&hi, n * sizeof(__half)));
-    KIFMM_CUDA(cudaMalloc(&lo, n * sizeof(__half)));
-    KIFMM_CUDA(cudaMalloc(&un, size_t(r + 1) * sizeof(float)));
-    KIFMM_CUDA(cudaMemset(hi + size_t(r) * tc::NP, 0, tc::NP * sizeof(__half)));
-    KIFMM_CUDA(cudaMemset(lo + size_t(r) * tc::NP, 0, tc::NP * sizeof(__half)));
-    KIFMM_CUDA(cudaMemset(un + r, 0, sizeof(float)));
-    *total += 2 * n * sizeof(__half) + size_t(r + 1) * sizeof(float);
-  }
-  // split rows [r0, r1) of the fp32 buffer X (row stride NP)
-  void split(const float* X, int r0, int r1, cudaStream_t s) const {
-    if (r1 <= r0) return;
-    tc::split_f16_rows_kernel<<<unsigned((r1 - r0 + 7) / 8), 256, 0, s>>>(X, r0, r1, rows, hi, lo, un);
-    KIFMM_LAUNCH_CHECK();
-  }
-};
 
 // The dense (gathered) fp32 GEMMs of the upward / downward passes -- factored check->equivalent solves,
 // M2M and L2L -- on the same tcgen05 kernel as M2L: 128-row tiles, one item per tile
@@ -1027,12 +1134,14 @@ struct TcGemm {
                                     tc::Cfg<false, 64, 2>::SMEM_BYTES));
   }
 
-  // dst[out rows] (=, or += when accumulate) A(split rows) . B^T
-  void run(const TcSplit& a, float* dst, bool accumulate, cudaStream_t s) const {
+  // dst[out rows] (=, or += when accumulate) A(split rows) . B^T; with out_split, the fp16 split of the
+  // output rows is written too (dst may then be null)
+  void run(const TcSplit& a, float* dst, bool accumulate, cudaStream_t s, const TcSplit* out_split = nullptr) const {
     if (!n_tiles) return;
     tc::m2l_tc_kernel<false, 64, 2><<<sched_g, tc::THREADS, tc::Cfg<false, 64, 2>::SMEM_BYTES, s>>>(
         tm_hi, tm_lo, a.hi, a.lo, d_items, d_sched, d_seg_mat, d_seg_in, a.rows, a.un, 1.f,
-        tc::Epi{nullptr, d_out, d_cu, dst, accumulate ? 1 : 0, 0});
+        tc::Epi{nullptr, d_out, d_cu, dst, accumulate ? 1 : 0, 0, out_split ? out_split->hi : nullptr,
+                out_split ? out_split->lo : nullptr, out_split ? out_split->un : nullptr});
     KIFMM_LAUNCH_CHECK();
   }
 };

@@ -152,7 +152,10 @@ __device__ __forceinline__ void p2p_round_f2(const float4* sh, int begin, int en
 // fp32 leaf_eval with two targets per thread: thread -> (slice tid / T2, target
 // pair tid % T2) with T2 = ceil(n_t / 2); the pair is (tt, tt + T2).  Same
 // staging rounds / items as leaf_eval_kernel (geometry leaf_slices(nt, true)).
-template <bool GRAD, bool ACC>
+// QUEUE: blocks take works from a global atomic counter until n_works are handed out (a few resident
+// blocks per SM run next to the tensor-core tree passes; a second full-size launch drains the rest).
+// Every work is computed by exactly one block, so results do not depend on the split.
+template <bool GRAD, bool ACC, bool QUEUE = false>
 __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<float> p,
                                                                        const LeafWork* __restrict__ works,
                                                                        const int4* __restrict__ rounds,
@@ -160,10 +163,19 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
                                                                        const float* __restrict__ M,
                                                                        const float* __restrict__ L,
                                                                        float* __restrict__ pot,
-                                                                       float* __restrict__ grad) {
+                                                                       float* __restrict__ grad, int n_works = 0,
+                                                                       int* __restrict__ queue = nullptr) {
   __shared__ float4 sh[kP2PCap];
-  const LeafWork w = works[blockIdx.x];
+  __shared__ int s_wi;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int wi = blockIdx.x;;) {
+  if (QUEUE) {
+    if (tid == 0) s_wi = atomicAdd(queue, 1);
+    __syncthreads();
+    wi = s_wi;
+    if (wi >= n_works) return;
+  }
+  const LeafWork w = works[wi];
   const int nt = w.t_count, T2 = (nt + 1) >> 1;
   const int R = leaf_slices(nt, true);
   const int slice = tid / T2, ta = tid - slice * T2, tb = ta + T2;
@@ -238,6 +250,9 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
       gp[1] = (ACC ? gp[1] : 0.f) - c * a[NC > 2 ? 2 : 0];
       gp[2] = (ACC ? gp[2] : 0.f) - c * a[NC > 3 ? 3 : 0];
     }
+  }
+  if (!QUEUE) return;
+  __syncthreads();
   }
 }
 
@@ -540,7 +555,10 @@ template <int KMAX>
 __global__ void __launch_bounds__(kCheckWarps * 32) check_f2_kernel(P2PParams<float> p,
                                                                      const CheckWork* __restrict__ works, int n_works,
                                                                      const int2* __restrict__ ranges, int ref_level,
-                                                                     float alpha, float* __restrict__ out, int ld_out) {
+                                                                     float alpha, float* __restrict__ out, int ld_out,
+                                                                     __half* __restrict__ sp_hi = nullptr,
+                                                                     __half* __restrict__ sp_lo = nullptr,
+                                                                     float* __restrict__ sp_un = nullptr) {
   constexpr int KP = KMAX / 2;
   constexpr bool ODD = (KMAX & 1) != 0;
   __shared__ float4 sh[kCheckWarps][32];
@@ -608,6 +626,7 @@ __global__ void __launch_bounds__(kCheckWarps * 32) check_f2_kernel(P2PParams<fl
   const int e = ref_level - w.level;  // |e| <= 15: exact power of two
   const float scale = float(kInv4PiD) * (e >= 0 ? float(1 << e) : 1.f / float(1 << (-e)));
   float* o = out + size_t(w.out_row) * ld_out;
+  float row[KMAX];
 #pragma unroll
   for (int m = 0; m < KMAX; ++m) {
     float a;
@@ -619,8 +638,11 @@ __global__ void __launch_bounds__(kCheckWarps * 32) check_f2_kernel(P2PParams<fl
       a = (m & 1) ? a1 : a0;
     }
     const int j = lane + 32 * m;
-    if (j < ld_out) o[j] = j < p.n_e ? a * scale : 0.f;
+    row[m] = j < p.n_e ? a * scale : 0.f;
+    if (j < ld_out) o[j] = row[m];
   }
+  // the fp16 split of the check row for the tcgen05 solve (ld_out == 32 KMAX)
+  if (sp_hi) split_row_warp<32 * KMAX>(row, lane, size_t(w.out_row), sp_hi, sp_lo, sp_un);
 }
 
 // Direct sum at `m` targets from all `n` sources (verification).

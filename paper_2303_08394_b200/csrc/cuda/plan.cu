@@ -177,11 +177,13 @@ __global__ void scatter_rows_kernel(const T* __restrict__ src, int ld, const int
 
 template <class T>
 void launch_check(int np, int n, const P2PParams<T>& pp, const CheckWork* works, const int2* ranges, const int* lvl,
-                  int ref, T alpha, T* out, cudaStream_t s) {
+                  int ref, T alpha, T* out, cudaStream_t s, const TcSplit* split = nullptr) {
   const int blocks = int(ceil_div(n, kCheckWarps));
   if constexpr (sizeof(T) == 4) {
     if (np == 160) {  // p = 6: packed fp32 kernel
-      check_f2_kernel<5><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, ref, alpha, out, np);
+      check_f2_kernel<5><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, ref, alpha, out, np,
+                                                             split ? split->hi : nullptr, split ? split->lo : nullptr,
+                                                             split ? split->un : nullptr);
       KIFMM_LAUNCH_CHECK();
       return;
     }
@@ -212,6 +214,30 @@ __global__ void m2m_reduce_kernel(const T* __restrict__ scratch, const int* __re
       if ((mask >> o) & 1) acc += scratch[(size_t(s) * 8 + o) * ld + c];
     M[size_t(parents[s]) * ld + c] = acc;
   }
+}
+
+// fp32 / p = 6 variant (warp per parent, same fixed octant order) that also writes the fp16 split of the
+// parent row for the next tcgen05 GEMM (M2M of the level above, M2L)
+__global__ void m2m_reduce_split_kernel(const float* __restrict__ scratch, const int* __restrict__ parents,
+                                        const int* __restrict__ masks, int n, float* __restrict__ M,
+                                        __half* __restrict__ hi, __half* __restrict__ lo, float* __restrict__ un) {
+  constexpr int W = tc::NP;
+  const int s = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (s >= n) return;
+  const int mask = masks[s];
+  float v[W / 32];
+#pragma unroll
+  for (int k = 0; k < W / 32; ++k) {
+    float acc = 0.f;
+#pragma unroll
+    for (int o = 0; o < 8; ++o)
+      if ((mask >> o) & 1) acc += scratch[(size_t(s) * 8 + o) * W + lane + 32 * k];
+    v[k] = acc;
+  }
+  const size_t row = size_t(parents[s]);
+#pragma unroll
+  for (int k = 0; k < W / 32; ++k) M[row * W + lane + 32 * k] = v[k];
+  split_row_warp<W>(v, lane, row, hi, lo, un);
 }
 
 // Y[out(r)] += sum over a tile's pieces (fixed order) of partial[slot][r]   (rows x ld per piece)
@@ -260,6 +286,8 @@ struct kifmm_gpu_plan {
   int device = 0;
   int precision = 32;
   bool leaf_packed = false;
+  int near_bps = 2;     // queue mode: near-field blocks per SM next to the tree passes (KIFMM_NEAR_BPS, 0 = off)
+  DevMem near_counter;  // queue mode work counter
   bool grad = false;
   int64_t N = 0, nl = 0, nn = 0;
   int depth = 0, ne = 0, nc = 0, np = 0, ref_level = 2, cut = 2;
@@ -293,6 +321,8 @@ struct kifmm_gpu_plan {
   bool gemm_tc = false;
   TcSplit sp_cu, sp_tmp, sp_M, sp_cd, sp_L;
   TcGemm tg_up1, tg_up2, tg_dn1, tg_dn2;
+  DevMem dn_extra;  // down-check rows with P2L but no M2L (split after M2L)
+  int n_dn_extra = 0;
   DevMem m2m_scratch;
   DevMem m2l_red_out, m2l_red_slot, m2l_partial;
   int m2l_red_tiles = 0;
@@ -610,7 +640,9 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     m2m_scratch_rows = std::max<int64_t>(m2m_scratch_rows, int64_t(parents.size()) * 8);
     return g;
   };
-  const int up_floor = world > 1 ? cut : 0;
+  // parents above level 2 get no M2M: V / W members are all at level >= 2, so multipoles of levels 0-1
+  // feed no operator (the reference's M2M loop computes them, without observable effect)
+  const int up_floor = world > 1 ? std::max(cut, 2) : 2;
   for (int l = depth - 1; l >= up_floor; --l) {
     std::vector<int64_t> parents;
     for (int64_t n = t.level_ptr[l]; n < t.level_ptr[l + 1]; ++n)
@@ -618,7 +650,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     if (!parents.empty()) m2m_levels.push_back(m2m_tiles(parents));
   }
   if (world > 1) {
-    for (int l = std::min(cut, depth) - 1; l >= 0; --l) {
+    for (int l = std::min(cut, depth) - 1; l >= 2; --l) {
       std::vector<int64_t> parents;
       for (int64_t n = t.level_ptr[l]; n < t.level_ptr[l + 1]; ++n)
         if (!is_leaf(n)) parents.push_back(n);
@@ -759,6 +791,13 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   for (int64_t n = 0; n < nn; ++n)
     if (active[n] && node_lvl(n) >= 2) dn_nodes.push_back(n);
   {
+    std::vector<int> extra;  // P2L rows outside every M2L tile (M2L tiles cover exactly the nonempty V lists)
+    for (int64_t n : dn_nodes)
+      if (t.v_ptr[n] == t.v_ptr[n + 1] && t.x_ptr[n] != t.x_ptr[n + 1]) extra.push_back(int(n));
+    n_dn_extra = int(extra.size());
+    dn_extra.upload(extra, &dev_bytes);
+  }
+  {
     std::vector<TileSpec> a, b;
     for (size_t s0 = 0; s0 < dn_nodes.size(); s0 += ld_tiles) {
       TileSpec x, y;
@@ -835,6 +874,17 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     leaf_packed = precision == 32 && !(e && std::string(e) == "scalar");
   }
   const bool packed = leaf_packed;
+  if (packed) {
+    if (const char* e = std::getenv("KIFMM_NEAR_BPS")) near_bps = std::max(0, std::atoi(e));
+    near_counter.alloc(sizeof(int), &dev_bytes);
+    // full shared-memory carveout, so an SM running near-field blocks need not drain before a tcgen05
+    // CTA (which needs the maximum carveout) can start next to them
+    for (const void* f : {(const void*)leaf_eval_f2_kernel<true, false, true>,
+                          (const void*)leaf_eval_f2_kernel<false, false, true>,
+                          (const void*)leaf_eval_f2_kernel<true, false, false>,
+                          (const void*)leaf_eval_f2_kernel<false, false, false>})
+      KIFMM_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  }
   auto build_leaf_plan = [&](bool near_part, LeafPlan& lp) {
     std::vector<LeafWork> w;
     std::vector<int4> rounds, items;
@@ -1071,32 +1121,57 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
                                                                src4.as<v4_t<T>>());
   KIFMM_LAUNCH_CHECK();
   ++launches;
-  // near field has no dependency on the tree passes: fork it onto the low-priority side stream
+  // near field has no dependency on the tree passes: fork it onto the low-priority side stream --
+  // either all of it, or (queue mode, fp32) a few blocks per SM that run next to the tensor-core tree
+  // kernels and take works from a shared counter, drained by a full launch after L2L
+  const bool queue_mode = !timed && leaf_packed && near_bps > 0 && leaf_near.n;
+  auto near_queue = [&](cudaStream_t st, int grid) {
+    if constexpr (sizeof(T) == 4) {
+      const LeafWork* w = leaf_near.works.as<LeafWork>();
+      const int4* r = leaf_near.rounds.as<int4>();
+      const int4* it = leaf_near.items.as<int4>();
+      float* g = grad ? grad_buf.as<float>() : nullptr;
+      int* qc = near_counter.as<int>();
+      if (grad)
+        leaf_eval_f2_kernel<true, false, true><<<grid, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<float>(),
+                                                                            g, leaf_near.n, qc);
+      else
+        leaf_eval_f2_kernel<false, false, true><<<grid, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp,
+                                                                             pot.as<float>(), g, leaf_near.n, qc);
+      KIFMM_LAUNCH_CHECK();
+      ++launches;
+    }
+  };
   if (!timed && leaf_near.n) {
+    if (queue_mode) KIFMM_CUDA(cudaMemsetAsync(near_counter.p, 0, sizeof(int), s));
     KIFMM_CUDA(cudaEventRecord(ev_fork, s));
     KIFMM_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
-    leaf(leaf_near, false, side);
+    if (queue_mode)
+      near_queue(side, std::min(leaf_near.n, near_bps * sm_count()));
+    else
+      leaf(leaf_near, false, side);
     KIFMM_CUDA(cudaEventRecord(ev_join, side));
   }
   // upward: P2M check -> factored solve
   if (n_p2m) {
     launch_check<T>(np, n_p2m, pp, p2m_works.as<CheckWork>(), p2m_ranges.as<int2>(), node_level.as<int>(),
-                    ref_level, T(alpha_out), check_up.as<T>(), s);
+                    ref_level, T(alpha_out), check_up.as<T>(), s, gemm_tc ? &sp_cu : nullptr);
     KIFMM_LAUNCH_CHECK();
     ++launches;
   }
   // tcgen05 GEMM: split the fp32 source rows, then dst (=/+=) A . B^T
-  auto tgemm = [&](const TcGemm& g, const TcSplit& sp, const T* X, int r0, int r1, T* Y, bool acc) {
+  // tcgen05 GEMMs: the A rows arrive already split by their producer (check kernel, previous GEMM's
+  // epilogue, M2M / M2L reductions); the epilogue writes the fp32 rows (Y, may be null) and their split
+  auto tgemm = [&](const TcGemm& g, const TcSplit& a, T* Y, bool acc, const TcSplit* out_split) {
     if constexpr (sizeof(T) == 4) {
       if (!g.n_tiles) return;
-      sp.split(X, r0, r1, s);
-      g.run(sp, Y, acc, s);
-      launches += 2;
+      g.run(a, Y, acc, s, out_split);
+      ++launches;
     }
   };
   if (gemm_tc) {
-    tgemm(tg_up1, sp_cu, check_up.as<T>(), 0, int(le - lb), tmp.as<T>(), false);
-    tgemm(tg_up2, sp_tmp, tmp.as<T>(), 0, int(le - lb), Mp, false);
+    tgemm(tg_up1, sp_cu, nullptr, false, &sp_tmp);
+    tgemm(tg_up2, sp_tmp, Mp, false, &sp_M);
   } else {
     gemm(solve_up1, check_up.as<T>(), w_us_u.as<T>(), tmp.as<T>(), false, true);
     gemm(solve_up2, tmp.as<T>(), w_vt_u.as<T>(), Mp, false, true);
@@ -1104,12 +1179,17 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   mark();  // 1
   // M2M, levels d-1 .. floor
   auto m2m_level = [&](const M2MLevel& lv) {
-    if (gemm_tc)
-      tgemm(lv.tc, sp_M, Mp, lv.r0, lv.r1, m2m_scratch.as<T>(), false);
-    else
+    if (gemm_tc) {
+      if constexpr (sizeof(T) == 4) {
+        tgemm(lv.tc, sp_M, m2m_scratch.as<T>(), false, nullptr);
+        m2m_reduce_split_kernel<<<unsigned((lv.n + 7) / 8), 256, 0, s>>>(
+            m2m_scratch.as<float>(), lv.parents.as<int>(), lv.masks.as<int>(), lv.n, Mp, sp_M.hi, sp_M.lo, sp_M.un);
+      }
+    } else {
       gemm(lv.tiles, Mp, w_m2m.as<T>(), m2m_scratch.as<T>(), false, true);
-    m2m_reduce_kernel<T><<<lv.n, 128, 0, s>>>(m2m_scratch.as<T>(), lv.parents.as<int>(), lv.masks.as<int>(), lv.n,
-                                             np, Mp);
+      m2m_reduce_kernel<T><<<lv.n, 128, 0, s>>>(m2m_scratch.as<T>(), lv.parents.as<int>(), lv.masks.as<int>(), lv.n,
+                                               np, Mp);
+    }
     KIFMM_LAUNCH_CHECK();
     ++launches;
   };
@@ -1119,6 +1199,12 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   if (world > 1) {
     exchange(s);
     launches += 2;
+    if constexpr (sizeof(T) == 4) {
+      if (gemm_tc) {  // received rows: refresh the fp16 split of every multipole
+        sp_M.split(Mp, 0, int(nn), s);
+        ++launches;
+      }
+    }
     for (auto& lv : m2m_top) m2m_level(*lv);
   }
   mark();  // 3
@@ -1134,8 +1220,23 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   // M2L over all levels at once, accumulated as reference-level check potentials
   if (m2l_backend >= 2) {
     if constexpr (sizeof(T) == 4) {
-      m2l_tc.launch(Mp, check_dn.as<float>(), np, s);
-      launches += m2l_tc.launches();
+      if (gemm_tc && m2l_backend == 2) {  // multipoles already split; the reduce splits the check rows
+        m2l_tc.launch_presplit(sp_M, check_dn.as<float>(), &sp_cd, s);
+        launches += 2;
+        if (n_dn_extra) {  // P2L-only check rows (no V list): split them here
+          tc::split_f16_list_kernel<<<unsigned((n_dn_extra + 7) / 8), 256, 0, s>>>(
+              check_dn.as<float>(), dn_extra.as<int>(), n_dn_extra, sp_cd.hi, sp_cd.lo, sp_cd.un);
+          KIFMM_LAUNCH_CHECK();
+          ++launches;
+        }
+      } else {
+        m2l_tc.launch(Mp, check_dn.as<float>(), np, s);
+        launches += m2l_tc.launches();
+        if (gemm_tc) {
+          sp_cd.split(check_dn.as<float>(), 0, int(nn), s);
+          ++launches;
+        }
+      }
     }
   } else {
     gemm(m2l, Mp, w_m2l.as<T>(), m2l_partial.as<T>(), false, true);
@@ -1149,8 +1250,8 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   mark();  // 5
   // factored downward solve (dc2e at the reference level; M2L/P2L level factors folded)
   if (gemm_tc) {
-    tgemm(tg_dn1, sp_cd, check_dn.as<T>(), 0, int(nn), tmp.as<T>(), false);
-    tgemm(tg_dn2, sp_tmp, tmp.as<T>(), 0, sp_tmp.rows, Lp, false);
+    tgemm(tg_dn1, sp_cd, nullptr, false, &sp_tmp);
+    tgemm(tg_dn2, sp_tmp, Lp, false, &sp_L);
   } else {
     gemm(solve_dn1, check_dn.as<T>(), w_us_d.as<T>(), tmp.as<T>(), false, true);
     gemm(solve_dn2, tmp.as<T>(), w_vt_d.as<T>(), Lp, false, true);
@@ -1159,14 +1260,15 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   // L2L top-down
   for (auto& lv : l2l_levels) {
     if (gemm_tc)
-      tgemm(lv->tc, sp_L, Lp, lv->r0, lv->r1, Lp, true);
+      tgemm(lv->tc, sp_L, Lp, true, &sp_L);  // reads parent rows (level l), writes child rows (l + 1)
     else
       gemm(lv->tiles, Lp, w_l2l.as<T>(), Lp, true, true);
   }
   mark();  // 7
   // leaves: near field (side stream, or here when timed) then L2P + M2P
   if (timed) leaf(leaf_near, false, s);
-  else if (leaf_near.n) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+  if (queue_mode) near_queue(s, leaf_near.n);  // drain the works the side-stream blocks did not take
+  if (!timed && leaf_near.n) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
   bool fused_out = false;  // the packed far kernel wrote the final (input-order) output
   if constexpr (sizeof(T) == 4) {
     if (leaf_packed && n_far) {

@@ -1,6 +1,7 @@
 """Summarise ncu reports into profiles/ (run here, no GPU needed).
 
-usage: python tools/ncu_summary.py name=report.ncu-rep [...] > profiles/<round>_ncu_summary.md
+usage: python tools/ncu_summary.py name=report.ncu-rep[:i,j,...] [...] > profiles/<round>_ncu_summary.md
+(name1,name2=report picks the report's kernels in order; default: the first kernel only)
 Writes/updates profiles/ncu_summary.json with per-kernel figures used by bench.py.
 """
 import csv
@@ -49,8 +50,9 @@ def main():
     print("| kernel | name | duration | DRAM read+write / launch | tensor pipe % | SM thru % | L2 sectors % | regs |")
     print("|---|---|---|---|---|---|---|---|")
     for arg in sys.argv[1:]:
-        name, path = arg.split("=", 1)
-        for d in raw(path)[:1]:
+        names, path = arg.split("=", 1)
+        names = names.split(",")
+        for name, d in zip(names, raw(path)):
             dur = d.get("gpu__time_duration.sum", ("0", ""))
             rb = to_bytes(*d.get("dram__bytes_read.sum", ("0", "byte")))
             wb = to_bytes(*d.get("dram__bytes_write.sum", ("0", "byte")))
