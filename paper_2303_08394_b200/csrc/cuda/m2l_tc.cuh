@@ -62,18 +62,23 @@ constexpr int EPI_WARP0 = 8;                      // epilogue warps 8..15
 constexpr int PROD_WARP0 = 4;                     // A producer warps 4..7
 constexpr int FWD_WARP = 2;                       // A-arrival forwarder (pair)
 constexpr int THREADS = 512;
-constexpr int LAUNCH_REGS = 96, LOW_REGS = 56, EPI_REGS = 136;
+#ifndef KIFMM_TC_LAUNCH_REGS
+#define KIFMM_TC_LAUNCH_REGS 96
+#define KIFMM_TC_LOW_REGS 56
+#define KIFMM_TC_EPI_REGS 136
+#endif
+constexpr int LAUNCH_REGS = KIFMM_TC_LAUNCH_REGS, LOW_REGS = KIFMM_TC_LOW_REGS, EPI_REGS = KIFMM_TC_EPI_REGS;
 static_assert(4 * 32 * LOW_REGS * 2 + 8 * 32 * EPI_REGS <= THREADS * LAUNCH_REGS, "setmaxnreg budget");
 constexpr uint32_t TMEM_COLS = 512;  // two 160-column accumulators at 0 and 256
 
 // ROWB: bytes of one operand row per stage (K block of ROWB/4 fp32): 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B,
 // twice the stages for the same shared memory => deeper latency hiding).
 #ifndef KIFMM_TC_STAGE_KB
-#define KIFMM_TC_STAGE_KB 184
+#define KIFMM_TC_STAGE_KB 160
 #endif
-// shared memory for pipeline stages: 184 KB (7 stages for the f16 pair, 5 for the single CTA) leaves
-// room on the SM for two near-field blocks next to a tcgen05 CTA (measured 6 % faster end to end than a
-// full 216 KB pipeline with the near field waiting for whole SMs)
+// shared memory for pipeline stages: 160 KB (6 stages for the f16 pair, 4 for the single CTA) leaves
+// room on the SM for two near-field blocks next to a tcgen05 CTA (measured 6-7 % faster end to end than
+// a full 216 KB pipeline with the near field waiting for whole SMs; 112-184 KB measured within noise)
 constexpr int kStageBudgetKB = KIFMM_TC_STAGE_KB;
 
 template <bool PAIR, int ROWB, int ES = 4>
