@@ -152,10 +152,11 @@ __device__ __forceinline__ void p2p_round_f2(const float4* sh, int begin, int en
 // fp32 leaf_eval with two targets per thread: thread -> (slice tid / T2, target
 // pair tid % T2) with T2 = ceil(n_t / 2); the pair is (tt, tt + T2).  Same
 // staging rounds / items as leaf_eval_kernel (geometry leaf_slices(nt, true)).
-// QUEUE: blocks take works from a global atomic counter until n_works are handed out (a few resident
-// blocks per SM run next to the tensor-core tree passes; a second full-size launch drains the rest).
-// Every work is computed by exactly one block, so results do not depend on the split.
-template <bool GRAD, bool ACC, bool QUEUE = false>
+// QUEUE: blocks take works from a global atomic counter queue[0] until n_works are handed out.  The
+// side launch (DRAIN = false: a few resident blocks per SM next to the tensor-core tree passes) stops
+// taking works once the drain launch (a full-size grid after L2L) has raised queue[1], so the tail runs
+// at full occupancy.  Every work is computed by exactly one block: results do not depend on the split.
+template <bool GRAD, bool ACC, bool QUEUE = false, bool DRAIN = false>
 __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<float> p,
                                                                        const LeafWork* __restrict__ works,
                                                                        const int4* __restrict__ rounds,
@@ -168,9 +169,10 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
   __shared__ float4 sh[kP2PCap];
   __shared__ int s_wi;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (QUEUE && DRAIN && blockIdx.x == 0 && tid == 0) atomicExch(queue + 1, 1);
   for (int wi = blockIdx.x;;) {
   if (QUEUE) {
-    if (tid == 0) s_wi = atomicAdd(queue, 1);
+    if (tid == 0) s_wi = (!DRAIN && atomicAdd(queue + 1, 0) != 0) ? n_works : atomicAdd(queue, 1);
     __syncthreads();
     wi = s_wi;
     if (wi >= n_works) return;
@@ -350,6 +352,9 @@ struct FarWork {
   int node0, kind0, pad0, pad1;
 };
 constexpr int kFarWarps = 6;
+#ifndef KIFMM_FAR_MINB
+#define KIFMM_FAR_MINB 1
+#endif
 constexpr int kFarMaxNe = 224;
 
 template <class T, bool GRAD>
@@ -403,7 +408,7 @@ __global__ void __launch_bounds__(kFarWarps * 32) far_kernel(P2PParams<T> p, con
 // pot_out[perm[t]] (input order) or back to pot[t] when perm is null.  Every
 // owned leaf has a work item (surf_begin == surf_end: output write only).
 template <bool GRAD>
-__global__ void __launch_bounds__(kFarWarps * 32) far_f2_kernel(P2PParams<float> p,
+__global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_f2_kernel(P2PParams<float> p,
                                                                  const FarWork* __restrict__ works, int n_works,
                                                                  const int2* __restrict__ surfaces,
                                                                  const float* __restrict__ M,

@@ -17,6 +17,8 @@
 
 #include "common.cuh"
 #include "gemm.cuh"
+#include <cstdio>
+
 #include "m2l_tc.cuh"
 #include "morton.hpp"
 #include "p2p.cuh"
@@ -287,7 +289,9 @@ struct kifmm_gpu_plan {
   int precision = 32;
   bool leaf_packed = false;
   int near_bps = 2;     // queue mode: near-field blocks per SM next to the tree passes (KIFMM_NEAR_BPS, 0 = off)
-  DevMem near_counter;  // queue mode work counter
+  DevMem near_counter;  // queue mode work counter [, counter at the drain launch (KIFMM_NEAR_DEBUG)]
+  bool near_debug = false, near_skip = false, far_as_leaf = false, near_corun = false;
+  int near_fork_at = 0;  // 0: at the start of the evaluate, 1: just before M2L
   bool grad = false;
   int64_t N = 0, nl = 0, nn = 0;
   int depth = 0, ne = 0, nc = 0, np = 0, ref_level = 2, cut = 2;
@@ -876,11 +880,17 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   const bool packed = leaf_packed;
   if (packed) {
     if (const char* e = std::getenv("KIFMM_NEAR_BPS")) near_bps = std::max(0, std::atoi(e));
-    near_counter.alloc(sizeof(int), &dev_bytes);
+    near_counter.alloc(3 * sizeof(int), &dev_bytes);
+    near_debug = std::getenv("KIFMM_NEAR_DEBUG") != nullptr;
+    near_skip = std::getenv("KIFMM_NEAR_SKIP") != nullptr;  // timing experiments only: wrong results
+    if (const char* e = std::getenv("KIFMM_NEAR_FORK")) near_fork_at = std::string(e) == "m2l" ? 1 : 0;
+    near_corun = std::getenv("KIFMM_NEAR_CORUN") != nullptr;
     // full shared-memory carveout, so an SM running near-field blocks need not drain before a tcgen05
     // CTA (which needs the maximum carveout) can start next to them
-    for (const void* f : {(const void*)leaf_eval_f2_kernel<true, false, true>,
-                          (const void*)leaf_eval_f2_kernel<false, false, true>,
+    for (const void* f : {(const void*)leaf_eval_f2_kernel<true, false, true, false>,
+                          (const void*)leaf_eval_f2_kernel<false, false, true, false>,
+                          (const void*)leaf_eval_f2_kernel<true, false, true, true>,
+                          (const void*)leaf_eval_f2_kernel<false, false, true, true>,
                           (const void*)leaf_eval_f2_kernel<true, false, false>,
                           (const void*)leaf_eval_f2_kernel<false, false, false>})
       KIFMM_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -973,6 +983,8 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     lp.items.upload(items, &dev_bytes);
   };
   build_leaf_plan(true, leaf_near);
+  if (const char* e = std::getenv("KIFMM_FAR")) far_as_leaf = packed && std::string(e) == "leaf";
+  if (far_as_leaf) build_leaf_plan(false, leaf_far);  // experiments: far field on the block kernel
   // far field: one warp-work per owned leaf with any L2P / M2P surface
   {
     std::vector<int4> fw;
@@ -1124,34 +1136,43 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   // near field has no dependency on the tree passes: fork it onto the low-priority side stream --
   // either all of it, or (queue mode, fp32) a few blocks per SM that run next to the tensor-core tree
   // kernels and take works from a shared counter, drained by a full launch after L2L
-  const bool queue_mode = !timed && leaf_packed && near_bps > 0 && leaf_near.n;
-  auto near_queue = [&](cudaStream_t st, int grid) {
+  // (KIFMM_NEAR_CORUN: experiments -- the timed run co-runs the near field with M2L to time M2L under load)
+  const bool corun = timed && near_corun && leaf_packed;
+  const bool queue_mode = (!timed || corun) && leaf_packed && near_bps > 0 && leaf_near.n && !near_skip;
+  auto near_queue = [&](cudaStream_t st, int grid, bool drain) {
     if constexpr (sizeof(T) == 4) {
       const LeafWork* w = leaf_near.works.as<LeafWork>();
       const int4* r = leaf_near.rounds.as<int4>();
       const int4* it = leaf_near.items.as<int4>();
       float* g = grad ? grad_buf.as<float>() : nullptr;
       int* qc = near_counter.as<int>();
-      if (grad)
-        leaf_eval_f2_kernel<true, false, true><<<grid, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<float>(),
-                                                                            g, leaf_near.n, qc);
+      float* pt = pot.as<float>();
+      const int n = leaf_near.n;
+      if (grad && drain)
+        leaf_eval_f2_kernel<true, false, true, true><<<grid, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pt, g, n, qc);
+      else if (grad)
+        leaf_eval_f2_kernel<true, false, true, false><<<grid, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pt, g, n, qc);
+      else if (drain)
+        leaf_eval_f2_kernel<false, false, true, true><<<grid, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pt, g, n, qc);
       else
-        leaf_eval_f2_kernel<false, false, true><<<grid, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp,
-                                                                             pot.as<float>(), g, leaf_near.n, qc);
+        leaf_eval_f2_kernel<false, false, true, false><<<grid, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pt, g, n, qc);
       KIFMM_LAUNCH_CHECK();
       ++launches;
     }
   };
-  if (!timed && leaf_near.n) {
-    if (queue_mode) KIFMM_CUDA(cudaMemsetAsync(near_counter.p, 0, sizeof(int), s));
-    KIFMM_CUDA(cudaEventRecord(ev_fork, s));
-    KIFMM_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
-    if (queue_mode)
-      near_queue(side, std::min(leaf_near.n, near_bps * sm_count()));
-    else
-      leaf(leaf_near, false, side);
-    KIFMM_CUDA(cudaEventRecord(ev_join, side));
-  }
+  auto fork_near = [&]() {
+    if ((!timed || corun) && leaf_near.n && !near_skip) {
+      if (queue_mode) KIFMM_CUDA(cudaMemsetAsync(near_counter.p, 0, 2 * sizeof(int), s));
+      KIFMM_CUDA(cudaEventRecord(ev_fork, s));
+      KIFMM_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+      if (queue_mode)
+        near_queue(side, std::min(leaf_near.n, near_bps * sm_count()), false);
+      else
+        leaf(leaf_near, false, side);
+      KIFMM_CUDA(cudaEventRecord(ev_join, side));
+    }
+  };
+  if (near_fork_at == 0 && !corun) fork_near();
   // upward: P2M check -> factored solve
   if (n_p2m) {
     launch_check<T>(np, n_p2m, pp, p2m_works.as<CheckWork>(), p2m_ranges.as<int2>(), node_level.as<int>(),
@@ -1217,6 +1238,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     ++launches;
   }
   mark();  // 4
+  if (near_fork_at == 1 || corun) fork_near();  // experiments (KIFMM_NEAR_FORK=m2l): near field next to M2L only
   // M2L over all levels at once, accumulated as reference-level check potentials
   if (m2l_backend >= 2) {
     if constexpr (sizeof(T) == 4) {
@@ -1266,12 +1288,16 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   }
   mark();  // 7
   // leaves: near field (side stream, or here when timed) then L2P + M2P
-  if (timed) leaf(leaf_near, false, s);
-  if (queue_mode) near_queue(s, leaf_near.n);  // drain the works the side-stream blocks did not take
-  if (!timed && leaf_near.n) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+  if (timed && !corun) leaf(leaf_near, false, s);
+  if (queue_mode && near_debug)  // experiments: how many works the side blocks had taken at this point
+    KIFMM_CUDA(cudaMemcpyAsync(near_counter.as<int>() + 2, near_counter.as<int>(), sizeof(int),
+                               cudaMemcpyDeviceToDevice, s));
+  if (queue_mode) near_queue(s, leaf_near.n, true);  // drain the works the side-stream blocks did not take
+  if ((!timed || corun) && leaf_near.n && !near_skip) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
   bool fused_out = false;  // the packed far kernel wrote the final (input-order) output
+  if (far_as_leaf) leaf(leaf_far, true, s);
   if constexpr (sizeof(T) == 4) {
-    if (leaf_packed && n_far) {
+    if (leaf_packed && n_far && !far_as_leaf) {
       if (input_order && world > 1) {
         KIFMM_CUDA(cudaMemsetAsync(pot_out.p, 0, pot_out.bytes, s));
         if (grad) KIFMM_CUDA(cudaMemsetAsync(grad_out.p, 0, grad_out.bytes, s));
@@ -1292,7 +1318,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
       fused_out = true;
     }
   }
-  if (!fused_out && n_far) {
+  if (!fused_out && n_far && !far_as_leaf) {
     const int blocks = int(ceil_div(n_far, kFarWarps));
     T* g = grad ? grad_buf.as<T>() : nullptr;
     if (grad)
@@ -1484,6 +1510,12 @@ kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* p, const void* charges, void* po
       p->run<double>(s, input_order != 0, timed);
     }
     KIFMM_CUDA(cudaEventRecord(ev[12], s));
+    if (p->near_debug && p->near_counter.p) {
+      int c[3];
+      KIFMM_CUDA(cudaMemcpyAsync(c, p->near_counter.p, sizeof(c), cudaMemcpyDeviceToHost, s));
+      KIFMM_CUDA(cudaStreamSynchronize(s));
+      std::fprintf(stderr, "near queue: %d of %d works taken before the drain\n", c[2], p->leaf_near.n);
+    }
     const void* ps = input_order ? p->pot_out.p : p->pot.p;
     const void* gs = input_order ? p->grad_out.p : p->grad_buf.p;
     if (input_order || p->world == 1) {
