@@ -80,6 +80,9 @@ constexpr uint32_t TMEM_COLS = 512;  // two 160-column accumulators at 0 and 256
 // room on the SM for two near-field blocks next to a tcgen05 CTA (measured 6-7 % faster end to end than
 // a full 216 KB pipeline with the near field waiting for whole SMs; 112-184 KB measured within noise)
 constexpr int kStageBudgetKB = KIFMM_TC_STAGE_KB;
+#ifndef KIFMM_TC_EG
+#define KIFMM_TC_EG 1
+#endif
 
 template <bool PAIR, int ROWB, int ES = 4>
 struct Cfg {
@@ -90,6 +93,10 @@ struct Cfg {
   static constexpr int B_BYTES = NB * ROWB;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = (kStageBudgetKB * 1024) / STAGE_BYTES;
+  // stages can be released to the producers in groups of EG (one tcgen05.commit per group; a commit
+  // costs ~50 cycles of MMA issue in tools/ubench/mma_pair.cu) -- measured slower in the kernel (the
+  // shorter effective lookahead costs more than the commits save), so EG = 1
+  static constexpr int EG = (STAGES % KIFMM_TC_EG == 0) ? KIFMM_TC_EG : 1;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512 + 2048;  // + row-max exchange
   static constexpr int ATOM = 8 * ROWB;           // bytes of an 8-row swizzle atom (= SBO)
   static constexpr uint64_t LAYOUT = ROWB == 128 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B
@@ -278,7 +285,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   auto b_hi = [&](int s) { return sbase + s * C::STAGE_BYTES + 2 * C::A_BYTES; };
   auto b_lo = [&](int s) { return sbase + s * C::STAGE_BYTES + 2 * C::A_BYTES + C::B_BYTES; };
   auto full = [&](int s) { return smem_u32(&bars[s]); };
-  auto empty = [&](int s) { return smem_u32(&bars[C::STAGES + s]); };
+  auto empty = [&](int s) { return smem_u32(&bars[C::STAGES + s / C::EG]); };  // one barrier per stage group
   auto tfull = [&](int b) { return smem_u32(&bars[2 * C::STAGES + b]); };
   auto tempty = [&](int b) { return smem_u32(&bars[2 * C::STAGES + 2 + b]); };
   auto afull = [&](int s) { return smem_u32(&bars[2 * C::STAGES + 4 + s]); };
@@ -492,7 +499,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
                 mma<PAIR, ES>(d, dah, dbl, 1u);
                 mma<PAIR, ES>(d, dal, dbh, 1u);
               }
-              commit<PAIR>(empty(s));
+              if (s % C::EG == C::EG - 1) commit<PAIR>(empty(s));
             }
             commit<PAIR>(tfull(b));
           }
