@@ -128,6 +128,22 @@ __device__ __forceinline__ void split_row_warp(const float (&v)[W / 32], int lan
   if (lane == 0) un[row] = ldexpf(1.f, -e);
 }
 
+// Timeline probes (experiments, KIFMM_TIMELINE): kernel `id` records the earliest block start and the
+// latest block end (globaltimer ns) of its launch.
+__device__ unsigned long long g_timeline[16][2];
+__device__ int g_timeline_on;
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void timeline_begin(int id) {
+  if (threadIdx.x == 0 && g_timeline_on) atomicMin(&g_timeline[id][0], globaltimer());
+}
+__device__ __forceinline__ void timeline_end(int id) {
+  if (threadIdx.x == 0 && g_timeline_on) atomicMax(&g_timeline[id][1], globaltimer());
+}
+
 // Far-away zero-charge source used to pad staged source rounds (contributes exactly 0).
 constexpr double kFarAway = 1e15;
 

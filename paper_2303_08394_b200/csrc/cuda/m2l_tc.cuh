@@ -159,6 +159,28 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (spin > (1u << 28)) asm volatile("trap;");
   }
 }
+// Wait with a nanosleep back-off, for roles whose barrier completes on a coarse time scale (epilogue,
+// producers): their spinning would otherwise take issue slots from blocks of other kernels sharing
+// the SM (the near field runs next to these kernels).
+#ifndef KIFMM_TC_SLEEP_NS
+#define KIFMM_TC_SLEEP_NS 64
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t spin = 0;; ++spin) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (KIFMM_TC_SLEEP_NS > 0) __nanosleep(KIFMM_TC_SLEEP_NS);
+    if (spin > (1u << 26)) asm volatile("trap;");
+  }
+}
+
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -324,6 +346,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   if (PAIR) cluster_sync();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  timeline_begin(PAIR ? 1 : 2);
   if (warp >= EPI_WARP0) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
 
@@ -345,7 +368,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
           const int sr = seg_in[size_t(it.seg_begin + j) * rows + rank * BM + row];
           f = sr < 0 ? 0.f : row_unscale[sr] * k_unscale;
         }
-        mbar_wait(tfull(b), (gj >> 1) & 1);
+        mbar_wait_sleep(tfull(b), (gj >> 1) & 1);
         __syncwarp();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * 256 + h * EPI_COLS);
@@ -491,7 +514,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
               mbar_wait(full(s), round & 1);
               if (prof) t_fu += clock64() - c0;
               asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  #pragma unroll
+#pragma unroll
               for (int k = 0; k < ROWB / 32; ++k) {  // 32 bytes of K per MMA (8 tf32 / 16 f16)
                 const uint64_t dah = make_desc<ROWB>(a_hi(s) + 32 * k), dal = make_desc<ROWB>(a_lo(s) + 32 * k);
                 const uint64_t dbh = make_desc<ROWB>(b_hi(s) + 32 * k), dbl = make_desc<ROWB>(b_lo(s) + 32 * k);
@@ -527,11 +550,11 @@ __global__ void __maxnreg__(LAUNCH_REGS)
           const int seg = it.seg_begin + i / NKB, kb = i % NKB;
           if (seg != cur_seg) {
             cur_seg = seg;
-  #pragma unroll
+#pragma unroll
             for (int j = 0; j < J; ++j) src[j] = seg_in[size_t(seg) * rows + rank * BM + r0 + RPI * j];
           }
-          mbar_wait(empty(s), (round & 1) ^ 1);
-  #pragma unroll
+          mbar_wait_sleep(empty(s), (round & 1) ^ 1);
+#pragma unroll
           for (int j = 0; j < J; ++j) {
             const int r = r0 + RPI * j;
             const int sw = ROWB == 128 ? (r & 7) : ((r & 7) >> 1);  // Swizzle<3,4,3> / Swizzle<2,4,3>
@@ -571,6 +594,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  timeline_end(PAIR ? 1 : 2);
   if (PAIR) cluster_sync();
   if (warp == 0) {
     __syncwarp();

@@ -169,13 +169,17 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
   __shared__ float4 sh[kP2PCap];
   __shared__ int s_wi;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (QUEUE) timeline_begin(DRAIN ? 4 : 3);
   if (QUEUE && DRAIN && blockIdx.x == 0 && tid == 0) atomicExch(queue + 1, 1);
   for (int wi = blockIdx.x;;) {
   if (QUEUE) {
     if (tid == 0) s_wi = (!DRAIN && atomicAdd(queue + 1, 0) != 0) ? n_works : atomicAdd(queue, 1);
     __syncthreads();
     wi = s_wi;
-    if (wi >= n_works) return;
+    if (wi >= n_works) {
+      timeline_end(DRAIN ? 4 : 3);
+      return;
+    }
   }
   const LeafWork w = works[wi];
   const int nt = w.t_count, T2 = (nt + 1) >> 1;
@@ -418,6 +422,7 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_f2_kernel(
   __shared__ float4 sh[kFarWarps][kFarMaxNe + 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wi = blockIdx.x * kFarWarps + warp;
+  timeline_begin(5);
   if (wi >= n_works) return;
   const FarWork w = works[wi];
   const int t0 = w.t0, nt = w.count, T2 = (nt + 1) >> 1;
@@ -471,6 +476,7 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_f2_kernel(
       if (GRAD || (d & 3) == 0) v[d] += (slice == 0 && lane + k * T2 < 32) ? o : 0.f;
     }
   }
+  timeline_end(5);
   if (slice != 0) return;
   const float c = float(kInv4PiD);
   float* po = perm ? pot_out : pot;

@@ -1269,6 +1269,9 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
       ++launches;
     }
   }
+  if (queue_mode && near_debug && std::getenv("KIFMM_NEAR_DEBUG_M2L"))  // experiments: snapshot after M2L
+    KIFMM_CUDA(cudaMemcpyAsync(near_counter.as<int>() + 2, near_counter.as<int>(), sizeof(int),
+                               cudaMemcpyDeviceToDevice, s));
   mark();  // 5
   // factored downward solve (dc2e at the reference level; M2L/P2L level factors folded)
   if (gemm_tc) {
@@ -1289,10 +1292,12 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   mark();  // 7
   // leaves: near field (side stream, or here when timed) then L2P + M2P
   if (timed && !corun) leaf(leaf_near, false, s);
-  if (queue_mode && near_debug)  // experiments: how many works the side blocks had taken at this point
+  if (queue_mode && near_debug && !std::getenv("KIFMM_NEAR_DEBUG_M2L"))  // experiments: works taken by now
     KIFMM_CUDA(cudaMemcpyAsync(near_counter.as<int>() + 2, near_counter.as<int>(), sizeof(int),
                                cudaMemcpyDeviceToDevice, s));
-  if (queue_mode) near_queue(s, leaf_near.n, true);  // drain the works the side-stream blocks did not take
+  // drain the works the side-stream blocks did not take (persistent: at most 8 blocks per SM, so an
+  // empty queue costs one short wave instead of a block per leaf)
+  if (queue_mode) near_queue(s, std::min(leaf_near.n, 8 * sm_count()), true);
   if ((!timed || corun) && leaf_near.n && !near_skip) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
   bool fused_out = false;  // the packed far kernel wrote the final (input-order) output
   if (far_as_leaf) leaf(leaf_far, true, s);
@@ -1510,6 +1515,28 @@ kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* p, const void* charges, void* po
       p->run<double>(s, input_order != 0, timed);
     }
     KIFMM_CUDA(cudaEventRecord(ev[12], s));
+    if (std::getenv("KIFMM_TIMELINE")) {
+      unsigned long long tl[16][2];
+      KIFMM_CUDA(cudaStreamSynchronize(s));
+      KIFMM_CUDA(cudaMemcpyFromSymbol(tl, g_timeline, sizeof(tl)));
+      unsigned long long t0 = ~0ull;
+      for (auto& r : tl)
+        if (r[1]) t0 = std::min(t0, r[0]);
+      const char* names[] = {"", "m2l", "tc-gemms", "near-side", "near-drain", "far", "", "", "", "", "", "", "", "",
+                             "", ""};
+      for (int i = 0; i < 16; ++i)
+        if (tl[i][1])
+          std::fprintf(stderr, "timeline %-10s start %8.1f us  end %8.1f us\n", names[i], (tl[i][0] - t0) * 1e-3,
+                       (tl[i][1] - t0) * 1e-3);
+      unsigned long long init[16][2];
+      for (auto& r : init) {
+        r[0] = ~0ull;
+        r[1] = 0;
+      }
+      KIFMM_CUDA(cudaMemcpyToSymbol(g_timeline, init, sizeof(init)));
+      int on = 1;
+      KIFMM_CUDA(cudaMemcpyToSymbol(g_timeline_on, &on, sizeof(on)));
+    }
     if (p->near_debug && p->near_counter.p) {
       int c[3];
       KIFMM_CUDA(cudaMemcpyAsync(c, p->near_counter.p, sizeof(c), cudaMemcpyDeviceToHost, s));
