@@ -174,3 +174,29 @@ def test_run_api(require_gpu):  # run(particles, config) -> potenti
     pot, grad, tm = fmm.run(pos, q, fmm.FmmConfig(p=6, n_crit=50, precision=64))
     assert grad is None and tm["total_ms"] > 0 and "tree_s" in tm
     assert fmm.relative_error(pot[:500], oracle.direct(pos, q, targets=np.arange(500))) <= 1e-5
+
+
+def test_near_queue_mode_bit_identical(require_gpu, monkeypatch):
+    """Queue mode (near field taken by side-stream blocks from a counter, drained after L2L) computes
+    every leaf in exactly one block: results equal the one-block-per-leaf launch bit for bit."""
+    pos, q = generators.sample("two-cluster", 60000, seed=21, charges="signed", fp32=True)
+    cfg = fmm.FmmConfig(p=6, n_crit=40, precision=32, gradient=True)
+    out = {}
+    for bps in ("0", "1", "2"):
+        monkeypatch.setenv("KIFMM_NEAR_BPS", bps)
+        with fmm.Fmm(pos, cfg) as f:
+            out[bps] = f.evaluate(q)[:2]
+    for bps in ("1", "2"):
+        assert np.array_equal(out[bps][0], out["0"][0]) and np.array_equal(out[bps][1], out["0"][1])
+
+
+def test_simt_gemms_with_tcgen05_m2l(require_gpu, monkeypatch):
+    """fp32 solves / M2M / L2L on the SIMT GEMM (KIFMM_TC_GEMM=0) next to the tcgen05 M2L."""
+    monkeypatch.setenv("KIFMM_TC_GEMM", "0")
+    pos, q = generators.sample("sphere-surface", 30000, seed=22, charges="signed", fp32=True)
+    with fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=50, precision=32, gradient=True)) as f:
+        assert f.info()["m2l_backend"] == 2
+        pot, grad, _ = f.evaluate(q)
+        ref, gref = _ref(f, q, True)
+    assert fmm.relative_error(pot, ref) <= 1e-5
+    assert fmm.relative_error(grad, gref) <= 5e-5
