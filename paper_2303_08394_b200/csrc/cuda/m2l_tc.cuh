@@ -181,6 +181,12 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
   }
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile("{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}" : "=r"(e));
+  return e != 0;
+}
+
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -231,6 +237,28 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uin
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+// The three MMAs of one K step of the 3-term split: D (+)= A_hi B_hi, += A_hi B_lo, += A_lo B_hi.
+template <bool PAIR, int ES>
+__device__ __forceinline__ void mma3(uint32_t tmem_d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                     uint32_t idesc, uint32_t accumulate) {
+#define KIFMM_MMA3(GROUP, KIND)                                                                  \
+  asm volatile(                                                                                  \
+      "{\n.reg .pred p, t;\nsetp.ne.b32 p, %6, 0;\nsetp.eq.b32 t, %6, %6;\n"                \
+      "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %1, %3, %5, p;\n"                 \
+      "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %1, %4, %5, t;\n"                 \
+      "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %2, %3, %5, t;\n}" ::"r"(tmem_d), \
+      "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(accumulate))
+  if constexpr (PAIR && ES == 4)
+    KIFMM_MMA3("2", "tf32");
+  else if constexpr (ES == 4)
+    KIFMM_MMA3("1", "tf32");
+  else if constexpr (PAIR)
+    KIFMM_MMA3("2", "f16");
+  else
+    KIFMM_MMA3("1", "f16");
+#undef KIFMM_MMA3
+}
+
 // tcgen05.commit: arrive on `bar` (in both CTAs of the pair when PAIR) once prior MMAs complete
 template <bool PAIR>
 __device__ __forceinline__ void commit(uint32_t bar) {
@@ -347,6 +375,10 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
   timeline_begin(PAIR ? 1 : 2);
+  if (PAIR && blockIdx.x == 0 && threadIdx.x == 0 && g_timeline_on) {  // SM clock probe (experiments)
+    g_timeline[8][0] = globaltimer();
+    g_timeline[8][1] = clock64();
+  }
   if (warp >= EPI_WARP0) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
 
@@ -493,11 +525,20 @@ __global__ void __maxnreg__(LAUNCH_REGS)
         }
       }
     } else if (warp == 1) {
-      // ---------------- MMA issuer (leader only): a fresh accumulator per tap
-      if (rank == 0 && lane == 0) {
-        int gi = 0, gj = 0;
+      // ---------------- MMA issuer (leader only): a fresh accumulator per tap.  Kept short: the
+      //                  tensor pipe waits on this one thread, and every instruction it issues competes
+      //                  for its SMSP with the epilogue / producer warps (and co-resident blocks), so
+      //                  the stage / parity counters run without div/mod, descriptors are a base plus
+      //                  an offset, and the three MMAs of a K step are one asm block.
+      if (rank == 0) {  // the whole warp walks the loop (warp-uniform values); one elected lane issues
         const bool prof = (epi.debug & 8) != 0;
         unsigned long long t_all = clock64(), t_te = 0, t_fu = 0;
+        const uint64_t dah0 = make_desc<ROWB>(a_hi(0)), dal0 = make_desc<ROWB>(a_lo(0));
+        const uint64_t dbh0 = make_desc<ROWB>(b_hi(0)), dbl0 = make_desc<ROWB>(b_lo(0));
+        constexpr uint64_t SD = uint64_t(C::STAGE_BYTES >> 4);  // descriptor start-address step per stage
+        constexpr uint32_t IDESC = C::IDESC;
+        int s = 0, gj = 0, ntaps = 0, nst = 0;
+        uint32_t ph = 0;
         for (int kk = k_begin; kk < k_end; ++kk) {
           const Item it = items[sched_list[kk]];
           const int ntap = it.seg_end - it.seg_begin;
@@ -508,28 +549,35 @@ __global__ void __maxnreg__(LAUNCH_REGS)
             if (prof) t_te += clock64() - c0;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t d = tmem_base + uint32_t(b * 256);
-            for (int kb = 0; kb < NKB; ++kb, ++gi) {
-              const int s = gi % C::STAGES, round = gi / C::STAGES;
+            for (int kb = 0; kb < NKB; ++kb) {
               c0 = prof ? clock64() : 0;
-              mbar_wait(full(s), round & 1);
+              mbar_wait(full(s), ph);
               if (prof) t_fu += clock64() - c0;
               asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+              const uint64_t so = uint64_t(s) * SD;
+              if (elect_one()) {
 #pragma unroll
-              for (int k = 0; k < ROWB / 32; ++k) {  // 32 bytes of K per MMA (8 tf32 / 16 f16)
-                const uint64_t dah = make_desc<ROWB>(a_hi(s) + 32 * k), dal = make_desc<ROWB>(a_lo(s) + 32 * k);
-                const uint64_t dbh = make_desc<ROWB>(b_hi(s) + 32 * k), dbl = make_desc<ROWB>(b_lo(s) + 32 * k);
-                mma<PAIR, ES>(d, dah, dbh, (kb > 0 || k > 0) ? 1u : 0u);
-                mma<PAIR, ES>(d, dah, dbl, 1u);
-                mma<PAIR, ES>(d, dal, dbh, 1u);
+                for (int k = 0; k < ROWB / 32; ++k) {  // 32 bytes of K per MMA (8 tf32 / 16 f16)
+                  const uint64_t o = so + uint64_t(2 * k);
+                  mma3<PAIR, ES>(d, dah0 + o, dal0 + o, dbh0 + o, dbl0 + o, IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+                }
+                if (s % C::EG == C::EG - 1) commit<PAIR>(empty(s));
               }
-              if (s % C::EG == C::EG - 1) commit<PAIR>(empty(s));
+              __syncwarp();
+              if (++s == C::STAGES) {
+                s = 0;
+                ph ^= 1u;
+              }
+              ++nst;
             }
-            commit<PAIR>(tfull(b));
+            if (elect_one()) commit<PAIR>(tfull(b));
+            __syncwarp();
+            ++ntaps;
           }
         }
-        if (prof && (blockIdx.x == 0 || blockIdx.x == 64))
+        if (prof && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 64))
           printf("cta %d: total %llu wait_tempty %llu wait_full %llu taps %d stages %d\n", int(blockIdx.x),
-                 clock64() - t_all, t_te, t_fu, gj, gi);
+                 clock64() - t_all, t_te, t_fu, ntaps, nst);
       }
     } else if (warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
       // ---------------- A producers: thread -> (16-byte chunk c, rows r0 + 16 j) of this CTA, cp.async
@@ -595,6 +643,10 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   timeline_end(PAIR ? 1 : 2);
+  if (PAIR && blockIdx.x == 0 && threadIdx.x == 0 && g_timeline_on) {
+    g_timeline[9][0] = globaltimer();
+    g_timeline[9][1] = clock64();
+  }
   if (PAIR) cluster_sync();
   if (warp == 0) {
     __syncwarp();

@@ -201,6 +201,37 @@ void launch_check(int np, int n, const P2PParams<T>& pp, const CheckWork* works,
   KIFMM_LAUNCH_CHECK();
 }
 
+// Experiments only (KIFMM_CORUN_DUMMY): a co-running load of one kind -- 0 FFMA chains, 1 LDS.128
+// broadcasts, 2 MUFU.RSQ -- for `iters` rounds, to see which resource slows the tensor-core kernels.
+__global__ void __launch_bounds__(128) dummy_load_kernel(int kind, int iters, float* out) {
+  __shared__ float4 sh[256];
+  sh[threadIdx.x] = make_float4(threadIdx.x, 1.f, 2.f, 3.f);
+  sh[threadIdx.x + 128] = make_float4(threadIdx.x, 1.f, 2.f, 3.f);
+  __syncthreads();
+  float a[8];
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x + i;
+  for (int it = 0; it < iters; ++it) {
+    if (kind == 0) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = fmaf(a[i], 0.999f, 0.001f);
+    } else if (kind == 1) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float4 v = sh[(it * 16 + u) & 255];
+        a[u & 7] += v.x + v.y;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) a[u & 7] = rsqrtf(a[u & 7] + 1.f);
+    }
+  }
+  float t = 0.f;
+  for (int i = 0; i < 8; ++i) t += a[i];
+  if (t == -1.f) out[0] = t;
+}
+
 // M2M split over octants: partial products land in scratch rows (slot*8 + octant)
 // and are summed here in fixed octant order (deterministic, no atomics).
 template <class T>
@@ -1238,6 +1269,12 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     ++launches;
   }
   mark();  // 4
+  if (const char* e = std::getenv("KIFMM_CORUN_DUMMY"); e && timed) {  // experiments: a dummy load next to M2L
+    KIFMM_CUDA(cudaEventRecord(ev_fork, s));
+    KIFMM_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    dummy_load_kernel<<<2 * sm_count(), 128, 0, side>>>(std::atoi(e), 20000, pot.as<float>());
+    KIFMM_CUDA(cudaEventRecord(ev_join, side));
+  }
   if (near_fork_at == 1 || corun) fork_near();  // experiments (KIFMM_NEAR_FORK=m2l): near field next to M2L only
   // M2L over all levels at once, accumulated as reference-level check potentials
   if (m2l_backend >= 2) {
@@ -1524,7 +1561,10 @@ kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* p, const void* charges, void* po
         if (r[1]) t0 = std::min(t0, r[0]);
       const char* names[] = {"", "m2l", "tc-gemms", "near-side", "near-drain", "far", "", "", "", "", "", "", "", "",
                              "", ""};
-      for (int i = 0; i < 16; ++i)
+      if (tl[9][0] > tl[8][0])
+        std::fprintf(stderr, "timeline m2l CTA 0 SM clock %.0f MHz\n",
+                     double(tl[9][1] - tl[8][1]) / double(tl[9][0] - tl[8][0]) * 1e3);
+      for (int i = 0; i < 8; ++i)
         if (tl[i][1])
           std::fprintf(stderr, "timeline %-10s start %8.1f us  end %8.1f us\n", names[i], (tl[i][0] - t0) * 1e-3,
                        (tl[i][1] - t0) * 1e-3);
