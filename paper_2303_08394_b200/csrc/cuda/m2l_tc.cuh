@@ -502,25 +502,33 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(LOW_REGS));
     if (warp == 0) {
-      // ---------------- B producer: this CTA's rows of K_t hi/lo (TMA tile, swizzled)
-      if (lane == 0) {
-        int gi = 0;
+      // ---------------- B producer: this CTA's rows of K_t hi/lo (TMA tile, swizzled); the whole warp
+      //                  walks the loop (uniform values), one elected lane issues
+      {
+        int s = 0, kb = 0;
+        uint32_t ph = 0;
         for (int kk = k_begin; kk < k_end; ++kk) {
           const Item it = items[sched_list[kk]];
-          const int nstage = (it.seg_end - it.seg_begin) * NKB;
-          for (int i = 0; i < nstage; ++i, ++gi) {
-            const int s = gi % C::STAGES, round = gi / C::STAGES;
-            mbar_wait(empty(s), (round & 1) ^ 1);
-            const int seg = it.seg_begin + i / NKB, kb = i % NKB;
+          for (int seg = it.seg_begin; seg < it.seg_end; ++seg) {
             const int row = seg_mat[seg] * NP + int(rank) * C::NB;
-            if (epi.debug & 2) {
-              if (rank == 0) mbar_expect_tx(full(s), 0);
-              continue;
+            for (kb = 0; kb < NKB; ++kb) {
+              mbar_wait(empty(s), ph ^ 1u);
+              if (elect_one()) {
+                if (epi.debug & 2) {
+                  if (rank == 0) mbar_expect_tx(full(s), 0);
+                } else {
+                  if (rank == 0) mbar_expect_tx(full(s), C::TX);
+                  const uint32_t fb = leader(full(s));
+                  tma_tile<PAIR>(b_hi(s), &tm_khi, fb, kb * KB, row);
+                  tma_tile<PAIR>(b_lo(s), &tm_klo, fb, kb * KB, row);
+                }
+              }
+              __syncwarp();
+              if (++s == C::STAGES) {
+                s = 0;
+                ph ^= 1u;
+              }
             }
-            if (rank == 0) mbar_expect_tx(full(s), C::TX);
-            const uint32_t fb = leader(full(s));
-            tma_tile<PAIR>(b_hi(s), &tm_khi, fb, kb * KB, row);
-            tma_tile<PAIR>(b_lo(s), &tm_klo, fb, kb * KB, row);
           }
         }
       }
@@ -588,20 +596,20 @@ __global__ void __maxnreg__(LAUNCH_REGS)
       const int t = threadIdx.x - 32 * PROD_WARP0;  // 0..127
       const int c = t % CH, r0 = t / CH;
       int src[J];
-      int gi = 0;
+      int s = 0;
+      uint32_t ph = 0;
       for (int kk = k_begin; kk < k_end; ++kk) {
         const Item it = items[sched_list[kk]];
         const int nstage = (it.seg_end - it.seg_begin) * NKB;
         int cur_seg = -1;
-        for (int i = 0; i < nstage; ++i, ++gi) {
-          const int s = gi % C::STAGES, round = gi / C::STAGES;
-          const int seg = it.seg_begin + i / NKB, kb = i % NKB;
+        int seg = it.seg_begin, kb = 0;
+        for (int i = 0; i < nstage; ++i) {
           if (seg != cur_seg) {
             cur_seg = seg;
 #pragma unroll
             for (int j = 0; j < J; ++j) src[j] = seg_in[size_t(seg) * rows + rank * BM + r0 + RPI * j];
           }
-          mbar_wait_sleep(empty(s), (round & 1) ^ 1);
+          mbar_wait_sleep(empty(s), ph ^ 1u);
 #pragma unroll
           for (int j = 0; j < J; ++j) {
             const int r = r0 + RPI * j;
@@ -622,19 +630,32 @@ __global__ void __maxnreg__(LAUNCH_REGS)
           // (as CUTLASS's cp.async UMMA mainloops do; the full barrier's count includes these arrivals)
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(PAIR ? afull(s) : full(s))
                        : "memory");
+          if (++s == C::STAGES) {
+            s = 0;
+            ph ^= 1u;
+          }
+          if (++kb == NKB) {
+            kb = 0;
+            ++seg;
+          }
         }
       }
     } else if (warp == FWD_WARP) {
       // ---------------- forwarder (pair): this CTA's A rows landed -> one arrive on the leader's stage barrier
-      if (PAIR && lane == 0) {
-        int gi = 0;
+      if (PAIR) {
+        int s = 0;
+        uint32_t ph = 0;
         for (int kk = k_begin; kk < k_end; ++kk) {
           const Item it = items[sched_list[kk]];
           const int nstage = (it.seg_end - it.seg_begin) * NKB;
-          for (int i = 0; i < nstage; ++i, ++gi) {
-            const int s = gi % C::STAGES, round = gi / C::STAGES;
-            mbar_wait(afull(s), round & 1);
-            mbar_arrive_cluster(leader(full(s)));
+          for (int i = 0; i < nstage; ++i) {
+            mbar_wait(afull(s), ph);
+            if (elect_one()) mbar_arrive_cluster(leader(full(s)));
+            __syncwarp();
+            if (++s == C::STAGES) {
+              s = 0;
+              ph ^= 1u;
+            }
           }
         }
       }
