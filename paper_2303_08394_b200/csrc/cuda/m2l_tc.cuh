@@ -69,7 +69,8 @@ constexpr int THREADS = 512;
 #endif
 constexpr int LAUNCH_REGS = KIFMM_TC_LAUNCH_REGS, LOW_REGS = KIFMM_TC_LOW_REGS, EPI_REGS = KIFMM_TC_EPI_REGS;
 static_assert(4 * 32 * LOW_REGS * 2 + 8 * 32 * EPI_REGS <= THREADS * LAUNCH_REGS, "setmaxnreg budget");
-constexpr uint32_t TMEM_COLS = 512;  // two 160-column accumulators at 0 and 256
+constexpr uint32_t TMEM_COLS = 512;  // NACC 160-column accumulators at 0, 160, 320
+constexpr int NACC = 3;              // accumulator buffers: the MMA runs up to two taps ahead of the epilogue
 
 // ROWB: bytes of one operand row per stage (K block of ROWB/4 fp32): 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B,
 // twice the stages for the same shared memory => deeper latency hiding).
@@ -317,7 +318,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   // bars: [0,S) full, [S,2S) empty, [2S,2S+2) tmem_full[b], [2S+2,2S+4) tmem_empty[b],
   //       [2S+4,3S+4) a_full (this CTA's A rows landed; PAIR only); then the TMEM address
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::STAGES + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::STAGES + 2 * NACC);
   float* xmax = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 512);  // [2][2][128]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
@@ -337,8 +338,8 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   auto full = [&](int s) { return smem_u32(&bars[s]); };
   auto empty = [&](int s) { return smem_u32(&bars[C::STAGES + s / C::EG]); };  // one barrier per stage group
   auto tfull = [&](int b) { return smem_u32(&bars[2 * C::STAGES + b]); };
-  auto tempty = [&](int b) { return smem_u32(&bars[2 * C::STAGES + 2 + b]); };
-  auto afull = [&](int s) { return smem_u32(&bars[2 * C::STAGES + 4 + s]); };
+  auto tempty = [&](int b) { return smem_u32(&bars[2 * C::STAGES + NACC + b]); };
+  auto afull = [&](int s) { return smem_u32(&bars[2 * C::STAGES + 2 * NACC + s]); };
   // barriers the MMA waits on live in the leader; their cluster addresses
   auto leader = [&](uint32_t a) { return PAIR ? mapa(a, 0) : a; };
 
@@ -350,7 +351,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
       mbar_init(empty(s), 1);  // one tcgen05.commit per stage (multicast to both CTAs when PAIR)
       mbar_init(afull(s), 128);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       mbar_init(tfull(b), 1);
       mbar_init(tempty(b), C::CTAS * EPI_WARPS);  // one elected lane per epilogue warp per CTA
     }
@@ -386,24 +387,24 @@ __global__ void __maxnreg__(LAUNCH_REGS)
     //                  and columns [h*80, h*80+80), h = (w-6)/4
     const int q = warp & 3, h = (warp - EPI_WARP0) >> 2;
     const int row = q * 32 + lane;
-    int gj = 0;
+    int b = 0;
+    uint32_t tph = 0;
     for (int kk = k_begin; kk < k_end; ++kk) {
       const Item it = items[sched_list[kk]];
       const int ntap = it.seg_end - it.seg_begin;
       float acc[EPI_COLS];
 #pragma unroll
       for (int k = 0; k < EPI_COLS; ++k) acc[k] = 0.f;
-      for (int j = 0; j < ntap; ++j, ++gj) {
-        const int b = gj & 1;
+      for (int j = 0; j < ntap; ++j) {
         float f = 1.f;  // f16 kind: undo the per-row (source) and K_t power-of-two scalings
         if constexpr (ES == 2) {
           const int sr = seg_in[size_t(it.seg_begin + j) * rows + rank * BM + row];
           f = sr < 0 ? 0.f : row_unscale[sr] * k_unscale;
         }
-        mbar_wait_sleep(tfull(b), (gj >> 1) & 1);
+        mbar_wait_sleep(tfull(b), tph);
         __syncwarp();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * 256 + h * EPI_COLS);
+        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * NP + h * EPI_COLS);
 #pragma unroll
         for (int cb = 0; cb < ((epi.debug & 4) ? 0 : EPI_COLS / 16); ++cb) {
           uint32_t v[16];
@@ -423,6 +424,10 @@ __global__ void __maxnreg__(LAUNCH_REGS)
             mbar_arrive_cluster(leader(tempty(b)));
           else
             mbar_arrive_local(tempty(b));
+        }
+        if (++b == NACC) {
+          b = 0;
+          tph ^= 1u;
         }
       }
       if (epi.direct_out) {
@@ -545,18 +550,17 @@ __global__ void __maxnreg__(LAUNCH_REGS)
         const uint64_t dbh0 = make_desc<ROWB>(b_hi(0)), dbl0 = make_desc<ROWB>(b_lo(0));
         constexpr uint64_t SD = uint64_t(C::STAGE_BYTES >> 4);  // descriptor start-address step per stage
         constexpr uint32_t IDESC = C::IDESC;
-        int s = 0, gj = 0, ntaps = 0, nst = 0;
-        uint32_t ph = 0;
+        int s = 0, gj = 0, ntaps = 0, nst = 0, ab = 0;
+        uint32_t ph = 0, aph = 0;
         for (int kk = k_begin; kk < k_end; ++kk) {
           const Item it = items[sched_list[kk]];
           const int ntap = it.seg_end - it.seg_begin;
           for (int j = 0; j < ntap; ++j, ++gj) {
-            const int b = gj & 1;
             unsigned long long c0 = prof ? clock64() : 0;
-            mbar_wait(tempty(b), ((gj >> 1) & 1) ^ 1);
+            mbar_wait(tempty(ab), aph ^ 1u);
             if (prof) t_te += clock64() - c0;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t d = tmem_base + uint32_t(b * 256);
+            const uint32_t d = tmem_base + uint32_t(ab * NP);
             for (int kb = 0; kb < NKB; ++kb) {
               c0 = prof ? clock64() : 0;
               mbar_wait(full(s), ph);
@@ -578,7 +582,11 @@ __global__ void __maxnreg__(LAUNCH_REGS)
               }
               ++nst;
             }
-            if (elect_one()) commit<PAIR>(tfull(b));
+            if (elect_one()) commit<PAIR>(tfull(ab));
+            if (++ab == NACC) {
+              ab = 0;
+              aph ^= 1u;
+            }
             __syncwarp();
             ++ntaps;
           }
