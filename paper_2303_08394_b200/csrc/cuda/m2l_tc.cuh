@@ -166,6 +166,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 #ifndef KIFMM_TC_SLEEP_NS
 #define KIFMM_TC_SLEEP_NS 64
 #endif
+#ifndef KIFMM_TC_PROD_SLEEP
+#define KIFMM_TC_PROD_SLEEP 0  // producers poll without back-off (their wait gates the refill)
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   for (uint32_t spin = 0;; ++spin) {
@@ -617,7 +620,11 @@ __global__ void __maxnreg__(LAUNCH_REGS)
 #pragma unroll
             for (int j = 0; j < J; ++j) src[j] = seg_in[size_t(seg) * rows + rank * BM + r0 + RPI * j];
           }
+#if KIFMM_TC_PROD_SLEEP
           mbar_wait_sleep(empty(s), ph ^ 1u);
+#else
+          mbar_wait(empty(s), ph ^ 1u);
+#endif
 #pragma unroll
           for (int j = 0; j < J; ++j) {
             const int r = r0 + RPI * j;
