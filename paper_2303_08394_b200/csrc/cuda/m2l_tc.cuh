@@ -398,12 +398,18 @@ __global__ void __maxnreg__(LAUNCH_REGS)
       float acc[EPI_COLS];
 #pragma unroll
       for (int k = 0; k < EPI_COLS; ++k) acc[k] = 0.f;
-      for (int j = 0; j < ntap; ++j) {
-        float f = 1.f;  // f16 kind: undo the per-row (source) and K_t power-of-two scalings
+      // f16 kind: the per-row (source) and K_t power-of-two unscale of each tap, loaded one tap ahead
+      auto unscale_of = [&](int j) {
         if constexpr (ES == 2) {
           const int sr = seg_in[size_t(it.seg_begin + j) * rows + rank * BM + row];
-          f = sr < 0 ? 0.f : row_unscale[sr] * k_unscale;
+          return sr < 0 ? 0.f : row_unscale[sr] * k_unscale;
         }
+        return 1.f;
+      };
+      float f_next = ntap > 0 ? unscale_of(0) : 1.f;
+      for (int j = 0; j < ntap; ++j) {
+        const float f = f_next;
+        if (j + 1 < ntap) f_next = unscale_of(j + 1);
         mbar_wait_sleep(tfull(b), tph);
         __syncwarp();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -517,8 +523,10 @@ __global__ void __maxnreg__(LAUNCH_REGS)
         uint32_t ph = 0;
         for (int kk = k_begin; kk < k_end; ++kk) {
           const Item it = items[sched_list[kk]];
+          int mat_next = it.seg_end > it.seg_begin ? seg_mat[it.seg_begin] : 0;  // one tap ahead
           for (int seg = it.seg_begin; seg < it.seg_end; ++seg) {
-            const int row = seg_mat[seg] * NP + int(rank) * C::NB;
+            const int row = mat_next * NP + int(rank) * C::NB;
+            if (seg + 1 < it.seg_end) mat_next = seg_mat[seg + 1];
             for (kb = 0; kb < NKB; ++kb) {
               mbar_wait(empty(s), ph ^ 1u);
               if (elect_one()) {
@@ -612,13 +620,20 @@ __global__ void __maxnreg__(LAUNCH_REGS)
       for (int kk = k_begin; kk < k_end; ++kk) {
         const Item it = items[sched_list[kk]];
         const int nstage = (it.seg_end - it.seg_begin) * NKB;
-        int cur_seg = -1;
         int seg = it.seg_begin, kb = 0;
-        for (int i = 0; i < nstage; ++i) {
-          if (seg != cur_seg) {
-            cur_seg = seg;
+        // the gather rows of the next tap are loaded one tap ahead (their latency is otherwise exposed
+        // at every tap start)
+        int nxt[J];
 #pragma unroll
-            for (int j = 0; j < J; ++j) src[j] = seg_in[size_t(seg) * rows + rank * BM + r0 + RPI * j];
+        for (int j = 0; j < J; ++j) nxt[j] = seg < it.seg_end ? seg_in[size_t(seg) * rows + rank * BM + r0 + RPI * j] : -1;
+        for (int i = 0; i < nstage; ++i) {
+          if (kb == 0) {
+#pragma unroll
+            for (int j = 0; j < J; ++j) src[j] = nxt[j];
+            if (seg + 1 < it.seg_end) {
+#pragma unroll
+              for (int j = 0; j < J; ++j) nxt[j] = seg_in[size_t(seg + 1) * rows + rank * BM + r0 + RPI * j];
+            }
           }
 #if KIFMM_TC_PROD_SLEEP
           mbar_wait_sleep(empty(s), ph ^ 1u);
