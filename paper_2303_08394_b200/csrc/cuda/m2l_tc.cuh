@@ -242,6 +242,15 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uin
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 // The three MMAs of one K step of the 3-term split: D (+)= A_hi B_hi, += A_hi B_lo, += A_lo B_hi.
+#ifndef KIFMM_MMA3_BFIRST
+#define KIFMM_MMA3_ORDER(GROUP, KIND)                                            \
+  "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %1, %4, %5, t;\n"      \
+  "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %2, %3, %5, t;\n"
+#else  // experiment: A_lo B_hi second (B_hi reused by consecutive MMAs)
+#define KIFMM_MMA3_ORDER(GROUP, KIND)                                            \
+  "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %2, %3, %5, t;\n"      \
+  "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %1, %4, %5, t;\n"
+#endif
 template <bool PAIR, int ES>
 __device__ __forceinline__ void mma3(uint32_t tmem_d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
                                      uint32_t idesc, uint32_t accumulate) {
@@ -249,8 +258,8 @@ __device__ __forceinline__ void mma3(uint32_t tmem_d, uint64_t ah, uint64_t al, 
   asm volatile(                                                                                  \
       "{\n.reg .pred p, t;\nsetp.ne.b32 p, %6, 0;\nsetp.eq.b32 t, %6, %6;\n"                \
       "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %1, %3, %5, p;\n"                 \
-      "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %1, %4, %5, t;\n"                 \
-      "tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %2, %3, %5, t;\n}" ::"r"(tmem_d), \
+      KIFMM_MMA3_ORDER(GROUP, KIND)                                                              \
+      "}" ::"r"(tmem_d),                                                                         \
       "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(accumulate))
   if constexpr (PAIR && ES == 4)
     KIFMM_MMA3("2", "tf32");
