@@ -611,7 +611,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
             ++ntaps;
           }
         }
-        if (prof && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 64))
+        if (prof && lane == 0)
           printf("cta %d: total %llu wait_tempty %llu wait_full %llu taps %d stages %d\n", int(blockIdx.x),
                  clock64() - t_all, t_te, t_fu, ntaps, nst);
       }
@@ -1029,37 +1029,71 @@ struct M2LTcPlan {
     n_tiles = int(tile_seg.size()) - 1;
     n_segs = int(seg_mat.size());
     slots = int64_t(n_segs) * rows;
-    // ---- items: split each tile's taps into balanced chunks (~8 per SM or SM pair; measured best at
-    //      config 2 among 2/4/8/16 per SM)
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int64_t target_items = int64_t(8) * (pair ? sms / 2 : sms);
-    int chunk = int(std::max<int64_t>(8, (n_segs + target_items - 1) / std::max<int64_t>(1, target_items)));
-    if (const char* e = std::getenv("KIFMM_TC_CHUNK")) chunk = std::max(1, std::atoi(e));
+    // ---- items and their schedule over the persistent CTAs (pairs).  Default: McNaughton's wrap-around
+    //      rule -- tiles are laid end to end (taps as the unit of work) and cut into G consecutive bins of
+    //      equal length, so every CTA gets the same number of taps (+- 1) and a tile is split only where a
+    //      bin boundary falls (few partial slots).  KIFMM_TC_SCHED=lpt: fixed-size chunks (KIFMM_TC_CHUNK)
+    //      assigned longest-first (the previous scheme; up to one chunk of imbalance).
+    const int G = std::max(1, pair ? sm_count() / 2 : sm_count());
+    bool wrap = true;
+    if (const char* e = std::getenv("KIFMM_TC_SCHED")) wrap = std::string(e) != "lpt";
     std::vector<tc::Item> items;
     std::vector<int> tile_slot{0};
-    for (int ti = 0; ti < n_tiles; ++ti) {
-      const int a = tile_seg[ti], b = tile_seg[ti + 1];
-      const int pieces = std::max(1, (b - a + chunk - 1) / chunk);
-      for (int pc = 0; pc < pieces; ++pc) {
-        const int sa = a + int(int64_t(b - a) * pc / pieces), sb = a + int(int64_t(b - a) * (pc + 1) / pieces);
-        items.push_back({ti, sa, sb, int(items.size())});
+    std::vector<int> sched;
+    if (wrap) {
+      const int64_t total_taps = n_segs;
+      const int bins = int(std::max<int64_t>(1, std::min<int64_t>(G, total_taps)));
+      std::vector<std::vector<int>> lists(bins);
+      int bin = 0;
+      int64_t fill = 0;
+      const int64_t cap = (total_taps + bins - 1) / bins;
+      for (int ti = 0; ti < n_tiles; ++ti) {
+        int a = tile_seg[ti];
+        const int b = tile_seg[ti + 1];
+        while (a < b) {
+          const int take = int(std::min<int64_t>(b - a, cap - fill));
+          lists[bin].push_back(int(items.size()));
+          items.push_back({ti, a, a + take, int(items.size())});
+          a += take;
+          fill += take;
+          if (fill == cap && bin + 1 < bins) {
+            ++bin;
+            fill = 0;
+          }
+        }
+        tile_slot.push_back(int(items.size()));
       }
-      tile_slot.push_back(int(items.size()));
+      sched_g = bins;
+      sched.push_back(0);
+      for (auto& l : lists) sched.push_back(sched.back() + int(l.size()));
+      for (auto& l : lists) sched.insert(sched.end(), l.begin(), l.end());
+    } else {
+      const int64_t target_items = int64_t(8) * G;
+      int chunk = int(std::max<int64_t>(8, (n_segs + target_items - 1) / std::max<int64_t>(1, target_items)));
+      if (const char* e = std::getenv("KIFMM_TC_CHUNK")) chunk = std::max(1, std::atoi(e));
+      for (int ti = 0; ti < n_tiles; ++ti) {
+        const int a = tile_seg[ti], b = tile_seg[ti + 1];
+        const int pieces = std::max(1, (b - a + chunk - 1) / chunk);
+        for (int pc = 0; pc < pieces; ++pc) {
+          const int sa = a + int(int64_t(b - a) * pc / pieces), sb = a + int(int64_t(b - a) * (pc + 1) / pieces);
+          items.push_back({ti, sa, sb, int(items.size())});
+        }
+        tile_slot.push_back(int(items.size()));
+      }
+      // longest first (slots keep the fixed reduction order)
+      std::stable_sort(items.begin(), items.end(), [](const tc::Item& x, const tc::Item& y) {
+        return (x.seg_end - x.seg_begin) > (y.seg_end - y.seg_begin);
+      });
+      sched_g = std::max(1, std::min(int(items.size()), G));
+      sched = lpt_schedule(items, sched_g);
     }
     n_items = int(items.size());
-    // launch order: longest items first (slots keep the fixed reduction order)
-    std::stable_sort(items.begin(), items.end(), [](const tc::Item& x, const tc::Item& y) {
-      return (x.seg_end - x.seg_begin) > (y.seg_end - y.seg_begin);
-    });
     up(&d_tile_out, tile_out, total);
     up(&d_tile_slot, tile_slot, total);
     up(&d_seg_mat, seg_mat, total);
     up(&d_seg_in, seg_in, total);
     up(&d_items, items, total);
-    sched_g = std::max(1, std::min(n_items, pair ? sm_count() / 2 : sm_count()));
-    if (const char* e = std::getenv("KIFMM_TC_GRID")) sched_g = std::max(1, std::min(n_items, std::atoi(e)));
-    up(&d_sched, lpt_schedule(items, sched_g), total);
+    up(&d_sched, sched, total);
     // ---- K_t split into tf32 hi / lo, padded to 160 x 160 per transfer vector
     const int ne = ops.n_e, nc = ops.n_c, nt = ops.n_m2l;
     std::vector<float> khi(size_t(nt) * tc::NP * tc::NP, 0.f), klo(khi.size(), 0.f);
