@@ -173,7 +173,13 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
   if (QUEUE && DRAIN && blockIdx.x == 0 && tid == 0) atomicExch(queue + 1, 1);
   for (int wi = blockIdx.x;;) {
   if (QUEUE) {
-    if (tid == 0) s_wi = (!DRAIN && atomicAdd(queue + 1, 0) != 0) ? n_works : atomicAdd(queue, 1);
+    if (tid == 0) {
+      // side blocks pause while queue[3] is raised (the M2L kernel runs) -- co-running warps slow the
+      // tensor-core pipeline more than the near field gains
+      if (!DRAIN)
+        while (atomicAdd(queue + 3, 0) != 0 && atomicAdd(queue + 1, 0) == 0) __nanosleep(2000);
+      s_wi = (!DRAIN && atomicAdd(queue + 1, 0) != 0) ? n_works : atomicAdd(queue, 1);
+    }
     __syncthreads();
     wi = s_wi;
     if (wi >= n_works) {

@@ -319,6 +319,7 @@ struct kifmm_gpu_plan {
   int device = 0;
   int precision = 32;
   bool leaf_packed = false;
+  bool near_pause = false;  // side blocks sleep during M2L (KIFMM_NEAR_PAUSE=1; measured slower: 1.63 vs 1.52 ms)
   int near_bps = 2;     // queue mode: near-field blocks per SM next to the tree passes (KIFMM_NEAR_BPS, 0 = off)
   DevMem near_counter;  // queue mode work counter [, counter at the drain launch (KIFMM_NEAR_DEBUG)]
   bool near_debug = false, near_skip = false, far_as_leaf = false, near_corun = false;
@@ -911,7 +912,8 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   const bool packed = leaf_packed;
   if (packed) {
     if (const char* e = std::getenv("KIFMM_NEAR_BPS")) near_bps = std::max(0, std::atoi(e));
-    near_counter.alloc(3 * sizeof(int), &dev_bytes);
+    near_counter.alloc(4 * sizeof(int), &dev_bytes);
+    if (const char* e = std::getenv("KIFMM_NEAR_PAUSE")) near_pause = std::atoi(e) != 0;
     near_debug = std::getenv("KIFMM_NEAR_DEBUG") != nullptr;
     near_skip = std::getenv("KIFMM_NEAR_SKIP") != nullptr;  // timing experiments only: wrong results
     if (const char* e = std::getenv("KIFMM_NEAR_FORK")) near_fork_at = std::string(e) == "m2l" ? 1 : 0;
@@ -1193,7 +1195,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   };
   auto fork_near = [&]() {
     if ((!timed || corun) && leaf_near.n && !near_skip) {
-      if (queue_mode) KIFMM_CUDA(cudaMemsetAsync(near_counter.p, 0, 2 * sizeof(int), s));
+      if (queue_mode) KIFMM_CUDA(cudaMemsetAsync(near_counter.p, 0, 4 * sizeof(int), s));
       KIFMM_CUDA(cudaEventRecord(ev_fork, s));
       KIFMM_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
       if (queue_mode)
@@ -1276,6 +1278,8 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     KIFMM_CUDA(cudaEventRecord(ev_join, side));
   }
   if (near_fork_at == 1 || corun) fork_near();  // experiments (KIFMM_NEAR_FORK=m2l): near field next to M2L only
+  if (queue_mode && near_pause)  // side near-field blocks sleep while M2L runs
+    KIFMM_CUDA(cudaMemsetAsync(near_counter.as<int>() + 3, 0x01, 1, s));
   // M2L over all levels at once, accumulated as reference-level check potentials
   if (m2l_backend >= 2) {
     if constexpr (sizeof(T) == 4) {
@@ -1306,6 +1310,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
       ++launches;
     }
   }
+  if (queue_mode && near_pause) KIFMM_CUDA(cudaMemsetAsync(near_counter.as<int>() + 3, 0, sizeof(int), s));
   if (queue_mode && near_debug && std::getenv("KIFMM_NEAR_DEBUG_M2L"))  // experiments: snapshot after M2L
     KIFMM_CUDA(cudaMemcpyAsync(near_counter.as<int>() + 2, near_counter.as<int>(), sizeof(int),
                                cudaMemcpyDeviceToDevice, s));
