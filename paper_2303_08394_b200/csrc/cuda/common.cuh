@@ -137,11 +137,16 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// compiled in only with -DKIFMM_TIMELINE_PROBES (they cost registers in the far kernel)
 __device__ __forceinline__ void timeline_begin(int id) {
+#ifdef KIFMM_TIMELINE_PROBES
   if (threadIdx.x == 0 && g_timeline_on) atomicMin(&g_timeline[id][0], globaltimer());
+#endif
 }
 __device__ __forceinline__ void timeline_end(int id) {
+#ifdef KIFMM_TIMELINE_PROBES
   if (threadIdx.x == 0 && g_timeline_on) atomicMax(&g_timeline[id][1], globaltimer());
+#endif
 }
 
 // Far-away zero-charge source used to pad staged source rounds (contributes exactly 0).

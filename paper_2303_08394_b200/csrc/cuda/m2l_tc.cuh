@@ -388,10 +388,12 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
   timeline_begin(PAIR ? 1 : 2);
+#ifdef KIFMM_TIMELINE_PROBES
   if (PAIR && blockIdx.x == 0 && threadIdx.x == 0 && g_timeline_on) {  // SM clock probe (experiments)
     g_timeline[8][0] = globaltimer();
     g_timeline[8][1] = clock64();
   }
+#endif
   if (warp >= EPI_WARP0) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
 
@@ -703,10 +705,12 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   timeline_end(PAIR ? 1 : 2);
+#ifdef KIFMM_TIMELINE_PROBES
   if (PAIR && blockIdx.x == 0 && threadIdx.x == 0 && g_timeline_on) {
     g_timeline[9][0] = globaltimer();
     g_timeline[9][1] = clock64();
   }
+#endif
   if (PAIR) cluster_sync();
   if (warp == 0) {
     __syncwarp();

@@ -362,9 +362,6 @@ struct FarWork {
   int node0, kind0, pad0, pad1;
 };
 constexpr int kFarWarps = 6;
-#ifndef KIFMM_FAR_MINB
-#define KIFMM_FAR_MINB 1
-#endif
 constexpr int kFarMaxNe = 224;
 
 template <class T, bool GRAD>
@@ -418,7 +415,7 @@ __global__ void __launch_bounds__(kFarWarps * 32) far_kernel(P2PParams<T> p, con
 // pot_out[perm[t]] (input order) or back to pot[t] when perm is null.  Every
 // owned leaf has a work item (surf_begin == surf_end: output write only).
 template <bool GRAD>
-__global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_f2_kernel(P2PParams<float> p,
+__global__ void __launch_bounds__(kFarWarps * 32) far_f2_kernel(P2PParams<float> p,
                                                                  const FarWork* __restrict__ works, int n_works,
                                                                  const int2* __restrict__ surfaces,
                                                                  const float* __restrict__ M,
