@@ -176,8 +176,11 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
     if (tid == 0) {
       // side blocks pause while queue[3] is raised (the M2L kernel runs) -- co-running warps slow the
       // tensor-core pipeline more than the near field gains
+      // (queue[3] = 1: all side blocks pause; 2: the odd ones)
       if (!DRAIN)
-        while (atomicAdd(queue + 3, 0) != 0 && atomicAdd(queue + 1, 0) == 0) __nanosleep(2000);
+        for (int pz; (pz = atomicAdd(queue + 3, 0)) != 0 && (pz == 1 || (blockIdx.x & 1)) &&
+                     atomicAdd(queue + 1, 0) == 0;)
+          __nanosleep(2000);
       s_wi = (!DRAIN && atomicAdd(queue + 1, 0) != 0) ? n_works : atomicAdd(queue, 1);
     }
     __syncthreads();

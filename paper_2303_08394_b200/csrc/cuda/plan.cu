@@ -319,7 +319,7 @@ struct kifmm_gpu_plan {
   int device = 0;
   int precision = 32;
   bool leaf_packed = false;
-  bool near_pause = false;  // side blocks sleep during M2L (KIFMM_NEAR_PAUSE=1; measured slower: 1.63 vs 1.52 ms)
+  int near_pause = 0;  // side blocks sleep during M2L: 1 all, 2 half (KIFMM_NEAR_PAUSE; 1 measured slower)
   int near_bps = 2;     // queue mode: near-field blocks per SM next to the tree passes (KIFMM_NEAR_BPS, 0 = off)
   DevMem near_counter;  // queue mode work counter [, counter at the drain launch (KIFMM_NEAR_DEBUG)]
   bool near_debug = false, near_skip = false, far_as_leaf = false, near_corun = false;
@@ -913,7 +913,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   if (packed) {
     if (const char* e = std::getenv("KIFMM_NEAR_BPS")) near_bps = std::max(0, std::atoi(e));
     near_counter.alloc(4 * sizeof(int), &dev_bytes);
-    if (const char* e = std::getenv("KIFMM_NEAR_PAUSE")) near_pause = std::atoi(e) != 0;
+    if (const char* e = std::getenv("KIFMM_NEAR_PAUSE")) near_pause = std::atoi(e);
     near_debug = std::getenv("KIFMM_NEAR_DEBUG") != nullptr;
     near_skip = std::getenv("KIFMM_NEAR_SKIP") != nullptr;  // timing experiments only: wrong results
     if (const char* e = std::getenv("KIFMM_NEAR_FORK")) near_fork_at = std::string(e) == "m2l" ? 1 : 0;
@@ -1279,7 +1279,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   }
   if (near_fork_at == 1 || corun) fork_near();  // experiments (KIFMM_NEAR_FORK=m2l): near field next to M2L only
   if (queue_mode && near_pause)  // side near-field blocks sleep while M2L runs
-    KIFMM_CUDA(cudaMemsetAsync(near_counter.as<int>() + 3, 0x01, 1, s));
+    KIFMM_CUDA(cudaMemsetAsync(near_counter.as<int>() + 3, near_pause, 1, s));
   // M2L over all levels at once, accumulated as reference-level check potentials
   if (m2l_backend >= 2) {
     if constexpr (sizeof(T) == 4) {
