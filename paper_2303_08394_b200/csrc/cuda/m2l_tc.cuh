@@ -54,18 +54,19 @@ namespace tc {
 constexpr int BM = 128;  // target rows per CTA
 constexpr int NP = 160;  // check points / equivalent points, padded (p = 6)
 // Warpgroups: 0 = {TMA + TMEM alloc, MMA issuer, A-arrival forwarder (pair), idle}, 1 = A producers,
-// 2-3 = epilogue.  The kernel launches with 96 registers per thread (__maxnreg__) and rebalances with
-// setmaxnreg (warpgroups 0-1 down to 56, epilogue up to 136): a CTA holds 48 K registers instead of
-// 60 K, leaving registers on the SM for small blocks of other kernels next to it.
+// 2-3 = epilogue.  The kernel launches with 80 registers per thread (__maxnreg__) and rebalances with
+// setmaxnreg (warpgroups 0-1 down to 48, epilogue up to 112): a CTA holds 40 K registers, leaving
+// room on the SM for three near-field blocks next to it (measured fastest end to end, despite a few
+// hundred bytes of epilogue spills; 96/56/136 with two near blocks: +2.5 %).
 constexpr int EPI_WARPS = 8, EPI_COLS = NP / 2;   // 2 warps per TMEM lane quarter, 80 columns each
 constexpr int EPI_WARP0 = 8;                      // epilogue warps 8..15
 constexpr int PROD_WARP0 = 4;                     // A producer warps 4..7
 constexpr int FWD_WARP = 2;                       // A-arrival forwarder (pair)
 constexpr int THREADS = 512;
 #ifndef KIFMM_TC_LAUNCH_REGS
-#define KIFMM_TC_LAUNCH_REGS 96
-#define KIFMM_TC_LOW_REGS 56
-#define KIFMM_TC_EPI_REGS 136
+#define KIFMM_TC_LAUNCH_REGS 80
+#define KIFMM_TC_LOW_REGS 48
+#define KIFMM_TC_EPI_REGS 112
 #endif
 constexpr int LAUNCH_REGS = KIFMM_TC_LAUNCH_REGS, LOW_REGS = KIFMM_TC_LOW_REGS, EPI_REGS = KIFMM_TC_EPI_REGS;
 static_assert(4 * 32 * LOW_REGS * 2 + 8 * 32 * EPI_REGS <= THREADS * LAUNCH_REGS, "setmaxnreg budget");
@@ -75,11 +76,11 @@ constexpr int NACC = 3;              // accumulator buffers: the MMA runs up to 
 // ROWB: bytes of one operand row per stage (K block of ROWB/4 fp32): 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B,
 // twice the stages for the same shared memory => deeper latency hiding).
 #ifndef KIFMM_TC_STAGE_KB
-#define KIFMM_TC_STAGE_KB 160
+#define KIFMM_TC_STAGE_KB 136
 #endif
-// shared memory for pipeline stages: 160 KB (6 stages for the f16 pair, 4 for the single CTA) leaves
-// room on the SM for two near-field blocks next to a tcgen05 CTA (measured 6-7 % faster end to end than
-// a full 216 KB pipeline with the near field waiting for whole SMs; 112-184 KB measured within noise)
+// shared memory for pipeline stages: 136 KB (5 stages for the f16 pair, 3 for the single CTA) leaves
+// room on the SM for three near-field blocks next to a tcgen05 CTA (a full 216 KB pipeline, with the
+// near field waiting for whole SMs, measured 6-7 % slower end to end; M2L alone is insensitive to 112-216)
 constexpr int kStageBudgetKB = KIFMM_TC_STAGE_KB;
 #ifndef KIFMM_TC_EG
 #define KIFMM_TC_EG 1

@@ -320,7 +320,7 @@ struct kifmm_gpu_plan {
   int precision = 32;
   bool leaf_packed = false;
   int near_pause = 0;  // side blocks sleep during M2L: 1 all, 2 half (KIFMM_NEAR_PAUSE; 1 measured slower)
-  int near_bps = 2;     // queue mode: near-field blocks per SM next to the tree passes (KIFMM_NEAR_BPS, 0 = off)
+  int near_bps = 3;     // queue mode: near-field blocks per SM next to the tree passes (KIFMM_NEAR_BPS, 0 = off)
   DevMem near_counter;  // queue mode work counter [, counter at the drain launch (KIFMM_NEAR_DEBUG)]
   bool near_debug = false, near_skip = false, far_as_leaf = false, near_corun = false;
   int near_fork_at = 0;  // 0: at the start of the evaluate, 1: just before M2L
