@@ -296,7 +296,8 @@ struct LeafPlan {
 
 struct M2MLevel {
   GemmTiles tiles;  // one tile per (64 parents, octant)   [SIMT]
-  TcGemm tc;        // one tile per (128 parents, octant)  [tcgen05]
+  TcGemm tc;        // one tile per (128 parents, octant), or per 128 parents with 8 octant taps (direct)
+  bool direct = false;
   int r0 = 0, r1 = 0;  // child rows to split before the tcgen05 GEMM
   DevMem parents, masks;
   int n = 0;
@@ -320,7 +321,8 @@ struct kifmm_gpu_plan {
   int precision = 32;
   bool leaf_packed = false;
   int near_pause = 0;  // side blocks sleep during M2L: 1 all, 2 half (KIFMM_NEAR_PAUSE; 1 measured slower)
-  int near_bps = 3;     // queue mode: near-field blocks per SM next to the tree passes (KIFMM_NEAR_BPS, 0 = off)
+  int near_bps = 3;  // queue mode: near-field blocks per SM next to the tree passes (KIFMM_NEAR_BPS, 0 = off)
+  bool m2m_parent_tiles = false;  // KIFMM_M2M=parent: 8-tap parent tiles, direct (measured slower)
   DevMem near_counter;  // queue mode work counter [, counter at the drain launch (KIFMM_NEAR_DEBUG)]
   bool near_debug = false, near_skip = false, far_as_leaf = false, near_corun = false;
   int near_fork_at = 0;  // 0: at the start of the evaluate, 1: just before M2L
@@ -624,6 +626,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
 
   // ---- M2M per level (owned internal nodes), then the redundant top levels
   const std::vector<double> b_m2m = gemm_tc ? octant_b(ops.m2m) : std::vector<double>();
+  if (const char* e = std::getenv("KIFMM_M2M")) m2m_parent_tiles = std::string(e) == "parent";
   auto m2m_tiles = [&](std::vector<int64_t>& parents) {
     const int BMS = gemm_tc ? tc::BM : 64;
     std::vector<TileSpec> tiles;
@@ -654,7 +657,31 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       msk.push_back(m);
     }
     auto g = std::make_unique<M2MLevel>();
-    if (gemm_tc) {
+    if (gemm_tc && m2m_parent_tiles) {
+      // parent-major tiles: 128 parents x up to 8 octant taps accumulate in the epilogue and are written
+      // straight into M (+ split) -- no scratch rows, no reduction launch
+      std::vector<TileSpec> pt;
+      for (size_t s0 = 0; s0 < parents.size(); s0 += tc::BM) {
+        TileSpec ts;
+        ts.out.assign(tc::BM, -1);
+        for (int r = 0; r < tc::BM && s0 + r < parents.size(); ++r) ts.out[r] = int(parents[s0 + r]);
+        for (int o = 0; o < 8; ++o) {
+          std::vector<int> in(tc::BM, -1);
+          bool any = false;
+          for (int r = 0; r < tc::BM && s0 + r < parents.size(); ++r) {
+            const int64_t ch = t.node_children[8 * parents[s0 + r] + o];
+            if (ch >= 0) {
+              in[r] = int(ch);
+              any = true;
+            }
+          }
+          if (any) ts.segs.push_back({o, in});
+        }
+        pt.push_back(std::move(ts));
+      }
+      g->tc.build(pt, b_m2m, 8, &dev_bytes);
+      g->direct = true;
+    } else if (gemm_tc) {
       g->tc.build(tiles, b_m2m, 8, &dev_bytes);
       int64_t lo = INT64_MAX, hi = -1;  // child rows (one level: contiguous node range)
       for (int64_t pn : parents)
@@ -1233,6 +1260,10 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   mark();  // 1
   // M2M, levels d-1 .. floor
   auto m2m_level = [&](const M2MLevel& lv) {
+    if (gemm_tc && lv.direct) {
+      tgemm(lv.tc, sp_M, Mp, false, &sp_M);
+      return;
+    }
     if (gemm_tc) {
       if constexpr (sizeof(T) == 4) {
         tgemm(lv.tc, sp_M, m2m_scratch.as<T>(), false, nullptr);
