@@ -100,13 +100,18 @@ __device__ __forceinline__ void p2p_round(const v4_t<T>* sh, int begin, int end,
 // one target and unrolls sources by 8; the packed fp32 kernel gives every
 // thread two targets (one FP32x2 lane pair) and unrolls by 4.  Sections are
 // padded to a multiple of leaf_unroll * R so every slice gets whole unroll groups.
+#ifndef KIFMM_NEAR_NPAIR
+#define KIFMM_NEAR_NPAIR 1  // target pairs per thread in the packed kernel (1: 2 targets, 2: 4 targets)
+#endif
+constexpr int kNearNPair = KIFMM_NEAR_NPAIR;
 __host__ __device__ inline int leaf_slices(int nt, bool packed) {
-  const int tt = packed ? (nt + 1) / 2 : nt;
+  const int tpt = packed ? 2 * kNearNPair : 1;  // targets per thread
+  const int tt = (nt + tpt - 1) / tpt;
   const int mx = packed ? 16 : 8;
   const int r = 128 / (tt > 0 ? tt : 1);
   return r < 1 ? 1 : (r > mx ? mx : r);
 }
-__host__ __device__ inline int leaf_unroll(bool packed) { return packed ? 4 : 8; }
+__host__ __device__ inline int leaf_unroll(bool packed) { return packed ? 4 / kNearNPair : 8; }
 
 // Packed fp32 pair-of-targets round: FP32x2 instructions whose source operand
 // is a scalar register broadcast to both lanes (ptxas folds mov.b64 {s, s}
@@ -114,6 +119,51 @@ __host__ __device__ inline int leaf_unroll(bool packed) { return packed ? 4 : 8;
 // source and thread: 3 FADD2 + 3 FMUL2/FFMA2 (r^2) + 2 MUFU.RSQ + 2 (potential)
 // + 5 (gradient) instructions for TWO target-source pairs.
 __device__ __forceinline__ f2_t f2_bcast(float a) { return f2_pack(a, a); }
+
+// NP target pairs per thread: one staged source (one LDS.128) feeds NP lane pairs.
+template <bool GRAD, bool MASK, int NP>
+__device__ __forceinline__ void p2p_round_fn(const float4* sh, int begin, int end, const f2_t (&x)[NP],
+                                             const f2_t (&y)[NP], const f2_t (&z)[NP], f2_t (&ph)[NP],
+                                             f2_t (&gx)[NP], f2_t (&gy)[NP], f2_t (&gz)[NP]) {
+  constexpr int U = 4 / NP;  // sources per unrolled step
+  f2_t a_ph[NP], a_gx[NP], a_gy[NP], a_gz[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) a_ph[k] = a_gx[k] = a_gy[k] = a_gz[k] = 0;
+#pragma unroll 2
+  for (int j = begin; j < end; j += U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float4 s = sh[j + u];
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const f2_t dx = f2_sub(x[k], f2_bcast(s.x)), dy = f2_sub(y[k], f2_bcast(s.y)), dz = f2_sub(z[k], f2_bcast(s.z));
+        const f2_t r2 = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+        float ra, rb;
+        f2_unpack(r2, ra, rb);
+        const f2_t ri = MASK ? f2_pack(rinv_masked(ra), rinv_masked(rb)) : f2_pack(rinv(ra), rinv(rb));
+        if (GRAD) {
+          const f2_t qr = f2_mul(f2_bcast(s.w), ri);
+          a_ph[k] = f2_add(a_ph[k], qr);
+          const f2_t qr3 = f2_mul(qr, f2_mul(ri, ri));
+          a_gx[k] = f2_fma(qr3, dx, a_gx[k]);
+          a_gy[k] = f2_fma(qr3, dy, a_gy[k]);
+          a_gz[k] = f2_fma(qr3, dz, a_gz[k]);
+        } else {
+          a_ph[k] = f2_fma(f2_bcast(s.w), ri, a_ph[k]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    ph[k] = f2_add(ph[k], a_ph[k]);
+    if (GRAD) {
+      gx[k] = f2_add(gx[k], a_gx[k]);
+      gy[k] = f2_add(gy[k], a_gy[k]);
+      gz[k] = f2_add(gz[k], a_gz[k]);
+    }
+  }
+}
 
 template <bool GRAD, bool MASK>
 __device__ __forceinline__ void p2p_round_f2(const float4* sh, int begin, int end, f2_t x, f2_t y, f2_t z, f2_t& ph,
@@ -191,15 +241,22 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
     }
   }
   const LeafWork w = works[wi];
-  const int nt = w.t_count, T2 = (nt + 1) >> 1;
+  constexpr int NPR = kNearNPair, TPT = 2 * NPR;  // target pairs / targets per thread
+  const int nt = w.t_count, TT = (nt + TPT - 1) / TPT;
   const int R = leaf_slices(nt, true);
-  const int slice = tid / T2, ta = tid - slice * T2, tb = ta + T2;
-  const bool active = slice < R, has_b = active && tb < nt;
-
-  const float4 xa = p.src[w.t_begin + (active ? ta : 0)];
-  const float4 xb = p.src[w.t_begin + (has_b ? tb : 0)];
-  const f2_t x = f2_pack(xa.x, xb.x), y = f2_pack(xa.y, xb.y), z = f2_pack(xa.z, xb.z);
-  f2_t ph = 0, gx = 0, gy = 0, gz = 0;
+  const int slice = tid / TT, t0 = tid - slice * TT;  // targets t0 + m TT, m < TPT
+  const bool active = slice < R;
+  f2_t x[NPR], y[NPR], z[NPR], ph[NPR], gx[NPR], gy[NPR], gz[NPR];
+#pragma unroll
+  for (int k = 0; k < NPR; ++k) {
+    const int ta = t0 + (2 * k) * TT, tb = t0 + (2 * k + 1) * TT;
+    const float4 xa = p.src[w.t_begin + (active && ta < nt ? ta : 0)];
+    const float4 xb = p.src[w.t_begin + (active && tb < nt ? tb : 0)];
+    x[k] = f2_pack(xa.x, xb.x);
+    y[k] = f2_pack(xa.y, xb.y);
+    z[k] = f2_pack(xa.z, xb.z);
+    ph[k] = gx[k] = gy[k] = gz[k] = 0;
+  }
   const float fa = float(kFarAway);
   auto put = [&](int i, float4 v) { sh[i] = v; };
 
@@ -224,28 +281,32 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
     if (active) {
       if (S) {
         const int per = S / R;
-        p2p_round_f2<GRAD, true>(sh, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
+        p2p_round_fn<GRAD, true, NPR>(sh, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
       }
       if (O) {
         const int per = O / R;
-        p2p_round_f2<GRAD, false>(sh, S + slice * per, S + slice * per + per, x, y, z, ph, gx, gy, gz);
+        p2p_round_fn<GRAD, false, NPR>(sh, S + slice * per, S + slice * per + per, x, y, z, ph, gx, gy, gz);
       }
     }
     __syncthreads();
   }
 
-  float* red = reinterpret_cast<float*>(sh);  // [slice][component][n_t]: R * n_t <= 256
+  float* red = reinterpret_cast<float*>(sh);  // [slice][component][n_t]: R * n_t <= 128 TPT
   constexpr int NC = GRAD ? 4 : 1;
   if (active) {
-    float a[4], b[4];
-    f2_unpack(ph, a[0], b[0]);
-    f2_unpack(gx, a[1], b[1]);
-    f2_unpack(gy, a[2], b[2]);
-    f2_unpack(gz, a[3], b[3]);
 #pragma unroll
-    for (int d = 0; d < NC; ++d) {
-      red[(slice * NC + d) * nt + ta] = a[d];
-      if (has_b) red[(slice * NC + d) * nt + tb] = b[d];
+    for (int k = 0; k < NPR; ++k) {
+      float a[4], b[4];
+      f2_unpack(ph[k], a[0], b[0]);
+      f2_unpack(gx[k], a[1], b[1]);
+      f2_unpack(gy[k], a[2], b[2]);
+      f2_unpack(gz[k], a[3], b[3]);
+      const int ta = t0 + (2 * k) * TT, tb = t0 + (2 * k + 1) * TT;
+#pragma unroll
+      for (int d = 0; d < NC; ++d) {
+        if (ta < nt) red[(slice * NC + d) * nt + ta] = a[d];
+        if (tb < nt) red[(slice * NC + d) * nt + tb] = b[d];
+      }
     }
   }
   __syncthreads();
