@@ -626,7 +626,19 @@ __global__ void __maxnreg__(LAUNCH_REGS)
       constexpr int J = BM / RPI;       // passes (rows per thread)
       const int t = threadIdx.x - 32 * PROD_WARP0;  // 0..127
       const int c = t % CH, r0 = t / CH;
-      int src[J];
+      // per-thread constants: swizzled shared-memory offsets of its rows; per tap: the global byte
+      // offsets of its gathered rows (zero-filled when absent); per stage only the K-block advances
+      uint32_t soff[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int r = r0 + RPI * j;
+        const int sw = ROWB == 128 ? (r & 7) : ((r & 7) >> 1);  // Swizzle<3,4,3> / Swizzle<2,4,3>
+        soff[j] = uint32_t((r >> 3) * C::ATOM + (r & 7) * ROWB + ((c ^ sw) << 4));
+      }
+      const char* mh = static_cast<const char*>(m_hi) + c * 16;
+      const char* ml = static_cast<const char*>(m_lo) + c * 16;
+      size_t gofs[J];
+      int gsz[J];
       int s = 0;
       uint32_t ph = 0;
       for (int kk = k_begin; kk < k_end; ++kk) {
@@ -641,7 +653,11 @@ __global__ void __maxnreg__(LAUNCH_REGS)
         for (int i = 0; i < nstage; ++i) {
           if (kb == 0) {
 #pragma unroll
-            for (int j = 0; j < J; ++j) src[j] = nxt[j];
+            for (int j = 0; j < J; ++j) {
+              const bool ok = nxt[j] >= 0;  // absent source: zero-fill, no global read
+              gofs[j] = size_t(ok ? nxt[j] : zero_row) * (NP * ES);
+              gsz[j] = ok ? 16 : 0;
+            }
             if (seg + 1 < it.seg_end) {
 #pragma unroll
               for (int j = 0; j < J; ++j) nxt[j] = seg_in[size_t(seg + 1) * rows + rank * BM + r0 + RPI * j];
@@ -652,21 +668,18 @@ __global__ void __maxnreg__(LAUNCH_REGS)
 #else
           mbar_wait(empty(s), ph ^ 1u);
 #endif
+          if (!(epi.debug & 1)) {
+            const uint32_t ahs = a_hi(s), als = a_lo(s);
+            const size_t kbo = size_t(kb) * ROWB;
 #pragma unroll
-          for (int j = 0; j < J; ++j) {
-            const int r = r0 + RPI * j;
-            const int sw = ROWB == 128 ? (r & 7) : ((r & 7) >> 1);  // Swizzle<3,4,3> / Swizzle<2,4,3>
-            const uint32_t off = uint32_t((r >> 3) * C::ATOM + (r & 7) * ROWB + ((c ^ sw) << 4));
-            const bool ok = src[j] >= 0;  // absent source: zero-fill, no global read
-            const size_t g = size_t(ok ? src[j] : zero_row) * NP * ES + kb * ROWB + c * 16;  // bytes
-            const int sz = ok ? 16 : 0;
-            if (epi.debug & 1) continue;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_hi(s) + off),
-                         "l"(static_cast<const char*>(m_hi) + g), "r"(sz)
-                         : "memory");
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(a_lo(s) + off),
-                         "l"(static_cast<const char*>(m_lo) + g), "r"(sz)
-                         : "memory");
+            for (int j = 0; j < J; ++j) {
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ahs + soff[j]),
+                           "l"(mh + gofs[j] + kbo), "r"(gsz[j])
+                           : "memory");
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(als + soff[j]),
+                           "l"(ml + gofs[j] + kbo), "r"(gsz[j])
+                           : "memory");
+            }
           }
           // non-blocking: the barrier receives this thread's arrival when its copies have landed
           // (as CUTLASS's cp.async UMMA mainloops do; the full barrier's count includes these arrivals)
