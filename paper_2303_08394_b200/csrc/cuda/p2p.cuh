@@ -504,17 +504,22 @@ __global__ void __launch_bounds__(kFarWarps * 32) far_f2_kernel(P2PParams<float>
   const bool out_a = slice == 0, out_b = slice == 0 && tb < nt;
   float pv[2] = {0.f, 0.f}, gv[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
   int ov[2] = {0, 0};
+  auto load_out = [&]() {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int t = t0 + (h ? tb : ta);
-    if (h ? out_b : out_a) {
-      pv[h] = pot[t];
-      if (GRAD)
+    for (int h = 0; h < 2; ++h) {
+      const int t = t0 + (h ? tb : ta);
+      if (h ? out_b : out_a) {
+        pv[h] = pot[t];
+        if (GRAD)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) gv[h][d] = grad[3 * size_t(t) + d];
-      ov[h] = perm ? perm[t] : t;
+          for (int d = 0; d < 3; ++d) gv[h][d] = grad[3 * size_t(t) + d];
+        ov[h] = perm ? perm[t] : t;
+      }
     }
-  }
+  };
+#ifndef KIFMM_FAR_LATE_OUT
+  load_out();  // prefetch the near-field result and the output permutation
+#endif
   const f2_t x = f2_pack(xa.x, xb.x), y = f2_pack(xa.y, xb.y), z = f2_pack(xa.z, xb.z);
   f2_t ph = 0, gx = 0, gy = 0, gz = 0;
   const float fa = float(kFarAway);
@@ -545,6 +550,9 @@ __global__ void __launch_bounds__(kFarWarps * 32) far_f2_kernel(P2PParams<float>
   }
   timeline_end(5);
   if (slice != 0) return;
+#ifdef KIFMM_FAR_LATE_OUT
+  load_out();
+#endif
   const float c = float(kInv4PiD);
   float* po = perm ? pot_out : pot;
   float* go = perm ? grad_out : grad;
