@@ -1009,13 +1009,15 @@ struct M2LTcPlan {
     for (const auto& g0 : groups) {
       std::vector<int64_t> grp(g0.begin(), g0.end());
       if (by_sig) {
-        std::vector<std::pair<uint64_t, int64_t>> key;
-        for (int64_t b : grp) {
-          std::vector<int> tv(t.v_tv + t.v_ptr[b], t.v_tv + t.v_ptr[b + 1]);
-          std::sort(tv.begin(), tv.end());
-          uint64_t h = 1469598103934665603ull ^ uint64_t(tv.size());
-          for (int x : tv) h = (h ^ uint64_t(x)) * 1099511628211ull;
-          key.push_back({h, b});
+        std::vector<std::pair<uint64_t, int64_t>> key(grp.size());
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < int64_t(grp.size()); ++i) {
+          const int64_t b = grp[i];
+          uint64_t bits[(316 + 63) / 64] = {};  // order-free signature: the set of transfer vectors
+          for (int64_t e = t.v_ptr[b]; e < t.v_ptr[b + 1]; ++e) bits[t.v_tv[e] >> 6] |= uint64_t(1) << (t.v_tv[e] & 63);
+          uint64_t h = 1469598103934665603ull;
+          for (uint64_t w : bits) h = (h ^ w) * 1099511628211ull;
+          key[i] = {h, b};
         }
         std::stable_sort(key.begin(), key.end(),
                          [](const auto& x, const auto& y) { return x.first < y.first; });
@@ -1023,25 +1025,42 @@ struct M2LTcPlan {
       }
       sorted_groups.push_back(std::move(grp));
     }
-    for (const auto& grp : sorted_groups) {
-      for (size_t s0 = 0; s0 < grp.size(); s0 += size_t(rows)) {
-        std::vector<int> out(rows, -1);
-        std::map<int, std::vector<int>> taps;
-        for (int r = 0; r < rows && s0 + r < grp.size(); ++r) {
-          const int64_t b = grp[s0 + r];
-          out[r] = int(b);
-          for (int64_t e = t.v_ptr[b]; e < t.v_ptr[b + 1]; ++e) {
-            auto& v = taps[t.v_tv[e]];
-            if (v.empty()) v.assign(rows, -1);
-            v[r] = int(t.v_idx[e]);
-          }
-        }
-        tile_out.insert(tile_out.end(), out.begin(), out.end());
-        for (auto& kv : taps) {
-          seg_mat.push_back(kv.first);
-          seg_in.insert(seg_in.end(), kv.second.begin(), kv.second.end());
-        }
-        tile_seg.push_back(int(seg_mat.size()));
+    // tiles: (group, first row); built in two parallel passes (tap sets, then the rows)
+    std::vector<std::pair<int, size_t>> tiles_def;
+    for (int gi = 0; gi < int(sorted_groups.size()); ++gi)
+      for (size_t s0 = 0; s0 < sorted_groups[gi].size(); s0 += size_t(rows)) tiles_def.push_back({gi, s0});
+    const int nt_tiles = int(tiles_def.size());
+    std::vector<std::vector<int>> tile_taps(nt_tiles);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int ti = 0; ti < nt_tiles; ++ti) {
+      const auto& grp = sorted_groups[tiles_def[ti].first];
+      const size_t s0 = tiles_def[ti].second;
+      uint64_t bits[(316 + 63) / 64] = {};
+      for (int r = 0; r < rows && s0 + r < grp.size(); ++r)
+        for (int64_t e = t.v_ptr[grp[s0 + r]]; e < t.v_ptr[grp[s0 + r] + 1]; ++e)
+          bits[t.v_tv[e] >> 6] |= uint64_t(1) << (t.v_tv[e] & 63);
+      for (int w = 0; w < (316 + 63) / 64; ++w)  // ascending transfer-vector id
+        for (uint64_t m = bits[w]; m; m &= m - 1) tile_taps[ti].push_back(64 * w + __builtin_ctzll(m));
+    }
+    tile_seg.assign(nt_tiles + 1, 0);
+    for (int ti = 0; ti < nt_tiles; ++ti) tile_seg[ti + 1] = tile_seg[ti] + int(tile_taps[ti].size());
+    tile_out.assign(size_t(nt_tiles) * rows, -1);
+    seg_mat.assign(tile_seg[nt_tiles], 0);
+    seg_in.assign(size_t(tile_seg[nt_tiles]) * rows, -1);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int ti = 0; ti < nt_tiles; ++ti) {
+      const auto& grp = sorted_groups[tiles_def[ti].first];
+      const size_t s0 = tiles_def[ti].second;
+      int slot[316];
+      for (size_t k = 0; k < tile_taps[ti].size(); ++k) {
+        slot[tile_taps[ti][k]] = tile_seg[ti] + int(k);
+        seg_mat[tile_seg[ti] + k] = tile_taps[ti][k];
+      }
+      for (int r = 0; r < rows && s0 + r < grp.size(); ++r) {
+        const int64_t b = grp[s0 + r];
+        tile_out[size_t(ti) * rows + r] = int(b);
+        for (int64_t e = t.v_ptr[b]; e < t.v_ptr[b + 1]; ++e)
+          seg_in[size_t(slot[t.v_tv[e]]) * rows + r] = int(t.v_idx[e]);
       }
     }
     n_tiles = int(tile_seg.size()) - 1;
@@ -1115,6 +1134,7 @@ struct M2LTcPlan {
     // ---- K_t split into tf32 hi / lo, padded to 160 x 160 per transfer vector
     const int ne = ops.n_e, nc = ops.n_c, nt = ops.n_m2l;
     std::vector<float> khi(size_t(nt) * tc::NP * tc::NP, 0.f), klo(khi.size(), 0.f);
+#pragma omp parallel for schedule(static)
     for (int v = 0; v < nt; ++v)
       for (int c = 0; c < nc; ++c)
         for (int e = 0; e < ne; ++e) {
@@ -1151,7 +1171,8 @@ struct M2LTcPlan {
     if (const char* e = std::getenv("KIFMM_TC_KIND")) f16 = std::string(e) != "tf32";
     if (f16) {
       std::vector<__half> h16(khi.size()), l16(khi.size());
-      for (size_t i = 0; i < khi.size(); ++i) {
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < int64_t(khi.size()); ++i) {
         const float x = (khi[i] + klo[i]) * kKScale;  // (hi + lo) == the fp32 K_t value exactly
         const __half h = __float2half_rn(x);
         h16[i] = h;

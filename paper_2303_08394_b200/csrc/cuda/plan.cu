@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "gemm.cuh"
+#include <chrono>
 #include <cstdio>
 
 #include "m2l_tc.cuh"
@@ -459,6 +460,15 @@ void kifmm_gpu_plan::upload_static(const kifmm_tree_view& t, const kifmm_operato
 }
 
 void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t, const kifmm_operator_view& ops) {
+  // plan-creation phase timing (KIFMM_PLAN_TIMING=1 prints host wall times per phase)
+  const bool ptime = std::getenv("KIFMM_PLAN_TIMING") != nullptr;
+  auto pt0 = std::chrono::steady_clock::now();
+  auto ptick = [&](const char* what) {
+    if (!ptime) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "plan %-22s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - pt0).count());
+    pt0 = now;
+  };
   opt = o;
   device = o.device;
   precision = o.precision;
@@ -497,6 +507,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   }
   for (auto& e : ev) KIFMM_CUDA(cudaEventCreate(&e));
 
+  ptick("setup");
   // ---- partition
   std::vector<int64_t> lbeg(world + 1, 0);
   lbeg[world] = nl;
@@ -582,6 +593,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     return b;
   };
 
+  ptick("partition+static upload");
   // ---- P2M: one check work per owned leaf, solve rows = slots
   {
     std::vector<CheckWork> w;
@@ -624,6 +636,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     }
   }
 
+  ptick("P2M + up solves");
   // ---- M2M per level (owned internal nodes), then the redundant top levels
   const std::vector<double> b_m2m = gemm_tc ? octant_b(ops.m2m) : std::vector<double>();
   if (const char* e = std::getenv("KIFMM_M2M")) m2m_parent_tiles = std::string(e) == "parent";
@@ -751,6 +764,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
 
   m2m_scratch.alloc(size_t(std::max<int64_t>(1, m2m_scratch_rows)) * np * es, &dev_bytes);
 
+  ptick("M2M");
   // ---- P2L check works: active nodes with X members
   {
     std::vector<CheckWork> w;
@@ -770,6 +784,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     p2l_ranges.upload(rg, &dev_bytes);
   }
 
+  ptick("P2L");
   // ---- M2L tiles: active targets at level >= 2 grouped by (level, octant), Z-order inside
   std::vector<std::vector<int64_t>> m2l_groups;
   {
@@ -849,6 +864,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     info.m2l_padded_pairs = m2l.slots;
   }
 
+  ptick("M2L");
   // ---- downward solves over active nodes at level >= 2 (slots -> tmp rows)
   std::vector<int64_t> dn_nodes;
   for (int64_t n = 0; n < nn; ++n)
@@ -896,6 +912,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   }
   const std::vector<double> b_l2l = gemm_tc ? octant_b(ops.l2l) : std::vector<double>();
 
+  ptick("down solves");
   // ---- L2L per level: active children at l+1 (l >= 2), grouped by octant
   for (int l = 2; l < depth; ++l) {
     std::vector<TileSpec> tiles;
@@ -928,6 +945,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     }
   }
 
+  ptick("L2L");
   // ---- leaf works, <= 128 targets per work, staged in rounds:
   //      near plan = self + U-list particles (runs on the side stream from the start),
   //      far plan  = L2P + M2P surfaces (after L2L; accumulates into the near result)
@@ -1043,6 +1061,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     lp.items.upload(items, &dev_bytes);
   };
   build_leaf_plan(true, leaf_near);
+  ptick("near-field plan");
   if (const char* e = std::getenv("KIFMM_FAR")) far_as_leaf = packed && std::string(e) == "leaf";
   if (far_as_leaf) build_leaf_plan(false, leaf_far);  // experiments: far field on the block kernel
   // far field: one warp-work per owned leaf with any L2P / M2P surface
@@ -1095,7 +1114,9 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   info.n_c = nc;
   info.ne_pad = np;
   info.m2l_backend = m2l_backend;
+  ptick("far-field plan");
   KIFMM_CUDA(cudaDeviceSynchronize());
+  ptick("device sync");
   info.device_bytes = int64_t(dev_bytes);
 }
 
