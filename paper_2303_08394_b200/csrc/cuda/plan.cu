@@ -410,16 +410,21 @@ std::vector<T> to_t(const std::vector<double>& v) {
 template <class T>
 void kifmm_gpu_plan::upload_static(const kifmm_tree_view& t, const kifmm_operator_view& ops) {
   // positions (x, y, z, 0)
-  std::vector<T> p4(size_t(N) * 4, T(0));
-  for (int64_t i = 0; i < N; ++i)
+  std::vector<T> p4(size_t(N) * 4);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < N; ++i) {
     for (int d = 0; d < 3; ++d) p4[4 * i + d] = T(t.positions[3 * i + d]);
+    p4[4 * i + 3] = T(0);
+  }
   pos4.upload(p4, &dev_bytes);
   std::vector<int> pm(N);
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < N; ++i) pm[i] = int(t.original_index[i]);
   perm.upload(pm, &dev_bytes);
   // node geometry (center, half side) computed in fp64 then rounded
   std::vector<T> g(size_t(nn) * 4);
   std::vector<int> lv(nn);
+#pragma omp parallel for schedule(static)
   for (int64_t n = 0; n < nn; ++n) {
     const uint64_t k = t.node_key[n];
     const auto a = key_anchor(k);
@@ -974,12 +979,25 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       KIFMM_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   }
   auto build_leaf_plan = [&](bool near_part, LeafPlan& lp) {
-    std::vector<LeafWork> w;
-    std::vector<int4> rounds, items;
     struct Src {
       int kind, a, len;
     };
-    for (int64_t l = lb; l < le; ++l) {
+    // leaves in chunks built in parallel (local works / rounds / items), then concatenated in order
+    struct Part {
+      std::vector<LeafWork> w;
+      std::vector<int4> rounds, items;
+      int64_t near_pairs = 0, l2p_pairs = 0, m2p_pairs = 0;
+    };
+    constexpr int64_t kChunk = 2048;
+    const int64_t nparts = (le - lb + kChunk - 1) / kChunk;
+    std::vector<Part> parts(size_t(std::max<int64_t>(nparts, 0)));
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t pi = 0; pi < nparts; ++pi) {
+    Part& P = parts[pi];
+    std::vector<LeafWork>& w = P.w;
+    std::vector<int4>& rounds = P.rounds;
+    std::vector<int4>& items = P.items;
+    for (int64_t l = lb + pi * kChunk; l < std::min(le, lb + (pi + 1) * kChunk); ++l) {
       const int64_t node = t.leaf_node[l];
       std::vector<Src> self, other;
       const int64_t ntl = t.leaf_ptr[l + 1] - t.leaf_ptr[l];
@@ -1001,15 +1019,15 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
           }
         }
         if (cur_b >= 0) other.push_back({kSrcParticles, cur_b, cur_e - cur_b});
-        info.near_pairs += ntl * src_cnt;
+        P.near_pairs += ntl * src_cnt;
       } else {
         if (node_lvl(node) >= 2) {
           other.push_back({kSrcL2P, int(node), ne});
-          info.l2p_pairs += ntl * ne;
+          P.l2p_pairs += ntl * ne;
         }
         for (int64_t e = t.w_ptr[l]; e < t.w_ptr[l + 1]; ++e) {
           other.push_back({kSrcM2P, int(t.w_idx[e]), ne});
-          info.m2p_pairs += ntl * ne;
+          P.m2p_pairs += ntl * ne;
         }
         if (other.empty()) continue;
       }
@@ -1054,6 +1072,26 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
         }
         w.push_back({int(l), int(t0), nt, rb, int(rounds.size())});
       }
+    }
+    }
+    std::vector<LeafWork> w;
+    std::vector<int4> rounds, items;
+    for (auto& P : parts) {
+      const int rb = int(rounds.size()), ib = int(items.size());
+      for (LeafWork x : P.w) {
+        x.round_begin += rb;
+        x.round_end += rb;
+        w.push_back(x);
+      }
+      for (int4 r : P.rounds) {
+        r.x += ib;
+        r.y += ib;
+        rounds.push_back(r);
+      }
+      items.insert(items.end(), P.items.begin(), P.items.end());
+      info.near_pairs += P.near_pairs;
+      info.l2p_pairs += P.l2p_pairs;
+      info.m2p_pairs += P.m2p_pairs;
     }
     lp.n = int(w.size());
     lp.works.upload(w, &dev_bytes);
