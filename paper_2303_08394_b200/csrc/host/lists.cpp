@@ -14,6 +14,8 @@
 //                 P2L can target non-leaf nodes.
 #include <algorithm>
 #include <array>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -63,6 +65,14 @@ const std::vector<std::array<int, 3>>& transfer_vector_table() { return tv_table
 
 void build_lists(Tree& t, int threads) {
   threads = resolve_threads(threads);
+  const bool tt = std::getenv("KIFMM_TREE_TIMING") != nullptr;
+  auto tt0 = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!tt) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "lists %-25s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - tt0).count());
+    tt0 = now;
+  };
   const int64_t nl = t.n_leaves(), nn = t.n_nodes();
   auto is_leaf = [&](int64_t node) { return t.node_leaf[node] >= 0; };
 
@@ -114,47 +124,78 @@ void build_lists(Tree& t, int threads) {
   to_csr(u, t.u_ptr, t.u_idx);
   std::vector<std::vector<int64_t>>().swap(u);
 
-  // ---------------- V
-  std::vector<std::vector<int64_t>> v(nn);
-  std::vector<std::vector<int32_t>> vt(nn);
-  parallel_for_dynamic(size_t(nn), threads, [&](size_t bi) {
-    const uint64_t b = t.node_key[bi];
-    if (key_level(b) < 2) return;
-    const auto ab = key_anchor(b);
+  tick("U");
+  // ---------------- V: two passes straight into CSR (count, then fill).  Members come out in
+  // ascending raw key without a sort: the parent's neighbours are visited in ascending key order and
+  // the children of one parent in octant order, which is ascending key, and the children of a smaller
+  // parent all precede those of a larger one.
+  // node anchors decoded once; same-level adjacency is then max |anchor difference| <= 1
+  std::vector<std::array<int32_t, 3>> anc(nn);
+  parallel_for(size_t(nn), threads, [&](size_t i) {
+    const auto a = key_anchor(t.node_key[i]);
+    anc[i] = {int32_t(a[0]), int32_t(a[1]), int32_t(a[2])};
+  });
+  std::array<int16_t, 343> tv_of;  // (dx+3)*49 + (dy+3)*7 + (dz+3) -> transfer-vector id
+  for (int i = 0; i < 343; ++i) tv_of[i] = int16_t(transfer_vector_id(i / 49 - 3, (i / 7) % 7 - 3, i % 7 - 3));
+  // per parent: its colleagues (same-level neighbours that exist and are internal), sorted by key,
+  // shared by its (up to 8) children
+  auto colleagues = [&](int64_t pi, int64_t* out) {
     uint64_t nb[26];
-    const int cnt = key_neighbors(key_parent(b), nb);
-    std::vector<std::pair<uint64_t, int64_t>> mem;
+    const int cnt = key_neighbors(t.node_key[pi], nb);
+    std::sort(nb, nb + cnt);
+    int m = 0;
     for (int j = 0; j < cnt; ++j) {
       const int64_t qi = t.node_map.find(nb[j]);
-      if (qi < 0 || is_leaf(qi)) continue;
-      for (int o = 0; o < 8; ++o) {
-        const int64_t c = t.node_children[8 * qi + o];
-        if (c < 0 || keys_adjacent(t.node_key[c], b)) continue;
-        mem.push_back({t.node_key[c], c});
-      }
+      if (qi >= 0 && !is_leaf(qi)) out[m++] = qi;
     }
-    std::sort(mem.begin(), mem.end());
-    auto& out = v[bi];
-    auto& tv = vt[bi];
-    out.reserve(mem.size());
-    tv.reserve(mem.size());
-    for (auto& m : mem) {
-      const auto as = key_anchor(m.first);
-      const int id = transfer_vector_id(int(as[0]) - int(ab[0]), int(as[1]) - int(ab[1]),
-                                        int(as[2]) - int(ab[2]));
-      if (id < 0) throw InvalidArgument("v_list: transfer vector outside [-3,3]^3");
-      out.push_back(m.second);
-      tv.push_back(id);
+    return m;
+  };
+  auto v_child = [&](int64_t bi, const int64_t* col, int m, auto&& emit) {
+    const auto& ab = anc[bi];
+    for (int j = 0; j < m; ++j)
+      for (int o = 0; o < 8; ++o) {
+        const int64_t c = t.node_children[8 * col[j] + o];
+        if (c < 0) continue;
+        const int dx = anc[c][0] - ab[0], dy = anc[c][1] - ab[1], dz = anc[c][2] - ab[2];
+        if (std::abs(dx) <= 1 && std::abs(dy) <= 1 && std::abs(dz) <= 1) continue;  // adjacent (same level)
+        emit(c, (dx + 3) * 49 + (dy + 3) * 7 + (dz + 3));
+      }
+  };
+  t.v_ptr.assign(nn + 1, 0);
+  parallel_for_dynamic(size_t(nn), threads, [&](size_t pi) {
+    if (is_leaf(int64_t(pi)) || key_level(t.node_key[pi]) < 1) return;  // parents of level >= 2 nodes
+    int64_t col[26];
+    const int m = colleagues(int64_t(pi), col);
+    for (int o = 0; o < 8; ++o) {
+      const int64_t bi = t.node_children[8 * pi + o];
+      if (bi < 0) continue;
+      int64_t k = 0;
+      v_child(bi, col, m, [&](int64_t, int) { ++k; });
+      t.v_ptr[bi + 1] = k;
     }
   });
-  to_csr(v, t.v_ptr, t.v_idx);
-  {
-    std::vector<int64_t> dummy;
-    to_csr(vt, dummy, t.v_tv);
-  }
-  std::vector<std::vector<int64_t>>().swap(v);
-  std::vector<std::vector<int32_t>>().swap(vt);
+  for (int64_t i = 0; i < nn; ++i) t.v_ptr[i + 1] += t.v_ptr[i];
+  t.v_idx.resize(t.v_ptr[nn]);
+  t.v_tv.resize(t.v_ptr[nn]);
+  parallel_for_dynamic(size_t(nn), threads, [&](size_t pi) {
+    if (is_leaf(int64_t(pi)) || key_level(t.node_key[pi]) < 1) return;
+    int64_t col[26];
+    const int m = colleagues(int64_t(pi), col);
+    for (int o = 0; o < 8; ++o) {
+      const int64_t bi = t.node_children[8 * pi + o];
+      if (bi < 0) continue;
+      int64_t e = t.v_ptr[bi];
+      v_child(bi, col, m, [&](int64_t c, int code) {
+        const int id = tv_of[code];
+        if (id < 0) throw InvalidArgument("v_list: transfer vector outside [-3,3]^3");
+        t.v_idx[e] = c;
+        t.v_tv[e] = id;
+        ++e;
+      });
+    }
+  });
 
+  tick("V");
   // ---------------- W
   std::vector<std::vector<int64_t>> w(nl);
   parallel_for_dynamic(size_t(nl), threads, [&](size_t li) {
@@ -189,6 +230,7 @@ void build_lists(Tree& t, int threads) {
   to_csr(w, t.w_ptr, t.w_idx);
   std::vector<std::vector<int64_t>>().swap(w);
 
+  tick("W");
   // ---------------- X = dual of W (on all nodes)
   t.x_ptr.assign(nn + 1, 0);
   for (int64_t li = 0; li < nl; ++li)
@@ -201,6 +243,7 @@ void build_lists(Tree& t, int threads) {
     for (int64_t li = 0; li < nl; ++li)
       for (int64_t e = t.w_ptr[li]; e < t.w_ptr[li + 1]; ++e) t.x_idx[fill[t.w_idx[e]]++] = li;
   }
+  tick("X");
 }
 
 }  // namespace kifmm

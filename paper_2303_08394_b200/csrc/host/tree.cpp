@@ -3,8 +3,13 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <limits>
+#include <memory>
+#include <omp.h>
 #include <parallel/algorithm>
 #include <string>
 
@@ -58,6 +63,15 @@ void build_tree(Tree& t, const double* pos, int64_t n, int n_crit, const double*
   threads = resolve_threads(threads);
   t = Tree{};
   t.n = n;
+  // phase timing (KIFMM_TREE_TIMING=1)
+  const bool tt = std::getenv("KIFMM_TREE_TIMING") != nullptr;
+  auto tt0 = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!tt) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "tree %-26s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - tt0).count());
+    tt0 = now;
+  };
 
   // ---- domain: tight bounding cube, 1e-10 relative margin per side
   if (domain) {
@@ -85,8 +99,11 @@ void build_tree(Tree& t, const double* pos, int64_t n, int n_crit, const double*
     t.side = side;
   }
 
+  tick("domain");
   // ---- fine codes and the Morton permutation
-  std::vector<std::pair<uint64_t, int64_t>> ci(n);
+  // (code, index) pairs without value-initialisation (first touched by the parallel loop below)
+  using CI = std::pair<uint64_t, int64_t>;
+  std::unique_ptr<CI[]> ci(new CI[size_t(n)]);
   std::atomic<bool> bad{false};
   std::string bad_msg;
   parallel_for(size_t(n), threads, [&](size_t i) {
@@ -100,10 +117,48 @@ void build_tree(Tree& t, const double* pos, int64_t n, int n_crit, const double*
     }
   });
   if (bad) throw InvalidArgument(bad_msg);
-  if (threads > 1 && n > 100000)
-    __gnu_parallel::sort(ci.begin(), ci.end());
-  else
-    std::sort(ci.begin(), ci.end());
+  tick("fine codes");
+  if (threads > 1 && n > 100000) {
+    // parallel bucket sort: 4096 buckets on the top 12 bits of the 45-bit fine code (counting pass,
+    // scatter, then each bucket sorted independently); equal to a full sort of the (code, index) pairs
+    constexpr int kB = 4096, kShift = 45 - 12;
+    std::vector<int64_t> cnt(size_t(threads) * kB, 0);
+    const int64_t per = (n + threads - 1) / threads;
+#pragma omp parallel num_threads(threads)
+    {
+      const int th = omp_get_thread_num();
+      const int64_t a = std::min<int64_t>(n, th * per), b = std::min<int64_t>(n, a + per);
+      int64_t* c = cnt.data() + size_t(th) * kB;
+      for (int64_t i = a; i < b; ++i) ++c[ci[i].first >> kShift];
+    }
+    std::vector<int64_t> start(kB + 1, 0);
+    {
+      int64_t acc = 0;
+      for (int k = 0; k < kB; ++k) {
+        start[k] = acc;
+        for (int th = 0; th < threads; ++th) {
+          const int64_t v = cnt[size_t(th) * kB + k];
+          cnt[size_t(th) * kB + k] = acc;  // becomes this thread's write cursor in bucket k
+          acc += v;
+        }
+      }
+      start[kB] = acc;
+    }
+    std::unique_ptr<CI[]> tmp(new CI[size_t(n)]);
+#pragma omp parallel num_threads(threads)
+    {
+      const int th = omp_get_thread_num();
+      const int64_t a = std::min<int64_t>(n, th * per), b = std::min<int64_t>(n, a + per);
+      int64_t* c = cnt.data() + size_t(th) * kB;
+      for (int64_t i = a; i < b; ++i) tmp[c[ci[i].first >> kShift]++] = ci[i];
+    }
+#pragma omp parallel for schedule(dynamic, 8) num_threads(threads)
+    for (int k = 0; k < kB; ++k) std::sort(tmp.get() + start[k], tmp.get() + start[k + 1]);
+    ci.swap(tmp);
+  } else {
+    std::sort(ci.get(), ci.get() + n);
+  }
+  tick("sort");
   t.codes.resize(n);
   t.original_index.resize(n);
   t.positions.resize(3 * n);
@@ -112,8 +167,9 @@ void build_tree(Tree& t, const double* pos, int64_t n, int n_crit, const double*
     t.original_index[i] = ci[i].second;
     for (int d = 0; d < 3; ++d) t.positions[3 * i + d] = pos[3 * ci[i].second + d];
   });
-  std::vector<std::pair<uint64_t, int64_t>>().swap(ci);
+  ci.reset();
 
+  tick("codes+sort+permute");
   // ---- unbalanced adaptive leaves: depth-first in octant order => ascending raw
   struct Item {
     uint64_t key;
@@ -137,6 +193,7 @@ void build_tree(Tree& t, const double* pos, int64_t n, int n_crit, const double*
     }
   }
 
+  tick("adaptive split");
   // ---- 2:1 balance (design 190): split every leaf that has an
   // adjacent leaf more than one level finer, until a fixed point.  A coarser leaf
   // K adjacent to leaf A always covers one of A's 26 same-level neighbour boxes,
@@ -191,6 +248,7 @@ void build_tree(Tree& t, const double* pos, int64_t n, int n_crit, const double*
     leaves.swap(next);
   }
 
+  tick("balance");
   // ---- leaf particle ranges
   t.leaves = leaves;
   const int64_t nl = int64_t(leaves.size());
@@ -206,6 +264,7 @@ void build_tree(Tree& t, const double* pos, int64_t n, int n_crit, const double*
     if (l == kMaxLevel && cnt > n_crit) ++t.n_overfull;
   }
 
+  tick("leaf ranges");
   // ---- nodes: leaves and all their ancestors, level-major
   int depth = 0;
   for (uint64_t k : leaves) depth = std::max(depth, key_level(k));
@@ -249,6 +308,7 @@ void build_tree(Tree& t, const double* pos, int64_t n, int n_crit, const double*
     t.leaf_node[i] = ni;
     t.node_leaf[ni] = i;
   }
+  tick("nodes");
 }
 
 }  // namespace kifmm
