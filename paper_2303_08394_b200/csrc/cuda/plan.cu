@@ -128,6 +128,14 @@ void launch_gemm(int np, const GemmTiles& t, GemmArgs<T> a, cudaStream_t s) {
   }
 }
 
+// SIMT M2L-shaped GEMM tiles (rows per tile / fp64 rows per thread); experiment overrides
+#ifndef KIFMM_M2L_SIMT_BM
+#define KIFMM_M2L_SIMT_BM 64
+#endif
+#ifndef KIFMM_M2L_SIMT_TM64
+#define KIFMM_M2L_SIMT_TM64 8
+#endif
+
 // ------------------------------------------------------------------- NCCL
 // libnccl is opened lazily so single-GPU use has no NCCL dependency.
 struct Nccl {
@@ -1206,7 +1214,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     a.ldy = np;
     a.accumulate = acc ? 1 : 0;
     if (m2l_shape)
-      launch_gemm<T, 64, (sizeof(T) == 8 ? 8 : 4)>(np, tl, a, s);
+      launch_gemm<T, KIFMM_M2L_SIMT_BM, (sizeof(T) == 8 ? KIFMM_M2L_SIMT_TM64 : 4)>(np, tl, a, s);
     else
       launch_gemm<T, BMB, TMB>(np, tl, a, s);
     ++launches;
