@@ -801,7 +801,25 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   // ---- M2L tiles: active targets at level >= 2 grouped by (level, octant), Z-order inside
   std::vector<std::vector<int64_t>> m2l_groups;
   {
-    std::map<std::pair<int, int>, std::vector<int64_t>> groups;
+    std::map<std::array<int, 3>, std::vector<int64_t>> groups;
+    // boundary class of a target: which domain faces its parent touches (those V offsets are absent).
+    // 0 = interior; else 1 + 2 a + side for the first axis a whose parent coordinate is on a face --
+    // a face group collects the face rows with the edge / corner rows whose tap sets are subsets of it,
+    // so its tiles need (almost) no zero rows (KIFMM_M2L_CLASSES=1; measured more padded slots at
+    // config 2, 7.87 M vs 7.11 M: the extra partial tiles cost more than the tighter tap sets save)
+    bool by_class = false;
+    if (const char* e = std::getenv("KIFMM_M2L_CLASSES")) by_class = std::atoi(e) != 0;
+    auto bclass = [&](int64_t n) {
+      const int l = node_lvl(n);
+      if (!by_class || l < 3) return 0;
+      const auto pa = key_anchor(t.node_key[t.node_parent[n]]);
+      const uint32_t hi = (uint32_t(1) << (l - 1)) - 1;
+      for (int a = 0; a < 3; ++a) {
+        if (pa[a] == 0) return 1 + 2 * a;
+        if (pa[a] == hi) return 2 + 2 * a;
+      }
+      return 0;
+    };
     // levels with few targets are one group (octant classes would each fill a fraction of a tile with
     // zero rows); larger levels are split by octant (shared transfer-vector sets)
     std::map<int, int64_t> per_level;
@@ -810,7 +828,8 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     for (int64_t n = 0; n < nn; ++n) {
       if (!active[n] || node_lvl(n) < 2 || t.v_ptr[n] == t.v_ptr[n + 1]) continue;
       const int lvl = node_lvl(n);
-      groups[{lvl, per_level[lvl] <= 2048 ? 0 : key_octant(t.node_key[n])}].push_back(n);
+      const bool small = per_level[lvl] <= 2048;
+      groups[{lvl, small ? 0 : key_octant(t.node_key[n]), small ? 0 : bclass(n)}].push_back(n);
       info.m2l_pairs += t.v_ptr[n + 1] - t.v_ptr[n];
     }
     for (auto& kv : groups) m2l_groups.push_back(kv.second);
