@@ -72,6 +72,14 @@ __device__ __forceinline__ f2_t f2_pack(float a, float b) {
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
   return r;
 }
+// A loop-invariant pair built once by a real FADD2 (a + -0 == a exactly, also for +-0): packed straight from
+// two scalars (e.g. the .x of two float4 loads), ptxas keeps the halves apart and rebuilds the 64-bit pair
+// with two MOVs at every use inside the loop.
+__device__ __forceinline__ f2_t f2_pair(float a, float b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a, b)), "l"(f2_pack(-0.f, -0.f)));
+  return r;
+}
 __device__ __forceinline__ void f2_unpack(f2_t v, float& a, float& b) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
 }

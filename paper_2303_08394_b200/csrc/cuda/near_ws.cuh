@@ -1,0 +1,223 @@
+// Near field (self + U list), fp32, warp-specialised and persistent.
+//
+// leaf_eval_f2_kernel launches one 128-thread block per leaf work: every block
+// starts with a chain of dependent global loads (work -> round -> items ->
+// sources) before its first FP32x2 instruction, and at 8 blocks per SM those
+// start-up stalls left the FMA pipe idle ~28 % of the time (ncu, config 2).
+// Here one producer warp per block walks the same work / round / item lists
+// and stages each round's sources into a ring
+// of shared-memory stages with cp.async, signalling a full mbarrier with
+// cp.async.mbarrier.arrive.noinc; four consumer warps compute exactly what
+// leaf_eval_f2_kernel computes -- same slice geometry, same p2p_round_fn,
+// same fixed-order slice reduction -- so the result is bit-identical to it and
+// independent of which block took which work.  Works come from an atomic
+// counter (queue[0]), as in queue mode:
+//   MODE 0  standalone: the launch takes every work
+//   MODE 1  side: stops taking works once queue[1] is raised (by MODE 2)
+//   MODE 2  drain: raises queue[1] and takes what is left
+#pragma once
+
+#include "m2l_tc.cuh"
+#include "p2p.cuh"
+
+namespace kifmm {
+namespace gpu {
+
+static_assert(kNearNPair == 1, "near_ws_kernel mirrors the one-pair-per-thread geometry");
+constexpr int kNearStages = 2;
+constexpr int kNearWsThreads = 160;  // warps 0-3 consumers, warp 4 producer
+
+struct NearStage {
+  float4 src[kP2PCap];  // [self section, padded to S][other sources, padded to O]; reused for the reduction
+  int wi, S, O, flags;      // flags: bit 0 first round of the work, bit 1 last round; wi < 0: stop
+  int t_begin, t_count, pad0, pad1;
+};
+
+struct NearSmem {
+  NearStage st[kNearStages];
+  unsigned long long full[kNearStages], empty[kNearStages];
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void near_consumer_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+#ifndef KIFMM_NEAR_WS_MINB
+#define KIFMM_NEAR_WS_MINB 6  // blocks per SM the register allocation is sized for (6: 64 registers)
+#endif
+template <bool GRAD, int MODE>
+__global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_kernel(P2PParams<float> p,
+                                                                   const LeafWork* __restrict__ works,
+                                                                   const int4* __restrict__ rounds,
+                                                                   const int4* __restrict__ items,
+                                                                   float* __restrict__ pot, float* __restrict__ grad,
+                                                                   int n_works, int* __restrict__ queue) {
+  __shared__ __align__(16) NearSmem sm;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kNearStages; ++s) {
+      tc::mbar_init(tc::smem_u32(&sm.full[s]), 64);  // 32 producer arrives + 32 cp.async completions
+      tc::mbar_init(tc::smem_u32(&sm.empty[s]), 4);  // one per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (MODE == 2 && blockIdx.x == 0) atomicExch(queue + 1, 1);
+  }
+  __syncthreads();
+  timeline_begin(MODE == 2 ? 4 : 3);
+
+  if (warp == 4) {  // ---------------- producer
+    int stage = 0;
+    uint32_t phase = 0;
+    const float fa = float(kFarAway);
+    const float4 far4 = make_float4(fa, fa, fa, 0.f);
+    for (;;) {
+      int wi = 0;
+      if (lane == 0) {
+        if (MODE == 1) {  // side blocks: optional pause while M2L runs (queue[3]), stop once draining
+          for (int pz; (pz = atomicAdd(queue + 3, 0)) != 0 && (pz == 1 || (blockIdx.x & 1)) &&
+                       atomicAdd(queue + 1, 0) == 0;)
+            __nanosleep(2000);
+          wi = atomicAdd(queue + 1, 0) != 0 ? n_works : atomicAdd(queue, 1);
+        } else {
+          wi = atomicAdd(queue, 1);
+        }
+      }
+      wi = __shfl_sync(0xffffffffu, wi, 0);
+      if (wi >= n_works) {  // tell the consumers to stop
+        tc::mbar_wait(tc::smem_u32(&sm.empty[stage]), phase ^ 1);
+        if (lane == 0) sm.st[stage].wi = -1;
+        tc::mbar_arrive_local(tc::smem_u32(&sm.full[stage]));
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&sm.full[stage]))
+                     : "memory");
+        break;
+      }
+      const LeafWork w = works[wi];
+      for (int r = w.round_begin; r < w.round_end; ++r) {
+        const int4 rd = rounds[r];
+        // item descriptors of this round, one per lane (loaded before the stage wait: latency overlap)
+        int4 my_item = make_int4(0, 0, 0, 0);
+        if (rd.x + lane < rd.y) my_item = items[rd.x + lane];
+        tc::mbar_wait(tc::smem_u32(&sm.empty[stage]), phase ^ 1);
+        NearStage& S = sm.st[stage];
+        const uint32_t sbase = tc::smem_u32(S.src);
+        for (int kb = rd.x; kb < rd.y; kb += 32) {
+          if (kb != rd.x && kb + lane < rd.y) my_item = items[kb + lane];
+          const int nk = min(32, rd.y - kb);
+          for (int k = 0; k < nk; ++k) {
+            const int a = __shfl_sync(0xffffffffu, my_item.y, k), len = __shfl_sync(0xffffffffu, my_item.z, k),
+                      dst = __shfl_sync(0xffffffffu, my_item.w, k);
+            for (int i = lane; i < len; i += 32) cp_async16(sbase + 16u * uint32_t(dst + i), p.src + a + i);
+          }
+        }
+        const int Ssz = rd.z & 0xFFFF, ns = rd.z >> 16, Osz = rd.w & 0xFFFF, no = rd.w >> 16;
+        for (int i = ns + lane; i < Ssz; i += 32) S.src[i] = far4;
+        for (int i = Ssz + no + lane; i < Ssz + Osz; i += 32) S.src[i] = far4;
+        if (lane == 0) {
+          S.wi = wi;
+          S.S = Ssz;
+          S.O = Osz;
+          S.flags = (r == w.round_begin ? 1 : 0) | (r == w.round_end - 1 ? 2 : 0);
+          S.t_begin = w.t_begin;
+          S.t_count = w.t_count;
+        }
+        tc::mbar_arrive_local(tc::smem_u32(&sm.full[stage]));  // release: padding + header stores
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&sm.full[stage]))
+                     : "memory");
+        if (++stage == kNearStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    timeline_end(MODE == 2 ? 4 : 3);
+    return;
+  }
+
+  // ---------------- consumers (warps 0-3): geometry and arithmetic of leaf_eval_f2_kernel
+  int stage = 0;
+  uint32_t phase = 0;
+  int nt = 0, TT = 1, R = 1, slice = 0, t0 = 0;
+  bool active = false;
+  f2_t x[1], y[1], z[1], ph[1], gx[1], gy[1], gz[1];
+  for (;;) {
+    tc::mbar_wait(tc::smem_u32(&sm.full[stage]), phase);
+    NearStage& S = sm.st[stage];
+    if (S.wi < 0) break;
+    const int flags = S.flags;
+    if (flags & 1) {  // first round of a work
+      nt = S.t_count;
+      TT = (nt + 1) / 2;
+      R = leaf_slices(nt, true);
+      slice = tid / TT;
+      t0 = tid - slice * TT;
+      active = slice < R;
+      const int ta = t0, tb = t0 + TT;
+      // targets straight from global (L2-resident; staging them too would cost the sixth block per SM)
+      const float4 xa = p.src[S.t_begin + (active && ta < nt ? ta : 0)];
+      const float4 xb = p.src[S.t_begin + (active && tb < nt ? tb : 0)];
+      x[0] = f2_pair(xa.x, xb.x);
+      y[0] = f2_pair(xa.y, xb.y);
+      z[0] = f2_pair(xa.z, xb.z);
+      ph[0] = gx[0] = gy[0] = gz[0] = 0;
+    }
+    const int Ssz = S.S, Osz = S.O;
+    if (active) {
+      if (Ssz) {
+        const int per = Ssz / R;
+        p2p_round_fn<GRAD, true, 1>(S.src, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
+      }
+      if (Osz) {
+        const int per = Osz / R;
+        p2p_round_fn<GRAD, false, 1>(S.src, Ssz + slice * per, Ssz + slice * per + per, x, y, z, ph, gx, gy, gz);
+      }
+    }
+    if (flags & 2) {  // last round: fixed-order slice reduction through this stage's source buffer
+      const int t_begin = S.t_begin;
+      near_consumer_sync();  // every consumer is done reading the sources
+      float* red = reinterpret_cast<float*>(S.src);  // [slice][component][n_t]
+      constexpr int NC = GRAD ? 4 : 1;
+      if (active) {
+        float a[4], b[4];
+        f2_unpack(ph[0], a[0], b[0]);
+        f2_unpack(gx[0], a[1], b[1]);
+        f2_unpack(gy[0], a[2], b[2]);
+        f2_unpack(gz[0], a[3], b[3]);
+        const int ta = t0, tb = t0 + TT;
+#pragma unroll
+        for (int d = 0; d < NC; ++d) {
+          if (ta < nt) red[(slice * NC + d) * nt + ta] = a[d];
+          if (tb < nt) red[(slice * NC + d) * nt + tb] = b[d];
+        }
+      }
+      near_consumer_sync();
+      if (tid < nt) {
+        const float c = float(kInv4PiD);
+        float a[NC];
+#pragma unroll
+        for (int d = 0; d < NC; ++d) a[d] = 0;
+        for (int sl = 0; sl < R; ++sl)
+#pragma unroll
+          for (int d = 0; d < NC; ++d) a[d] += red[(sl * NC + d) * nt + tid];
+        const int t = t_begin + tid;
+        pot[t] = 0.f + c * a[0];  // the expressions of leaf_eval_f2_kernel<.., ACC = false> (signed zeros)
+        if (GRAD) {
+          float* gp = grad + 3 * size_t(t);
+          gp[0] = 0.f - c * a[NC > 1 ? 1 : 0];
+          gp[1] = 0.f - c * a[NC > 2 ? 2 : 0];
+          gp[2] = 0.f - c * a[NC > 3 ? 3 : 0];
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive_local(tc::smem_u32(&sm.empty[stage]));
+    if (++stage == kNearStages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  timeline_end(MODE == 2 ? 4 : 3);
+}
+
+}  // namespace gpu
+}  // namespace kifmm

@@ -111,7 +111,10 @@ __host__ __device__ inline int leaf_slices(int nt, bool packed) {
   const int r = 128 / (tt > 0 ? tt : 1);
   return r < 1 ? 1 : (r > mx ? mx : r);
 }
-__host__ __device__ inline int leaf_unroll(bool packed) { return packed ? 4 / kNearNPair : 8; }
+#ifndef KIFMM_NEAR_UNROLL
+#define KIFMM_NEAR_UNROLL 4  // staged sources per unrolled step of the packed kernel (per target pair)
+#endif
+__host__ __device__ inline int leaf_unroll(bool packed) { return packed ? KIFMM_NEAR_UNROLL / kNearNPair : 8; }
 
 // Packed fp32 pair-of-targets round: FP32x2 instructions whose source operand
 // is a scalar register broadcast to both lanes (ptxas folds mov.b64 {s, s}
@@ -125,7 +128,7 @@ template <bool GRAD, bool MASK, int NP>
 __device__ __forceinline__ void p2p_round_fn(const float4* sh, int begin, int end, const f2_t (&x)[NP],
                                              const f2_t (&y)[NP], const f2_t (&z)[NP], f2_t (&ph)[NP],
                                              f2_t (&gx)[NP], f2_t (&gy)[NP], f2_t (&gz)[NP]) {
-  constexpr int U = 4 / NP;  // sources per unrolled step
+  constexpr int U = KIFMM_NEAR_UNROLL / NP;  // sources per unrolled step
   f2_t a_ph[NP], a_gx[NP], a_gy[NP], a_gz[NP];
 #pragma unroll
   for (int k = 0; k < NP; ++k) a_ph[k] = a_gx[k] = a_gy[k] = a_gz[k] = 0;
@@ -252,9 +255,9 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
     const int ta = t0 + (2 * k) * TT, tb = t0 + (2 * k + 1) * TT;
     const float4 xa = p.src[w.t_begin + (active && ta < nt ? ta : 0)];
     const float4 xb = p.src[w.t_begin + (active && tb < nt ? tb : 0)];
-    x[k] = f2_pack(xa.x, xb.x);
-    y[k] = f2_pack(xa.y, xb.y);
-    z[k] = f2_pack(xa.z, xb.z);
+    x[k] = f2_pair(xa.x, xb.x);
+    y[k] = f2_pair(xa.y, xb.y);
+    z[k] = f2_pair(xa.z, xb.z);
     ph[k] = gx[k] = gy[k] = gz[k] = 0;
   }
   const float fa = float(kFarAway);
@@ -520,7 +523,7 @@ __global__ void __launch_bounds__(kFarWarps * 32) far_f2_kernel(P2PParams<float>
 #ifndef KIFMM_FAR_LATE_OUT
   load_out();  // prefetch the near-field result and the output permutation
 #endif
-  const f2_t x = f2_pack(xa.x, xb.x), y = f2_pack(xa.y, xb.y), z = f2_pack(xa.z, xb.z);
+  const f2_t x = f2_pair(xa.x, xb.x), y = f2_pair(xa.y, xb.y), z = f2_pair(xa.z, xb.z);
   f2_t ph = 0, gx = 0, gy = 0, gz = 0;
   const float fa = float(kFarAway);
   for (int si = w.surf_begin; si < w.surf_end; ++si) {
@@ -665,9 +668,9 @@ __global__ void __launch_bounds__(kCheckWarps * 32) check_f2_kernel(P2PParams<fl
   f2_t yx[KP > 0 ? KP : 1], yy[KP > 0 ? KP : 1], yz[KP > 0 ? KP : 1], acc[KP > 0 ? KP : 1];
 #pragma unroll
   for (int m = 0; m < KP; ++m) {
-    yx[m] = f2_pack(coord(2 * m, 0), coord(2 * m + 1, 0));
-    yy[m] = f2_pack(coord(2 * m, 1), coord(2 * m + 1, 1));
-    yz[m] = f2_pack(coord(2 * m, 2), coord(2 * m + 1, 2));
+    yx[m] = f2_pair(coord(2 * m, 0), coord(2 * m + 1, 0));
+    yy[m] = f2_pair(coord(2 * m, 1), coord(2 * m + 1, 1));
+    yz[m] = f2_pair(coord(2 * m, 2), coord(2 * m + 1, 2));
     acc[m] = 0;
   }
   float ox = 0.f, oy = 0.f, oz = 0.f, oacc = 0.f;

@@ -23,6 +23,7 @@
 #include "m2l_tc.cuh"
 #include "morton.hpp"
 #include "p2p.cuh"
+#include "near_ws.cuh"
 
 namespace kifmm {
 namespace gpu {
@@ -329,6 +330,11 @@ struct kifmm_gpu_plan {
   int device = 0;
   int precision = 32;
   bool leaf_packed = false;
+  // warp-specialised persistent near-field kernel (KIFMM_NEAR_WS=1; bit-identical results).  Config 2: neutral
+  // in the full evaluate (1.361 vs 1.361 ms), standalone 2-4 % slower (its consumer barriers), so off
+  int near_ws = 0;
+  int near_ws_bps = 2;
+  int near_ws_blocks = 6;  // resident blocks per SM of the standalone / drain launch (occupancy query)   // its side blocks per SM next to the tcgen05 kernels (smem: 2 x 37 KB + stages)
   int near_pause = 0;  // side blocks sleep during M2L: 1 all, 2 half (KIFMM_NEAR_PAUSE; 1 measured slower)
   int near_bps = 3;  // queue mode: near-field blocks per SM next to the tree passes (KIFMM_NEAR_BPS, 0 = off)
   bool m2m_parent_tiles = false;  // KIFMM_M2M=parent: 8-tap parent tiles, direct (measured slower)
@@ -988,6 +994,8 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   }
   const bool packed = leaf_packed;
   if (packed) {
+    if (const char* e = std::getenv("KIFMM_NEAR_WS")) near_ws = std::atoi(e);
+    if (near_ws) near_bps = near_ws_bps;
     if (const char* e = std::getenv("KIFMM_NEAR_BPS")) near_bps = std::max(0, std::atoi(e));
     near_counter.alloc(4 * sizeof(int), &dev_bytes);
     if (const char* e = std::getenv("KIFMM_NEAR_PAUSE")) near_pause = std::atoi(e);
@@ -1001,9 +1009,15 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
                           (const void*)leaf_eval_f2_kernel<false, false, true, false>,
                           (const void*)leaf_eval_f2_kernel<true, false, true, true>,
                           (const void*)leaf_eval_f2_kernel<false, false, true, true>,
+                          (const void*)near_ws_kernel<true, 0>, (const void*)near_ws_kernel<true, 1>,
+                          (const void*)near_ws_kernel<true, 2>, (const void*)near_ws_kernel<false, 0>,
+                          (const void*)near_ws_kernel<false, 1>, (const void*)near_ws_kernel<false, 2>,
                           (const void*)leaf_eval_f2_kernel<true, false, false>,
                           (const void*)leaf_eval_f2_kernel<false, false, false>})
       KIFMM_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int nb = 0;
+    KIFMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, near_ws_kernel<true, 2>, kNearWsThreads, 0));
+    near_ws_blocks = std::max(1, nb);
   }
   auto build_leaf_plan = [&](bool near_part, LeafPlan& lp) {
     struct Src {
@@ -1247,6 +1261,18 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     const int4* it = lp.items.as<int4>();
     T* g = grad ? grad_buf.as<T>() : nullptr;
     if constexpr (sizeof(T) == 4) {
+      if (leaf_packed && near_ws && &lp == &leaf_near && !acc) {  // standalone persistent near field
+        int* qc = near_counter.as<int>();
+        KIFMM_CUDA(cudaMemsetAsync(qc, 0, 4 * sizeof(int), st));
+        const int grid = std::min(lp.n, near_ws_blocks * sm_count());
+        if (grad)
+          near_ws_kernel<true, 0><<<grid, kNearWsThreads, 0, st>>>(pp, w, r, it, pot.as<T>(), g, lp.n, qc);
+        else
+          near_ws_kernel<false, 0><<<grid, kNearWsThreads, 0, st>>>(pp, w, r, it, pot.as<T>(), g, lp.n, qc);
+        KIFMM_LAUNCH_CHECK();
+        ++launches;
+        return;
+      }
       if (leaf_packed) {
         if (grad && acc)
           leaf_eval_f2_kernel<true, true><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<T>(), g);
@@ -1294,6 +1320,19 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
       int* qc = near_counter.as<int>();
       float* pt = pot.as<float>();
       const int n = leaf_near.n;
+      if (near_ws) {
+        if (grad && drain)
+          near_ws_kernel<true, 2><<<grid, kNearWsThreads, 0, st>>>(pp, w, r, it, pt, g, n, qc);
+        else if (grad)
+          near_ws_kernel<true, 1><<<grid, kNearWsThreads, 0, st>>>(pp, w, r, it, pt, g, n, qc);
+        else if (drain)
+          near_ws_kernel<false, 2><<<grid, kNearWsThreads, 0, st>>>(pp, w, r, it, pt, g, n, qc);
+        else
+          near_ws_kernel<false, 1><<<grid, kNearWsThreads, 0, st>>>(pp, w, r, it, pt, g, n, qc);
+        KIFMM_LAUNCH_CHECK();
+        ++launches;
+        return;
+      }
       if (grad && drain)
         leaf_eval_f2_kernel<true, false, true, true><<<grid, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pt, g, n, qc);
       else if (grad)
@@ -1456,7 +1495,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
                                cudaMemcpyDeviceToDevice, s));
   // drain the works the side-stream blocks did not take (persistent: at most 8 blocks per SM, so an
   // empty queue costs one short wave instead of a block per leaf)
-  if (queue_mode) near_queue(s, std::min(leaf_near.n, 8 * sm_count()), true);
+  if (queue_mode) near_queue(s, std::min(leaf_near.n, (near_ws ? near_ws_blocks : 8) * sm_count()), true);
   if ((!timed || corun) && leaf_near.n && !near_skip) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
   bool fused_out = false;  // the packed far kernel wrote the final (input-order) output
   if (far_as_leaf) leaf(leaf_far, true, s);

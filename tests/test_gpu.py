@@ -182,12 +182,18 @@ def test_near_queue_mode_bit_identical(require_gpu, monkeypatch):
     pos, q = generators.sample("two-cluster", 60000, seed=21, charges="signed", fp32=True)
     cfg = fmm.FmmConfig(p=6, n_crit=40, precision=32, gradient=True)
     out = {}
-    for bps in ("0", "1", "2"):
-        monkeypatch.setenv("KIFMM_NEAR_BPS", bps)
-        with fmm.Fmm(pos, cfg) as f:
-            out[bps] = f.evaluate(q)[:2]
-    for bps in ("1", "2"):
-        assert np.array_equal(out[bps][0], out["0"][0]) and np.array_equal(out[bps][1], out["0"][1])
+    # KIFMM_NEAR_WS=0: one leaf_eval_f2 block per leaf work; 1: the warp-specialised persistent kernel
+    for ws in ("0", "1"):
+        for bps in ("0", "1", "2"):
+            monkeypatch.setenv("KIFMM_NEAR_WS", ws)
+            monkeypatch.setenv("KIFMM_NEAR_BPS", bps)
+            with fmm.Fmm(pos, cfg) as f:
+                out[ws, bps] = f.evaluate(q)[:2]
+                if bps == "0":
+                    out[ws, "timed"] = f.evaluate(q, timed=True)[:2]
+    ref = out["0", "0"]
+    for k, v in out.items():
+        assert np.array_equal(v[0], ref[0]) and np.array_equal(v[1], ref[1]), k
 
 
 def test_simt_gemms_with_tcgen05_m2l(require_gpu, monkeypatch):
