@@ -227,6 +227,13 @@ kifmm_status kifmm_gpu_plan_create(const kifmm_gpu_options* options, const kifmm
  * the potentials of its own particles (others left untouched). */
 kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* plan, const void* charges, void* potential,
                                 void* gradient, int32_t input_order, kifmm_gpu_timings* timings);
+/* n_rhs independent charge vectors through one plan (host buffers, as kifmm_gpu_evaluate;
+ * pinned buffers let the copies overlap): H2D of vector k+1 and D2H of the results of k-1 run
+ * under the evaluate of k on separate streams.  gradients may be NULL (or hold NULL entries)
+ * when no gradient is wanted.  Synchronous: returns when every result is in host memory.
+ * No reference counterpart (the reference's `run` takes one charge vector). */
+kifmm_status kifmm_gpu_evaluate_many(kifmm_gpu_plan* plan, int32_t n_rhs, const void* const* charges,
+                                     void* const* potentials, void* const* gradients, int32_t input_order);
 /* Device buffers on the plan's device; runs on `stream` (cudaStream_t or NULL
  * for the plan's stream) and does not synchronise. */
 kifmm_status kifmm_gpu_evaluate_device(kifmm_gpu_plan* plan, const void* d_charges,

@@ -119,6 +119,7 @@ _SIGS = {
                                     C.POINTER(P)]),
     "kifmm_gpu_evaluate": (i32, [P, P, P, P, i32, C.POINTER(GpuTimings)]),
     "kifmm_gpu_evaluate_device": (i32, [P, P, P, P, i32, P]),
+    "kifmm_gpu_evaluate_many": (i32, [P, i32, C.POINTER(P), C.POINTER(P), C.POINTER(P), i32]),
     "kifmm_gpu_plan_get_info": (i32, [P, C.POINTER(GpuPlanInfo)]),
     "kifmm_gpu_last_timings": (i32, [P, C.POINTER(GpuTimings)]),
     "kifmm_gpu_plan_destroy": (None, [P]),

@@ -387,6 +387,13 @@ struct kifmm_gpu_plan {
   int x_max = 0, x_total = 0, x_mine = 0;
   // graphs
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  // evaluate_many: copy-in / copy-out streams and double-buffered device staging (created on first use)
+  struct Pipe {
+    cudaStream_t cin = nullptr, cout = nullptr;
+    cudaEvent_t in_ready[2]{}, in_free[2]{}, out_ready[2]{}, out_free[2]{};
+    DevMem q[2], pot[2], grad[2];
+  };
+  std::unique_ptr<Pipe> pipe;
 
   ~kifmm_gpu_plan() {
     for (auto& g : graph)
@@ -395,6 +402,13 @@ struct kifmm_gpu_plan {
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
+    if (pipe) {
+      if (pipe->cin) cudaStreamDestroy(pipe->cin);
+      if (pipe->cout) cudaStreamDestroy(pipe->cout);
+      for (int b = 0; b < 2; ++b)
+        for (cudaEvent_t e : {pipe->in_ready[b], pipe->in_free[b], pipe->out_ready[b], pipe->out_free[b]})
+          if (e) cudaEventDestroy(e);
+    }
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (comm) Nccl::get().commDestroy(static_cast<ncclComm_t>(comm));
@@ -408,6 +422,29 @@ struct kifmm_gpu_plan {
   void run(cudaStream_t s, bool input_order, bool timed);
   void exchange(cudaStream_t s);
   void evaluate_device(const void* q, void* pot_dst, void* grad_dst, bool input_order, cudaStream_t user, bool timed);
+  // the captured evaluate graph of this output order on the plan stream (captured on first use)
+  void launch_graph(bool input_order) {
+    const int gi = input_order ? 1 : 0;
+    if (!graph[gi]) {
+      cudaGraph_t g;
+      KIFMM_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        if (precision == 32)
+          run<float>(stream, input_order, false);
+        else
+          run<double>(stream, input_order, false);
+      } catch (...) {
+        cudaStreamEndCapture(stream, &g);
+        throw;
+      }
+      KIFMM_CUDA(cudaStreamEndCapture(stream, &g));
+      KIFMM_CUDA(cudaGraphInstantiateWithFlags(&graph[gi], g, cudaGraphInstantiateFlagUseNodePriority));
+      cudaGraphDestroy(g);
+    }
+    KIFMM_CUDA(cudaGraphLaunch(graph[gi], stream));
+  }
+  void evaluate_many(int n_rhs, const void* const* charges, void* const* potentials, void* const* gradients,
+                     bool input_order);
 };
 
 namespace {
@@ -1656,6 +1693,76 @@ double fma_peak_impl(int device) {
 }
 }  // namespace
 
+// Many right-hand sides through one plan, software-pipelined over three streams: the H2D copy of
+// charges k+1 (copy-in stream) and the D2H copy of results k-1 (copy-out stream) run under the
+// evaluate of k (plan stream).  Device staging is double-buffered; the plan's own input / output
+// buffers are filled and drained with device-to-device copies on the plan stream (~7 us per
+// evaluate at config 2), so the captured graph is the same one evaluate() launches.
+void kifmm_gpu_plan::evaluate_many(int n_rhs, const void* const* charges, void* const* potentials,
+                                   void* const* gradients, bool input_order) {
+  KIFMM_CUDA(cudaSetDevice(device));
+  const size_t es = esz();
+  if (!pipe) {
+    auto P = std::make_unique<Pipe>();
+    KIFMM_CUDA(cudaStreamCreateWithFlags(&P->cin, cudaStreamNonBlocking));
+    KIFMM_CUDA(cudaStreamCreateWithFlags(&P->cout, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      for (cudaEvent_t* e : {&P->in_ready[b], &P->in_free[b], &P->out_ready[b], &P->out_free[b]})
+        KIFMM_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      P->q[b].alloc(size_t(N) * es, &dev_bytes);
+      P->pot[b].alloc(size_t(N) * es, &dev_bytes);
+      if (grad) P->grad[b].alloc(size_t(N) * 3 * es, &dev_bytes);
+    }
+    pipe = std::move(P);
+  }
+  Pipe& P = *pipe;
+  const bool full = input_order || world == 1;  // else: this rank's particle range (reordered order)
+  const size_t off = full ? 0 : size_t(pb), cnt = full ? size_t(N) : size_t(pe - pb);
+  const void* ps = input_order ? pot_out.p : pot.p;
+  const void* gs = input_order ? grad_out.p : grad_buf.p;
+  for (int k = 0; k < n_rhs; ++k) {
+    const int b = k & 1;
+    // copy-in: charges k into staging b once the evaluate of k-2 has consumed it
+    if (k >= 2) KIFMM_CUDA(cudaStreamWaitEvent(P.cin, P.in_free[b], 0));
+    KIFMM_CUDA(cudaMemcpyAsync(P.q[b].p, charges[k], size_t(N) * es, cudaMemcpyDefault, P.cin));
+    KIFMM_CUDA(cudaEventRecord(P.in_ready[b], P.cin));
+    // evaluate k on the plan stream
+    KIFMM_CUDA(cudaStreamWaitEvent(stream, P.in_ready[b], 0));
+    KIFMM_CUDA(cudaMemcpyAsync(q_in.p, P.q[b].p, size_t(N) * es, cudaMemcpyDeviceToDevice, stream));
+    KIFMM_CUDA(cudaEventRecord(P.in_free[b], stream));
+    if (opt.use_graph) {
+      launch_graph(input_order);
+    } else if (precision == 32) {
+      run<float>(stream, input_order, false);
+    } else {
+      run<double>(stream, input_order, false);
+    }
+    if (k >= 2) KIFMM_CUDA(cudaStreamWaitEvent(stream, P.out_free[b], 0));  // results k-2 have left staging b
+    if (cnt) {
+      KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(P.pot[b].p) + off * es, static_cast<const char*>(ps) + off * es,
+                                 cnt * es, cudaMemcpyDeviceToDevice, stream));
+      if (grad && gradients && gradients[k])
+        KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(P.grad[b].p) + 3 * off * es,
+                                   static_cast<const char*>(gs) + 3 * off * es, 3 * cnt * es, cudaMemcpyDeviceToDevice,
+                                   stream));
+    }
+    KIFMM_CUDA(cudaEventRecord(P.out_ready[b], stream));
+    // copy-out: results k to the caller's buffers
+    KIFMM_CUDA(cudaStreamWaitEvent(P.cout, P.out_ready[b], 0));
+    if (cnt) {
+      KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(potentials[k]) + off * es,
+                                 static_cast<const char*>(P.pot[b].p) + off * es, cnt * es, cudaMemcpyDefault, P.cout));
+      if (grad && gradients && gradients[k])
+        KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(gradients[k]) + 3 * off * es,
+                                   static_cast<const char*>(P.grad[b].p) + 3 * off * es, 3 * cnt * es,
+                                   cudaMemcpyDefault, P.cout));
+    }
+    KIFMM_CUDA(cudaEventRecord(P.out_free[b], P.cout));
+  }
+  KIFMM_CUDA(cudaStreamSynchronize(P.cout));
+  KIFMM_CUDA(cudaStreamSynchronize(stream));
+}
+
 // ====================================================================== ABI
 extern "C" {
 
@@ -1677,6 +1784,17 @@ kifmm_status kifmm_gpu_plan_create(const kifmm_gpu_options* options, const kifmm
       p->run<double>(p->stream, false, false);
     KIFMM_CUDA(cudaStreamSynchronize(p->stream));
     *out = p.release();
+  });
+}
+
+kifmm_status kifmm_gpu_evaluate_many(kifmm_gpu_plan* p, int32_t n_rhs, const void* const* charges,
+                                     void* const* potentials, void* const* gradients, int32_t input_order) {
+  return guard([&] {
+    if (!p || n_rhs < 0 || (n_rhs > 0 && (!charges || !potentials)))
+      throw InvalidArgument("evaluate_many: null argument or negative count");
+    for (int k = 0; k < n_rhs; ++k)
+      if (!charges[k] || !potentials[k]) throw InvalidArgument("evaluate_many: null charges / potential buffer");
+    p->evaluate_many(n_rhs, charges, potentials, gradients, input_order != 0);
   });
 }
 

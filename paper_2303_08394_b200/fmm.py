@@ -142,6 +142,35 @@ class Fmm:
                                      C.byref(tm) if tm is not None else None), "gpu_evaluate")
         return tm.as_dict() if tm is not None else None
 
+    def evaluate_many(self, charges, input_order: bool = True):
+        """Potentials (and gradients) for K independent charge vectors (array K x N), pipelined:
+        the copies of one vector overlap the evaluate of its neighbours (kifmm_gpu_evaluate_many).
+
+        Returns (potential K x N, gradient K x N x 3 | None).
+        """
+        q = np.ascontiguousarray(charges, dtype=self.dtype)
+        if q.ndim != 2 or q.shape[1] != self.n:
+            raise InvalidArgument(f"charges must have shape (K, {self.n})")
+        k = q.shape[0]
+        pot = np.empty((k, self.n), dtype=self.dtype)
+        grad = np.empty((k, self.n, 3), dtype=self.dtype) if self.config.gradient else None
+        self.evaluate_many_ptr([q[i].ctypes.data for i in range(k)], [pot[i].ctypes.data for i in range(k)],
+                               [grad[i].ctypes.data for i in range(k)] if grad is not None else None, input_order)
+        return pot, grad
+
+    def evaluate_many_ptr(self, q_ptrs, pot_ptrs, grad_ptrs=None, input_order: bool = True):
+        """Raw-pointer variant of evaluate_many (lists of host buffer addresses; pinned buffers overlap)."""
+        k = len(q_ptrs)
+        if len(pot_ptrs) != k or (grad_ptrs is not None and len(grad_ptrs) != k):
+            raise InvalidArgument("evaluate_many: pointer lists differ in length")
+        arr = C.c_void_p * max(k, 1)
+        qa, pa = arr(*q_ptrs), arr(*pot_ptrs)
+        ga = arr(*grad_ptrs) if grad_ptrs is not None else None
+        check(lib.kifmm_gpu_evaluate_many(self._h, k, C.cast(qa, C.POINTER(C.c_void_p)),
+                                          C.cast(pa, C.POINTER(C.c_void_p)),
+                                          C.cast(ga, C.POINTER(C.c_void_p)) if ga is not None else None,
+                                          1 if input_order else 0), "gpu_evaluate_many")
+
     def evaluate_device(self, d_charges: int, d_potential: int, d_gradient: int | None = None,
                         input_order: bool = True, stream: int | None = None):
         """Device-pointer variant; asynchronous on `stream` (cudaStream_t as int) or the plan stream."""

@@ -255,3 +255,24 @@ def test_coincident_particles(require_gpu):
         # fp64 stays at the parity bar
         tp, tg = TOL[precision] if precision == 64 else (2e-3, 1e-2)
         assert ep <= tp and eg <= tg, (precision, f.tree.depth, ep, eg)
+
+
+@pytest.mark.parametrize("gradient,input_order", [(True, True), (False, True), (True, False)])
+def test_evaluate_many_equals_evaluate(require_gpu, gradient, input_order):
+    """kifmm_gpu_evaluate_many (copies pipelined against the evaluates on three streams, double-buffered
+    staging) returns, for every right-hand side, exactly what one evaluate call returns."""
+    pos, _ = generators.sample("uniform-cube", 40000, seed=5, fp32=True)
+    cfg = fmm.FmmConfig(p=6, n_crit=40, precision=32, gradient=gradient)
+    qs = np.stack([generators.sample("uniform-cube", 40000, seed=100 + k, charges="signed", fp32=True)[1]
+                   for k in range(5)]).astype(np.float32)
+    with fmm.Fmm(pos, cfg) as f:
+        pots, grads = f.evaluate_many(qs, input_order=input_order)
+        for k in range(len(qs)):
+            p1, g1, _ = f.evaluate(qs[k], input_order=input_order)
+            assert np.array_equal(pots[k], p1)
+            if gradient:
+                assert np.array_equal(grads[k], g1)
+            else:
+                assert grads is None
+        empty = f.evaluate_many(np.zeros((0, 40000), np.float32))
+        assert empty[0].shape == (0, 40000)
