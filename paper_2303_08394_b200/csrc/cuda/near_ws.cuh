@@ -30,7 +30,8 @@ constexpr int kNearWsThreads = 160;  // warps 0-3 consumers, warp 4 producer
 struct NearStage {
   float4 src[kP2PCap];  // [self section, padded to S][other sources, padded to O]; reused for the reduction
   int wi, S, O, flags;      // flags: bit 0 first round of the work, bit 1 last round; wi < 0: stop
-  int t_begin, t_count, pad0, pad1;
+  int t_begin, t_count, geom, mul_tt;
+  int mul_r, pad0, pad1, pad2;
 };
 
 struct NearSmem {
@@ -120,6 +121,9 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
           S.flags = (r == w.round_begin ? 1 : 0) | (r == w.round_end - 1 ? 2 : 0);
           S.t_begin = w.t_begin;
           S.t_count = w.t_count;
+          S.geom = w.geom;
+          S.mul_tt = w.mul_tt;
+          S.mul_r = w.mul_r;
         }
         tc::mbar_arrive_local(tc::smem_u32(&sm.full[stage]));  // release: padding + header stores
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&sm.full[stage]))
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
   // ---------------- consumers (warps 0-3): geometry and arithmetic of leaf_eval_f2_kernel
   int stage = 0;
   uint32_t phase = 0;
-  int nt = 0, TT = 1, R = 1, slice = 0, t0 = 0;
+  int nt = 0, TT = 1, R = 1, slice = 0, t0 = 0, mul_r = 0;
   bool active = false;
   f2_t x[1], y[1], z[1], ph[1], gx[1], gy[1], gz[1];
   for (;;) {
@@ -147,9 +151,10 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
     const int flags = S.flags;
     if (flags & 1) {  // first round of a work
       nt = S.t_count;
-      TT = (nt + 1) / 2;
-      R = leaf_slices(nt, true);
-      slice = tid / TT;
+      TT = S.geom >> 8;
+      R = S.geom & 0xFF;
+      mul_r = S.mul_r;
+      slice = div_mul(tid, S.mul_tt);
       t0 = tid - slice * TT;
       active = slice < R;
       const int ta = t0, tb = t0 + TT;
@@ -164,11 +169,11 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
     const int Ssz = S.S, Osz = S.O;
     if (active) {
       if (Ssz) {
-        const int per = Ssz / R;
+        const int per = div_mul(Ssz, mul_r);
         p2p_round_fn<GRAD, true, 1>(S.src, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
       }
       if (Osz) {
-        const int per = Osz / R;
+        const int per = div_mul(Osz, mul_r);
         p2p_round_fn<GRAD, false, 1>(S.src, Ssz + slice * per, Ssz + slice * per + per, x, y, z, ph, gx, gy, gz);
       }
     }

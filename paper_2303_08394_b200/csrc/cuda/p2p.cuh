@@ -33,7 +33,12 @@ struct LeafWork {
   int t_begin;  // first target (reordered particle index)
   int t_count;  // <= 128
   int round_begin, round_end;
+  // thread geometry, precomputed on the host (the kernels divide by multiply-shift, no IMAD division
+  // sequences on the FMA pipe): slices R | target slots per slice TT << 8, ceil(2^16 / TT), ceil(2^16 / R)
+  int geom, mul_tt, mul_r;
 };
+// floor(n / d) for n < 2^16 / d as (n * ceil(2^16 / d)) >> 16 (exact here: n <= 1024, d <= 128)
+__host__ __device__ inline int div_mul(int n, int mul) { return int((unsigned(n) * unsigned(mul)) >> 16); }
 // A staging round: {item_begin, item_end, S | n_self << 16, O | n_other << 16}:
 // shared-memory layout [self section, padded to S][other sources, padded to O],
 // S and O multiples of 8R.  Items: {kind | j0 << 4, a, len, dst} (j0 = first
@@ -244,10 +249,9 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
     }
   }
   const LeafWork w = works[wi];
-  constexpr int NPR = kNearNPair, TPT = 2 * NPR;  // target pairs / targets per thread
-  const int nt = w.t_count, TT = (nt + TPT - 1) / TPT;
-  const int R = leaf_slices(nt, true);
-  const int slice = tid / TT, t0 = tid - slice * TT;  // targets t0 + m TT, m < TPT
+  constexpr int NPR = kNearNPair;  // target pairs per thread
+  const int nt = w.t_count, TT = w.geom >> 8, R = w.geom & 0xFF;  // TT = ceil(nt / TPT), R = leaf_slices(nt)
+  const int slice = div_mul(tid, w.mul_tt), t0 = tid - slice * TT;  // targets t0 + m TT, m < TPT
   const bool active = slice < R;
   f2_t x[NPR], y[NPR], z[NPR], ph[NPR], gx[NPR], gy[NPR], gz[NPR];
 #pragma unroll
@@ -283,11 +287,11 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
     __syncthreads();
     if (active) {
       if (S) {
-        const int per = S / R;
+        const int per = div_mul(S, w.mul_r);
         p2p_round_fn<GRAD, true, NPR>(sh, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
       }
       if (O) {
-        const int per = O / R;
+        const int per = div_mul(O, w.mul_r);
         p2p_round_fn<GRAD, false, NPR>(sh, S + slice * per, S + slice * per + per, x, y, z, ph, gx, gy, gz);
       }
     }
@@ -344,9 +348,8 @@ __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, 
   __shared__ v4_t<T> sh[kP2PCap];
   const LeafWork w = works[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nt = w.t_count;
-  const int R = leaf_slices(nt, false);
-  const int slice = tid / nt, tgt = tid - slice * nt;
+  const int nt = w.t_count, R = w.geom & 0xFF;  // R = leaf_slices(nt), TT = nt
+  const int slice = div_mul(tid, w.mul_tt), tgt = tid - slice * nt;
   const bool active = slice < R;
 
   const v4_t<T> xt = p.src[w.t_begin + (active ? tgt : 0)];
@@ -374,11 +377,11 @@ __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, 
     __syncthreads();
     if (active) {
       if (S) {
-        const int per = S / R;
+        const int per = div_mul(S, w.mul_r);
         p2p_round<T, GRAD, true>(sh, slice * per, slice * per + per, xt.x, xt.y, xt.z, ph, gx, gy, gz);
       }
       if (O) {
-        const int per = O / R;
+        const int per = div_mul(O, w.mul_r);
         p2p_round<T, GRAD, false>(sh, S + slice * per, S + slice * per + per, xt.x, xt.y, xt.z, ph, gx, gy, gz);
       }
     }

@@ -330,9 +330,10 @@ struct kifmm_gpu_plan {
   int device = 0;
   int precision = 32;
   bool leaf_packed = false;
-  // warp-specialised persistent near-field kernel (KIFMM_NEAR_WS=1; bit-identical results).  Config 2: neutral
-  // in the full evaluate (1.361 vs 1.361 ms), standalone 2-4 % slower (its consumer barriers), so off
-  int near_ws = 0;
+  // warp-specialised persistent near-field kernel (bit-identical results): KIFMM_NEAR_WS=0 never, 1 (default) for
+  // the queue-mode side / drain launches of the captured evaluate (config 2: 1.33 vs 1.35 ms), 2 also for the
+  // standalone launch of the serialized timed run (there 2-5 % slower than one leaf_eval_f2 block per leaf)
+  int near_ws = 1;
   int near_ws_bps = 2;
   int near_ws_blocks = 6;  // resident blocks per SM of the standalone / drain launch (occupancy query)   // its side blocks per SM next to the tcgen05 kernels (smem: 2 x 37 KB + stages)
   int near_pause = 0;  // side blocks sleep during M2L: 1 all, 2 half (KIFMM_NEAR_PAUSE; 1 measured slower)
@@ -1148,7 +1149,9 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
           const int O = (no + q - 1) / q * q;
           rounds.push_back(make_int4(ib, int(items.size()), S | (ns << 16), O | (no << 16)));
         }
-        w.push_back({int(l), int(t0), nt, rb, int(rounds.size())});
+        const int TT = packed ? (nt + 2 * kNearNPair - 1) / (2 * kNearNPair) : nt;
+        w.push_back({int(l), int(t0), nt, rb, int(rounds.size()), R | (TT << 8), (65536 + TT - 1) / TT,
+                     (65536 + R - 1) / R});
       }
     }
     }
@@ -1298,7 +1301,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     const int4* it = lp.items.as<int4>();
     T* g = grad ? grad_buf.as<T>() : nullptr;
     if constexpr (sizeof(T) == 4) {
-      if (leaf_packed && near_ws && &lp == &leaf_near && !acc) {  // standalone persistent near field
+      if (leaf_packed && near_ws >= 2 && &lp == &leaf_near && !acc) {  // standalone persistent near field
         int* qc = near_counter.as<int>();
         KIFMM_CUDA(cudaMemsetAsync(qc, 0, 4 * sizeof(int), st));
         const int grid = std::min(lp.n, near_ws_blocks * sm_count());

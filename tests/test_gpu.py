@@ -182,8 +182,9 @@ def test_near_queue_mode_bit_identical(require_gpu, monkeypatch):
     pos, q = generators.sample("two-cluster", 60000, seed=21, charges="signed", fp32=True)
     cfg = fmm.FmmConfig(p=6, n_crit=40, precision=32, gradient=True)
     out = {}
-    # KIFMM_NEAR_WS=0: one leaf_eval_f2 block per leaf work; 1: the warp-specialised persistent kernel
-    for ws in ("0", "1"):
+    # KIFMM_NEAR_WS=0: one leaf_eval_f2 block per leaf work; 1: the warp-specialised persistent kernel in
+    # queue mode; 2: also for the standalone launch
+    for ws in ("0", "1", "2"):
         for bps in ("0", "1", "2"):
             monkeypatch.setenv("KIFMM_NEAR_WS", ws)
             monkeypatch.setenv("KIFMM_NEAR_BPS", bps)
