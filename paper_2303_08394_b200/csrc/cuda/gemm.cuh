@@ -177,5 +177,117 @@ __global__ void __launch_bounds__(GemmShape<T, N, BM, TM, TN, KC, STAGES>::NT, 1
   }
 }
 
+// FP64 variant on the warp-level FP64 tensor op (DMMA, mma.sync m8n8k4 f64): the same gathered,
+// segmented tile (64 rows x N, cp.async pipeline over (segment, 16-wide K chunk)), but each warp owns a
+// 32 x N/4 block of 4 x N/32 DMMA accumulators fed by register fragments -- per 4-wide k step a lane
+// loads 4 + N/32 doubles from shared memory for 4 N/32 DMMAs (256 FMAs each), where the SIMT kernel's
+// shared-memory operand traffic held DFMA at ~50 % of the FP64 peak (config 4, p = 7).
+// Fragments (PTX m8n8k4 .f64): A[8x4] lane l -> (row l/4, k l%4); B[4x8] -> (k l%4, col l/4);
+// C/D[8x8] -> (row l/4, cols 2 (l%4) + {0, 1}).
+// Shared layout (a 64-bit fragment load is served per half-warp, 16 lanes x 8 B = one 128-B wavefront):
+// A rows padded to 20 doubles (160 B: the 4 rows of a half-warp start 32 B apart), B rows to N + 4
+// doubles (the 4 k rows of a half-warp start 32 B apart).  B rows at N + 8 put k and k + 2 on the
+// same banks: 5.6e9 bank conflicts in one config-4 M2L launch (ncu).
+template <int N>
+struct DmmaShape {
+  static constexpr int BM = 64, KC = 16, STAGES = 3, NT = 256;
+  static constexpr int AST = KC + 4, BST = N + 4;
+  static constexpr int NB = N / 32;  // 8-wide column blocks per warp (warps: 2 along M x 4 along N)
+  static constexpr int A_ELEMS = BM * AST, W_ELEMS = KC * BST, STAGE_ELEMS = A_ELEMS + W_ELEMS;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
+  static_assert(N % 32 == 0, "DMMA gemm: N multiple of 32");
+};
+
+template <int N>
+__global__ void __launch_bounds__(256, 1) gather_dmma_kernel(GemmArgs<double> a) {
+  using S = DmmaShape<N>;
+  constexpr int BM = S::BM, KC = S::KC, STAGES = S::STAGES;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>(smem_raw);
+  const int tile = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int seg0 = a.tile_seg[tile], seg1 = a.tile_seg[tile + 1];
+  const int kchunks = a.K / KC;
+  const int iters = (seg1 - seg0) * kchunks;
+
+  auto load_stage = [&](int it, int stage) {
+    const int seg = seg0 + it / kchunks;
+    const int kc = (it % kchunks) * KC;
+    double* As = smem + stage * S::STAGE_ELEMS;
+    double* Ws = As + S::A_ELEMS;
+    constexpr int ACH = BM * (KC / 2);  // 16-byte chunks
+    for (int c = tid; c < ACH; c += S::NT) {
+      const int row = c / (KC / 2), col = c % (KC / 2);
+      const int src = a.seg_in[size_t(seg) * BM + row];
+      const double* g = a.X + size_t(src < 0 ? 0 : src) * a.ldx + kc + col * 2;
+      cp_async16(As + row * S::AST + col * 2, g, src >= 0);
+    }
+    const double* wm_ = a.W + size_t(a.seg_mat[seg]) * a.K * N + size_t(kc) * N;
+    constexpr int WCH = KC * N / 2;
+    for (int c = tid; c < WCH; c += S::NT) {
+      const int k = c / (N / 2), col = c % (N / 2);
+      cp_async16(Ws + k * S::BST + col * 2, wm_ + size_t(k) * N + col * 2, true);
+    }
+  };
+
+  double acc[4][S::NB][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < S::NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < iters) load_stage(s, s);
+    cp_async_commit();
+  }
+  const int ar = wm * 32 + (lane >> 2), ak = lane & 3;         // A fragment coordinates
+  const int bk = lane & 3, bn = wn * (N / 4) + (lane >> 2);    // B fragment coordinates
+  for (int it = 0; it < iters; ++it) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = it + STAGES - 1;
+      if (nxt < iters) load_stage(nxt, nxt % STAGES);
+      cp_async_commit();
+    }
+    const double* As = smem + (it % STAGES) * S::STAGE_ELEMS;
+    const double* Ws = As + S::A_ELEMS;
+#pragma unroll
+    for (int ks = 0; ks < KC; ks += 4) {
+      double af[4], bf[S::NB];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[(ar + 8 * i) * S::AST + ks + ak];
+#pragma unroll
+      for (int j = 0; j < S::NB; ++j) bf[j] = Ws[(ks + bk) * S::BST + bn + 8 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < S::NB; ++j)
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                       : "d"(af[i]), "d"(bf[j]));
+    }
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = wm * 32 + 8 * i + (lane >> 2);
+    const int out = a.tile_out[size_t(tile) * BM + row];
+    if (out < 0) continue;
+    double* y = a.Y + size_t(out) * a.ldy;
+#pragma unroll
+    for (int j = 0; j < S::NB; ++j) {
+      const int col = wn * (N / 4) + 8 * j + 2 * (lane & 3);
+      double2 v = make_double2(0.0, 0.0);
+      if (a.accumulate) v = *reinterpret_cast<const double2*>(y + col);
+      v.x += acc[i][j][0];
+      v.y += acc[i][j][1];
+      *reinterpret_cast<double2*>(y + col) = v;
+    }
+  }
+}
+
 }  // namespace gpu
 }  // namespace kifmm

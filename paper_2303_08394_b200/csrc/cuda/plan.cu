@@ -98,8 +98,27 @@ struct KC_<double> {
   static constexpr int v = 16;
 };
 
+// fp64 64-row tiles run on the DMMA kernel (KIFMM_DMMA=0: the SIMT DFMA kernel)
+inline bool use_dmma() {  // read per launch (a captured graph keeps the choice of its capture)
+  const char* e = std::getenv("KIFMM_DMMA");
+  return !(e && std::atoi(e) == 0);
+}
+
 template <class T, int N, int BM, int TM>
 void launch_gemm_n(const GemmTiles& t, const GemmArgs<T>& a, cudaStream_t s) {
+  if constexpr (sizeof(T) == 8 && BM == 64 && N % 32 == 0) {
+    if (use_dmma()) {
+      auto kern = gather_dmma_kernel<N>;
+      static bool attr = false;
+      if (!attr) {
+        KIFMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(DmmaShape<N>::SMEM)));
+        attr = true;
+      }
+      kern<<<t.n_tiles, DmmaShape<N>::NT, DmmaShape<N>::SMEM, s>>>(a);
+      KIFMM_LAUNCH_CHECK();
+      return;
+    }
+  }
   constexpr int KC = KC_<T>::v;
   using S = GemmShape<T, N, BM, TM, 8, KC, 3>;
   auto kern = gather_gemm_kernel<T, N, BM, TM, 8, KC, 3>;

@@ -277,3 +277,19 @@ def test_evaluate_many_equals_evaluate(require_gpu, gradient, input_order):
                 assert grads is None
         empty = f.evaluate_many(np.zeros((0, 40000), np.float32))
         assert empty[0].shape == (0, 40000)
+
+
+@pytest.mark.parametrize("p", [5, 6, 7])
+def test_fp64_dmma_gemm_matches_simt(require_gpu, monkeypatch, p):
+    """fp64 GEMMs (solves, M2M, M2L, L2L) on the DMMA tensor op agree with the SIMT DFMA kernel
+    (KIFMM_DMMA=0) to fp64 rounding, and both with the oracle within the fp64 gate."""
+    pos, q = generators.sample("two-cluster", 6000, seed=41, charges="signed")
+    out = {}
+    for dm in ("0", "1"):
+        monkeypatch.setenv("KIFMM_DMMA", dm)
+        with fmm.Fmm(pos, fmm.FmmConfig(p=p, n_crit=30, precision=64, gradient=True)) as f:
+            out[dm] = f.evaluate(q)[:2]
+            ref, gref = _ref(f, q, True)
+    assert fmm.relative_error(out["1"][0], out["0"][0]) <= 1e-13
+    assert fmm.relative_error(out["1"][0], ref) <= 1e-12
+    assert fmm.relative_error(out["1"][1], gref) <= 1e-11
