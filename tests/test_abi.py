@@ -60,3 +60,22 @@ def test_gpu_plan_fails_loudly_without_device():
     pos, q = generators.sample("uniform-cube", 500, seed=0)
     with pytest.raises(DeviceError):
         fmm.Fmm(pos, fmm.FmmConfig(p=3, n_crit=20))
+
+
+def test_null_plan_arguments_rejected():
+    """Every evaluate entry point validates its arguments before touching a device (no CUDA needed):
+    a null plan is KIFMM_E_INVALID_ARGUMENT, raised as the reference's InvalidArgument class."""
+    import ctypes as C
+
+    from paper_2303_08394_b200._lib import check, lib
+    from paper_2303_08394_b200.errors import InvalidArgument
+
+    buf = (C.c_float * 4)()
+    ptrs = (C.c_void_p * 1)(C.cast(buf, C.c_void_p))
+    pp = C.cast(ptrs, C.POINTER(C.c_void_p))
+    with pytest.raises(InvalidArgument):
+        check(lib.kifmm_gpu_evaluate(None, buf, buf, None, 1, None), "evaluate")
+    with pytest.raises(InvalidArgument):
+        check(lib.kifmm_gpu_evaluate_many(None, 1, pp, pp, None, 1), "evaluate_many")
+    with pytest.raises(InvalidArgument):
+        check(lib.kifmm_gpu_evaluate_device(None, buf, buf, None, 1, None), "evaluate_device")
