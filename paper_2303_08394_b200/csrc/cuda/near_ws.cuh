@@ -6,8 +6,8 @@
 // start-up stalls left the FMA pipe idle ~28 % of the time (ncu, config 2).
 // Here one producer warp per block walks the same work / round / item lists
 // and stages each round's sources into a ring
-// of shared-memory stages with cp.async, signalling a full mbarrier with
-// cp.async.mbarrier.arrive.noinc; four consumer warps compute exactly what
+// of shared-memory stages with one cp.async.bulk per contiguous source range
+// (completing on the stage's full mbarrier); four consumer warps compute exactly what
 // leaf_eval_f2_kernel computes -- same slice geometry, same p2p_round_fn,
 // same fixed-order slice reduction -- so the result is bit-identical to it and
 // independent of which block took which work.  Works come from an atomic
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < kNearStages; ++s) {
-      tc::mbar_init(tc::smem_u32(&sm.full[s]), 64);  // 32 producer arrives + 32 cp.async completions
+      tc::mbar_init(tc::smem_u32(&sm.full[s]), 32);  // one arrival per producer lane (+ the bulk-copy bytes)
       tc::mbar_init(tc::smem_u32(&sm.empty[s]), 4);  // one per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -89,8 +89,6 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
         tc::mbar_wait(tc::smem_u32(&sm.empty[stage]), phase ^ 1);
         if (lane == 0) sm.st[stage].wi = -1;
         tc::mbar_arrive_local(tc::smem_u32(&sm.full[stage]));
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&sm.full[stage]))
-                     : "memory");
         break;
       }
       const LeafWork w = works[wi];
@@ -102,16 +100,20 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
         tc::mbar_wait(tc::smem_u32(&sm.empty[stage]), phase ^ 1);
         NearStage& S = sm.st[stage];
         const uint32_t sbase = tc::smem_u32(S.src);
+        const int Ssz = rd.z & 0xFFFF, ns = rd.z >> 16, Osz = rd.w & 0xFFFF, no = rd.w >> 16;
+        // one cp.async.bulk per contiguous source range (lane k: item k), completing on the full barrier
+        // (lane 0 adds the round's byte count to its arrival below)
         for (int kb = rd.x; kb < rd.y; kb += 32) {
           if (kb != rd.x && kb + lane < rd.y) my_item = items[kb + lane];
-          const int nk = min(32, rd.y - kb);
-          for (int k = 0; k < nk; ++k) {
-            const int a = __shfl_sync(0xffffffffu, my_item.y, k), len = __shfl_sync(0xffffffffu, my_item.z, k),
-                      dst = __shfl_sync(0xffffffffu, my_item.w, k);
-            for (int i = lane; i < len; i += 32) cp_async16(sbase + 16u * uint32_t(dst + i), p.src + a + i);
+          if (kb + lane < rd.y) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    sbase + 16u * uint32_t(my_item.w)),
+                "l"(p.src + my_item.y), "r"(16u * uint32_t(my_item.z)), "r"(tc::smem_u32(&sm.full[stage]))
+                : "memory");
           }
         }
-        const int Ssz = rd.z & 0xFFFF, ns = rd.z >> 16, Osz = rd.w & 0xFFFF, no = rd.w >> 16;
         for (int i = ns + lane; i < Ssz; i += 32) S.src[i] = far4;
         for (int i = Ssz + no + lane; i < Ssz + Osz; i += 32) S.src[i] = far4;
         if (lane == 0) {
@@ -125,9 +127,12 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
           S.mul_tt = w.mul_tt;
           S.mul_r = w.mul_r;
         }
-        tc::mbar_arrive_local(tc::smem_u32(&sm.full[stage]));  // release: padding + header stores
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&sm.full[stage]))
-                     : "memory");
+        if (lane == 0)  // release: padding + header stores; the bulk copies' bytes
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&sm.full[stage])),
+                       "r"(16u * uint32_t(ns + no))
+                       : "memory");
+        else
+          tc::mbar_arrive_local(tc::smem_u32(&sm.full[stage]));
         if (++stage == kNearStages) {
           stage = 0;
           phase ^= 1;

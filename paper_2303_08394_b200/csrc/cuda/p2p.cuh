@@ -207,6 +207,17 @@ __device__ __forceinline__ void p2p_round_f2(const float4* sh, int begin, int en
   }
 }
 
+// mbarrier phase wait (try_wait suspends the thread for a hardware time slice between polls)
+__device__ __forceinline__ void wait_parity(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+}
+
 // fp32 leaf_eval with two targets per thread: thread -> (slice tid / T2, target
 // pair tid % T2) with T2 = ceil(n_t / 2); the pair is (tt, tt + T2).  Same
 // staging rounds / items as leaf_eval_kernel (geometry leaf_slices(nt, true)).
@@ -226,7 +237,20 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
                                                                        int* __restrict__ queue = nullptr) {
   __shared__ float4 sh[kP2PCap];
   __shared__ int s_wi;
+  __shared__ __align__(8) unsigned long long s_bar;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // the near plan (ACC = false) has particle items only: staged with bulk copies (far-as-leaf plans
+  // carry computed surface sources and keep the per-lane staging)
+  constexpr bool BULK = !ACC;
+  const uint32_t bar = uint32_t(__cvta_generic_to_shared(&s_bar));
+  uint32_t bar_phase = 0;
+  if constexpr (BULK) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   if (QUEUE) timeline_begin(DRAIN ? 4 : 3);
   if (QUEUE && DRAIN && blockIdx.x == 0 && tid == 0) atomicExch(queue + 1, 1);
   for (int wi = blockIdx.x;;) {
@@ -270,6 +294,22 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
   for (int r = w.round_begin; r < w.round_end; ++r) {
     const int4 rd = rounds[r];
     const int S = rd.z & 0xFFFF, ns = rd.z >> 16, O = rd.w & 0xFFFF, no = rd.w >> 16;
+    if constexpr (BULK) {
+      // near plan (particle items only): one cp.async.bulk per contiguous source range, completing on the
+      // block's mbarrier (thread 0 arrives with the round's byte count) -- no per-source load/store pairs
+      if (tid == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(16u * uint32_t(ns + no))
+                     : "memory");
+      for (int k = rd.x + tid; k < rd.y; k += kP2PThreads) {
+        const int4 item = items[k];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                uint32_t(__cvta_generic_to_shared(sh + item.w))),
+            "l"(p.src + item.y), "r"(16u * uint32_t(item.z)), "r"(bar)
+            : "memory");
+      }
+    } else {
     for (int k = rd.x + warp; k < rd.y; k += 4) {
       const int4 item = items[k];
       const int kind = item.x & 0xF, j0 = item.x >> 4;
@@ -282,8 +322,13 @@ __global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<
         for (int i = lane; i < item.z; i += 32) put(item.w + i, surface_source(p, item.y, alpha, dens, j0 + i));
       }
     }
+    }
     for (int i = ns + tid; i < S; i += kP2PThreads) put(i, make_float4(fa, fa, fa, 0.f));
     for (int i = S + no + tid; i < S + O; i += kP2PThreads) put(i, make_float4(fa, fa, fa, 0.f));
+    if constexpr (BULK) {
+      wait_parity(bar, bar_phase);
+      bar_phase ^= 1u;
+    }
     __syncthreads();
     if (active) {
       if (S) {
