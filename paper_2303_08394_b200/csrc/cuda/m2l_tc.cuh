@@ -99,7 +99,9 @@ struct Cfg {
   // costs ~50 cycles of MMA issue in tools/ubench/mma_pair.cu) -- measured slower in the kernel (the
   // shorter effective lookahead costs more than the commits save), so EG = 1
   static constexpr int EG = (STAGES % KIFMM_TC_EG == 0) ? KIFMM_TC_EG : 1;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512 + 2048;  // + row-max exchange
+  // + barriers, row-max exchange, and (single CTA: direct GEMM epilogue) the 8 x 32 x 20-float transpose buffer
+  //   and the column unscale
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512 + 2048 + (PAIR ? 0 : 8 * 32 * 20 * 4 + NP * 4);
   static constexpr int ATOM = 8 * ROWB;           // bytes of an 8-row swizzle atom (= SBO)
   static constexpr uint64_t LAYOUT = ROWB == 128 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B
   static constexpr int CTAS = PAIR ? 2 : 1;
@@ -333,8 +335,20 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   //       [2S+4,3S+4) a_full (this CTA's A rows landed; PAIR only); then the TMEM address
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * C::STAGES + 2 * NACC);
   float* xmax = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 512);  // [2][2][128]
+  float* tbuf = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 2560);  // !PAIR: [8 warps][32][20]
+  float* s_colun = tbuf + (PAIR ? 0 : 8 * 32 * 20);                                   // !PAIR: [NP] col_unscale
+  if (!PAIR && epi.direct_out && threadIdx.x < NP) s_colun[threadIdx.x] = epi.col_unscale[threadIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
+#ifdef KIFMM_TC_PROBE  // experiments: phase timestamps of CTA 0 (globaltimer ns), printed at the end
+  __shared__ unsigned long long probe[12];
+  if (threadIdx.x < 12) probe[threadIdx.x] = 0;
+  if (threadIdx.x == 0) probe[0] = globaltimer();
+#define TC_PROBE(i, cond) \
+  if ((cond) && blockIdx.x == 0) probe[i] = globaltimer();
+#else
+#define TC_PROBE(i, cond)
+#endif
   // persistent: this CTA (pair) g0 runs the items sched[gs + 1 + k], k in [sched[g0], sched[g0 + 1]) -- a
   // longest-processing-time-first assignment made on the host; every role walks the same item sequence
   // with running stage (gi) and tap (gj) counters, so the pipeline runs on across item boundaries
@@ -388,6 +402,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   if (PAIR) cluster_sync();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  TC_PROBE(1, threadIdx.x == 0)
   timeline_begin(PAIR ? 1 : 2);
 #ifdef KIFMM_TIMELINE_PROBES
   if (PAIR && blockIdx.x == 0 && threadIdx.x == 0 && g_timeline_on) {  // SM clock probe (experiments)
@@ -423,6 +438,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
         const float f = f_next;
         if (j + 1 < ntap) f_next = unscale_of(j + 1);
         mbar_wait_sleep(tfull(b), tph);
+        TC_PROBE(4, warp == EPI_WARP0 && lane == 0 && kk == k_begin && j == 0)
         __syncwarp();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * NP + h * EPI_COLS);
@@ -451,7 +467,113 @@ __global__ void __maxnreg__(LAUNCH_REGS)
           tph ^= 1u;
         }
       }
-      if (epi.direct_out) {
+      TC_PROBE(6, warp == EPI_WARP0 && lane == 0 && kk == k_begin)
+      if (!PAIR && epi.direct_out) {
+        // Direct GEMM epilogue, coalesced: a thread holds one output ROW, so row-per-thread global
+        // loads / stores touch 32 rows (32 lines) per instruction -- 5-12 us per tile in the small
+        // GEMMs (globaltimer probes, KIFMM_TC_PROBE).  The warp transposes its 32 x 80 block through
+        // shared memory in 16-column chunks; lane (rr, sub) then owns rows rr + 8 i (i < 4) and
+        // columns 4 sub .. 4 sub + 3 of every chunk, so one instruction covers 8 rows x 64 bytes.
+        // Same operations per element as the row path below (bit-identical results).
+        constexpr int TP = 20, NCH = EPI_COLS / 16;
+        float* tb = tbuf + (warp - EPI_WARP0) * (32 * TP);
+        const int sub = lane & 3, rr = lane >> 2;
+        const int my_out = epi.direct_out[size_t(it.tile) * rows + row];
+        int outs[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) outs[i] = __shfl_sync(0xffffffffu, my_out, rr + 8 * i);
+        float* base = epi.dst ? epi.dst : epi.partial;
+        float4 val[NCH][4];
+        // transpose and column-unscale (shared memory only: no global load waits behind the __syncwarps)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<float4*>(tb + lane * TP + 4 * j) =
+                make_float4(acc[16 * c + 4 * j], acc[16 * c + 4 * j + 1], acc[16 * c + 4 * j + 2], acc[16 * c + 4 * j + 3]);
+          __syncwarp();
+          const float4 u = *reinterpret_cast<const float4*>(s_colun + h * EPI_COLS + 16 * c + 4 * sub);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float4 v = *reinterpret_cast<const float4*>(tb + (rr + 8 * i) * TP + 4 * sub);
+            v.x *= u.x;
+            v.y *= u.y;
+            v.z *= u.z;
+            v.w *= u.w;
+            val[c][i] = v;
+          }
+        }
+        if (epi.accumulate) {  // independent loads, one latency
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (outs[i] >= 0) {
+                const float4 o = *reinterpret_cast<const float4*>(base + size_t(outs[i]) * NP + h * EPI_COLS + 16 * c +
+                                                                  4 * sub);
+                val[c][i].x += o.x;
+                val[c][i].y += o.y;
+                val[c][i].z += o.z;
+                val[c][i].w += o.w;
+              }
+        }
+        if (epi.dst) {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (outs[i] >= 0)
+                *reinterpret_cast<float4*>(epi.dst + size_t(outs[i]) * NP + h * EPI_COLS + 16 * c + 4 * sub) = val[c][i];
+        }
+        TC_PROBE(7, warp == EPI_WARP0 && lane == 0 && kk == k_begin)
+        if (epi.split_hi) {
+          float mx[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float m = 0.f;
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+              m = fmaxf(m, fmaxf(fmaxf(fabsf(val[c][i].x), fabsf(val[c][i].y)), fmaxf(fabsf(val[c][i].z), fabsf(val[c][i].w))));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+            mx[i] = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+          }
+          // row max over both column halves (partner warp: same lane quarter, other half), named barrier
+          // 1 + q (64 threads); xmax is double-buffered by item parity
+          float* xm = xmax + (kk & 1) * 256;
+          if (sub == 0)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xm[h * 128 + q * 32 + rr + 8 * i] = mx[i];
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+          TC_PROBE(8, warp == EPI_WARP0 && lane == 0 && kk == k_begin)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (outs[i] < 0) continue;
+            const float m = fmaxf(mx[i], xm[(1 - h) * 128 + q * 32 + rr + 8 * i]);
+            const int e = f16_row_exponent(m);
+            const float sc = ldexpf(1.f, e);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+              const float x[4] = {val[c][i].x * sc, val[c][i].y * sc, val[c][i].z * sc, val[c][i].w * sc};
+              uint32_t wh[2], wl[2];
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const __half h0 = __float2half_rn(x[2 * u]), h1 = __float2half_rn(x[2 * u + 1]);
+                const __half2 hh = __halves2half2(h0, h1);
+                const __half2 ll = __halves2half2(__float2half_rn(x[2 * u] - __half2float(h0)),
+                                                  __float2half_rn(x[2 * u + 1] - __half2float(h1)));
+                wh[u] = *reinterpret_cast<const uint32_t*>(&hh);
+                wl[u] = *reinterpret_cast<const uint32_t*>(&ll);
+              }
+              const size_t o = size_t(outs[i]) * NP + h * EPI_COLS + 16 * c + 4 * sub;
+              *reinterpret_cast<uint2*>(epi.split_hi + o) = make_uint2(wh[0], wh[1]);
+              *reinterpret_cast<uint2*>(epi.split_lo + o) = make_uint2(wl[0], wl[1]);
+            }
+            if (h == 0 && sub == 0) epi.split_un[outs[i]] = ldexpf(1.f, -e);
+          }
+          TC_PROBE(9, warp == EPI_WARP0 && lane == 0 && kk == k_begin)
+        }
+      } else if (epi.direct_out) {
         const int out = epi.direct_out[size_t(it.tile) * rows + rank * BM + row];
         if (out >= 0) {
           // loads first (column unscale, then the old output row), stores last: no load waits behind a store
@@ -481,6 +603,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
               o4[k] = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
           }
         }
+        TC_PROBE(7, warp == EPI_WARP0 && lane == 0 && kk == k_begin)
         if (epi.split_hi) {
           // row max over both column halves: the partner warp (same lane quarter, other half) meets
           // this one on named barrier 1 + q (64 threads); xmax is double-buffered by item parity
@@ -492,6 +615,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
           float* xm = xmax + (kk & 1) * 256;
           xm[h * 128 + row] = mx;
           asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+          TC_PROBE(8, warp == EPI_WARP0 && lane == 0 && kk == k_begin)
           mx = fmaxf(mx, xm[(1 - h) * 128 + row]);
           if (out >= 0) {
             const int e = f16_row_exponent(mx);
@@ -516,6 +640,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
             }
             if (h == 0) epi.split_un[out] = ldexpf(1.f, -e);
           }
+          TC_PROBE(9, warp == EPI_WARP0 && lane == 0 && kk == k_begin)
         }
       } else {
         float4* o4 =
@@ -587,6 +712,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
             for (int kb = 0; kb < NKB; ++kb) {
               c0 = prof ? clock64() : 0;
               mbar_wait(full(s), ph);
+              TC_PROBE(2, lane == 0 && nst == 0)
               if (prof) t_fu += clock64() - c0;
               asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
               const uint64_t so = uint64_t(s) * SD;
@@ -614,6 +740,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
             ++ntaps;
           }
         }
+        TC_PROBE(3, lane == 0)
         if (prof && lane == 0)
           printf("cta %d: total %llu wait_tempty %llu wait_full %llu taps %d stages %d\n", int(blockIdx.x),
                  clock64() - t_all, t_te, t_fu, ntaps, nst);
@@ -716,9 +843,18 @@ __global__ void __maxnreg__(LAUNCH_REGS)
       }
     }
   }
+  TC_PROBE(5, warp == EPI_WARP0 && lane == 0)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   timeline_end(PAIR ? 1 : 2);
+#ifdef KIFMM_TC_PROBE
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("tcprobe pair=%d grid=%d items=%d setup %.2f first_full %.2f last_mma %.2f first_epi %.2f epi_end %.2f | item0: tmem done %.2f loads+dst %.2f xchg %.2f split %.2f us\n",
+           int(PAIR), int(gridDim.x), k_end - k_begin, (probe[1] - probe[0]) * 1e-3, (probe[2] - probe[0]) * 1e-3,
+           (probe[3] - probe[0]) * 1e-3, (probe[4] - probe[0]) * 1e-3, (probe[5] - probe[0]) * 1e-3,
+           (probe[6] - probe[0]) * 1e-3, (probe[7] - probe[0]) * 1e-3, (probe[8] - probe[0]) * 1e-3,
+           (probe[9] - probe[0]) * 1e-3);
+#endif
 #ifdef KIFMM_TIMELINE_PROBES
   if (PAIR && blockIdx.x == 0 && threadIdx.x == 0 && g_timeline_on) {
     g_timeline[9][0] = globaltimer();
