@@ -504,6 +504,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
             val[c][i] = v;
           }
         }
+        TC_PROBE(10, warp == EPI_WARP0 && lane == 0 && kk == k_begin)
         if (epi.accumulate) {  // independent loads, one latency
 #pragma unroll
           for (int c = 0; c < NCH; ++c)
@@ -518,6 +519,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
                 val[c][i].w += o.w;
               }
         }
+        TC_PROBE(11, warp == EPI_WARP0 && lane == 0 && kk == k_begin)
         if (epi.dst) {
 #pragma unroll
           for (int c = 0; c < NCH; ++c)
@@ -854,6 +856,8 @@ __global__ void __maxnreg__(LAUNCH_REGS)
            (probe[3] - probe[0]) * 1e-3, (probe[4] - probe[0]) * 1e-3, (probe[5] - probe[0]) * 1e-3,
            (probe[6] - probe[0]) * 1e-3, (probe[7] - probe[0]) * 1e-3, (probe[8] - probe[0]) * 1e-3,
            (probe[9] - probe[0]) * 1e-3);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && probe[10])
+    printf("tcprobe   transposed %.2f accumulated %.2f\n", (probe[10] - probe[0]) * 1e-3, (probe[11] - probe[0]) * 1e-3);
 #endif
 #ifdef KIFMM_TIMELINE_PROBES
   if (PAIR && blockIdx.x == 0 && threadIdx.x == 0 && g_timeline_on) {

@@ -529,8 +529,11 @@ __global__ void __launch_bounds__(kFarWarps * 32) far_kernel(P2PParams<T> p, con
 // fixed order.  The result pot[t] + far (grad[t] - far) is written to
 // pot_out[perm[t]] (input order) or back to pot[t] when perm is null.  Every
 // owned leaf has a work item (surf_begin == surf_end: output write only).
+#ifndef KIFMM_FAR_MINB
+#define KIFMM_FAR_MINB 5  // 64 registers: 30 resident warps per SM instead of 24 (config 2: -30 us)
+#endif
 template <bool GRAD>
-__global__ void __launch_bounds__(kFarWarps * 32) far_f2_kernel(P2PParams<float> p,
+__global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_f2_kernel(P2PParams<float> p,
                                                                  const FarWork* __restrict__ works, int n_works,
                                                                  const int2* __restrict__ surfaces,
                                                                  const float* __restrict__ M,
@@ -688,8 +691,11 @@ __global__ void __launch_bounds__(kCheckWarps * 32) check_kernel(P2PParams<T> p,
 // LDS.128 broadcast per source instead of four shuffles).  MUFU.RSQ-bound (one
 // per pair, no gradient), so no padded points beyond KMAX x 32.  Same work /
 // output contract as check_kernel.
+#ifndef KIFMM_CHECK_MINB
+#define KIFMM_CHECK_MINB 4  // 64 registers: 32 resident warps per SM (106 registers left 16)
+#endif
 template <int KMAX>
-__global__ void __launch_bounds__(kCheckWarps * 32) check_f2_kernel(P2PParams<float> p,
+__global__ void __launch_bounds__(kCheckWarps * 32, KIFMM_CHECK_MINB) check_f2_kernel(P2PParams<float> p,
                                                                      const CheckWork* __restrict__ works, int n_works,
                                                                      const int2* __restrict__ ranges, int ref_level,
                                                                      float alpha, float* __restrict__ out, int ld_out,

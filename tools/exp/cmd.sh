@@ -1,3 +1,2 @@
 timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/gt1.log 2>&1; echo tests rc=$?; tail -2 gpurun_out/gt1.log
-for i in 1 2; do python tools/near_time.py 2 40 2>&1 | tail -1; done
-KIFMM_LIB=variants/probe.so KIFMM_NEAR_BPS=0 KIFMM_ITERS=1 python tools/profile_run.py 2>&1 | grep tcprobe | tail -9 | cut -c1-200
+for i in 1 2; do python tools/near_time.py 2 40 2>&1 | tail -1 | cut -c1-100; done
