@@ -157,6 +157,14 @@ __device__ __forceinline__ void timeline_end(int id) {
 #endif
 }
 
+// Programmatic dependent launch (kernels launched with cudaLaunchAttributeProgrammaticStreamSerialization):
+// pdl_trigger lets the next kernel of the stream start launching (its CTAs take SMs this grid leaves
+// free and run their set-up); pdl_wait blocks until every prerequisite grid has completed and its
+// memory is visible.  Every kernel launched with the attribute calls pdl_wait before it touches data
+// an earlier kernel writes (or reads: WAR); without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Far-away zero-charge source used to pad staged source rounds (contributes exactly 0).
 constexpr double kFarAway = 1e15;
 

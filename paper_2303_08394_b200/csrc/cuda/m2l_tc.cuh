@@ -402,6 +402,10 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   if (PAIR) cluster_sync();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  // set-up done (barriers, TMEM, tensor-map prefetch): let the next kernel start launching, then wait
+  // for the previous one before reading the schedule's operands
+  if (threadIdx.x == 0) pdl_trigger();
+  pdl_wait();
   TC_PROBE(1, threadIdx.x == 0)
   timeline_begin(PAIR ? 1 : 2);
 #ifdef KIFMM_TIMELINE_PROBES
@@ -926,6 +930,8 @@ __global__ void split_f16_rows_kernel(const float* __restrict__ M, int r0, int r
 // Split the listed rows (warp per row).
 __global__ void split_f16_list_kernel(const float* __restrict__ X, const int* __restrict__ list, int n,
                                       __half* __restrict__ hi, __half* __restrict__ lo, float* __restrict__ un) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= n) return;
   const int row = list[i];
@@ -941,6 +947,8 @@ __global__ void m2l_tc_reduce_split_kernel(const float* __restrict__ partial, co
                                            const int* __restrict__ tile_slot, int rows, float* __restrict__ check,
                                            __half* __restrict__ hi, __half* __restrict__ lo,
                                            float* __restrict__ un) {
+  pdl_trigger();
+  pdl_wait();
   const int tile = blockIdx.x;
   const int r = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -1025,6 +1033,30 @@ inline int sm_count() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+// launch attribute for programmatic dependent launch (KIFMM_PDL=0: ordinary stream order)
+inline cudaLaunchAttribute pdl_attr() {
+  static const int on = [] {
+    const char* e = std::getenv("KIFMM_PDL");
+    return e ? std::atoi(e) : 1;
+  }();
+  cudaLaunchAttribute a{};
+  a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a.val.programmaticStreamSerializationAllowed = on ? 1 : 0;
+  return a;
+}
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1] = {pdl_attr()};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KIFMM_CUDA(cudaLaunchKernelEx(&cfg, k, args...));
 }
 
 inline bool m2l_tc_available() {
@@ -1349,23 +1381,25 @@ struct M2LTcPlan {
     const float ku = ES == 4 ? 1.f : 1.f / kKScale;
     if (P) {
       cudaLaunchConfig_t cfg{};
-      cudaLaunchAttribute attr[1];
+      cudaLaunchAttribute attr[2];
       attr[0].id = cudaLaunchAttributeClusterDimension;
       attr[0].val.clusterDim.x = 2;
       attr[0].val.clusterDim.y = 1;
       attr[0].val.clusterDim.z = 1;
+      attr[1] = pdl_attr();
       cfg.gridDim = dim3(2 * sched_g);
       cfg.blockDim = dim3(tc::THREADS);
       cfg.dynamicSmemBytes = tc::Cfg<P, R, ES>::SMEM_BYTES;
       cfg.stream = s;
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = 2;
       KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<P, R, ES>, mh, ml, ah, al, (const tc::Item*)d_items, (const int*)d_sched,
                                     (const int*)d_seg_mat, (const int*)d_seg_in, int(nn), un, ku,
                                     tc::Epi{d_partial, nullptr, nullptr, nullptr, 0, tc_debug(), nullptr, nullptr, nullptr}));
     } else {
-      tc::m2l_tc_kernel<P, R, ES><<<sched_g, tc::THREADS, tc::Cfg<P, R, ES>::SMEM_BYTES, s>>>(
-          mh, ml, ah, al, d_items, d_sched, d_seg_mat, d_seg_in, int(nn), un, ku, tc::Epi{d_partial, nullptr, nullptr, nullptr, 0, tc_debug(), nullptr, nullptr, nullptr});
+      launch_pdl(tc::m2l_tc_kernel<P, R, ES>, dim3(sched_g), dim3(tc::THREADS), tc::Cfg<P, R, ES>::SMEM_BYTES, s, mh, ml,
+                 ah, al, (const tc::Item*)d_items, (const int*)d_sched, (const int*)d_seg_mat, (const int*)d_seg_in,
+                 int(nn), un, ku, tc::Epi{d_partial, nullptr, nullptr, nullptr, 0, tc_debug(), nullptr, nullptr, nullptr});
     }
     KIFMM_LAUNCH_CHECK();
   }
@@ -1379,9 +1413,9 @@ struct M2LTcPlan {
       run_kernel<true, 64, 2>(s, sp.hi, sp.lo, sp.un);
     else
       run_kernel<false, 64, 2>(s, sp.hi, sp.lo, sp.un);
-    tc::m2l_tc_reduce_split_kernel<<<dim3(n_tiles, (rows + 7) / 8), 256, 0, s>>>(
-        d_partial, d_tile_out, d_tile_slot, rows, check, cd ? cd->hi : nullptr, cd ? cd->lo : nullptr,
-        cd ? cd->un : nullptr);
+    launch_pdl(tc::m2l_tc_reduce_split_kernel, dim3(n_tiles, (rows + 7) / 8), dim3(256), 0, s, (const float*)d_partial,
+               (const int*)d_tile_out, (const int*)d_tile_slot, rows, check, cd ? cd->hi : (__half*)nullptr,
+               cd ? cd->lo : (__half*)nullptr, cd ? cd->un : (float*)nullptr);
     KIFMM_LAUNCH_CHECK();
   }
 
@@ -1499,10 +1533,11 @@ struct TcGemm {
   // output rows is written too (dst may then be null)
   void run(const TcSplit& a, float* dst, bool accumulate, cudaStream_t s, const TcSplit* out_split = nullptr) const {
     if (!n_tiles) return;
-    tc::m2l_tc_kernel<false, 64, 2><<<sched_g, tc::THREADS, tc::Cfg<false, 64, 2>::SMEM_BYTES, s>>>(
-        tm_hi, tm_lo, a.hi, a.lo, d_items, d_sched, d_seg_mat, d_seg_in, a.rows, a.un, 1.f,
-        tc::Epi{nullptr, d_out, d_cu, dst, accumulate ? 1 : 0, 0, out_split ? out_split->hi : nullptr,
-                out_split ? out_split->lo : nullptr, out_split ? out_split->un : nullptr});
+    launch_pdl(tc::m2l_tc_kernel<false, 64, 2>, dim3(sched_g), dim3(tc::THREADS), tc::Cfg<false, 64, 2>::SMEM_BYTES, s,
+               tm_hi, tm_lo, (const void*)a.hi, (const void*)a.lo, (const tc::Item*)d_items, (const int*)d_sched,
+               (const int*)d_seg_mat, (const int*)d_seg_in, a.rows, (const float*)a.un, 1.f,
+               tc::Epi{nullptr, d_out, d_cu, dst, accumulate ? 1 : 0, 0, out_split ? out_split->hi : nullptr,
+                       out_split ? out_split->lo : nullptr, out_split ? out_split->un : nullptr});
     KIFMM_LAUNCH_CHECK();
   }
 };

@@ -284,6 +284,8 @@ __global__ void m2m_reduce_split_kernel(const float* __restrict__ scratch, const
                                         const int* __restrict__ masks, int n, float* __restrict__ M,
                                         __half* __restrict__ hi, __half* __restrict__ lo, float* __restrict__ un) {
   constexpr int W = tc::NP;
+  pdl_trigger();
+  pdl_wait();
   const int s = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (s >= n) return;
   const int mask = masks[s];
@@ -1359,6 +1361,9 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   };
 
   mark();  // 0
+  // zero the down-check rows here, not just before P2L / M2L: a memset between the M2M and M2L kernels
+  // would break their programmatic (PDL) launch edge
+  KIFMM_CUDA(cudaMemsetAsync(check_dn.p, 0, check_dn.bytes, s));
   pack_sources_kernel<T><<<int(ceil_div(N, 256)), 256, 0, s>>>(pos4.as<v4_t<T>>(), q_in.as<T>(),
                                                                input_order ? perm.as<int>() : nullptr, int(N),
                                                                src4.as<v4_t<T>>());
@@ -1451,8 +1456,9 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     if (gemm_tc) {
       if constexpr (sizeof(T) == 4) {
         tgemm(lv.tc, sp_M, m2m_scratch.as<T>(), false, nullptr);
-        m2m_reduce_split_kernel<<<unsigned((lv.n + 7) / 8), 256, 0, s>>>(
-            m2m_scratch.as<float>(), lv.parents.as<int>(), lv.masks.as<int>(), lv.n, Mp, sp_M.hi, sp_M.lo, sp_M.un);
+        launch_pdl(m2m_reduce_split_kernel, dim3(unsigned((lv.n + 7) / 8)), dim3(256), 0, s,
+                   (const float*)m2m_scratch.as<float>(), (const int*)lv.parents.as<int>(),
+                   (const int*)lv.masks.as<int>(), lv.n, Mp, sp_M.hi, sp_M.lo, sp_M.un);
       }
     } else {
       gemm(lv.tiles, Mp, w_m2m.as<T>(), m2m_scratch.as<T>(), false, true);
@@ -1477,8 +1483,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     for (auto& lv : m2m_top) m2m_level(*lv);
   }
   mark();  // 3
-  // downward: P2L check into the down-check buffer
-  KIFMM_CUDA(cudaMemsetAsync(check_dn.p, 0, check_dn.bytes, s));
+  // downward: P2L check into the down-check buffer (zeroed at the start of the evaluate)
   if (n_p2l) {
     launch_check<T>(np, n_p2l, pp, p2l_works.as<CheckWork>(), p2l_ranges.as<int2>(), node_level.as<int>(),
                     ref_level, T(alpha_in), check_dn.as<T>(), s);
