@@ -364,6 +364,13 @@ def main():
     p2p = {"achieved_tflops": p2p_pairs * pair_flops / (ph["leaf_ms"] * 1e-3) / 1e12 if ph["leaf_ms"] else None,
            "peak_tflops": fp32_peak, "pairs": p2p_pairs, "flop_per_pair": pair_flops, "leaf_ms": ph["leaf_ms"]}
     p2p["frac"] = p2p["achieved_tflops"] / fp32_peak if p2p["achieved_tflops"] else None
+    # nominal: SMs x 128 FP32 lanes (64 FP64) x 2 flop x max SM clock; the FFMA probe above
+    # runs at whatever clock the power cap allows at that moment
+    nominal = torch.cuda.get_device_properties(local).multi_processor_count * (128 if prec == 32 else 64) * 2 * \
+        (clk.summary().get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
+    p2p["peak_nominal_tflops"] = nominal
+    p2p["frac_nominal"] = p2p["achieved_tflops"] / nominal if p2p["achieved_tflops"] else None
+    p2p["span"] = "near field (self + U list) and far field (L2P + M2P) kernels of the serialized timed run"
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
