@@ -42,6 +42,8 @@
 #include <cstring>
 #include <map>
 #include <queue>
+#include <set>
+#include <array>
 #include <string>
 #include <vector>
 
@@ -1162,6 +1164,60 @@ struct M2LTcPlan {
     if (r != CUDA_SUCCESS) throw DeviceError(KIFMM_E_CUDA, "cuTensorMapEncodeTiled failed");
   }
 
+  // Tile-aligned sub-groups of one large (level, octant) group.  Its targets fall into tap-set classes:
+  // interior (all transfer vectors of the octant), and boundary classes whose parents touch domain
+  // faces, edges, corners -- each a subset of the interior set.  A tile pays for the union of its rows'
+  // taps, so a tile straddling two face classes pays for most of the interior set on every row.  Here:
+  // whole tiles of interior rows; then each boundary class (largest first) with the unplaced classes
+  // that are subsets of it and still fit in its last tile; then the interior tail; then what is left.
+  // Config 2, level 5: 6.06 M -> 5.75 M computed pair slots (5.40 M real).
+  template <class TreeView>
+  void split_by_face(const TreeView& t, const std::vector<int64_t>& grp, std::vector<std::vector<int64_t>>& out) {
+    constexpr int NW = (316 + 63) / 64;
+    using Sig = std::array<uint64_t, NW>;
+    std::map<Sig, std::vector<int64_t>> bys;
+    for (int64_t b : grp) {
+      Sig sg{};
+      for (int64_t e = t.v_ptr[b]; e < t.v_ptr[b + 1]; ++e) sg[t.v_tv[e] >> 6] |= uint64_t(1) << (t.v_tv[e] & 63);
+      bys[sg].push_back(b);
+    }
+    auto pop = [](const Sig& x) {
+      int c = 0;
+      for (uint64_t w : x) c += __builtin_popcountll(w);
+      return c;
+    };
+    std::vector<const Sig*> sets;
+    for (auto& kv : bys) sets.push_back(&kv.first);
+    std::stable_sort(sets.begin(), sets.end(), [&](const Sig* a, const Sig* b) { return pop(*a) > pop(*b); });
+    auto subset = [](const Sig& a, const Sig& b) {  // a within b
+      for (int w = 0; w < NW; ++w)
+        if (a[w] & ~b[w]) return false;
+      return true;
+    };
+    std::set<const Sig*> placed{sets[0]};
+    const std::vector<int64_t>& inter = bys[*sets[0]];
+    const size_t full = inter.size() / size_t(rows) * size_t(rows);
+    if (full) out.emplace_back(inter.begin(), inter.begin() + full);
+    for (size_t i = 1; i < sets.size(); ++i) {
+      if (placed.count(sets[i])) continue;
+      placed.insert(sets[i]);
+      std::vector<int64_t> ch = bys[*sets[i]];
+      for (size_t j = 1; j < sets.size(); ++j) {
+        if (placed.count(sets[j]) || !subset(*sets[j], *sets[i])) continue;
+        const size_t cap = (ch.size() + size_t(rows) - 1) / size_t(rows) * size_t(rows);
+        if (ch.size() + bys[*sets[j]].size() > cap) continue;
+        placed.insert(sets[j]);
+        ch.insert(ch.end(), bys[*sets[j]].begin(), bys[*sets[j]].end());
+      }
+      out.push_back(std::move(ch));
+    }
+    if (full < inter.size()) out.emplace_back(inter.begin() + full, inter.end());
+    std::vector<int64_t> left;
+    for (const Sig* sg : sets)
+      if (!placed.count(sg)) left.insert(left.end(), bys[*sg].begin(), bys[*sg].end());
+    if (!left.empty()) out.push_back(std::move(left));
+  }
+
   template <class TreeView, class OpsView>
   void build(const TreeView& t, const std::vector<std::vector<int64_t>>& groups, int np, const OpsView& ops,
              size_t* total) {
@@ -1177,6 +1233,8 @@ struct M2LTcPlan {
     // (nearly) all of its rows: boundary targets no longer pad interior tiles with zero rows.
     bool by_sig = true;
     if (const char* e = std::getenv("KIFMM_TC_SIG")) by_sig = std::atoi(e) != 0;
+    bool by_face = true;  // KIFMM_TC_FACE=0: large groups as one sorted run (tiles straddle tap sets)
+    if (const char* e = std::getenv("KIFMM_TC_FACE")) by_face = std::atoi(e) != 0;
     std::vector<std::vector<int64_t>> sorted_groups;
     for (const auto& g0 : groups) {
       std::vector<int64_t> grp(g0.begin(), g0.end());
@@ -1194,6 +1252,10 @@ struct M2LTcPlan {
         std::stable_sort(key.begin(), key.end(),
                          [](const auto& x, const auto& y) { return x.first < y.first; });
         for (size_t i = 0; i < grp.size(); ++i) grp[i] = key[i].second;
+      }
+      if (by_face && int64_t(grp.size()) >= 8 * int64_t(rows)) {
+        split_by_face(t, grp, sorted_groups);
+        continue;
       }
       sorted_groups.push_back(std::move(grp));
     }
