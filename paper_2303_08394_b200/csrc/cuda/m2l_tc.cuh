@@ -1171,21 +1171,45 @@ struct M2LTcPlan {
   // whole tiles of interior rows; then each boundary class (largest first) with the unplaced classes
   // that are subsets of it and still fit in its last tile; then the interior tail; then what is left.
   // Config 2, level 5: 6.06 M -> 5.75 M computed pair slots (5.40 M real).
+  // Applied only where it pays: at most 64 distinct tap sets (uniform regions; adaptive trees have
+  // thousands, and per-class tiles would multiply the padding -- config 5 M2L 18 -> 207 ms), and only
+  // when the computed slots (sum over tiles of rows x |union of taps|) drop.
   template <class TreeView>
   void split_by_face(const TreeView& t, const std::vector<int64_t>& grp, std::vector<std::vector<int64_t>>& out) {
     constexpr int NW = (316 + 63) / 64;
     using Sig = std::array<uint64_t, NW>;
-    std::map<Sig, std::vector<int64_t>> bys;
-    for (int64_t b : grp) {
+    auto sig_of = [&](int64_t b) {
       Sig sg{};
       for (int64_t e = t.v_ptr[b]; e < t.v_ptr[b + 1]; ++e) sg[t.v_tv[e] >> 6] |= uint64_t(1) << (t.v_tv[e] & 63);
-      bys[sg].push_back(b);
-    }
+      return sg;
+    };
     auto pop = [](const Sig& x) {
       int c = 0;
       for (uint64_t w : x) c += __builtin_popcountll(w);
       return c;
     };
+    auto slots_of = [&](const std::vector<std::vector<int64_t>>& gs) {
+      int64_t tot = 0;
+      for (const auto& g : gs)
+        for (size_t s0 = 0; s0 < g.size(); s0 += size_t(rows)) {
+          Sig u{};
+          for (size_t r = s0; r < std::min(g.size(), s0 + size_t(rows)); ++r) {
+            const Sig x = sig_of(g[r]);
+            for (int w = 0; w < NW; ++w) u[w] |= x[w];
+          }
+          tot += int64_t(rows) * pop(u);
+        }
+      return tot;
+    };
+    std::map<Sig, std::vector<int64_t>> bys;
+    for (int64_t b : grp) {
+      bys[sig_of(b)].push_back(b);
+      if (bys.size() > 64) {
+        out.push_back(grp);
+        return;
+      }
+    }
+    std::vector<std::vector<int64_t>> cand;
     std::vector<const Sig*> sets;
     for (auto& kv : bys) sets.push_back(&kv.first);
     std::stable_sort(sets.begin(), sets.end(), [&](const Sig* a, const Sig* b) { return pop(*a) > pop(*b); });
@@ -1197,7 +1221,7 @@ struct M2LTcPlan {
     std::set<const Sig*> placed{sets[0]};
     const std::vector<int64_t>& inter = bys[*sets[0]];
     const size_t full = inter.size() / size_t(rows) * size_t(rows);
-    if (full) out.emplace_back(inter.begin(), inter.begin() + full);
+    if (full) cand.emplace_back(inter.begin(), inter.begin() + full);
     for (size_t i = 1; i < sets.size(); ++i) {
       if (placed.count(sets[i])) continue;
       placed.insert(sets[i]);
@@ -1209,13 +1233,17 @@ struct M2LTcPlan {
         placed.insert(sets[j]);
         ch.insert(ch.end(), bys[*sets[j]].begin(), bys[*sets[j]].end());
       }
-      out.push_back(std::move(ch));
+      cand.push_back(std::move(ch));
     }
-    if (full < inter.size()) out.emplace_back(inter.begin() + full, inter.end());
+    if (full < inter.size()) cand.emplace_back(inter.begin() + full, inter.end());
     std::vector<int64_t> left;
     for (const Sig* sg : sets)
       if (!placed.count(sg)) left.insert(left.end(), bys[*sg].begin(), bys[*sg].end());
-    if (!left.empty()) out.push_back(std::move(left));
+    if (!left.empty()) cand.push_back(std::move(left));
+    if (slots_of(cand) < slots_of({grp}))
+      for (auto& g : cand) out.push_back(std::move(g));
+    else
+      out.push_back(grp);
   }
 
   template <class TreeView, class OpsView>
