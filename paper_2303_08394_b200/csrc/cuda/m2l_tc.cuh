@@ -1561,7 +1561,8 @@ struct TcGemm {
 
   // tiles: out (128 rows, -1 pad) + segs (matrix, 128 input rows or -1)
   template <class Tile>
-  void build(const std::vector<Tile>& tiles, const std::vector<double>& B, int n_mats, size_t* total) {
+  void build(const std::vector<Tile>& tiles, const std::vector<double>& B, int n_mats, size_t* total,
+             int max_ctas = 0) {
     constexpr int NP = tc::NP;
     if (B.size() != size_t(n_mats) * NP * NP) throw InvalidArgument("TcGemm: B size");
     std::vector<int> out, seg_mat, seg_in;
@@ -1581,7 +1582,7 @@ struct TcGemm {
     M2LTcPlan::up(&d_seg_mat, seg_mat, total);
     M2LTcPlan::up(&d_seg_in, seg_in, total);
     M2LTcPlan::up(&d_items, items, total);
-    sched_g = std::max(1, std::min(n_tiles, sm_count()));
+    sched_g = std::max(1, std::min(n_tiles, max_ctas > 0 ? max_ctas : sm_count()));
     M2LTcPlan::up(&d_sched, lpt_schedule(items, sched_g), total);
     std::vector<float> cu(NP, 1.f);
     std::vector<__half> hi(B.size()), lo(B.size());
@@ -1621,6 +1622,11 @@ struct TcGemm {
 
   // dst[out rows] (=, or += when accumulate) A(split rows) . B^T; with out_split, the fp16 split of the
   // output rows is written too (dst may then be null)
+  // fewest persistent CTAs with the same makespan (whole tiles per CTA): frees SMs for a concurrent chain
+  static int min_ctas(int tiles) {
+    const int per = (tiles + sm_count() - 1) / sm_count();
+    return (tiles + per - 1) / per;
+  }
   void run(const TcSplit& a, float* dst, bool accumulate, cudaStream_t s, const TcSplit* out_split = nullptr) const {
     if (!n_tiles) return;
     launch_pdl(tc::m2l_tc_kernel<false, 64, 2>, dim3(sched_g), dim3(tc::THREADS), tc::Cfg<false, 64, 2>::SMEM_BYTES, s,

@@ -396,6 +396,15 @@ struct kifmm_gpu_plan {
   bool gemm_tc = false;
   TcSplit sp_cu, sp_tmp, sp_M, sp_cd, sp_L;
   TcGemm tg_up1, tg_up2, tg_dn1, tg_dn2;
+  // split downward chain (tcgen05 path): second solve GEMM for the levels above the deepest one, then the
+  // L2L chain into those levels on side2, concurrent with the deepest level's second solve on the plan
+  // stream (run on the fewest CTAs with the same makespan, leaving SMs to the chain); joined before the
+  // last L2L level.  KIFMM_DN_SPLIT=0: one second-solve GEMM, then the L2L levels in order.
+  bool dn_split = false;
+  int dn_split_level = 0;  // child level of the last L2L level (the deepest)
+  TcGemm tg_dn2_up, tg_dn2_lo;
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t ev_dn_fork = nullptr, ev_dn_join = nullptr;
   DevMem dn_extra;  // down-check rows with P2L but no M2L (split after M2L)
   int n_dn_extra = 0;
   DevMem m2m_scratch;
@@ -424,6 +433,9 @@ struct kifmm_gpu_plan {
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
+    if (side2) cudaStreamDestroy(side2);
+    if (ev_dn_fork) cudaEventDestroy(ev_dn_fork);
+    if (ev_dn_join) cudaEventDestroy(ev_dn_join);
     if (pipe) {
       if (pipe->cin) cudaStreamDestroy(pipe->cin);
       if (pipe->cout) cudaStreamDestroy(pipe->cout);
@@ -580,6 +592,9 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     KIFMM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     KIFMM_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, hi));
     KIFMM_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+    KIFMM_CUDA(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, hi));
+    KIFMM_CUDA(cudaEventCreateWithFlags(&ev_dn_fork, cudaEventDisableTiming));
+    KIFMM_CUDA(cudaEventCreateWithFlags(&ev_dn_join, cudaEventDisableTiming));
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   }
@@ -993,7 +1008,33 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       std::vector<double> b1, b2;
       factored_b(ops.dc2e_u, ops.dc2e_s, ops.dc2e_v, ops.dc2e_rank, b1, b2);
       tg_dn1.build(a, b1, 1, &dev_bytes);
-      tg_dn2.build(b, b2, 1, &dev_bytes);
+      // rows of the deepest level start at dn_nodes[k] (level-major order); tiles of the second solve are
+      // cut there so the upper levels' rows finish first
+      size_t k = 0;
+      while (k < dn_nodes.size() && node_lvl(dn_nodes[k]) < depth) ++k;
+      dn_split = depth >= 4 && k > 0 && k < dn_nodes.size();
+      if (const char* e = std::getenv("KIFMM_DN_SPLIT")) dn_split = dn_split && std::atoi(e) != 0;
+      if (dn_split) {
+        dn_split_level = depth;
+        std::vector<TileSpec> bu, bl;
+        for (size_t s0 = 0; s0 < dn_nodes.size();) {
+          const size_t e0 = std::min(dn_nodes.size(), s0 < k ? std::min(k, s0 + ld_tiles) : s0 + ld_tiles);
+          TileSpec y;
+          std::vector<int> slots(ld_tiles, -1), nodes(ld_tiles, -1);
+          for (size_t r = s0; r < e0; ++r) {
+            slots[r - s0] = int(r);
+            nodes[r - s0] = int(dn_nodes[r]);
+          }
+          y.out = nodes;
+          y.segs.push_back({0, slots});
+          (s0 < k ? bu : bl).push_back(std::move(y));
+          s0 = e0;
+        }
+        tg_dn2_up.build(bu, b2, 1, &dev_bytes);
+        tg_dn2_lo.build(bl, b2, 1, &dev_bytes, TcGemm::min_ctas(int(bl.size())));
+      } else {
+        tg_dn2.build(b, b2, 1, &dev_bytes);
+      }
     } else {
       solve_dn1.build(a, ld_tiles, &dev_bytes);
       solve_dn2.build(b, ld_tiles, &dev_bytes);
@@ -1536,22 +1577,46 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
                                cudaMemcpyDeviceToDevice, s));
   mark();  // 5
   // factored downward solve (dc2e at the reference level; M2L/P2L level factors folded)
-  if (gemm_tc) {
-    tgemm(tg_dn1, sp_cd, nullptr, false, &sp_tmp);
-    tgemm(tg_dn2, sp_tmp, Lp, false, &sp_L);
-  } else {
-    gemm(solve_dn1, check_dn.as<T>(), w_us_d.as<T>(), tmp.as<T>(), false, true);
-    gemm(solve_dn2, tmp.as<T>(), w_vt_d.as<T>(), Lp, false, true);
+  bool l2l_done = false;
+  if (gemm_tc && dn_split) {
+    if constexpr (sizeof(T) == 4) {
+      tgemm(tg_dn1, sp_cd, nullptr, false, &sp_tmp);
+      tgemm(tg_dn2_up, sp_tmp, Lp, false, &sp_L);
+      // L2L into the upper levels on side2, next to the deepest level's second solve
+      KIFMM_CUDA(cudaEventRecord(ev_dn_fork, s));
+      KIFMM_CUDA(cudaStreamWaitEvent(side2, ev_dn_fork, 0));
+      const size_t nl2l = l2l_levels.size();
+      for (size_t i = 0; i + 1 < nl2l; ++i) {
+        l2l_levels[i]->tc.run(sp_L, Lp, true, side2, &sp_L);
+        ++launches;
+      }
+      KIFMM_CUDA(cudaEventRecord(ev_dn_join, side2));
+      tgemm(tg_dn2_lo, sp_tmp, Lp, false, &sp_L);
+      mark();  // 6
+      KIFMM_CUDA(cudaStreamWaitEvent(s, ev_dn_join, 0));
+      if (nl2l) tgemm(l2l_levels[nl2l - 1]->tc, sp_L, Lp, true, &sp_L);
+      mark();  // 7
+      l2l_done = true;
+    }
   }
-  mark();  // 6
-  // L2L top-down
-  for (auto& lv : l2l_levels) {
-    if (gemm_tc)
-      tgemm(lv->tc, sp_L, Lp, true, &sp_L);  // reads parent rows (level l), writes child rows (l + 1)
-    else
-      gemm(lv->tiles, Lp, w_l2l.as<T>(), Lp, true, true);
+  if (!l2l_done) {
+    if (gemm_tc) {
+      tgemm(tg_dn1, sp_cd, nullptr, false, &sp_tmp);
+      tgemm(tg_dn2, sp_tmp, Lp, false, &sp_L);
+    } else {
+      gemm(solve_dn1, check_dn.as<T>(), w_us_d.as<T>(), tmp.as<T>(), false, true);
+      gemm(solve_dn2, tmp.as<T>(), w_vt_d.as<T>(), Lp, false, true);
+    }
+    mark();  // 6
+    // L2L top-down
+    for (auto& lv : l2l_levels) {
+      if (gemm_tc)
+        tgemm(lv->tc, sp_L, Lp, true, &sp_L);  // reads parent rows (level l), writes child rows (l + 1)
+      else
+        gemm(lv->tiles, Lp, w_l2l.as<T>(), Lp, true, true);
+    }
+    mark();  // 7
   }
-  mark();  // 7
   // leaves: near field (side stream, or here when timed) then L2P + M2P
   if (timed && !corun) leaf(leaf_near, false, s);
   if (queue_mode && near_debug && !std::getenv("KIFMM_NEAR_DEBUG_M2L"))  // experiments: works taken by now
