@@ -1038,11 +1038,9 @@ inline int sm_count() {
 }
 
 // launch attribute for programmatic dependent launch (KIFMM_PDL=0: ordinary stream order)
-inline cudaLaunchAttribute pdl_attr() {
-  static const int on = [] {
-    const char* e = std::getenv("KIFMM_PDL");
-    return e ? std::atoi(e) : 1;
-  }();
+inline cudaLaunchAttribute pdl_attr() {  // read per launch (a captured graph keeps the choice of its capture)
+  const char* env = std::getenv("KIFMM_PDL");
+  const int on = env ? std::atoi(env) : 1;
   cudaLaunchAttribute a{};
   a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
   a.val.programmaticStreamSerializationAllowed = on ? 1 : 0;

@@ -293,3 +293,23 @@ def test_fp64_dmma_gemm_matches_simt(require_gpu, monkeypatch, p):
     assert fmm.relative_error(out["1"][0], out["0"][0]) <= 1e-13
     assert fmm.relative_error(out["1"][0], ref) <= 1e-12
     assert fmm.relative_error(out["1"][1], gref) <= 1e-11
+
+
+def test_schedule_switches_bit_identical(require_gpu, monkeypatch):
+    """Scheduling-only switches change no arithmetic: the split downward chain (KIFMM_DN_SPLIT) and
+    programmatic dependent launch (KIFMM_PDL) give bit-identical results; the tap-set face split of the
+    M2L tiles (KIFMM_TC_FACE) regroups rows into tiles and stays within fp32 rounding."""
+    pos, q = generators.sample("uniform-cube", 200000, seed=13, charges="signed", fp32=True)
+    cfg = fmm.FmmConfig(p=6, n_crit=40, precision=32, gradient=True)
+    out = {}
+    for name, env in [("ref", {}), ("nosplit", {"KIFMM_DN_SPLIT": "0"}), ("nopdl", {"KIFMM_PDL": "0"}),
+                      ("noface", {"KIFMM_TC_FACE": "0"})]:
+        for k in ("KIFMM_DN_SPLIT", "KIFMM_PDL", "KIFMM_TC_FACE"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with fmm.Fmm(pos, cfg) as f:
+            out[name] = f.evaluate(q)[:2]
+    for name in ("nosplit", "nopdl"):
+        assert np.array_equal(out[name][0], out["ref"][0]) and np.array_equal(out[name][1], out["ref"][1]), name
+    assert fmm.relative_error(out["noface"][0], out["ref"][0]) <= 1e-6
