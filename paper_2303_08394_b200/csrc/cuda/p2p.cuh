@@ -623,6 +623,81 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_f2_kernel(
   }
 }
 
+// Far field with one HALF-warp per work (plans whose works carry at most one surface, i.e. L2P only:
+// uniform trees).  far_f2_kernel gives a work the whole warp as 16 target pairs x 2 source slices, so
+// every warp pays its start-up loads and a shuffle reduction for 76 sources per lane; here lanes 0-15
+// and 16-31 take two consecutive works, each lane owns targets (hl, hl + 16) of its work and runs all
+// n_e sources, with no reduction.  The halves stage their surfaces in shared-memory slots 64 bytes
+// apart modulo 128, so the two broadcast addresses of an LDS.128 fall on different banks.
+constexpr int kFarHwSlot = 164;  // float4 per half-warp slot: >= n_e padded to 4 (p <= 6), 2624 B = 64 mod 128
+template <bool GRAD>
+__global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_hw_kernel(
+    P2PParams<float> p, const FarWork* __restrict__ works, int n_works, const float* __restrict__ M,
+    const float* __restrict__ L, float* pot, float* grad, const int* __restrict__ perm, float* pot_out,
+    float* grad_out) {
+  __shared__ float4 sh[kFarWarps][2][kFarHwSlot];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+  const int wi = (blockIdx.x * kFarWarps + warp) * 2 + half;
+  timeline_begin(5);
+  if ((blockIdx.x * kFarWarps + warp) * 2 >= n_works) return;  // whole warp idle
+  const bool valid = wi < n_works;
+  FarWork w{};
+  if (valid) w = works[wi];
+  const int t0 = w.t0, nt = valid ? w.count : 0;
+  const int ta = hl, tb = hl + 16;
+  const bool has_a = ta < nt, has_b = tb < nt;
+  const float4 xa = p.src[t0 + (has_a ? ta : 0)], xb = p.src[t0 + (has_b ? tb : 0)];
+  // the near-field result and the output permutation, prefetched
+  float pv[2] = {0.f, 0.f}, gv[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+  int ov[2] = {0, 0};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = t0 + (h ? tb : ta);
+    if (h ? has_b : has_a) {
+      pv[h] = pot[t];
+      if (GRAD)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) gv[h][d] = grad[3 * size_t(t) + d];
+      ov[h] = perm ? perm[t] : t;
+    }
+  }
+  const f2_t x = f2_pair(xa.x, xb.x), y = f2_pair(xa.y, xb.y), z = f2_pair(xa.z, xb.z);
+  f2_t ph = 0, gx = 0, gy = 0, gz = 0;
+  const bool has_surf = valid && w.surf_end > w.surf_begin;
+  const int pad = (p.n_e + 3) & ~3;
+  float4* my = sh[warp][half];
+  {
+    const float fa = float(kFarAway);
+    const bool l2p = w.kind0 == kSrcL2P;
+    const float alpha = l2p ? p.alpha_outer : p.alpha_inner;
+    const float* dens = l2p ? L : M;
+    for (int j = hl; j < pad; j += 16)
+      my[j] = (has_surf && j < p.n_e) ? surface_source(p, w.node0, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
+  }
+  __syncwarp();
+  p2p_round_f2<GRAD, false>(my, 0, pad, x, y, z, ph, gx, gy, gz);
+  timeline_end(5);
+  float v[8];
+  f2_unpack(ph, v[0], v[4]);
+  f2_unpack(gx, v[1], v[5]);
+  f2_unpack(gy, v[2], v[6]);
+  f2_unpack(gz, v[3], v[7]);
+  const float c = float(kInv4PiD);
+  float* po = perm ? pot_out : pot;
+  float* go = perm ? grad_out : grad;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (!(h ? has_b : has_a)) continue;
+    const int o = ov[h];
+    po[o] = pv[h] + c * v[4 * h];
+    if (GRAD) {
+      go[3 * size_t(o)] = gv[h][0] - c * v[4 * h + 1];
+      go[3 * size_t(o) + 1] = gv[h][1] - c * v[4 * h + 2];
+      go[3 * size_t(o) + 2] = gv[h][2] - c * v[4 * h + 3];
+    }
+  }
+}
+
 // Check potentials on a node's surface (alpha) from particle ranges: one warp
 // per work item, lane l owns check points l, l+32, ... (KMAX x 32 >= n_c); each
 // lane loads one source and the warp broadcasts it with shuffles.

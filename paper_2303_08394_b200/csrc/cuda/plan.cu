@@ -388,6 +388,7 @@ struct kifmm_gpu_plan {
   LeafPlan leaf_near, leaf_far;
   DevMem far_works, far_surfaces, leaf_ptr_dev;  // far_works: int4 (scalar kernel) or FarWork (packed)
   int n_far = 0;
+  bool far_hw = false;  // half-warp far kernel (every work has at most one surface; KIFMM_FAR_HW=0: off)
   int n_p2m = 0, n_p2l = 0;
   GemmTiles solve_up1, solve_up2, solve_dn1, solve_dn2, m2l;
   std::vector<std::unique_ptr<M2MLevel>> m2m_levels, m2m_top;
@@ -1275,6 +1276,9 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       }
     }
     n_far = int(packed ? fw2.size() : fw.size());
+    far_hw = packed && ne <= 4 * (kFarHwSlot / 4) &&
+             std::all_of(fw2.begin(), fw2.end(), [](const FarWork& x) { return x.surf_end - x.surf_begin <= 1; });
+    if (const char* e = std::getenv("KIFMM_FAR_HW")) far_hw = far_hw && std::atoi(e) != 0;
     if (packed)
       far_works.upload(fw2, &dev_bytes);
     else
@@ -1638,7 +1642,14 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
       float* g = grad ? grad_buf.as<float>() : nullptr;
       const int* pm = input_order ? perm.as<int>() : nullptr;
       float* go = grad ? grad_out.as<float>() : nullptr;
-      if (grad)
+      const int hw_blocks = int(ceil_div(n_far, 2 * kFarWarps));
+      if (far_hw && grad)
+        far_hw_kernel<true><<<hw_blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far, Mp, Lp,
+                                                                 pot.as<float>(), g, pm, pot_out.as<float>(), go);
+      else if (far_hw)
+        far_hw_kernel<false><<<hw_blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far, Mp, Lp,
+                                                                  pot.as<float>(), g, pm, pot_out.as<float>(), go);
+      else if (grad)
         far_f2_kernel<true><<<blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far, far_surfaces.as<int2>(),
                                                               Mp, Lp, pot.as<float>(), g, pm, pot_out.as<float>(), go);
       else
