@@ -39,9 +39,6 @@ struct NearSmem {
   unsigned long long full[kNearStages], empty[kNearStages];
 };
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
 __device__ __forceinline__ void near_consumer_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 #ifndef KIFMM_NEAR_WS_MINB
