@@ -225,8 +225,11 @@ __device__ __forceinline__ void wait_parity(uint32_t bar, uint32_t parity) {
 // side launch (DRAIN = false: a few resident blocks per SM next to the tensor-core tree passes) stops
 // taking works once the drain launch (a full-size grid after L2L) has raised queue[1], so the tail runs
 // at full occupancy.  Every work is computed by exactly one block: results do not depend on the split.
+#ifndef KIFMM_NEAR_MINB
+#define KIFMM_NEAR_MINB 9  // 56 registers: 9 blocks per SM (standalone near 1.5 % faster than 8 at 64)
+#endif
 template <bool GRAD, bool ACC, bool QUEUE = false, bool DRAIN = false>
-__global__ void __launch_bounds__(kP2PThreads, 8) leaf_eval_f2_kernel(P2PParams<float> p,
+__global__ void __launch_bounds__(kP2PThreads, KIFMM_NEAR_MINB) leaf_eval_f2_kernel(P2PParams<float> p,
                                                                        const LeafWork* __restrict__ works,
                                                                        const int4* __restrict__ rounds,
                                                                        const int4* __restrict__ items,
