@@ -633,8 +633,11 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_f2_kernel(
 // n_e sources, with no reduction.  The halves stage their surfaces in shared-memory slots 64 bytes
 // apart modulo 128, so the two broadcast addresses of an LDS.128 fall on different banks.
 constexpr int kFarHwSlot = 164;  // float4 per half-warp slot: >= n_e padded to 4 (p <= 6), 2624 B = 64 mod 128
+#ifndef KIFMM_FARHW_MINB
+#define KIFMM_FARHW_MINB KIFMM_FAR_MINB
+#endif
 template <bool GRAD>
-__global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_hw_kernel(
+__global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kernel(
     P2PParams<float> p, const FarWork* __restrict__ works, int n_works, const float* __restrict__ M,
     const float* __restrict__ L, float* pot, float* grad, const int* __restrict__ perm, float* pot_out,
     float* grad_out) {

@@ -1,3 +1,1 @@
-for v in base n9 n10 base n9 n10; do KIFMM_NEAR_BPS=0 KIFMM_LIB=variants/$v.so python tools/near_time.py 2 10 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['lib'], d['leaf_ms'])"; done
-KIFMM_NEAR_BPS=0 KIFMM_ITERS=1 KIFMM_LIB=variants/n9.so timeout 600 ncu --metrics gpu__time_duration.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active -k regex:leaf_eval_f2 -c 1 python tools/profile_run.py 2>&1 | grep -E "duration|fma" 
-KIFMM_NEAR_BPS=0 KIFMM_ITERS=1 KIFMM_LIB=variants/n10.so timeout 600 ncu --metrics gpu__time_duration.sum,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active -k regex:leaf_eval_f2 -c 1 python tools/profile_run.py 2>&1 | grep -E "duration|fma"
+for v in base fh6 fh7 base fh6 fh7; do KIFMM_LIB=variants/$v.so python tools/near_time.py 2 40 2>&1 | tail -1 | cut -c1-100; done
