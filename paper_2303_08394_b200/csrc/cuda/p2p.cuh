@@ -626,8 +626,7 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_f2_kernel(
   }
 }
 
-// Far field with one HALF-warp per work (plans whose works carry at most one surface, i.e. L2P only:
-// uniform trees).  far_f2_kernel gives a work the whole warp as 16 target pairs x 2 source slices, so
+// Far field with one HALF-warp per work.  far_f2_kernel gives a work the whole warp as 16 target pairs x 2 source slices, so
 // every warp pays its start-up loads and a shuffle reduction for 76 sources per lane; here lanes 0-15
 // and 16-31 take two consecutive works, each lane owns targets (hl, hl + 16) of its work and runs all
 // n_e sources, with no reduction.  The halves stage their surfaces in shared-memory slots 64 bytes
@@ -638,9 +637,9 @@ constexpr int kFarHwSlot = 164;  // float4 per half-warp slot: >= n_e padded to 
 #endif
 template <bool GRAD>
 __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kernel(
-    P2PParams<float> p, const FarWork* __restrict__ works, int n_works, const float* __restrict__ M,
-    const float* __restrict__ L, float* pot, float* grad, const int* __restrict__ perm, float* pot_out,
-    float* grad_out) {
+    P2PParams<float> p, const FarWork* __restrict__ works, int n_works, const int2* __restrict__ surfaces,
+    const float* __restrict__ M, const float* __restrict__ L, float* pot, float* grad, const int* __restrict__ perm,
+    float* pot_out, float* grad_out) {
   __shared__ float4 sh[kFarWarps][2][kFarHwSlot];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
   const int wi = (blockIdx.x * kFarWarps + warp) * 2 + half;
@@ -669,19 +668,24 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
   }
   const f2_t x = f2_pair(xa.x, xb.x), y = f2_pair(xa.y, xb.y), z = f2_pair(xa.z, xb.z);
   f2_t ph = 0, gx = 0, gy = 0, gz = 0;
-  const bool has_surf = valid && w.surf_end > w.surf_begin;
+  // surfaces of this half's work; the halves loop to the longer list (works are paired by surface count
+  // on the host, so the shorter one idles rarely)
+  const int ns = valid ? w.surf_end - w.surf_begin : 0;
+  const int ns_max = max(ns, __shfl_xor_sync(0xffffffffu, ns, 16));
   const int pad = (p.n_e + 3) & ~3;
   float4* my = sh[warp][half];
-  {
-    const float fa = float(kFarAway);
-    const bool l2p = w.kind0 == kSrcL2P;
+  const float fa = float(kFarAway);
+  for (int k = 0; k < ns_max; ++k) {
+    const int2 sf = k == 0 ? make_int2(w.node0, w.kind0) : k < ns ? surfaces[w.surf_begin + k] : make_int2(0, 0);
+    const bool l2p = sf.y == kSrcL2P;
     const float alpha = l2p ? p.alpha_outer : p.alpha_inner;
     const float* dens = l2p ? L : M;
+    __syncwarp();
     for (int j = hl; j < pad; j += 16)
-      my[j] = (has_surf && j < p.n_e) ? surface_source(p, w.node0, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
+      my[j] = (k < ns && j < p.n_e) ? surface_source(p, sf.x, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
+    __syncwarp();
+    p2p_round_f2<GRAD, false>(my, 0, pad, x, y, z, ph, gx, gy, gz);
   }
-  __syncwarp();
-  p2p_round_f2<GRAD, false>(my, 0, pad, x, y, z, ph, gx, gy, gz);
   timeline_end(5);
   float v[8];
   f2_unpack(ph, v[0], v[4]);

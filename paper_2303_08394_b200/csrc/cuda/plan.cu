@@ -1276,9 +1276,14 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       }
     }
     n_far = int(packed ? fw2.size() : fw.size());
-    far_hw = packed && ne <= 4 * (kFarHwSlot / 4) &&
-             std::all_of(fw2.begin(), fw2.end(), [](const FarWork& x) { return x.surf_end - x.surf_begin <= 1; });
+    far_hw = packed && ne <= 4 * (kFarHwSlot / 4);
     if (const char* e = std::getenv("KIFMM_FAR_HW")) far_hw = far_hw && std::atoi(e) != 0;
+    // half-warp kernel: a warp's two works loop to the longer surface list -- pair works of equal
+    // surface counts (stable sort by count; every work writes only its own targets, order is free)
+    if (far_hw && packed)
+      std::stable_sort(fw2.begin(), fw2.end(), [](const FarWork& a, const FarWork& b) {
+        return a.surf_end - a.surf_begin > b.surf_end - b.surf_begin;
+      });
     if (packed)
       far_works.upload(fw2, &dev_bytes);
     else
@@ -1644,11 +1649,13 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
       float* go = grad ? grad_out.as<float>() : nullptr;
       const int hw_blocks = int(ceil_div(n_far, 2 * kFarWarps));
       if (far_hw && grad)
-        far_hw_kernel<true><<<hw_blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far, Mp, Lp,
-                                                                 pot.as<float>(), g, pm, pot_out.as<float>(), go);
+        far_hw_kernel<true><<<hw_blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far,
+                                                                 far_surfaces.as<int2>(), Mp, Lp, pot.as<float>(), g,
+                                                                 pm, pot_out.as<float>(), go);
       else if (far_hw)
-        far_hw_kernel<false><<<hw_blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far, Mp, Lp,
-                                                                  pot.as<float>(), g, pm, pot_out.as<float>(), go);
+        far_hw_kernel<false><<<hw_blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far,
+                                                                  far_surfaces.as<int2>(), Mp, Lp, pot.as<float>(), g,
+                                                                  pm, pot_out.as<float>(), go);
       else if (grad)
         far_f2_kernel<true><<<blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far, far_surfaces.as<int2>(),
                                                               Mp, Lp, pot.as<float>(), g, pm, pot_out.as<float>(), go);
