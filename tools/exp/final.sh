@@ -1,3 +1,5 @@
+# Round-end evidence run on the GPU box: gpu tests, smoke, bench (+ reference arm), launch list, ncu --set full capture.
+# usage: gpurun -- bash tools/exp/final.sh   (outputs under gpurun_out/)
 set -x
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; echo tests rc=$?; tail -2 gpurun_out/gputests.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?; cat gpurun_out/smoke.log
