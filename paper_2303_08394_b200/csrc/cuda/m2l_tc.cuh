@@ -957,16 +957,19 @@ __global__ void m2l_tc_reduce_split_kernel(const float* __restrict__ partial, co
   const int out = tile_out[size_t(tile) * rows + r];
   if (out < 0) return;
   const int s0 = tile_slot[tile], s1 = tile_slot[tile + 1];
+  // check == nullptr: no P2L rows, the check rows would be zeros and only their split is read later --
+  // neither read nor written (48 MB less traffic at config 2; 0.f + x keeps the sums bit-identical)
   float v[NP / 32];
 #pragma unroll
-  for (int k = 0; k < NP / 32; ++k) v[k] = check[size_t(out) * NP + lane + 32 * k];
+  for (int k = 0; k < NP / 32; ++k) v[k] = check ? check[size_t(out) * NP + lane + 32 * k] : 0.f;
   for (int sl = s0; sl < s1; ++sl) {
     const float* pr = partial + (size_t(sl) * rows + r) * NP;
 #pragma unroll
     for (int k = 0; k < NP / 32; ++k) v[k] += pr[lane + 32 * k];
   }
+  if (check)
 #pragma unroll
-  for (int k = 0; k < NP / 32; ++k) check[size_t(out) * NP + lane + 32 * k] = v[k];
+    for (int k = 0; k < NP / 32; ++k) check[size_t(out) * NP + lane + 32 * k] = v[k];
   if (hi) split_row_warp<NP>(v, lane, size_t(out), hi, lo, un);
 }
 

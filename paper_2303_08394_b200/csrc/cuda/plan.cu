@@ -1413,7 +1413,8 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   mark();  // 0
   // zero the down-check rows here, not just before P2L / M2L: a memset between the M2M and M2L kernels
   // would break their programmatic (PDL) launch edge
-  KIFMM_CUDA(cudaMemsetAsync(check_dn.p, 0, check_dn.bytes, s));
+  if (!(gemm_tc && m2l_backend == 2 && !n_p2l && world == 1))  // else nothing reads the fp32 check rows
+    KIFMM_CUDA(cudaMemsetAsync(check_dn.p, 0, check_dn.bytes, s));
   pack_sources_kernel<T><<<int(ceil_div(N, 256)), 256, 0, s>>>(pos4.as<v4_t<T>>(), q_in.as<T>(),
                                                                input_order ? perm.as<int>() : nullptr, int(N),
                                                                src4.as<v4_t<T>>());
@@ -1554,7 +1555,8 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   if (m2l_backend >= 2) {
     if constexpr (sizeof(T) == 4) {
       if (gemm_tc && m2l_backend == 2) {  // multipoles already split; the reduce splits the check rows
-        m2l_tc.launch_presplit(sp_M, check_dn.as<float>(), &sp_cd, s);
+        // no P2L rows: the fp32 check rows are never read (only their split) -- skip them entirely
+        m2l_tc.launch_presplit(sp_M, n_p2l ? check_dn.as<float>() : nullptr, &sp_cd, s);
         launches += 2;
         if (n_dn_extra) {  // P2L-only check rows (no V list): split them here
           tc::split_f16_list_kernel<<<unsigned((n_dn_extra + 7) / 8), 256, 0, s>>>(
