@@ -186,7 +186,9 @@ typedef struct kifmm_gpu_options {
   int32_t world_size;     /* 1 = single GPU */
   int32_t cut_level;      /* partition alignment level for world_size > 1 (default 2) */
   const void* nccl_unique_id; /* 128 bytes from kifmm_gpu_nccl_unique_id() on rank 0 */
-  int32_t m2l_backend;    /* 0 auto, 1 SIMT (fp32/fp64), 2 tcgen05 3xTF32 (fp32 only) */
+  int32_t m2l_backend;    /* 0 auto, 1 SIMT (fp32) / DMMA (fp64), 2 tcgen05 (fp32 only): kind::f16
+                             3-term fp16 split by default -- reported as 2 -- or kind::tf32 3xTF32 with
+                             KIFMM_TC_KIND=tf32 -- reported as 3 */
   int32_t use_graph;      /* capture the evaluate in a CUDA graph */
 } kifmm_gpu_options;
 
@@ -223,8 +225,11 @@ kifmm_status kifmm_gpu_plan_create(const kifmm_gpu_options* options, const kifmm
 /* Host buffers.  input_order = 1: charges/potential/gradient are in the caller's
  * input order and the (un)permutation runs on the device; 0: reordered order.
  * charges/potential are fp32 or fp64 per options.precision; gradient is N x 3 or NULL.
- * With world_size > 1 every rank passes the full charge vector and receives
- * the potentials of its own particles (others left untouched). */
+ * With world_size > 1 every rank passes the full charge vector and receives the potentials of its
+ * own particles: with input_order = 1 the other ranks' entries are written as 0 (sum the ranks'
+ * outputs, or take each rank's owned slice, to assemble the result); with input_order = 0 only this
+ * rank's contiguous reordered range [owned_particle_begin, owned_particle_end) is written and the rest
+ * of the caller's buffer is left untouched. */
 kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* plan, const void* charges, void* potential,
                                 void* gradient, int32_t input_order, kifmm_gpu_timings* timings);
 /* n_rhs independent charge vectors through one plan (host buffers, as kifmm_gpu_evaluate;
@@ -240,7 +245,9 @@ kifmm_status kifmm_gpu_evaluate_device(kifmm_gpu_plan* plan, const void* d_charg
                                        void* d_potential, void* d_gradient, int32_t input_order,
                                        void* stream);
 kifmm_status kifmm_gpu_plan_get_info(const kifmm_gpu_plan* plan, kifmm_gpu_plan_info* info);
-/* Per-phase device timings of the last evaluate_device call (events on the plan stream). */
+/* Per-phase device timings (CUDA events on the plan stream) of the last kifmm_gpu_evaluate call that
+ * passed a timings struct (a serialized, instrumented run; evaluate_device / evaluate_many are never
+ * instrumented and do not update them). */
 kifmm_status kifmm_gpu_last_timings(kifmm_gpu_plan* plan, kifmm_gpu_timings* timings);
 void kifmm_gpu_plan_destroy(kifmm_gpu_plan* plan);
 

@@ -3,8 +3,11 @@
 // fp64 CPU restatement of the KIFMM evaluate as SPEC.md defines it.  Each step
 // cites the SPEC line it follows.  Written independently of the product
 // library (it only shares the plain-data view structs of include/kifmm.h).
-// Parallel loops follow proj/src/parallel.hpp:28-43 (static schedule, one
-// owner per output slice), so results do not depend on the thread count.
+// Parallel loops follow the ownership rule of proj/src/parallel.hpp:28-43 (one
+// owner per output slice, no shared accumulators), so results do not depend on
+// the thread count; the schedule is dynamic (chunks of 8) rather than
+// parallel.hpp's static one because leaf costs are uneven -- the schedule only
+// decides which thread computes a slice, never the arithmetic order inside it.
 #include "oracle.h"
 
 #include <omp.h>

@@ -1,12 +1,14 @@
-// M2L on the 5th-generation tensor cores: tcgen05 kind::tf32 with 3xTF32 error
-// compensation (SURVEY 7.3 "M2L batching").
+// M2L on the 5th-generation tensor cores (SURVEY 7.3 "M2L batching").
 //
-// Work: for a tile of same-octant-class target nodes and one transfer vector t,
+// Work: for a tile of same-class target nodes and one transfer vector t,
 //   D[rows x 160] += A_t[rows x 160] . K_t^T,  A_t rows = multipoles of the
 // V-list sources at offset t (a zero row where absent), K_t = reference-level
-// kernel matrix (n_c x n_e, K-major).  fp32 operands are split x = hi + lo (hi =
-// tf32 round-to-nearest) and D += A_hi B_hi + A_hi B_lo + A_lo B_hi keeps fp32-
-// level accuracy (the dropped A_lo B_lo term is ~2^-22 relative).
+// kernel matrix (n_c x n_e, K-major).  Two error-compensated operand formats
+// (template ES):
+//   ES = 2 (default, m2l_backend 2): kind::f16.  fp32 values are scaled by a power of two
+//          (per multipole row; 2^8 for K_t) and split x = hi + lo in fp16, and
+//          D += A_hi B_hi + A_hi B_lo + A_lo B_hi (the dropped lo.lo term is ~2^-22 relative).
+//   ES = 4 (m2l_backend 3, KIFMM_TC_KIND=tf32): kind::tf32 with the same 3-term split in tf32 (3xTF32).
 //
 // K_t hi/lo arrive by TMA (SWIZZLE_128B, mbarrier transaction counts); the
 // gathered A rows (missing sources read an appended zero row) are copied by 128
@@ -113,6 +115,12 @@ struct Cfg {
                                     (uint32_t((CTAS * BM) >> 4) << 24);
 };
 
+#ifdef KIFMM_EXPERIMENTS
+#define TC_DBG(bit) (epi.debug & (bit))
+#else
+#define TC_DBG(bit) 0
+#endif
+
 struct Item {
   int tile, seg_begin, seg_end, slot;
 };
@@ -129,7 +137,8 @@ struct Epi {
   const float* col_unscale;
   float* dst;
   int accumulate;
-  int debug;  // experiments only (KIFMM_TC_DBG): bit 0 skips the A gathers, bit 1 the B TMA loads
+  int debug;  // experiments only (-DKIFMM_EXPERIMENTS, KIFMM_TC_DBG): bit 0 skips the A gathers, bit 1 the B
+              // TMA loads; the product build compiles every TC_DBG test to 0
   __half* split_hi;
   __half* split_lo;
   float* split_un;
@@ -449,7 +458,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * NP + h * EPI_COLS);
 #pragma unroll
-        for (int cb = 0; cb < ((epi.debug & 4) ? 0 : EPI_COLS / 16); ++cb) {
+        for (int cb = 0; cb < (TC_DBG(4) ? 0 : EPI_COLS / 16); ++cb) {
           uint32_t v[16];
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -675,7 +684,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
             for (kb = 0; kb < NKB; ++kb) {
               mbar_wait(empty(s), ph ^ 1u);
               if (elect_one()) {
-                if (epi.debug & 2) {
+                if (TC_DBG(2)) {
                   if (rank == 0) mbar_expect_tx(full(s), 0);
                 } else {
                   if (rank == 0) mbar_expect_tx(full(s), C::TX);
@@ -700,7 +709,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
       //                  the stage / parity counters run without div/mod, descriptors are a base plus
       //                  an offset, and the three MMAs of a K step are one asm block.
       if (rank == 0) {  // the whole warp walks the loop (warp-uniform values); one elected lane issues
-        const bool prof = (epi.debug & 8) != 0;
+        const bool prof = TC_DBG(8) != 0;
         unsigned long long t_all = clock64(), t_te = 0, t_fu = 0;
         const uint64_t dah0 = make_desc<ROWB>(a_hi(0)), dal0 = make_desc<ROWB>(a_lo(0));
         const uint64_t dbh0 = make_desc<ROWB>(b_hi(0)), dbl0 = make_desc<ROWB>(b_lo(0));
@@ -803,7 +812,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
 #else
           mbar_wait(empty(s), ph ^ 1u);
 #endif
-          if (!(epi.debug & 1)) {
+          if (!TC_DBG(1)) {
             const uint32_t ahs = a_hi(s), als = a_lo(s);
             const size_t kbo = size_t(kb) * ROWB;
 #pragma unroll
@@ -1021,13 +1030,17 @@ inline std::vector<int> lpt_schedule(const std::vector<tc::Item>& items, int g) 
   return out;
 }
 
-inline int tc_debug() {
+#ifdef KIFMM_EXPERIMENTS
+inline int tc_debug() {  // experiments only: skips operand loads (wrong results), never in the product build
   static const int d = [] {
     const char* e = std::getenv("KIFMM_TC_DBG");
     return e ? std::atoi(e) : 0;
   }();
   return d;
 }
+#else
+inline int tc_debug() { return 0; }
+#endif
 
 inline int sm_count() {
   static int n = 0;

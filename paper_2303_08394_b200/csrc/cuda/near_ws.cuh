@@ -72,10 +72,12 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
     for (;;) {
       int wi = 0;
       if (lane == 0) {
-        if (MODE == 1) {  // side blocks: optional pause while M2L runs (queue[3]), stop once draining
+        if (MODE == 1) {  // side blocks: stop once draining
+#ifdef KIFMM_EXPERIMENTS  // optional pause while M2L runs (queue[3], KIFMM_NEAR_PAUSE)
           for (int pz; (pz = atomicAdd(queue + 3, 0)) != 0 && (pz == 1 || (blockIdx.x & 1)) &&
                        atomicAdd(queue + 1, 0) == 0;)
             __nanosleep(2000);
+#endif
           wi = atomicAdd(queue + 1, 0) != 0 ? n_works : atomicAdd(queue, 1);
         } else {
           wi = atomicAdd(queue, 1);

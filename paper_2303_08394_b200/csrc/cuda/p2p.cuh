@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(kP2PThreads, KIFMM_NEAR_MINB) leaf_eval_f2_ker
   for (int wi = blockIdx.x;;) {
   if (QUEUE) {
     if (tid == 0) {
+#ifdef KIFMM_EXPERIMENTS
       // side blocks pause while queue[3] is raised (the M2L kernel runs) -- co-running warps slow the
       // tensor-core pipeline more than the near field gains
       // (queue[3] = 1: all side blocks pause; 2: the odd ones)
@@ -266,6 +267,7 @@ __global__ void __launch_bounds__(kP2PThreads, KIFMM_NEAR_MINB) leaf_eval_f2_ker
         for (int pz; (pz = atomicAdd(queue + 3, 0)) != 0 && (pz == 1 || (blockIdx.x & 1)) &&
                      atomicAdd(queue + 1, 0) == 0;)
           __nanosleep(2000);
+#endif
       s_wi = (!DRAIN && atomicAdd(queue + 1, 0) != 0) ? n_works : atomicAdd(queue, 1);
     }
     __syncthreads();

@@ -230,6 +230,7 @@ void launch_check(int np, int n, const P2PParams<T>& pp, const CheckWork* works,
   KIFMM_LAUNCH_CHECK();
 }
 
+#ifdef KIFMM_EXPERIMENTS
 // Experiments only (KIFMM_CORUN_DUMMY): a co-running load of one kind -- 0 FFMA chains, 1 LDS.128
 // broadcasts, 2 MUFU.RSQ -- for `iters` rounds, to see which resource slows the tensor-core kernels.
 __global__ void __launch_bounds__(128) dummy_load_kernel(int kind, int iters, float* out) {
@@ -260,6 +261,7 @@ __global__ void __launch_bounds__(128) dummy_load_kernel(int kind, int iters, fl
   for (int i = 0; i < 8; ++i) t += a[i];
   if (t == -1.f) out[0] = t;
 }
+#endif
 
 // M2M split over octants: partial products land in scratch rows (slot*8 + octant)
 // and are summed here in fixed octant order (deterministic, no atomics).
@@ -373,6 +375,7 @@ struct kifmm_gpu_plan {
   size_t dev_bytes = 0;
   cudaStream_t stream = nullptr, side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_done = nullptr;  // end of the last evaluate (any entry point, any stream)
   std::array<cudaEvent_t, 16> ev{};
   kifmm_gpu_plan_info info{};
   kifmm_gpu_timings last{};
@@ -446,6 +449,7 @@ struct kifmm_gpu_plan {
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_done) cudaEventDestroy(ev_done);
     if (comm) Nccl::get().commDestroy(static_cast<ncclComm_t>(comm));
   }
 
@@ -457,8 +461,10 @@ struct kifmm_gpu_plan {
   void run(cudaStream_t s, bool input_order, bool timed);
   void exchange(cudaStream_t s);
   void evaluate_device(const void* q, void* pot_dst, void* grad_dst, bool input_order, cudaStream_t user, bool timed);
-  // the captured evaluate graph of this output order on the plan stream (captured on first use)
-  void launch_graph(bool input_order) {
+  // the captured evaluate graph of this output order (captured on the plan stream on first use, with the
+  // capture always ended -- also when a launch throws -- so the stream never stays in capture mode),
+  // launched on `s`
+  void launch_graph(bool input_order, cudaStream_t s) {
     const int gi = input_order ? 1 : 0;
     if (!graph[gi]) {
       cudaGraph_t g;
@@ -473,11 +479,20 @@ struct kifmm_gpu_plan {
         throw;
       }
       KIFMM_CUDA(cudaStreamEndCapture(stream, &g));
-      KIFMM_CUDA(cudaGraphInstantiateWithFlags(&graph[gi], g, cudaGraphInstantiateFlagUseNodePriority));
+      const cudaError_t e = cudaGraphInstantiateWithFlags(&graph[gi], g, cudaGraphInstantiateFlagUseNodePriority);
       cudaGraphDestroy(g);
+      if (e != cudaSuccess) {
+        graph[gi] = nullptr;
+        KIFMM_CUDA(e);
+      }
     }
-    KIFMM_CUDA(cudaGraphLaunch(graph[gi], stream));
+    KIFMM_CUDA(cudaGraphLaunch(graph[gi], s));
   }
+  // Every evaluate entry point orders itself after the previous evaluate of this plan, whichever stream
+  // that one ran on (the plan's buffers -- q_in, src4, M, L, check rows, outputs, the near-field counter --
+  // are shared by all of them): wait on `ev_done` first, record it last.
+  void begin(cudaStream_t s) { KIFMM_CUDA(cudaStreamWaitEvent(s, ev_done, 0)); }
+  void finish(cudaStream_t s) { KIFMM_CUDA(cudaEventRecord(ev_done, s)); }
   void evaluate_many(int n_rhs, const void* const* charges, void* const* potentials, void* const* gradients,
                      bool input_order);
 };
@@ -598,6 +613,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_dn_join, cudaEventDisableTiming));
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    KIFMM_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
   }
   for (auto& e : ev) KIFMM_CUDA(cudaEventCreate(&e));
 
@@ -1099,11 +1115,13 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     if (near_ws) near_bps = near_ws_bps;
     if (const char* e = std::getenv("KIFMM_NEAR_BPS")) near_bps = std::max(0, std::atoi(e));
     near_counter.alloc(4 * sizeof(int), &dev_bytes);
+#ifdef KIFMM_EXPERIMENTS  // timing experiments only (tools/build_variant.sh); NEAR_SKIP gives wrong results
     if (const char* e = std::getenv("KIFMM_NEAR_PAUSE")) near_pause = std::atoi(e);
     near_debug = std::getenv("KIFMM_NEAR_DEBUG") != nullptr;
-    near_skip = std::getenv("KIFMM_NEAR_SKIP") != nullptr;  // timing experiments only: wrong results
+    near_skip = std::getenv("KIFMM_NEAR_SKIP") != nullptr;
     if (const char* e = std::getenv("KIFMM_NEAR_FORK")) near_fork_at = std::string(e) == "m2l" ? 1 : 0;
     near_corun = std::getenv("KIFMM_NEAR_CORUN") != nullptr;
+#endif
     // full shared-memory carveout, so an SM running near-field blocks need not drain before a tcgen05
     // CTA (which needs the maximum carveout) can start next to them
     for (const void* f : {(const void*)leaf_eval_f2_kernel<true, false, true, false>,
@@ -1542,12 +1560,14 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     ++launches;
   }
   mark();  // 4
+#ifdef KIFMM_EXPERIMENTS
   if (const char* e = std::getenv("KIFMM_CORUN_DUMMY"); e && timed) {  // experiments: a dummy load next to M2L
     KIFMM_CUDA(cudaEventRecord(ev_fork, s));
     KIFMM_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
     dummy_load_kernel<<<2 * sm_count(), 128, 0, side>>>(std::atoi(e), 20000, pot.as<float>());
     KIFMM_CUDA(cudaEventRecord(ev_join, side));
   }
+#endif
   if (near_fork_at == 1 || corun) fork_near();  // experiments (KIFMM_NEAR_FORK=m2l): near field next to M2L only
   if (queue_mode && near_pause)  // side near-field blocks sleep while M2L runs
     KIFMM_CUDA(cudaMemsetAsync(near_counter.as<int>() + 3, near_pause, 1, s));
@@ -1583,9 +1603,11 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     }
   }
   if (queue_mode && near_pause) KIFMM_CUDA(cudaMemsetAsync(near_counter.as<int>() + 3, 0, sizeof(int), s));
+#ifdef KIFMM_EXPERIMENTS
   if (queue_mode && near_debug && std::getenv("KIFMM_NEAR_DEBUG_M2L"))  // experiments: snapshot after M2L
     KIFMM_CUDA(cudaMemcpyAsync(near_counter.as<int>() + 2, near_counter.as<int>(), sizeof(int),
                                cudaMemcpyDeviceToDevice, s));
+#endif
   mark();  // 5
   // factored downward solve (dc2e at the reference level; M2L/P2L level factors folded)
   bool l2l_done = false;
@@ -1630,9 +1652,11 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
   }
   // leaves: near field (side stream, or here when timed) then L2P + M2P
   if (timed && !corun) leaf(leaf_near, false, s);
+#ifdef KIFMM_EXPERIMENTS
   if (queue_mode && near_debug && !std::getenv("KIFMM_NEAR_DEBUG_M2L"))  // experiments: works taken by now
     KIFMM_CUDA(cudaMemcpyAsync(near_counter.as<int>() + 2, near_counter.as<int>(), sizeof(int),
                                cudaMemcpyDeviceToDevice, s));
+#endif
   // drain the works the side-stream blocks did not take (persistent: at most 8 blocks per SM, so an
   // empty queue costs one short wave instead of a block per leaf)
   if (queue_mode) near_queue(s, std::min(leaf_near.n, (near_ws ? near_ws_blocks : 8) * sm_count()), true);
@@ -1710,26 +1734,10 @@ void kifmm_gpu_plan::evaluate_device(const void* q, void* pot_dst, void* grad_ds
   KIFMM_CUDA(cudaSetDevice(device));
   cudaStream_t s = user ? user : stream;
   const size_t es = esz();
+  begin(s);
   KIFMM_CUDA(cudaMemcpyAsync(q_in.p, q, size_t(N) * es, cudaMemcpyDefault, s));
-  const int gi = input_order ? 1 : 0;
   if (!timed && opt.use_graph) {
-    if (!graph[gi]) {
-      cudaGraph_t g;
-      KIFMM_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-      try {
-        if (precision == 32)
-          run<float>(stream, input_order, false);
-        else
-          run<double>(stream, input_order, false);
-      } catch (...) {
-        cudaStreamEndCapture(stream, &g);
-        throw;
-      }
-      KIFMM_CUDA(cudaStreamEndCapture(stream, &g));
-      KIFMM_CUDA(cudaGraphInstantiateWithFlags(&graph[gi], g, cudaGraphInstantiateFlagUseNodePriority));
-      cudaGraphDestroy(g);
-    }
-    KIFMM_CUDA(cudaGraphLaunch(graph[gi], s));
+    launch_graph(input_order, s);
   } else {
     if (precision == 32)
       run<float>(s, input_order, timed);
@@ -1750,6 +1758,7 @@ void kifmm_gpu_plan::evaluate_device(const void* q, void* pot_dst, void* grad_ds
       KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(grad_dst) + 3 * off, static_cast<const char*>(gs) + 3 * off,
                                  3 * cnt, cudaMemcpyDefault, s));
   }
+  finish(s);
 }
 
 namespace {
@@ -1828,6 +1837,7 @@ void kifmm_gpu_plan::evaluate_many(int n_rhs, const void* const* charges, void* 
     pipe = std::move(P);
   }
   Pipe& P = *pipe;
+  begin(stream);
   const bool full = input_order || world == 1;  // else: this rank's particle range (reordered order)
   const size_t off = full ? 0 : size_t(pb), cnt = full ? size_t(N) : size_t(pe - pb);
   const void* ps = input_order ? pot_out.p : pot.p;
@@ -1843,7 +1853,7 @@ void kifmm_gpu_plan::evaluate_many(int n_rhs, const void* const* charges, void* 
     KIFMM_CUDA(cudaMemcpyAsync(q_in.p, P.q[b].p, size_t(N) * es, cudaMemcpyDeviceToDevice, stream));
     KIFMM_CUDA(cudaEventRecord(P.in_free[b], stream));
     if (opt.use_graph) {
-      launch_graph(input_order);
+      launch_graph(input_order, stream);
     } else if (precision == 32) {
       run<float>(stream, input_order, false);
     } else {
@@ -1871,6 +1881,9 @@ void kifmm_gpu_plan::evaluate_many(int n_rhs, const void* const* charges, void* 
     }
     KIFMM_CUDA(cudaEventRecord(P.out_free[b], P.cout));
   }
+  KIFMM_CUDA(cudaStreamWaitEvent(stream, P.out_free[(n_rhs + 1) & 1], 0));  // the last copy-outs
+  if (n_rhs > 1) KIFMM_CUDA(cudaStreamWaitEvent(stream, P.out_free[n_rhs & 1], 0));
+  finish(stream);
   KIFMM_CUDA(cudaStreamSynchronize(P.cout));
   KIFMM_CUDA(cudaStreamSynchronize(stream));
 }
@@ -1918,31 +1931,21 @@ kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* p, const void* charges, void* po
     cudaStream_t s = p->stream;
     const size_t es = p->esz();
     auto& ev = p->ev;
+    p->begin(s);
     // events 10..13: H2D, compute, D2H boundaries
     KIFMM_CUDA(cudaEventRecord(ev[10], s));
     KIFMM_CUDA(cudaMemcpyAsync(p->q_in.p, charges, size_t(p->N) * es, cudaMemcpyDefault, s));
     KIFMM_CUDA(cudaEventRecord(ev[11], s));
     const bool timed = timings != nullptr;
-    const int gi = input_order ? 1 : 0;
     if (!timed && p->opt.use_graph) {
-      if (!p->graph[gi]) {
-        cudaGraph_t g;
-        KIFMM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        if (p->precision == 32)
-          p->run<float>(s, input_order != 0, false);
-        else
-          p->run<double>(s, input_order != 0, false);
-        KIFMM_CUDA(cudaStreamEndCapture(s, &g));
-        KIFMM_CUDA(cudaGraphInstantiateWithFlags(&p->graph[gi], g, cudaGraphInstantiateFlagUseNodePriority));
-        cudaGraphDestroy(g);
-      }
-      KIFMM_CUDA(cudaGraphLaunch(p->graph[gi], s));
+      p->launch_graph(input_order != 0, s);
     } else if (p->precision == 32) {
       p->run<float>(s, input_order != 0, timed);
     } else {
       p->run<double>(s, input_order != 0, timed);
     }
     KIFMM_CUDA(cudaEventRecord(ev[12], s));
+#ifdef KIFMM_EXPERIMENTS
     if (std::getenv("KIFMM_TIMELINE")) {
       unsigned long long tl[16][2];
       KIFMM_CUDA(cudaStreamSynchronize(s));
@@ -1974,6 +1977,7 @@ kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* p, const void* charges, void* po
       KIFMM_CUDA(cudaStreamSynchronize(s));
       std::fprintf(stderr, "near queue: %d of %d works taken before the drain\n", c[2], p->leaf_near.n);
     }
+#endif
     const void* ps = input_order ? p->pot_out.p : p->pot.p;
     const void* gs = input_order ? p->grad_out.p : p->grad_buf.p;
     if (input_order || p->world == 1) {
@@ -1990,6 +1994,7 @@ kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* p, const void* charges, void* po
       }
     }
     KIFMM_CUDA(cudaEventRecord(ev[13], s));
+    p->finish(s);
     KIFMM_CUDA(cudaStreamSynchronize(s));
     if (timed) {
       kifmm_gpu_timings t{};
