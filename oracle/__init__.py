@@ -35,7 +35,6 @@ _lib.oracle_upward_top.argtypes = [P, P, i32, P, i32]
 _lib.oracle_downward.argtypes = [P, P, P, P, i64, i64, P, P, i32, C.POINTER(Timings)]
 _lib.oracle_direct.argtypes = [P, P, i64, P, i64, P, P, i32]
 _lib.oracle_direct.restype = None
-_lib.oracle_lists_bruteforce.argtypes = [P, P, P, i64, P, P, P, i64, P, P, i64, P, P, i64]
 _lib.oracle_tree_leaves.argtypes = [P, i64, i32, P, i32, P, i64]
 _lib.oracle_tree_leaves.restype = i64
 _lib.oracle_relative_error.argtypes = [P, P, i64]
@@ -98,23 +97,47 @@ def direct(positions, charges, targets=None, gradient=False, threads=0):
     return (phi, g) if gradient else phi
 
 
-def lists_bruteforce(tree):
-    """Brute-force U/V/W/X CSR from the SPEC definitions, sized from the product's lists."""
-    nl, nn = tree.n_leaves, tree.n_nodes
-    cap = lambda ptr: int(ptr[-1]) + 1  # noqa: E731
-    u_ptr, u_idx = np.zeros(nl + 1, np.int64), np.zeros(cap(tree.u_ptr) * 2 + 64, np.int64)
-    v_ptr, v_idx = np.zeros(nn + 1, np.int64), np.zeros(cap(tree.v_ptr) * 2 + 64, np.int64)
-    v_tv = np.zeros(v_idx.shape[0], np.int32)
-    w_ptr, w_idx = np.zeros(nl + 1, np.int64), np.zeros(cap(tree.w_ptr) * 2 + 64, np.int64)
-    x_ptr, x_idx = np.zeros(nn + 1, np.int64), np.zeros(cap(tree.x_ptr) * 2 + 64, np.int64)
-    rc = _lib.oracle_lists_bruteforce(C.addressof(tree.view), u_ptr.ctypes.data, u_idx.ctypes.data, u_idx.size,
-                                      v_ptr.ctypes.data, v_idx.ctypes.data, v_tv.ctypes.data, v_idx.size,
-                                      w_ptr.ctypes.data, w_idx.ctypes.data, w_idx.size, x_ptr.ctypes.data,
-                                      x_idx.ctypes.data, x_idx.size)
+class Csr(C.Structure):
+    _fields_ = [("u_ptr", C.POINTER(i64)), ("u_idx", C.POINTER(i64)), ("v_ptr", C.POINTER(i64)),
+                ("v_idx", C.POINTER(i64)), ("v_tv", C.POINTER(i32)), ("w_ptr", C.POINTER(i64)),
+                ("w_idx", C.POINTER(i64)), ("x_ptr", C.POINTER(i64)), ("x_idx", C.POINTER(i64)),
+                ("n_u", i64), ("n_v", i64), ("n_w", i64), ("n_x", i64)]
+
+
+_lib.oracle_lists_subset.argtypes = [P, i64, P, i64, P, i32, C.POINTER(Csr)]
+_lib.oracle_csr_free.argtypes = [C.POINTER(Csr)]
+_lib.oracle_csr_free.restype = None
+
+
+def lists_for(tree, leaf_targets=None, node_targets=None, threads=0):
+    """Brute-force U/W (per target leaf) and V/X (per target node) lists from the SPEC definitions,
+    as CSR rows in the order of the given targets (all leaves / all nodes when None)."""
+    lt = np.arange(tree.n_leaves, dtype=np.int64) if leaf_targets is None else np.ascontiguousarray(
+        leaf_targets, dtype=np.int64)
+    nt = np.arange(tree.n_nodes, dtype=np.int64) if node_targets is None else np.ascontiguousarray(
+        node_targets, dtype=np.int64)
+    c = Csr()
+    rc = _lib.oracle_lists_subset(C.addressof(tree.view), lt.size, lt.ctypes.data, nt.size, nt.ctypes.data,
+                                  int(threads), C.byref(c))
     if rc != 0:
-        raise RuntimeError(f"brute-force list {rc} overflowed its buffer")
-    return {"u": (u_ptr, u_idx[:u_ptr[-1]]), "v": (v_ptr, v_idx[:v_ptr[-1]], v_tv[:v_ptr[-1]]),
-            "w": (w_ptr, w_idx[:w_ptr[-1]]), "x": (x_ptr, x_idx[:x_ptr[-1]])}
+        raise RuntimeError(f"oracle_lists_subset failed ({rc})")
+
+    def arr(p, n, dt):
+        return np.ctypeslib.as_array(p, shape=(int(n),)).astype(dt, copy=True) if n else np.zeros(0, dt)
+    try:
+        out = {"u": (arr(c.u_ptr, lt.size + 1, np.int64), arr(c.u_idx, c.n_u, np.int64)),
+               "v": (arr(c.v_ptr, nt.size + 1, np.int64), arr(c.v_idx, c.n_v, np.int64),
+                     arr(c.v_tv, c.n_v, np.int32)),
+               "w": (arr(c.w_ptr, lt.size + 1, np.int64), arr(c.w_idx, c.n_w, np.int64)),
+               "x": (arr(c.x_ptr, nt.size + 1, np.int64), arr(c.x_idx, c.n_x, np.int64))}
+    finally:
+        _lib.oracle_csr_free(C.byref(c))
+    return out
+
+
+def lists_bruteforce(tree, threads=0):
+    """Brute-force U/V/W/X CSR of the whole tree (every leaf / node a target)."""
+    return lists_for(tree, None, None, threads)
 
 
 def tree_leaves(positions, n_crit, domain, balance=True):

@@ -17,6 +17,7 @@
 #include <tuple>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <set>
@@ -201,6 +202,59 @@ void node_leaf_range(const kifmm_tree_view* t, int64_t node, int64_t& lo, int64_
   hi = t->node_leaf[b] + 1;
 }
 
+}  // namespace
+
+// Brute-force lists straight from the definitions (X on all nodes), for a
+// chosen set of target leaves (U, W) and target nodes (V, X).  Every target is checked against EVERY
+// candidate of the tree (no spatial pruning); geometry is integer intervals on the level-15 grid.
+namespace {
+struct Box {
+  int64_t lo[3], w;  // cube [lo, lo + w] per axis on the MAX_LEVEL grid
+  int l;
+};
+Box box_of(uint64_t k) {
+  Box b;
+  int64_t a[3];
+  anchor(k, a);
+  b.l = lev(k);
+  b.w = int64_t(1) << (MAXL - b.l);
+  for (int d = 0; d < 3; ++d) b.lo[d] = a[d] * b.w;
+  return b;
+}
+Box parent_box(const Box& b) {
+  Box p;
+  p.l = b.l - 1;
+  p.w = 2 * b.w;
+  for (int d = 0; d < 3; ++d) p.lo[d] = b.lo[d] - b.lo[d] % p.w;
+  return p;
+}
+// closed cubes share a point and neither contains the other
+bool adj(const Box& x, const Box& y) {
+  bool xin = true, yin = true;
+  for (int d = 0; d < 3; ++d) {
+    const int64_t xl = x.lo[d], xh = xl + x.w, yl = y.lo[d], yh = yl + y.w;
+    if (xl > yh || yl > xh) return false;
+    if (!(xl >= yl && xh <= yh)) xin = false;
+    if (!(yl >= xl && yh <= xh)) yin = false;
+  }
+  return !(xin || yin);
+}
+int tv_id(int dx, int dy, int dz) {  // rank among [-3,3]^3 offsets with Chebyshev norm >= 2, lexicographic
+  int id = 0;
+  for (int x = -3; x <= 3; ++x)
+    for (int y = -3; y <= 3; ++y)
+      for (int z = -3; z <= 3; ++z) {
+        if (std::max(std::abs(x), std::max(std::abs(y), std::abs(z))) < 2) continue;
+        if (std::make_tuple(x, y, z) < std::make_tuple(dx, dy, dz)) ++id;
+      }
+  return id;
+}
+template <class T>
+T* dup(const std::vector<T>& v) {
+  T* p = static_cast<T*>(std::malloc(sizeof(T) * std::max<size_t>(1, v.size())));
+  if (!v.empty()) std::memcpy(p, v.data(), sizeof(T) * v.size());
+  return p;
+}
 }  // namespace
 
 extern "C" {
@@ -413,91 +467,94 @@ double oracle_relative_error(const double* a, const double* b, int64_t n) {
   return double(std::sqrt(num / den));
 }
 
-int oracle_lists_bruteforce(const kifmm_tree_view* t, int64_t* u_ptr, int64_t* u_idx, int64_t u_cap, int64_t* v_ptr,
-                            int64_t* v_idx, int32_t* v_tv, int64_t v_cap, int64_t* w_ptr, int64_t* w_idx,
-                            int64_t w_cap, int64_t* x_ptr, int64_t* x_idx, int64_t x_cap) {
+
+int oracle_lists_subset(const kifmm_tree_view* t, int64_t n_lt, const int64_t* leaf_targets, int64_t n_nt,
+                        const int64_t* node_targets, int32_t threads, oracle_csr* out) {
+  threads = resolve(threads);
   const int64_t nn = t->n_nodes, nl = t->n_leaves;
-  // order of members: ascending raw key
-  auto by_key = [&](int64_t a, int64_t b) { return t->node_key[a] < t->node_key[b]; };
-  // U: all leaves adjacent to A, plus A
-  u_ptr[0] = 0;
-  for (int64_t a = 0; a < nl; ++a) {
-    std::vector<int64_t> mem;
-    const uint64_t ka = t->node_key[t->leaf_node[a]];
-    for (int64_t b = 0; b < nl; ++b) {
-      const uint64_t kb = t->node_key[t->leaf_node[b]];
-      if (a == b || adjacent(ka, kb)) mem.push_back(t->leaf_node[b]);
-    }
-    std::sort(mem.begin(), mem.end(), by_key);
-    if (u_ptr[a] + int64_t(mem.size()) > u_cap) return 1;
-    for (size_t i = 0; i < mem.size(); ++i) u_idx[u_ptr[a] + i] = t->node_leaf[mem[i]];
-    u_ptr[a + 1] = u_ptr[a] + int64_t(mem.size());
-  }
-  // V: same-level nodes whose parent is a same-level neighbour of parent(B), not adjacent to B
-  v_ptr[0] = 0;
-  for (int64_t b = 0; b < nn; ++b) {
-    std::vector<int64_t> mem;
-    const uint64_t kb = t->node_key[b];
-    const int l = lev(kb);
-    if (l >= 2) {
-      const uint64_t pb = parent_key(kb);
-      for (int64_t c = t->level_ptr[l]; c < t->level_ptr[l + 1]; ++c) {
-        const uint64_t kc = t->node_key[c];
-        const uint64_t pc = parent_key(kc);
-        if (pc != pb && adjacent(pc, pb) && !adjacent(kc, kb)) mem.push_back(c);
+  std::vector<Box> bx(nn);
+  pfor(nn, threads, [&](int64_t n) { bx[n] = box_of(t->node_key[n]); });
+  // members in ascending raw key: nodes are level-major, so sort candidates by key
+  std::vector<std::vector<int64_t>> U(n_lt), W(n_lt), V(n_nt), X(n_nt);
+  std::vector<std::vector<int32_t>> TV(n_nt);
+  auto by_key = [&](std::vector<int64_t>& m) {
+    std::sort(m.begin(), m.end(), [&](int64_t a, int64_t b) { return t->node_key[a] < t->node_key[b]; });
+  };
+  pfor(n_lt, threads, [&](int64_t i) {
+    const int64_t a = leaf_targets[i];
+    const int64_t na = t->leaf_node[a];
+    const Box& A = bx[na];
+    // U: every leaf adjacent to A, plus A itself
+    std::vector<int64_t> u;
+    for (int64_t b = 0; b < nl; ++b)
+      if (b == a || adj(A, bx[t->leaf_node[b]])) u.push_back(t->leaf_node[b]);
+    by_key(u);
+    for (auto& x : u) x = t->node_leaf[x];
+    U[i] = std::move(u);
+    // W: nodes strictly finer than A whose parent is adjacent to A, not adjacent to A
+    std::vector<int64_t> w;
+    for (int64_t c = 0; c < nn; ++c)
+      if (bx[c].l > A.l && adj(parent_box(bx[c]), A) && !adj(bx[c], A)) w.push_back(c);
+    by_key(w);
+    W[i] = std::move(w);
+  });
+  pfor(n_nt, threads, [&](int64_t i) {
+    const int64_t b = node_targets[i];
+    const Box& B = bx[b];
+    // V: same-level nodes whose parent is a same-level neighbour of parent(B), not adjacent to B
+    if (B.l >= 2) {
+      const Box PB = parent_box(B);
+      std::vector<int64_t> v;
+      for (int64_t c = t->level_ptr[B.l]; c < t->level_ptr[B.l + 1]; ++c) {
+        const Box PC = parent_box(bx[c]);
+        bool same = true;
+        for (int d = 0; d < 3; ++d) same = same && PC.lo[d] == PB.lo[d];
+        if (!same && adj(PC, PB) && !adj(bx[c], B)) v.push_back(c);
       }
+      by_key(v);
+      std::vector<int32_t> tv;
+      for (int64_t c : v)
+        tv.push_back(tv_id(int((bx[c].lo[0] - B.lo[0]) / B.w), int((bx[c].lo[1] - B.lo[1]) / B.w),
+                           int((bx[c].lo[2] - B.lo[2]) / B.w)));
+      V[i] = std::move(v);
+      TV[i] = std::move(tv);
     }
-    std::sort(mem.begin(), mem.end(), by_key);
-    if (v_ptr[b] + int64_t(mem.size()) > v_cap) return 2;
-    int64_t ab[3];
-    anchor(kb, ab);
-    for (size_t i = 0; i < mem.size(); ++i) {
-      int64_t as[3];
-      anchor(t->node_key[mem[i]], as);
-      const int dx = int(as[0] - ab[0]), dy = int(as[1] - ab[1]), dz = int(as[2] - ab[2]);
-      // id = rank of (dx,dy,dz) among [-3,3]^3 offsets with Chebyshev norm >= 2, lexicographic
-      int id = 0;
-      for (int x = -3; x <= 3; ++x)
-        for (int y = -3; y <= 3; ++y)
-          for (int z = -3; z <= 3; ++z) {
-            if (std::max(std::abs(x), std::max(std::abs(y), std::abs(z))) < 2) continue;
-            if (std::make_tuple(x, y, z) < std::make_tuple(dx, dy, dz)) ++id;
-          }
-      v_idx[v_ptr[b] + i] = mem[i];
-      v_tv[v_ptr[b] + i] = id;
+    // X: leaves A with B in W(A) -- coarser than B, adjacent to parent(B), not adjacent to B
+    if (B.l >= 1) {
+      const Box PB = parent_box(B);
+      std::vector<int64_t> x;
+      for (int64_t a = 0; a < nl; ++a) {
+        const Box& A = bx[t->leaf_node[a]];
+        if (A.l < B.l && adj(PB, A) && !adj(B, A)) x.push_back(a);  // leaves ascend in raw key
+      }
+      X[i] = std::move(x);
     }
-    v_ptr[b + 1] = v_ptr[b] + int64_t(mem.size());
-  }
-  // W: nodes strictly finer than A whose parent is adjacent to A, not adjacent to A
-  std::vector<std::vector<int64_t>> xs(nn);
-  w_ptr[0] = 0;
-  for (int64_t a = 0; a < nl; ++a) {
-    std::vector<int64_t> mem;
-    const uint64_t ka = t->node_key[t->leaf_node[a]];
-    for (int64_t c = 0; c < nn; ++c) {
-      const uint64_t kc = t->node_key[c];
-      if (lev(kc) <= lev(ka)) continue;
-      if (adjacent(parent_key(kc), ka) && !adjacent(kc, ka)) mem.push_back(c);
+  });
+  auto csr = [](const std::vector<std::vector<int64_t>>& L, int64_t** ptr, int64_t** idx, int64_t* total) {
+    std::vector<int64_t> p{0}, ix;
+    for (const auto& l : L) {
+      ix.insert(ix.end(), l.begin(), l.end());
+      p.push_back(int64_t(ix.size()));
     }
-    std::sort(mem.begin(), mem.end(), by_key);
-    if (w_ptr[a] + int64_t(mem.size()) > w_cap) return 3;
-    for (size_t i = 0; i < mem.size(); ++i) {
-      w_idx[w_ptr[a] + i] = mem[i];
-      xs[mem[i]].push_back(a);
-    }
-    w_ptr[a + 1] = w_ptr[a] + int64_t(mem.size());
-  }
-  // X: dual of W
-  x_ptr[0] = 0;
-  for (int64_t b = 0; b < nn; ++b) {
-    auto& mem = xs[b];
-    std::sort(mem.begin(), mem.end(),
-              [&](int64_t p, int64_t r) { return t->node_key[t->leaf_node[p]] < t->node_key[t->leaf_node[r]]; });
-    if (x_ptr[b] + int64_t(mem.size()) > x_cap) return 4;
-    for (size_t i = 0; i < mem.size(); ++i) x_idx[x_ptr[b] + i] = mem[i];
-    x_ptr[b + 1] = x_ptr[b] + int64_t(mem.size());
-  }
+    *ptr = dup(p);
+    *idx = dup(ix);
+    *total = int64_t(ix.size());
+  };
+  csr(U, &out->u_ptr, &out->u_idx, &out->n_u);
+  csr(W, &out->w_ptr, &out->w_idx, &out->n_w);
+  csr(V, &out->v_ptr, &out->v_idx, &out->n_v);
+  csr(X, &out->x_ptr, &out->x_idx, &out->n_x);
+  std::vector<int32_t> tvs;
+  for (const auto& l : TV) tvs.insert(tvs.end(), l.begin(), l.end());
+  out->v_tv = dup(tvs);
   return 0;
+}
+
+void oracle_csr_free(oracle_csr* c) {
+  for (void* p : {(void*)c->u_ptr, (void*)c->u_idx, (void*)c->v_ptr, (void*)c->v_idx, (void*)c->v_tv,
+                  (void*)c->w_ptr, (void*)c->w_idx, (void*)c->x_ptr, (void*)c->x_idx})
+    std::free(p);
+  std::memset(c, 0, sizeof(*c));
 }
 
 int64_t oracle_tree_leaves(const double* pos, int64_t n, int32_t n_crit, const double dom[4], int32_t balance,

@@ -54,14 +54,20 @@ int oracle_downward(const kifmm_tree_view* tree, const kifmm_operator_view* ops,
 void oracle_direct(const double* positions, const double* charges, int64_t n, const int64_t* targets,
                    int64_t m, double* potential, double* gradient, int32_t threads);
 
-/* Brute-force lists from the definitions (X on all nodes),
- * written in the same CSR layout as kifmm_tree_view.  Buffers sized by the
- * caller from the product's list sizes; returns 0 if every CSR fits and
- * matches in length, else the 1-based list id (1 U, 2 V, 3 W, 4 X) that differs
- * in total length.  The caller compares contents. */
-int oracle_lists_bruteforce(const kifmm_tree_view* tree, int64_t* u_ptr, int64_t* u_idx, int64_t u_cap,
-                            int64_t* v_ptr, int64_t* v_idx, int32_t* v_tv, int64_t v_cap, int64_t* w_ptr,
-                            int64_t* w_idx, int64_t w_cap, int64_t* x_ptr, int64_t* x_idx, int64_t x_cap);
+/* Brute-force lists from the definitions (X on all nodes) for the target leaves
+ * leaf_targets (U, W lists) and target nodes node_targets (V with transfer-vector ids, X), every target
+ * checked against every candidate of the tree, in the CSR layout of kifmm_tree_view (one row per
+ * target, in the order given; members in ascending raw key).  Arrays are malloc'ed; release them
+ * with oracle_csr_free. */
+typedef struct oracle_csr {
+  int64_t *u_ptr, *u_idx, *v_ptr, *v_idx;
+  int32_t* v_tv;
+  int64_t *w_ptr, *w_idx, *x_ptr, *x_idx;
+  int64_t n_u, n_v, n_w, n_x; /* total members */
+} oracle_csr;
+int oracle_lists_subset(const kifmm_tree_view* tree, int64_t n_leaf_targets, const int64_t* leaf_targets,
+                        int64_t n_node_targets, const int64_t* node_targets, int32_t threads, oracle_csr* out);
+void oracle_csr_free(oracle_csr* c);
 
 /* Brute-force recursive split + pairwise balance.
  * Writes the sorted leaf keys (capacity cap) and returns their count (or -1). */
