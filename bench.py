@@ -14,13 +14,15 @@ gradient, fp32.  Synthetic seeded data (splitmix64, generators.py).
           Fmm.evaluate_ptr per step (no overlap).
   roofline: the dominant kernel (M2L) -- useful flops 2*n_e*n_c per V pair over
           its measured launch time, against the measured peak of the unit it uses.
-  cpu_baseline: the fp64 C++ oracle (restatement of SPEC.md) on the host cores,
-          bounded sample (full upward pass + downward for a Morton range of leaves).
+  cpu_baseline: the fp64 C++ oracle (restatement of SPEC.md) on all host cores,
+          full evaluates (mean of 3).
 
-`--impl reference` times that CPU restatement alone (the reference ships no
-runnable FMM) and prints the same JSON schema with "impl": "reference".
-For N > 1 (torchrun) the leaves are Morton-partitioned across ranks (strong
-scaling of the same 1M-point problem) with an NCCL all-gather of multipoles.
+`--impl reference` times that CPU restatement alone -- full evaluates, inputs built
+in a child process so only liboracle.so is mapped (the reference ships no runnable
+FMM) -- and prints the same JSON schema with "impl": "reference".
+For N > 1 (torchrun, or `--gpus N` alone: bench.py then starts N ranks itself) the
+leaves are Morton-partitioned across ranks (strong scaling of the same 1M-point
+problem) with an NCCL all-gather of halo multipoles.
 """
 from __future__ import annotations
 
@@ -38,6 +40,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIG = 2
+# BASELINE.json configs (mirrors paper_2303_08394_b200.generators.CONFIGS, which the reference arm must not
+# import: importing the package maps the product library)
+CONFIGS_META = {
+    1: dict(kind="uniform-cube", p=5, n_crit=64, gradient=False),
+    2: dict(kind="uniform-cube", p=6, n_crit=150, gradient=True),
+    3: dict(kind="sphere-surface", p=6, n_crit=150, gradient=False),
+    4: dict(kind="uniform-cube", p=7, n_crit=150, gradient=False),
+    5: dict(kind="uniform-cube", p=6, n_crit=128, gradient=False),
+}
 
 
 def parse():
@@ -49,7 +60,6 @@ def parse():
     ap.add_argument("--config", type=int, default=CONFIG)
     ap.add_argument("--m2l-backend", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-fraction", type=float, default=0.25)
     return ap.parse_args()
 
 
@@ -142,58 +152,109 @@ def ncu_traffic(name):
         return None
 
 
-def cpu_sample(tree, ops, q_reordered, fraction, steps=1):
-    """Oracle (fp64 C++ restatement) on a bounded sample; returns (points/s, threads, desc, seconds)."""
-    import oracle  # CPU baseline leg only
+def cpu_info():
+    """Host CPU of the baseline run (nproc, model, OpenMP threads)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
-    nl = tree.n_leaves
-    take = max(1, int(round(nl * fraction)))
-    lb = (nl - take) // 2
-    le = lb + take
-    pts = int(tree.leaf_ptr[le] - tree.leaf_ptr[lb])
-    threads = os.cpu_count() or 1
+
+def oracle_full_evaluate(tree, ops, q_reordered, gradient, steps):
+    """The fp64 C++ oracle (restatement of SPEC.md's evaluate) -- the WHOLE evaluate (P2M, M2M, M2L,
+    P2L, L2L, L2P, M2P, near field over every leaf), all host threads; returns per-step seconds."""
+    import oracle  # CPU baseline / reference leg only
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        oracle.evaluate(tree, ops, q_reordered, gradient=True, threads=threads, leaf_range=(lb, le))
+        oracle.evaluate(tree, ops, q_reordered, gradient=gradient, threads=0)
         times.append(time.perf_counter() - t0)
-    t = float(np.mean(times))
-    desc = (f"fp64 oracle, full upward pass (P2M+M2M over all {nl} leaves) + downward/near field for a "
-            f"Morton range of {take} leaves ({pts} target points, {fraction:.4f} of the leaves); "
-            f"points/s = target points / wall time, mean of {steps}")
-    return pts / t, threads, desc, t
+    return times
 
 
 def run_reference(args):
+    """Reference arm: the reference's CPU evaluate, i.e. the oracle (the reference ships no runnable FMM,
+    SURVEY 0 / 8c), timed over full evaluates.  Its inputs (tree, lists, operators, charges) are built in
+    a child process (tools/ref_inputs.py) and loaded from .npz, so this process maps liboracle.so only."""
+    import tempfile
+
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_2303_08394_b200 import generators, host
-
-    c = generators.CONFIGS[args.config]
-    pos, q = generators.config_sample(args.config)
-    tree = host.Tree(pos, c["n_crit"])
-    ops = host.Operators(c["p"], domain_side=tree.side)
-    qr = q[tree.original_index]
-    for _ in range(max(0, min(args.warmup, 1))):
-        cpu_sample(tree, ops, qr, args.cpu_fraction / 2, 1)
-    value, threads, desc, t = cpu_sample(tree, ops, qr, args.cpu_fraction / 2, args.steps)
+    c = CONFIGS_META[args.config]
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, f"config{args.config}.npz")
+        t0 = time.perf_counter()
+        subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ref_inputs.py"), str(args.config), path],
+                       check=True)
+        setup_s = time.perf_counter() - t0
+        import oracle
+        from oracle import views
+        tree, ops = views.load(path)
+        with np.load(path) as z:
+            qr = np.ascontiguousarray(z["charges_reordered"])
+    steps, warm = max(1, min(args.steps, 10)), min(args.warmup, 1)
+    oracle_full_evaluate(tree, ops, qr, c["gradient"], warm)
+    times = oracle_full_evaluate(tree, ops, qr, c["gradient"], steps)
+    t = float(np.mean(times))
+    value = tree.n / t
+    threads = oracle.max_threads()
+    desc = (f"fp64 C++ oracle (restatement of SPEC.md's evaluate), the full evaluate of all {tree.n} points "
+            f"({tree.n_leaves} leaves) per step, {threads} OpenMP threads; mean of {steps} steps after {warm} "
+            f"warm-up (std {float(np.std(times)) * 1e3:.1f} ms); tree/lists/operators built in a child process")
     line = {
         "impl": "reference", "metric": "FMM evaluate points/sec at N=1M p=6", "value": value, "unit": "points/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"BASELINE config {args.config}: N={c['n']} {c['kind']}, p={c['p']}, "
-                               f"n_crit={c['n_crit']}, gradient={c['gradient']}", "parallelism": "cpu-openmp"},
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port", "sample": desc},
+        "config": {"workload": f"BASELINE config {args.config}: N={tree.n} {c['kind']}, p={c['p']}, "
+                               f"n_crit={c['n_crit']}, gradient={c['gradient']}", "parallelism": "cpu-openmp",
+                   "steps_requested": args.steps, "warmup_requested": args.warmup},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port", "sample": desc,
+                         **cpu_info(), "omp_max_threads": threads},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": round(setup_s, 2),
     }
     print(json.dumps(line), flush=True)
 
 
+def _free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def _rank_entry(rank, argv, world, port):
+    os.environ.update({"RANK": str(rank), "LOCAL_RANK": str(rank), "WORLD_SIZE": str(world),
+                       "LOCAL_WORLD_SIZE": str(world), "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    sys.argv = argv
+    main()
+
+
 def main():
     args = parse()
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None and int(env_world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}; refusing to time a different "
+                 "number of GPUs than requested")
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference(args)  # rank 0 only; CPU
+    if env_world is None and args.gpus > 1:
+        # not launched by torchrun: start one process per GPU ourselves (rendezvous on 127.0.0.1)
+        import torch
+        import torch.multiprocessing as mp
+        if torch.cuda.device_count() < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} CUDA devices visible")
+        mp.spawn(_rank_entry, args=(list(sys.argv), args.gpus, _free_port()), nprocs=args.gpus, join=True)
+        return
 
     import torch
 
@@ -228,6 +289,7 @@ def main():
                         m2l_backend=args.m2l_backend, rank=rank, world_size=world, nccl_unique_id=uid)
     f = fmm.Fmm(pos, cfg)
     info = f.info()
+    setup = {k: round(v, 3) for k, v in f.timings.items()}  # host tree + lists, operator precompute, plan
 
     # ---- device-resident run (value)
     dq = torch.from_numpy(q.astype(ndt)).to("cuda")
@@ -374,9 +436,13 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
+        import oracle
         qr = q[f.tree.original_index]
-        v, th, desc, _ = cpu_sample(f.tree, f.operators, qr, args.cpu_fraction, 1)
-        cpu = {"value": v, "unit": "points/s", "cores": th, "kind": "port", "sample": desc}
+        ts = oracle_full_evaluate(f.tree, f.operators, qr, c["gradient"], 3)
+        th = oracle.max_threads()
+        cpu = {"value": n / float(np.mean(ts)), "unit": "points/s", "cores": th, "kind": "port",
+               "sample": f"fp64 C++ oracle, the full evaluate of all {n} points per step, {th} OpenMP threads, "
+                         f"mean of 3 (std {float(np.std(ts)) * 1e3:.1f} ms)", **cpu_info(), "omp_max_threads": th}
 
     line = {
         "metric": "FMM evaluate points/sec at N=1M p=6", "value": value, "unit": "points/s", "n_gpus": world,
@@ -394,6 +460,9 @@ def main():
                 "single_call": {"value": e2e_single, "unit": "points/s",
                                 "api": "Fmm.evaluate_ptr (kifmm_gpu_evaluate) once per step, synchronous"}},
         "gpu_launches": int(info["kernel_launches"]) * args.steps,
+        "setup_s": dict(setup, note="tree_s: host C++ tree + U/V/W/X lists; precompute_s: operator cache (SVDs, "
+                                    "K_t); plan_s: GPU plan creation (upload, work lists, warm-up); all outside "
+                                    "the timed evaluate window (SURVEY 8d)"),
         "roofline": roof, "p2p": p2p, "phases_ms": ph, "clocks": clk.summary(), "cpu_baseline": cpu,
         "plan": {k: info[k] for k in ("n_leaves", "n_nodes", "near_pairs", "m2l_pairs", "m2l_padded_pairs",
                                       "device_bytes", "kernel_launches")},

@@ -37,6 +37,8 @@ _lib.oracle_direct.argtypes = [P, P, i64, P, i64, P, P, i32]
 _lib.oracle_direct.restype = None
 _lib.oracle_tree_leaves.argtypes = [P, i64, i32, P, i32, P, i64]
 _lib.oracle_tree_leaves.restype = i64
+_lib.oracle_max_threads.argtypes = []
+_lib.oracle_max_threads.restype = i32
 _lib.oracle_relative_error.argtypes = [P, P, i64]
 _lib.oracle_relative_error.restype = f64
 
@@ -151,6 +153,11 @@ def tree_leaves(positions, n_crit, domain, balance=True):
     if n < 0:
         raise RuntimeError("oracle_tree_leaves failed")
     return out[:n]
+
+
+def max_threads():
+    """OpenMP threads the oracle uses with threads = 0 (omp_get_max_threads())."""
+    return int(_lib.oracle_max_threads())
 
 
 def relative_error(a, b):

@@ -457,6 +457,8 @@ void oracle_direct(const double* pos, const double* q, int64_t n, const int64_t*
   });
 }
 
+int32_t oracle_max_threads(void) { return resolve(0); }
+
 double oracle_relative_error(const double* a, const double* b, int64_t n) {
   long double num = 0, den = 0;
   for (int64_t i = 0; i < n; ++i) {

@@ -74,6 +74,9 @@ void oracle_csr_free(oracle_csr* c);
 int64_t oracle_tree_leaves(const double* positions, int64_t n, int32_t n_crit, const double domain[4],
                            int32_t balance, uint64_t* leaves, int64_t cap);
 
+/* OpenMP threads the oracle uses with threads = 0 (resolve_threads(0), parallel.hpp:22-26). */
+int32_t oracle_max_threads(void);
+
 /* Relative L2 error ||a-b|| / ||b||; -1 when ||b|| = 0. */
 double oracle_relative_error(const double* a, const double* b, int64_t n);
 

@@ -37,12 +37,15 @@ CASES = [("uniform-cube", 6000, 40, 4), ("uniform-cube", 5000, 50, 6), ("sphere-
 
 
 @pytest.mark.parametrize("kind,n,n_crit,p", CASES)
-@pytest.mark.parametrize("precision", [64, 32])
-def test_parity_vs_oracle(require_gpu, kind, n, n_crit, p, precision):
+@pytest.mark.parametrize("precision,backend", [(64, 0), (32, 1), (32, 0)],
+                         ids=["fp64", "fp32-simt", "fp32-auto"])
+def test_parity_vs_oracle(require_gpu, kind, n, n_crit, p, precision, backend):
+    """backend 0 = the production choice (tcgen05 M2L and GEMMs for fp32 p = 6, DMMA for fp64),
+    1 = the SIMT M2L / GEMM kernels."""
     if precision == 32 and p >= 7:
         pytest.skip("fp32 at p=7: kept spectrum cond ~1e11, see test_fp32_p7_accuracy_bound")
     pos, q = generators.sample(kind, n, seed=7, charges="signed", fp32=precision == 32)
-    cfg = fmm.FmmConfig(p=p, n_crit=n_crit, precision=precision, gradient=True, m2l_backend=1)
+    cfg = fmm.FmmConfig(p=p, n_crit=n_crit, precision=precision, gradient=True, m2l_backend=backend)
     with fmm.Fmm(pos, cfg) as f:
         pot, grad, _ = f.evaluate(q)
         ref, gref = _ref(f, q, True)

@@ -1,0 +1,93 @@
+"""GPU evaluate vs the fp64 oracle at every BASELINE.json configuration, full size (north star:
+"potentials must match the reference's own FMM output within a relative L2 error of 1e-5 (fp32) or
+1e-12 (fp64); and both must be checked against direct summation on 1,000 sampled targets").
+
+The GPU runs the whole evaluate (production path: tcgen05 M2L / GEMMs for fp32 p = 6, DMMA for
+fp64).  The oracle runs its complete upward pass once (P2M + M2M over every leaf and level) and then
+its downward pass (M2L, P2L, L2L, L2P, M2P, near field) for three Morton ranges of target leaves --
+at the start, middle and end of the Z-order -- so the comparison covers every operator on
+size-independent samples in seconds.  Potential and gradient are gated separately.  Measured errors
+and their margin to the gate are printed and appended to gpurun_out/parity_r02.jsonl when that
+directory exists (the committed copy is profiles/r02_parity_configs.jsonl).
+"""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2303_08394_b200 import fmm, generators
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GATE = {32: (1e-5, 5e-5), 64: (1e-12, 1e-11)}
+FRACTION = {1: 0.2, 2: 0.01, 3: 0.01, 4: 0.004, 5: 0.001}  # leaves per sampled range
+
+
+def _log(rec):
+    print(json.dumps(rec))
+    out = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out):
+        with open(os.path.join(out, "parity_r02.jsonl"), "a") as f:
+            f.write(json.dumps(rec) + "\n")
+
+
+def _ranges(nl, frac):
+    take = max(1, int(nl * frac))
+    starts = [0, (nl - take) // 2, nl - take]
+    return [(s, s + take) for s in starts]
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_config_parity_vs_oracle(require_gpu, cid):
+    c = generators.CONFIGS[cid]
+    prec = c["precision"]
+    dt = np.float32 if prec == 32 else np.float64
+    pos, q = generators.config_sample(cid)
+    cfg = fmm.FmmConfig(p=c["p"], n_crit=c["n_crit"], precision=prec, gradient=c["gradient"])
+    t0 = time.time()
+    with fmm.Fmm(pos, cfg) as f:
+        t1 = time.time()
+        pot, grad, _ = f.evaluate(q.astype(dt), input_order=False)  # reordered order
+        pot_in, grad_in, _ = f.evaluate(q.astype(dt), input_order=True)
+        backend = f.info()["m2l_backend"]
+        tree, ops = f.tree, f.operators
+        qr = q[tree.original_index]
+        # input-order output is the permutation of the reordered one
+        assert np.array_equal(pot_in[tree.original_index], pot)
+        t2 = time.time()
+        M = oracle.upward_local(tree, ops, qr, 0, tree.n_leaves, 0)
+        ref_p, ref_g, got_p, got_g = [], [], [], []
+        for lb, le in _ranges(tree.n_leaves, FRACTION[cid]):
+            phi, g = oracle.downward(tree, ops, qr, M, lb, le, gradient=c["gradient"])
+            a, b = tree.leaf_ptr[lb], tree.leaf_ptr[le]
+            ref_p.append(phi[a:b])
+            got_p.append(pot[a:b])
+            if c["gradient"]:
+                ref_g.append(g[a:b])
+                got_g.append(grad[a:b])
+        t3 = time.time()
+        # direct summation on 1,000 sampled targets (input order), fp64 on the GPU (kernel K10)
+        tg = (generators.uniform(99, 0, 1000) * tree.n).astype(np.int64)
+        d = fmm.direct(pos, q, targets=tg, precision=64, gradient=c["gradient"])
+        dpot, dgrad = d if c["gradient"] else (d, None)
+    ref_p, got_p = np.concatenate(ref_p), np.concatenate(got_p)
+    ep = fmm.relative_error(got_p, ref_p)
+    gp, gg = GATE[prec]
+    rec = {"config": cid, "precision": prec, "p": c["p"], "n": int(tree.n), "leaves": int(tree.n_leaves),
+           "m2l_backend": backend, "sample_targets": int(got_p.size),
+           "sample": f"3 Morton ranges of {FRACTION[cid]:.3%} of the leaves (start / middle / end)",
+           "rel_l2_potential_vs_oracle": ep, "gate_potential": gp, "margin_potential": gp / max(ep, 1e-300),
+           "rel_l2_potential_vs_direct_1000": fmm.relative_error(pot_in[tg], dpot),
+           "seconds": {"plan": round(t1 - t0, 1), "oracle": round(t3 - t2, 1)}}
+    if c["gradient"]:
+        ref_g, got_g = np.concatenate(ref_g), np.concatenate(got_g)
+        eg = fmm.relative_error(got_g, ref_g)
+        rec.update({"rel_l2_gradient_vs_oracle": eg, "gate_gradient": gg, "margin_gradient": gg / max(eg, 1e-300),
+                    "rel_l2_gradient_vs_direct_1000": fmm.relative_error(grad_in[tg], dgrad)})
+    _log(rec)
+    assert ep <= gp, rec
+    if c["gradient"]:
+        assert eg <= gg, rec
