@@ -126,10 +126,34 @@ void kifmm_tree_destroy(kifmm_tree* tree);
 int32_t kifmm_transfer_vectors(int32_t out[316 * 3]);
 
 /* Contiguous Z-order leaf ranges per rank for multi-GPU, balanced
- * by estimated cost and aligned to level-`cut_level` boxes. leaf_begin has
- * world_size + 1 entries. */
+ * by estimated cost and aligned to level-`cut_level` boxes (0 = auto, see
+ * kifmm_halo_plan). leaf_begin has world_size + 1 entries. */
 kifmm_status kifmm_partition_leaves(const kifmm_tree_view* tree, int32_t n_e, int32_t gradient,
                                     int32_t world_size, int32_t cut_level, int64_t* leaf_begin);
+
+/* Halo-exchange tables of the multi-GPU evaluate, built on the host (no device needed)
+ * and used by kifmm_gpu_plan_create for world_size > 1.  Rank r owns leaves
+ * [leaf_begin[r], leaf_begin[r+1]) (ranges aligned to level-cut_level boxes; cut_level 0 = auto: the
+ * coarsest level >= 2 that balances the estimated cost within 5 %) and computes the multipoles of the
+ * nodes with up_owner == r, i.e. whose leaves all lie in its range; the few nodes spanning ranks
+ * (up_owner == -1) are recomputed by every rank from their children.  After the upward pass each rank r contributes the
+ * rows export_idx[export_ptr[r] .. export_ptr[r+1]) -- the multipoles it owns that another rank reads
+ * (V lists of its targets, W lists of its leaves, children of the redundant top nodes) -- to an
+ * all-gather of world_size slots of max_export rows each. */
+typedef struct kifmm_halo kifmm_halo;
+typedef struct kifmm_halo_view {
+  int32_t world_size, cut_level;
+  int64_t n_nodes;
+  const int64_t* leaf_begin;  /* world_size + 1 */
+  const int32_t* up_owner;    /* n_nodes */
+  const int64_t* export_ptr;  /* world_size + 1 */
+  const int64_t* export_idx;  /* export_ptr[world_size] node indices, ascending within a rank */
+  int64_t max_export;         /* rows per all-gather slot */
+} kifmm_halo_view;
+kifmm_status kifmm_halo_plan(const kifmm_tree_view* tree, int32_t n_e, int32_t gradient, int32_t world_size,
+                             int32_t cut_level, kifmm_halo** out);
+kifmm_status kifmm_halo_get_view(const kifmm_halo* halo, kifmm_halo_view* view);
+void kifmm_halo_destroy(kifmm_halo* halo);
 
 /* --------------------------------------------------------------- operators
  * SPEC.md:413-428, design 501-504.  Pseudo-inverses are stored FACTORED
@@ -184,12 +208,15 @@ typedef struct kifmm_gpu_options {
   int32_t device;         /* CUDA ordinal */
   int32_t rank;           /* multi-GPU: this process's rank (one process per GPU) */
   int32_t world_size;     /* 1 = single GPU */
-  int32_t cut_level;      /* partition alignment level for world_size > 1 (default 2) */
+  int32_t cut_level;      /* partition alignment level for world_size > 1 (0 = auto, kifmm_halo_plan) */
   const void* nccl_unique_id; /* 128 bytes from kifmm_gpu_nccl_unique_id() on rank 0 */
   int32_t m2l_backend;    /* 0 auto, 1 SIMT (fp32) / DMMA (fp64), 2 tcgen05 (fp32 only): kind::f16
                              3-term fp16 split by default -- reported as 2 -- or kind::tf32 3xTF32 with
                              KIFMM_TC_KIND=tf32 -- reported as 3 */
   int32_t use_graph;      /* capture the evaluate in a CUDA graph */
+  int32_t exchange;       /* world_size > 1: 0 = NCCL all-gather inside the evaluate (one process per GPU);
+                             1 = host: the caller moves the halo rows between kifmm_gpu_evaluate_upward and
+                             kifmm_gpu_evaluate_downward (no NCCL; e.g. ranks emulated by one process) */
 } kifmm_gpu_options;
 
 typedef struct kifmm_gpu_timings {
@@ -218,6 +245,8 @@ typedef struct kifmm_gpu_plan_info {
   int32_t m2l_backend;      /* backend actually used */
   int64_t device_bytes;     /* device memory held by the plan */
   int32_t kernel_launches;  /* kernels launched per evaluate */
+  int64_t halo_rows_max;    /* world_size > 1: rows per all-gather slot (kifmm_halo_view.max_export) */
+  int64_t halo_rows_mine;   /* rows this rank exports */
 } kifmm_gpu_plan_info;
 
 kifmm_status kifmm_gpu_plan_create(const kifmm_gpu_options* options, const kifmm_tree_view* tree,
@@ -244,6 +273,17 @@ kifmm_status kifmm_gpu_evaluate_many(kifmm_gpu_plan* plan, int32_t n_rhs, const 
 kifmm_status kifmm_gpu_evaluate_device(kifmm_gpu_plan* plan, const void* d_charges,
                                        void* d_potential, void* d_gradient, int32_t input_order,
                                        void* stream);
+/* Host-exchange halves of a multi-rank evaluate (options.exchange = 1).  upward: charges
+ * (host, full vector, input_order as in kifmm_gpu_evaluate) -> P2M + M2M of the rank's subtrees; writes
+ * the rank's export rows to export_rows (host, halo_rows_max x ne_pad values of the plan precision, rows
+ * in kifmm_halo_view export order, the tail unwritten).  downward: gathered (host, world_size slots laid
+ * out like export_rows, slot r = rank r's export_rows) -> import + redundant top M2M + downward pass +
+ * leaves; writes potential / gradient like kifmm_gpu_evaluate with the input_order of the upward call.
+ * Each call is synchronous; the two must alternate. */
+kifmm_status kifmm_gpu_evaluate_upward(kifmm_gpu_plan* plan, const void* charges, int32_t input_order,
+                                       void* export_rows);
+kifmm_status kifmm_gpu_evaluate_downward(kifmm_gpu_plan* plan, const void* gathered, void* potential,
+                                         void* gradient);
 kifmm_status kifmm_gpu_plan_get_info(const kifmm_gpu_plan* plan, kifmm_gpu_plan_info* info);
 /* Per-phase device timings (CUDA events on the plan stream) of the last kifmm_gpu_evaluate call that
  * passed a timings struct (a serialized, instrumented run; evaluate_device / evaluate_many are never

@@ -75,6 +75,17 @@ def upward_top(tree, ops, M, cut_level, threads=0):
     return M
 
 
+_lib.oracle_m2m_nodes.argtypes = [P, P, i64, P, P]
+
+
+def m2m_nodes(tree, ops, nodes, M):
+    """M2M of `nodes` (children before parents) into M (n_nodes x n_e, updated in place and returned)."""
+    nd = np.ascontiguousarray(nodes, dtype=np.int64)
+    assert M.flags.c_contiguous and M.dtype == np.float64
+    _lib.oracle_m2m_nodes(C.addressof(tree.view), C.addressof(ops.view), nd.size, nd.ctypes.data, M.ctypes.data)
+    return M
+
+
 def downward(tree, ops, charges_reordered, M, leaf_begin, leaf_end, gradient=False, threads=0):
     q = np.ascontiguousarray(charges_reordered, dtype=np.float64)
     M = np.ascontiguousarray(M, dtype=np.float64)

@@ -291,6 +291,12 @@ int oracle_upward_top(const kifmm_tree_view* t, const kifmm_operator_view* o, in
   return 0;
 }
 
+int oracle_m2m_nodes(const kifmm_tree_view* t, const kifmm_operator_view* o, int64_t n, const int64_t* nodes,
+                     double* M) {
+  for (int64_t i = 0; i < n; ++i) m2m_node(t, o, nodes[i], M);  // in the given (bottom-up) order
+  return 0;
+}
+
 int oracle_downward(const kifmm_tree_view* t, const kifmm_operator_view* o, const double* q, const double* M,
                     int64_t lb, int64_t le, double* phi, double* grad, int32_t threads, oracle_timings* tm) {
   threads = resolve(threads);

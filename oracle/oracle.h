@@ -45,6 +45,10 @@ int oracle_upward_local(const kifmm_tree_view* tree, const kifmm_operator_view* 
                         int32_t threads);
 int oracle_upward_top(const kifmm_tree_view* tree, const kifmm_operator_view* ops, int32_t cut_level,
                       double* multipole, int32_t threads);
+/* M2M of the listed non-leaf nodes, in the given order (children before parents):
+ * the multi-rank top of the tree, recomputed by every rank from gathered rows. */
+int oracle_m2m_nodes(const kifmm_tree_view* tree, const kifmm_operator_view* ops, int64_t n, const int64_t* nodes,
+                     double* multipole);
 int oracle_downward(const kifmm_tree_view* tree, const kifmm_operator_view* ops, const double* charges,
                     const double* multipole, int64_t leaf_begin, int64_t leaf_end, double* potential,
                     double* gradient, int32_t threads, oracle_timings* timings);

@@ -48,11 +48,19 @@ class OperatorView(C.Structure):
     ]
 
 
+class HaloView(C.Structure):
+    _fields_ = [
+        ("world_size", i32), ("cut_level", i32), ("n_nodes", i64),
+        ("leaf_begin", C.POINTER(i64)), ("up_owner", C.POINTER(i32)),
+        ("export_ptr", C.POINTER(i64)), ("export_idx", C.POINTER(i64)), ("max_export", i64),
+    ]
+
+
 class GpuOptions(C.Structure):
     _fields_ = [
         ("precision", i32), ("gradient", i32), ("device", i32), ("rank", i32),
         ("world_size", i32), ("cut_level", i32), ("nccl_unique_id", P),
-        ("m2l_backend", i32), ("use_graph", i32),
+        ("m2l_backend", i32), ("use_graph", i32), ("exchange", i32),
     ]
 
 
@@ -73,7 +81,7 @@ class GpuPlanInfo(C.Structure):
         ("near_pairs", i64), ("l2p_pairs", i64), ("m2p_pairs", i64), ("p2m_pairs", i64), ("p2l_pairs", i64),
         ("m2l_pairs", i64), ("m2l_padded_pairs", i64),
         ("n_e", i32), ("n_c", i32), ("ne_pad", i32), ("m2l_backend", i32),
-        ("device_bytes", i64), ("kernel_launches", i32),
+        ("device_bytes", i64), ("kernel_launches", i32), ("halo_rows_max", i64), ("halo_rows_mine", i64),
     ]
 
     def as_dict(self):
@@ -109,6 +117,9 @@ _SIGS = {
     "kifmm_tree_destroy": (None, [P]),
     "kifmm_transfer_vectors": (i32, [P]),
     "kifmm_partition_leaves": (i32, [C.POINTER(TreeView), i32, i32, i32, i32, P]),
+    "kifmm_halo_plan": (i32, [C.POINTER(TreeView), i32, i32, i32, i32, C.POINTER(P)]),
+    "kifmm_halo_get_view": (i32, [P, C.POINTER(HaloView)]),
+    "kifmm_halo_destroy": (None, [P]),
     "kifmm_precompute": (i32, [i32, f64, f64, f64, f64, i32, C.POINTER(P)]),
     "kifmm_operators_get_view": (i32, [P, C.POINTER(OperatorView)]),
     "kifmm_operators_destroy": (None, [P]),
@@ -120,6 +131,8 @@ _SIGS = {
     "kifmm_gpu_evaluate": (i32, [P, P, P, P, i32, C.POINTER(GpuTimings)]),
     "kifmm_gpu_evaluate_device": (i32, [P, P, P, P, i32, P]),
     "kifmm_gpu_evaluate_many": (i32, [P, i32, C.POINTER(P), C.POINTER(P), C.POINTER(P), i32]),
+    "kifmm_gpu_evaluate_upward": (i32, [P, P, i32, P]),
+    "kifmm_gpu_evaluate_downward": (i32, [P, P, P, P]),
     "kifmm_gpu_plan_get_info": (i32, [P, C.POINTER(GpuPlanInfo)]),
     "kifmm_gpu_last_timings": (i32, [P, C.POINTER(GpuTimings)]),
     "kifmm_gpu_plan_destroy": (None, [P]),

@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cstdio>
 
+#include "halo.hpp"
 #include "m2l_tc.cuh"
 #include "morton.hpp"
 #include "p2p.cuh"
@@ -194,16 +195,32 @@ __global__ void gather_rows_kernel(const T* __restrict__ src, int ld, const int*
   if (r >= n) return;
   for (int j = threadIdx.x; j < ld; j += blockDim.x) dst[size_t(r) * ld + j] = src[size_t(rows[r]) * ld + j];
 }
+// dst[rows[k]] = src[slot[k]] for the k-th received row (slot = rank * x_max + position in its export list)
 template <class T>
 __global__ void scatter_rows_kernel(const T* __restrict__ src, int ld, const int* __restrict__ rows,
-                                    const int* __restrict__ rank_of, int max_rows, int me, int n, T* __restrict__ dst) {
-  const int r = blockIdx.x;  // flat over all ranks' exported rows
-  if (r >= n || rank_of[r] == me) return;
-  const int rank = rank_of[r];
-  // position of this row inside its rank's slot = r - first row of that rank; stored in rows[n + r]
-  const int pos = rows[n + r];
-  const T* s = src + (size_t(rank) * max_rows + pos) * ld;
-  for (int j = threadIdx.x; j < ld; j += blockDim.x) dst[size_t(rows[r]) * ld + j] = s[j];
+                                    const int* __restrict__ slot, int n, T* __restrict__ dst) {
+  const int k = blockIdx.x;
+  if (k >= n) return;
+  const T* a = src + size_t(slot[k]) * ld;
+  T* b = dst + size_t(rows[k]) * ld;
+  for (int j = threadIdx.x; j < ld; j += blockDim.x) b[j] = a[j];
+}
+// fp32 / p = 6 (tcgen05 path): warp per received row, also writes the row's fp16 split (M2L A operand)
+__global__ void scatter_rows_split_kernel(const float* __restrict__ src, const int* __restrict__ rows,
+                                          const int* __restrict__ slot, int n, float* __restrict__ dst,
+                                          __half* __restrict__ hi, __half* __restrict__ lo, float* __restrict__ un) {
+  constexpr int W = tc::NP;
+  const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (k >= n) return;
+  const float* a = src + size_t(slot[k]) * W;
+  const size_t row = size_t(rows[k]);
+  float v[W / 32];
+#pragma unroll
+  for (int c = 0; c < W / 32; ++c) {
+    v[c] = a[lane + 32 * c];
+    dst[row * W + lane + 32 * c] = v[c];
+  }
+  split_row_warp<W>(v, lane, row, hi, lo, un);
 }
 
 template <class T>
@@ -367,7 +384,7 @@ struct kifmm_gpu_plan {
   int near_fork_at = 0;  // 0: at the start of the evaluate, 1: just before M2L
   bool grad = false;
   int64_t N = 0, nl = 0, nn = 0;
-  int depth = 0, ne = 0, nc = 0, np = 0, ref_level = 2, cut = 2;
+  int depth = 0, ne = 0, nc = 0, np = 0, ref_level = 2;
   int world = 1, rank = 0;
   int64_t lb = 0, le = 0, pb = 0, pe = 0;  // owned leaves / particles
   int m2l_backend = 1;
@@ -418,8 +435,9 @@ struct kifmm_gpu_plan {
   M2LTcPlan m2l_tc;
   // exchange
   void* comm = nullptr;
-  DevMem x_send, x_recv, x_rows, x_rank, x_my_rows;
+  DevMem x_send, x_recv, x_rows, x_rank /* source slot of each received row */, x_my_rows;
   int x_max = 0, x_total = 0, x_mine = 0;
+  bool host_phase_input_order = true;  // exchange = 1: the input_order of the pending upward half
   // graphs
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   // evaluate_many: copy-in / copy-out streams and double-buffered device staging (created on first use)
@@ -458,8 +476,12 @@ struct kifmm_gpu_plan {
   template <class T>
   void upload_static(const kifmm_tree_view& t, const kifmm_operator_view& ops);
   template <class T>
-  void run(cudaStream_t s, bool input_order, bool timed);
-  void exchange(cudaStream_t s);
+  // phase 1: upward pass (+ the export rows of a multi-rank plan into x_send); 2: exchange import +
+  // downward pass + leaves; 3: both, with the NCCL all-gather between them
+  void run(cudaStream_t s, bool input_order, bool timed, int phase = 3);
+  void gather_exports(cudaStream_t s);
+  void allgather(cudaStream_t s);
+  void scatter_imports(cudaStream_t s);
   void evaluate_device(const void* q, void* pot_dst, void* grad_dst, bool input_order, cudaStream_t user, bool timed);
   // the captured evaluate graph of this output order (captured on the plan stream on first use, with the
   // capture always ended -- also when a launch throws -- so the stream never stays in capture mode),
@@ -492,6 +514,28 @@ struct kifmm_gpu_plan {
   // that one ran on (the plan's buffers -- q_in, src4, M, L, check rows, outputs, the near-field counter --
   // are shared by all of them): wait on `ev_done` first, record it last.
   void begin(cudaStream_t s) { KIFMM_CUDA(cudaStreamWaitEvent(s, ev_done, 0)); }
+  void require_single_call() const {
+    if (world > 1 && opt.exchange == 1)
+      throw InvalidArgument("evaluate: a host-exchange plan runs as kifmm_gpu_evaluate_upward + _downward");
+  }
+  // results (input order: the full vector, other ranks' entries zero; reordered: this rank's range) -> dst
+  void copy_out(void* pot_dst, void* grad_dst, bool input_order, cudaStream_t s) {
+    const size_t es = esz();
+    const void* ps = input_order ? pot_out.p : pot.p;
+    const void* gs = input_order ? grad_out.p : grad_buf.p;
+    if (input_order || world == 1) {
+      if (pot_dst) KIFMM_CUDA(cudaMemcpyAsync(pot_dst, ps, size_t(N) * es, cudaMemcpyDefault, s));
+      if (grad && grad_dst) KIFMM_CUDA(cudaMemcpyAsync(grad_dst, gs, size_t(N) * 3 * es, cudaMemcpyDefault, s));
+    } else {
+      const size_t off = size_t(pb) * es, cnt = size_t(pe - pb) * es;
+      if (pot_dst && cnt)
+        KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(pot_dst) + off, static_cast<const char*>(ps) + off, cnt,
+                                   cudaMemcpyDefault, s));
+      if (grad && grad_dst && cnt)
+        KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(grad_dst) + 3 * off, static_cast<const char*>(gs) + 3 * off,
+                                   3 * cnt, cudaMemcpyDefault, s));
+    }
+  }
   void finish(cudaStream_t s) { KIFMM_CUDA(cudaEventRecord(ev_done, s)); }
   void evaluate_many(int n_rhs, const void* const* charges, void* const* potentials, void* const* gradients,
                      bool input_order);
@@ -581,7 +625,6 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   grad = o.gradient != 0;
   world = std::max(1, o.world_size);
   rank = o.rank;
-  cut = o.cut_level > 0 ? o.cut_level : 2;
   if (precision != 32 && precision != 64) throw InvalidArgument("gpu: precision must be 32 or 64");
   if (rank < 0 || rank >= world) throw InvalidArgument("gpu: rank out of range");
   if (ops.n_e != ops.n_c) throw InvalidArgument("gpu: n_c != n_e is not supported");
@@ -618,40 +661,18 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   for (auto& e : ev) KIFMM_CUDA(cudaEventCreate(&e));
 
   ptick("setup");
-  // ---- partition
-  std::vector<int64_t> lbeg(world + 1, 0);
-  lbeg[world] = nl;
-  if (world > 1) {
-    const kifmm_status st = kifmm_partition_leaves(&t, ne, grad ? 1 : 0, world, cut, lbeg.data());
-    if (st != KIFMM_OK) throw InvalidArgument(std::string("partition: ") + kifmm_last_error());
-  }
+  // ---- partition, owners, halo export tables (csrc/host/halo.cpp)
+  HaloPlan halo;
+  build_halo_plan(halo, t, ne, grad, world, std::max(0, o.cut_level));
+  const std::vector<int64_t>& lbeg = halo.leaf_begin;
   lb = lbeg[rank];
   le = lbeg[rank + 1];
   pb = t.leaf_ptr[lb];
   pe = t.leaf_ptr[le];
-
-  // leaf range covered by each node (leaves ascend in raw key = spatial order)
-  std::vector<int64_t> nlo(nn, INT64_MAX), nhi(nn, -1);
-  for (int64_t l = 0; l < nl; ++l)
-    for (int64_t n = t.leaf_node[l]; n >= 0; n = t.node_parent[n]) {
-      nlo[n] = std::min(nlo[n], l);
-      nhi[n] = std::max(nhi[n], l + 1);
-    }
   auto node_lvl = [&](int64_t n) { return key_level(t.node_key[n]); };
   auto is_leaf = [&](int64_t n) { return t.node_leaf[n] >= 0; };
-  // owner rank of a node for the upward pass: all leaves in one rank's range and (level >= cut or leaf)
-  auto owner_of_range = [&](int64_t lo, int64_t hi) -> int {
-    const int r = int(std::upper_bound(lbeg.begin(), lbeg.end(), lo) - lbeg.begin()) - 1;
-    return (hi <= lbeg[r + 1]) ? r : -1;
-  };
-  std::vector<int> up_owner(nn, -1);
-  for (int64_t n = 0; n < nn; ++n) {
-    if (world == 1) {
-      up_owner[n] = 0;
-      continue;
-    }
-    if (is_leaf(n) || node_lvl(n) >= cut) up_owner[n] = owner_of_range(nlo[n], nhi[n]);
-  }
+  // owner rank of a node's multipole in the upward pass (-1: every rank recomputes it after the exchange)
+  const std::vector<int32_t>& up_owner = halo.up_owner;
   // downward-active nodes: ancestors-or-self of owned leaves
   std::vector<char> active(nn, 0);
   for (int64_t l = lb; l < le; ++l)
@@ -828,48 +849,54 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   };
   // parents above level 2 get no M2M: V / W members are all at level >= 2, so multipoles of levels 0-1
   // feed no operator (the reference's M2M loop computes them, without observable effect)
-  const int up_floor = world > 1 ? std::max(cut, 2) : 2;
-  for (int l = depth - 1; l >= up_floor; --l) {
+  for (int l = depth - 1; l >= 2; --l) {
     std::vector<int64_t> parents;
     for (int64_t n = t.level_ptr[l]; n < t.level_ptr[l + 1]; ++n)
       if (!is_leaf(n) && up_owner[n] == rank) parents.push_back(n);
     if (!parents.empty()) m2m_levels.push_back(m2m_tiles(parents));
   }
   if (world > 1) {
-    for (int l = std::min(cut, depth) - 1; l >= 2; --l) {
+    // the nodes spanning ranks, recomputed by every rank after the exchange (children first)
+    for (int l = depth - 1; l >= 2; --l) {
       std::vector<int64_t> parents;
       for (int64_t n = t.level_ptr[l]; n < t.level_ptr[l + 1]; ++n)
-        if (!is_leaf(n)) parents.push_back(n);
+        if (!is_leaf(n) && up_owner[n] < 0) parents.push_back(n);
       if (!parents.empty()) m2m_top.push_back(m2m_tiles(parents));
     }
-    // exchange tables: every rank exports the multipoles it owns
-    std::vector<std::vector<int>> exp(world);
-    for (int64_t n = 0; n < nn; ++n)
-      if (up_owner[n] >= 0) exp[up_owner[n]].push_back(int(n));
-    x_max = 0;
-    for (auto& e : exp) x_max = std::max<int>(x_max, int(e.size()));
-    x_mine = int(exp[rank].size());
-    std::vector<int> rows, pos, rk;
+    // all-gather layout: every rank ships its export rows in a slot of x_max rows; this rank scatters the
+    // other ranks' rows into M (and, on the tcgen05 path, their fp16 split)
+    x_max = int(halo.max_export);
+    std::vector<int> mine, rows, src;
     for (int r = 0; r < world; ++r)
-      for (size_t i = 0; i < exp[r].size(); ++i) {
-        rows.push_back(exp[r][i]);
-        pos.push_back(int(i));
-        rk.push_back(r);
+      for (int64_t i = halo.export_ptr[r]; i < halo.export_ptr[r + 1]; ++i) {
+        if (r == rank) {
+          mine.push_back(int(halo.export_idx[i]));
+        } else {
+          rows.push_back(int(halo.export_idx[i]));
+          src.push_back(r * x_max + int(i - halo.export_ptr[r]));
+        }
       }
+    x_mine = int(mine.size());
     x_total = int(rows.size());
-    rows.insert(rows.end(), pos.begin(), pos.end());
+    x_my_rows.upload(mine, &dev_bytes);
     x_rows.upload(rows, &dev_bytes);
-    x_rank.upload(rk, &dev_bytes);
-    x_my_rows.upload(exp[rank], &dev_bytes);
+    x_rank.upload(src, &dev_bytes);
     x_send.alloc(size_t(std::max(1, x_max)) * np * es, &dev_bytes);
     x_recv.alloc(size_t(std::max(1, x_max)) * np * es * world, &dev_bytes);
-    if (!o.nccl_unique_id) throw InvalidArgument("gpu: world_size > 1 needs nccl_unique_id");
-    ncclUniqueId id;
-    std::memcpy(&id, o.nccl_unique_id, sizeof(id));
-    ncclComm_t c;
-    Nccl& nc_ = Nccl::get();
-    nc_.check(nc_.commInitRank(&c, world, id, rank), "ncclCommInitRank");
-    comm = c;
+    KIFMM_CUDA(cudaMemset(x_recv.p, 0, x_recv.bytes));  // a host-exchange plan's warm-up imports zeros
+    info.halo_rows_max = x_max;
+    info.halo_rows_mine = x_mine;
+    if (o.exchange == 0) {
+      if (!o.nccl_unique_id) throw InvalidArgument("gpu: world_size > 1 needs nccl_unique_id (or exchange = 1)");
+      ncclUniqueId id;
+      std::memcpy(&id, o.nccl_unique_id, sizeof(id));
+      ncclComm_t c;
+      Nccl& nc_ = Nccl::get();
+      nc_.check(nc_.commInitRank(&c, world, id, rank), "ncclCommInitRank");
+      comm = c;
+    } else if (o.exchange != 1) {
+      throw InvalidArgument("gpu: exchange must be 0 (NCCL) or 1 (host)");
+    }
   }
 
   m2m_scratch.alloc(size_t(std::max<int64_t>(1, m2m_scratch_rows)) * np * es, &dev_bytes);
@@ -1328,37 +1355,44 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   info.device_bytes = int64_t(dev_bytes);
 }
 
-void kifmm_gpu_plan::exchange(cudaStream_t s) {
-  if (world <= 1) return;
-  const size_t es = esz();
-  if (x_mine > 0) {
-    if (precision == 32)
-      gather_rows_kernel<float><<<x_mine, 128, 0, s>>>(M.as<float>(), np, x_my_rows.as<int>(), x_mine, x_send.as<float>());
-    else
-      gather_rows_kernel<double><<<x_mine, 128, 0, s>>>(M.as<double>(), np, x_my_rows.as<int>(), x_mine, x_send.as<double>());
-    KIFMM_LAUNCH_CHECK();
-  }
+// Multi-GPU exchange: this rank's export rows -> x_send; all-gather (NCCL, or the caller in
+// host mode); the other ranks' rows x_recv -> M (+ fp16 split).
+void kifmm_gpu_plan::gather_exports(cudaStream_t s) {
+  if (x_mine <= 0) return;
+  if (precision == 32)
+    gather_rows_kernel<float><<<x_mine, 128, 0, s>>>(M.as<float>(), np, x_my_rows.as<int>(), x_mine, x_send.as<float>());
+  else
+    gather_rows_kernel<double><<<x_mine, 128, 0, s>>>(M.as<double>(), np, x_my_rows.as<int>(), x_mine, x_send.as<double>());
+  KIFMM_LAUNCH_CHECK();
+}
+
+void kifmm_gpu_plan::allgather(cudaStream_t s) {
   Nccl& n = Nccl::get();
-  n.check(n.allGather(x_send.p, x_recv.p, size_t(x_max) * np, precision == 32 ? ncclFloat32 : ncclFloat64,
-                      static_cast<ncclComm_t>(comm), s),
+  n.check(n.allGather(x_send.p, x_recv.p, size_t(std::max(1, x_max)) * np,
+                      precision == 32 ? ncclFloat32 : ncclFloat64, static_cast<ncclComm_t>(comm), s),
           "ncclAllGather");
-  (void)es;
-  if (x_total > 0) {
-    if (precision == 32)
-      scatter_rows_kernel<float><<<x_total, 128, 0, s>>>(x_recv.as<float>(), np, x_rows.as<int>(), x_rank.as<int>(),
-                                                          x_max, rank, x_total, M.as<float>());
-    else
-      scatter_rows_kernel<double><<<x_total, 128, 0, s>>>(x_recv.as<double>(), np, x_rows.as<int>(), x_rank.as<int>(),
-                                                           x_max, rank, x_total, M.as<double>());
-    KIFMM_LAUNCH_CHECK();
+}
+
+void kifmm_gpu_plan::scatter_imports(cudaStream_t s) {
+  if (x_total <= 0) return;
+  if (precision == 32 && gemm_tc) {
+    scatter_rows_split_kernel<<<unsigned((x_total + 7) / 8), 256, 0, s>>>(
+        x_recv.as<float>(), x_rows.as<int>(), x_rank.as<int>(), x_total, M.as<float>(), sp_M.hi, sp_M.lo, sp_M.un);
+  } else if (precision == 32) {
+    scatter_rows_kernel<float><<<x_total, 128, 0, s>>>(x_recv.as<float>(), np, x_rows.as<int>(), x_rank.as<int>(),
+                                                       x_total, M.as<float>());
+  } else {
+    scatter_rows_kernel<double><<<x_total, 128, 0, s>>>(x_recv.as<double>(), np, x_rows.as<int>(),
+                                                        x_rank.as<int>(), x_total, M.as<double>());
   }
+  KIFMM_LAUNCH_CHECK();
 }
 
 template <class T>
-void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
+void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase) {
   constexpr int BMB = sizeof(T) == 4 ? 128 : 64;
   constexpr int TMB = sizeof(T) == 4 ? 8 : 4;
-  int ei = 0;
+  int ei = (phase & 1) ? 0 : 3;  // event slots of the phase-2 marks stay the same
   auto mark = [&]() {
     if (timed) KIFMM_CUDA(cudaEventRecord(ev[ei++], s));
   };
@@ -1428,16 +1462,19 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     ++launches;
   };
 
-  mark();  // 0
-  // zero the down-check rows here, not just before P2L / M2L: a memset between the M2M and M2L kernels
-  // would break their programmatic (PDL) launch edge
-  if (!(gemm_tc && m2l_backend == 2 && !n_p2l && world == 1))  // else nothing reads the fp32 check rows
-    KIFMM_CUDA(cudaMemsetAsync(check_dn.p, 0, check_dn.bytes, s));
-  pack_sources_kernel<T><<<int(ceil_div(N, 256)), 256, 0, s>>>(pos4.as<v4_t<T>>(), q_in.as<T>(),
-                                                               input_order ? perm.as<int>() : nullptr, int(N),
-                                                               src4.as<v4_t<T>>());
-  KIFMM_LAUNCH_CHECK();
-  ++launches;
+  const bool up = (phase & 1) != 0, down = (phase & 2) != 0;
+  if (up) {
+    mark();  // 0
+    // zero the down-check rows here, not just before P2L / M2L: a memset between the M2M and M2L kernels
+    // would break their programmatic (PDL) launch edge
+    if (!(gemm_tc && m2l_backend == 2 && !n_p2l && world == 1))  // else nothing reads the fp32 check rows
+      KIFMM_CUDA(cudaMemsetAsync(check_dn.p, 0, check_dn.bytes, s));
+    pack_sources_kernel<T><<<int(ceil_div(N, 256)), 256, 0, s>>>(pos4.as<v4_t<T>>(), q_in.as<T>(),
+                                                                 input_order ? perm.as<int>() : nullptr, int(N),
+                                                                 src4.as<v4_t<T>>());
+    KIFMM_LAUNCH_CHECK();
+    ++launches;
+  }
   // near field has no dependency on the tree passes: fork it onto the low-priority side stream --
   // either all of it, or (queue mode, fp32) a few blocks per SM that run next to the tensor-core tree
   // kernels and take works from a shared counter, drained by a full launch after L2L
@@ -1490,9 +1527,9 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
       KIFMM_CUDA(cudaEventRecord(ev_join, side));
     }
   };
-  if (near_fork_at == 0 && !corun) fork_near();
+  if (up && near_fork_at == 0 && !corun) fork_near();
   // upward: P2M check -> factored solve
-  if (n_p2m) {
+  if (up && n_p2m) {
     launch_check<T>(np, n_p2m, pp, p2m_works.as<CheckWork>(), p2m_ranges.as<int2>(), node_level.as<int>(),
                     ref_level, T(alpha_out), check_up.as<T>(), s, gemm_tc ? &sp_cu : nullptr);
     KIFMM_LAUNCH_CHECK();
@@ -1508,14 +1545,16 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
       ++launches;
     }
   };
-  if (gemm_tc) {
-    tgemm(tg_up1, sp_cu, nullptr, false, &sp_tmp);
-    tgemm(tg_up2, sp_tmp, Mp, false, &sp_M);
-  } else {
-    gemm(solve_up1, check_up.as<T>(), w_us_u.as<T>(), tmp.as<T>(), false, true);
-    gemm(solve_up2, tmp.as<T>(), w_vt_u.as<T>(), Mp, false, true);
+  if (up) {
+    if (gemm_tc) {
+      tgemm(tg_up1, sp_cu, nullptr, false, &sp_tmp);
+      tgemm(tg_up2, sp_tmp, Mp, false, &sp_M);
+    } else {
+      gemm(solve_up1, check_up.as<T>(), w_us_u.as<T>(), tmp.as<T>(), false, true);
+      gemm(solve_up2, tmp.as<T>(), w_vt_u.as<T>(), Mp, false, true);
+    }
+    mark();  // 1
   }
-  mark();  // 1
   // M2M, levels d-1 .. floor
   auto m2m_level = [&](const M2MLevel& lv) {
     if (gemm_tc && lv.direct) {
@@ -1537,20 +1576,28 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     KIFMM_LAUNCH_CHECK();
     ++launches;
   };
-  for (auto& lv : m2m_levels) m2m_level(*lv);
-  mark();  // 2
-  // multipole exchange (multi-GPU) and the redundant top of the tree
+  if (up) {
+    for (auto& lv : m2m_levels) m2m_level(*lv);
+    mark();  // 2
+  }
+  // multipole exchange (multi-GPU): export rows -> all-gather -> import rows (+ their fp16 split), then the
+  // nodes spanning ranks, recomputed by every rank
   if (world > 1) {
-    exchange(s);
-    launches += 2;
-    if constexpr (sizeof(T) == 4) {
-      if (gemm_tc) {  // received rows: refresh the fp16 split of every multipole
-        sp_M.split(Mp, 0, int(nn), s);
+    if (up) {
+      gather_exports(s);
+      launches += x_mine > 0;
+      if (phase == 3 && opt.exchange == 0) {
+        allgather(s);
         ++launches;
       }
     }
-    for (auto& lv : m2m_top) m2m_level(*lv);
+    if (down) {
+      scatter_imports(s);
+      launches += x_total > 0;
+      for (auto& lv : m2m_top) m2m_level(*lv);
+    }
   }
+  if (!down) return;
   mark();  // 3
   // downward: P2L check into the down-check buffer (zeroed at the start of the evaluate)
   if (n_p2l) {
@@ -1726,7 +1773,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed) {
     }
   }
   mark();  // 9
-  info.kernel_launches = launches;
+  if (phase == 3) info.kernel_launches = launches;
 }
 
 void kifmm_gpu_plan::evaluate_device(const void* q, void* pot_dst, void* grad_dst, bool input_order,
@@ -1734,6 +1781,7 @@ void kifmm_gpu_plan::evaluate_device(const void* q, void* pot_dst, void* grad_ds
   KIFMM_CUDA(cudaSetDevice(device));
   cudaStream_t s = user ? user : stream;
   const size_t es = esz();
+  require_single_call();
   begin(s);
   KIFMM_CUDA(cudaMemcpyAsync(q_in.p, q, size_t(N) * es, cudaMemcpyDefault, s));
   if (!timed && opt.use_graph) {
@@ -1744,20 +1792,7 @@ void kifmm_gpu_plan::evaluate_device(const void* q, void* pot_dst, void* grad_ds
     else
       run<double>(s, input_order, timed);
   }
-  const void* ps = input_order ? pot_out.p : pot.p;
-  const void* gs = input_order ? grad_out.p : grad_buf.p;
-  if (input_order || world == 1) {
-    if (pot_dst) KIFMM_CUDA(cudaMemcpyAsync(pot_dst, ps, size_t(N) * es, cudaMemcpyDefault, s));
-    if (grad && grad_dst) KIFMM_CUDA(cudaMemcpyAsync(grad_dst, gs, size_t(N) * 3 * es, cudaMemcpyDefault, s));
-  } else {
-    const size_t off = size_t(pb) * es, cnt = size_t(pe - pb) * es;
-    if (pot_dst && cnt)
-      KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(pot_dst) + off, static_cast<const char*>(ps) + off, cnt,
-                                 cudaMemcpyDefault, s));
-    if (grad && grad_dst && cnt)
-      KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(grad_dst) + 3 * off, static_cast<const char*>(gs) + 3 * off,
-                                 3 * cnt, cudaMemcpyDefault, s));
-  }
+  copy_out(pot_dst, grad_dst, input_order, s);
   finish(s);
 }
 
@@ -1837,6 +1872,7 @@ void kifmm_gpu_plan::evaluate_many(int n_rhs, const void* const* charges, void* 
     pipe = std::move(P);
   }
   Pipe& P = *pipe;
+  require_single_call();
   begin(stream);
   const bool full = input_order || world == 1;  // else: this rank's particle range (reordered order)
   const size_t off = full ? 0 : size_t(pb), cnt = full ? size_t(N) : size_t(pe - pb);
@@ -1927,6 +1963,7 @@ kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* p, const void* charges, void* po
                                 int32_t input_order, kifmm_gpu_timings* timings) {
   return guard([&] {
     if (!p || !charges || !potential) throw InvalidArgument("evaluate: null argument");
+    p->require_single_call();
     KIFMM_CUDA(cudaSetDevice(p->device));
     cudaStream_t s = p->stream;
     const size_t es = p->esz();
@@ -1978,21 +2015,7 @@ kifmm_status kifmm_gpu_evaluate(kifmm_gpu_plan* p, const void* charges, void* po
       std::fprintf(stderr, "near queue: %d of %d works taken before the drain\n", c[2], p->leaf_near.n);
     }
 #endif
-    const void* ps = input_order ? p->pot_out.p : p->pot.p;
-    const void* gs = input_order ? p->grad_out.p : p->grad_buf.p;
-    if (input_order || p->world == 1) {
-      KIFMM_CUDA(cudaMemcpyAsync(potential, ps, size_t(p->N) * es, cudaMemcpyDefault, s));
-      if (p->grad && gradient) KIFMM_CUDA(cudaMemcpyAsync(gradient, gs, size_t(p->N) * 3 * es, cudaMemcpyDefault, s));
-    } else {
-      const size_t off = size_t(p->pb) * es, cnt = size_t(p->pe - p->pb) * es;
-      if (cnt) {
-        KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(potential) + off, static_cast<const char*>(ps) + off, cnt,
-                                   cudaMemcpyDefault, s));
-        if (p->grad && gradient)
-          KIFMM_CUDA(cudaMemcpyAsync(static_cast<char*>(gradient) + 3 * off, static_cast<const char*>(gs) + 3 * off,
-                                     3 * cnt, cudaMemcpyDefault, s));
-      }
-    }
+    p->copy_out(potential, gradient, input_order != 0, s);
     KIFMM_CUDA(cudaEventRecord(ev[13], s));
     p->finish(s);
     KIFMM_CUDA(cudaStreamSynchronize(s));
@@ -2025,6 +2048,54 @@ kifmm_status kifmm_gpu_evaluate_device(kifmm_gpu_plan* p, const void* d_charges,
   return guard([&] {
     if (!p || !d_charges) throw InvalidArgument("evaluate_device: null argument");
     p->evaluate_device(d_charges, d_potential, d_gradient, input_order != 0, static_cast<cudaStream_t>(stream), false);
+  });
+}
+
+kifmm_status kifmm_gpu_evaluate_upward(kifmm_gpu_plan* p, const void* charges, int32_t input_order,
+                                       void* export_rows) {
+  return guard([&] {
+    if (!p || !charges) throw InvalidArgument("evaluate_upward: null argument");
+    if (p->world < 2 || p->opt.exchange != 1)
+      throw InvalidArgument("evaluate_upward: needs a multi-rank plan with exchange = 1 (host)");
+    if (p->x_max > 0 && !export_rows) throw InvalidArgument("evaluate_upward: null export buffer");
+    KIFMM_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = p->stream;
+    const size_t es = p->esz();
+    p->begin(s);
+    KIFMM_CUDA(cudaMemcpyAsync(p->q_in.p, charges, size_t(p->N) * es, cudaMemcpyDefault, s));
+    p->host_phase_input_order = input_order != 0;
+    if (p->precision == 32)
+      p->run<float>(s, input_order != 0, false, 1);
+    else
+      p->run<double>(s, input_order != 0, false, 1);
+    if (p->x_mine > 0)
+      KIFMM_CUDA(cudaMemcpyAsync(export_rows, p->x_send.p, size_t(p->x_mine) * p->np * es, cudaMemcpyDefault, s));
+    p->finish(s);
+    KIFMM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+kifmm_status kifmm_gpu_evaluate_downward(kifmm_gpu_plan* p, const void* gathered, void* potential, void* gradient) {
+  return guard([&] {
+    if (!p || !potential) throw InvalidArgument("evaluate_downward: null argument");
+    if (p->world < 2 || p->opt.exchange != 1)
+      throw InvalidArgument("evaluate_downward: needs a multi-rank plan with exchange = 1 (host)");
+    if (p->x_max > 0 && !gathered) throw InvalidArgument("evaluate_downward: null gathered buffer");
+    KIFMM_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = p->stream;
+    const size_t es = p->esz();
+    const bool io = p->host_phase_input_order;
+    p->begin(s);
+    if (p->x_max > 0)
+      KIFMM_CUDA(cudaMemcpyAsync(p->x_recv.p, gathered, size_t(p->world) * p->x_max * p->np * es, cudaMemcpyDefault,
+                                 s));
+    if (p->precision == 32)
+      p->run<float>(s, io, false, 2);
+    else
+      p->run<double>(s, io, false, 2);
+    p->copy_out(potential, gradient, io, s);
+    p->finish(s);
+    KIFMM_CUDA(cudaStreamSynchronize(s));
   });
 }
 

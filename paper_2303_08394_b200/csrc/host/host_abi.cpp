@@ -157,51 +157,88 @@ int32_t kifmm_transfer_vectors(int32_t out[316 * 3]) {
 }
 
 // Contiguous Z-order leaf ranges, cost-balanced, aligned to level-`cut` boxes.
+namespace {
+// estimated evaluate cost of every leaf: P2P pairs (near + L2P / M2P surfaces) x flops + its M2L
+std::vector<double> leaf_costs(const kifmm_tree_view* tv, int n_e, bool gradient) {
+  const int64_t nl = tv->n_leaves;
+  const double pair_flops = gradient ? 19.0 : 11.0;
+  std::vector<double> cost(nl, 0.0);
+  for (int64_t l = 0; l < nl; ++l) {
+    const int64_t nt = tv->leaf_ptr[l + 1] - tv->leaf_ptr[l];
+    int64_t src = 0;
+    for (int64_t e = tv->u_ptr[l]; e < tv->u_ptr[l + 1]; ++e) {
+      const int64_t s = tv->u_idx[e];
+      src += tv->leaf_ptr[s + 1] - tv->leaf_ptr[s];
+    }
+    src += n_e * (1 + (tv->w_ptr[l + 1] - tv->w_ptr[l]));
+    const int64_t node = tv->leaf_node[l];
+    const int64_t nv = tv->v_ptr[node + 1] - tv->v_ptr[node];
+    cost[l] = pair_flops * double(nt) * double(src) + 2.0 * n_e * n_e * double(nv) + 11.0 * nt * n_e;
+  }
+  return cost;
+}
+// ranges for one cut level; returns the largest rank cost over the mean
+double split_at_cut(const kifmm_tree_view* tv, const std::vector<double>& cost, int world, int cut,
+                    int64_t* leaf_begin) {
+  const int64_t nl = tv->n_leaves;
+  // groups = runs of leaves sharing the level-`cut` ancestor (coarser leaves are their own group)
+  std::vector<int64_t> gstart;
+  uint64_t prev = ~uint64_t(0);
+  for (int64_t l = 0; l < nl; ++l) {
+    const uint64_t k = tv->node_key[tv->leaf_node[l]];
+    const uint64_t g = key_level(k) >= cut ? key_ancestor(k, cut) : k;
+    if (g != prev) gstart.push_back(l);
+    prev = g;
+  }
+  gstart.push_back(nl);
+  const int64_t ng = int64_t(gstart.size()) - 1;
+  std::vector<double> prefix(ng + 1, 0.0);
+  for (int64_t g = 0; g < ng; ++g) {
+    double gc = 0;
+    for (int64_t l = gstart[g]; l < gstart[g + 1]; ++l) gc += cost[l];
+    prefix[g + 1] = prefix[g] + gc;
+  }
+  const double total = prefix[ng];
+  leaf_begin[0] = 0;
+  int64_t b = 0;
+  std::vector<int64_t> gb(world + 1, 0);
+  for (int r = 1; r < world; ++r) {
+    const double target = total * double(r) / double(world);
+    while (b < ng && std::abs(prefix[b + 1] - target) <= std::abs(prefix[b] - target)) ++b;
+    gb[r] = b;
+    leaf_begin[r] = gstart[b];
+  }
+  gb[world] = ng;
+  leaf_begin[world] = nl;
+  double worst = 0;
+  for (int r = 0; r < world; ++r) worst = std::max(worst, prefix[gb[r + 1]] - prefix[gb[r]]);
+  return total > 0 ? worst / (total / world) : 1.0;
+}
+}  // namespace
+
 kifmm_status kifmm_partition_leaves(const kifmm_tree_view* tv, int32_t n_e, int32_t gradient,
                                     int32_t world_size, int32_t cut_level, int64_t* leaf_begin) {
   return guard([&] {
-    if (!tv || !leaf_begin || world_size < 1 || n_e < 1) throw InvalidArgument("partition: bad argument");
-    const int64_t nl = tv->n_leaves;
-    const double pair_flops = gradient ? 19.0 : 11.0;
-    std::vector<double> cost(nl, 0.0);
-    for (int64_t l = 0; l < nl; ++l) {
-      const int64_t nt = tv->leaf_ptr[l + 1] - tv->leaf_ptr[l];
-      int64_t src = 0;
-      for (int64_t e = tv->u_ptr[l]; e < tv->u_ptr[l + 1]; ++e) {
-        const int64_t s = tv->u_idx[e];
-        src += tv->leaf_ptr[s + 1] - tv->leaf_ptr[s];
+    if (!tv || !leaf_begin || world_size < 1 || n_e < 1 || cut_level < 0)
+      throw InvalidArgument("partition: bad argument");
+    const std::vector<double> cost = leaf_costs(tv, n_e, gradient != 0);
+    if (cut_level > 0) {
+      split_at_cut(tv, cost, world_size, cut_level, leaf_begin);
+      return;
+    }
+    // auto: the coarsest cut level >= 2 whose ranges are within 5 % of the mean cost (clustered clouds
+    // put most leaves under few level-2 boxes), else the best balanced one
+    std::vector<int64_t> best(world_size + 1), cur(world_size + 1);
+    double best_imb = 1e300;
+    for (int cut = 2; cut <= std::max(2, tv->depth); ++cut) {
+      const double imb = split_at_cut(tv, cost, world_size, cut, cur.data());
+      if (imb < best_imb - 1e-12) {
+        best_imb = imb;
+        best = cur;
       }
-      src += n_e * (1 + (tv->w_ptr[l + 1] - tv->w_ptr[l]));
-      const int64_t node = tv->leaf_node[l];
-      const int64_t nv = tv->v_ptr[node + 1] - tv->v_ptr[node];
-      cost[l] = pair_flops * double(nt) * double(src) + 2.0 * n_e * n_e * double(nv) + 11.0 * nt * n_e;
+      if (imb <= 1.05) break;
     }
-    // groups = runs of leaves sharing the level-`cut` ancestor (coarser leaves are their own group)
-    std::vector<int64_t> gstart;
-    uint64_t prev = ~uint64_t(0);
-    for (int64_t l = 0; l < nl; ++l) {
-      const uint64_t k = tv->node_key[tv->leaf_node[l]];
-      const uint64_t g = key_level(k) >= cut_level ? key_ancestor(k, cut_level) : k;
-      if (g != prev) gstart.push_back(l);
-      prev = g;
-    }
-    gstart.push_back(nl);
-    const int64_t ng = int64_t(gstart.size()) - 1;
-    std::vector<double> prefix(ng + 1, 0.0);
-    for (int64_t g = 0; g < ng; ++g) {
-      double gc = 0;
-      for (int64_t l = gstart[g]; l < gstart[g + 1]; ++l) gc += cost[l];
-      prefix[g + 1] = prefix[g] + gc;
-    }
-    const double total = prefix[ng];
-    leaf_begin[0] = 0;
-    int64_t b = 0;
-    for (int r = 1; r < world_size; ++r) {
-      const double target = total * double(r) / double(world_size);
-      while (b < ng && std::abs(prefix[b + 1] - target) <= std::abs(prefix[b] - target)) ++b;
-      leaf_begin[r] = gstart[b];
-    }
-    leaf_begin[world_size] = nl;
+    std::copy(best.begin(), best.end(), leaf_begin);
   });
 }
 

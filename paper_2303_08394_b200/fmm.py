@@ -36,8 +36,9 @@ class FmmConfig:
     use_graph: bool = True
     rank: int = 0
     world_size: int = 1
-    cut_level: int = 2
+    cut_level: int = 0                # multi-GPU partition alignment level (0 = auto)
     nccl_unique_id: bytes | None = None
+    exchange: int = 0                # world_size > 1: 0 NCCL all-gather, 1 host (evaluate_upward / _downward)
     cache: str | None = None         # operator cache archive path
 
     def validate(self):
@@ -109,6 +110,7 @@ class Fmm:
             opts.nccl_unique_id = C.cast(self._uid, C.c_void_p)
         opts.m2l_backend = cfg.m2l_backend
         opts.use_graph = 1 if cfg.use_graph else 0
+        opts.exchange = int(cfg.exchange)
         h = C.c_void_p()
         check(lib.kifmm_gpu_plan_create(C.byref(opts), C.byref(self.tree.view), C.byref(self.operators.view),
                                         C.byref(h)), "gpu_plan_create")
@@ -178,6 +180,30 @@ class Fmm:
                                             C.c_void_p(d_gradient) if d_gradient else None,
                                             1 if input_order else 0, C.c_void_p(stream) if stream else None),
               "gpu_evaluate_device")
+
+    # ------------------------------------------- host-exchange multi-rank halves (exchange = 1)
+    def evaluate_upward(self, charges, input_order: bool = True) -> np.ndarray:
+        """Upward pass of this rank; returns its export rows (halo_rows_max x ne_pad, plan precision) for
+        the caller's all-gather (kifmm_gpu_evaluate_upward)."""
+        q = np.ascontiguousarray(charges, dtype=self.dtype)
+        if q.shape != (self.n,):
+            raise InvalidArgument(f"charges must have shape ({self.n},)")
+        inf = self.info()
+        rows = np.zeros((max(1, inf["halo_rows_max"]), inf["ne_pad"]), dtype=self.dtype)
+        check(lib.kifmm_gpu_evaluate_upward(self._h, q.ctypes.data, 1 if input_order else 0, rows.ctypes.data),
+              "gpu_evaluate_upward")
+        return rows[:inf["halo_rows_max"]]
+
+    def evaluate_downward(self, gathered):
+        """Downward pass of this rank from the all-gathered rows (world_size x halo_rows_max x ne_pad);
+        returns (potential, gradient | None) like evaluate() (kifmm_gpu_evaluate_downward)."""
+        g = np.ascontiguousarray(gathered, dtype=self.dtype)
+        pot = np.zeros(self.n, dtype=self.dtype)
+        grad = np.zeros((self.n, 3), dtype=self.dtype) if self.config.gradient else None
+        check(lib.kifmm_gpu_evaluate_downward(self._h, g.ctypes.data if g.size else None, pot.ctypes.data,
+                                              grad.ctypes.data if grad is not None else None),
+              "gpu_evaluate_downward")
+        return pot, grad
 
     def info(self) -> dict:
         inf = _lib.GpuPlanInfo()

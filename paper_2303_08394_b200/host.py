@@ -184,11 +184,15 @@ class Tree:
                          int(sz.max()) if sz.size else 0)
         return out
 
-    def partition(self, world_size: int, n_e: int, gradient: bool = False, cut_level: int = 2) -> np.ndarray:
+    def partition(self, world_size: int, n_e: int, gradient: bool = False, cut_level: int = 0) -> np.ndarray:
         out = np.zeros(world_size + 1, dtype=np.int64)
         check(lib.kifmm_partition_leaves(C.byref(self.view), int(n_e), int(gradient), int(world_size),
                                          int(cut_level), out.ctypes.data), "partition")
         return out
+
+    def halo(self, world_size: int, n_e: int, gradient: bool = False, cut_level: int = 0) -> "Halo":
+        """Multi-GPU partition + halo-exchange tables (kifmm_halo_plan)."""
+        return Halo(self, world_size, n_e, gradient, cut_level)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -200,6 +204,29 @@ class Tree:
             self.close()
         except Exception:
             pass
+
+
+class Halo:
+    """Partition and halo-exchange tables of a world_size-rank evaluate (include/kifmm.h kifmm_halo_view):
+    leaf_begin (world + 1), up_owner (n_nodes; -1 = recomputed by every rank), exports[r] (node rows rank
+    r contributes to the all-gather), max_export (rows per all-gather slot)."""
+
+    def __init__(self, tree: Tree, world_size: int, n_e: int, gradient: bool = False, cut_level: int = 0):
+        h = C.c_void_p()
+        check(lib.kifmm_halo_plan(C.byref(tree.view), int(n_e), int(gradient), int(world_size), int(cut_level),
+                                  C.byref(h)), "halo_plan")
+        try:
+            v = _lib.HaloView()
+            check(lib.kifmm_halo_get_view(h, C.byref(v)), "halo_view")
+            w = v.world_size
+            self.world_size, self.cut_level, self.max_export = w, v.cut_level, int(v.max_export)
+            self.leaf_begin = _arr(v.leaf_begin, w + 1, np.int64).copy()
+            self.up_owner = _arr(v.up_owner, v.n_nodes, np.int32).copy()
+            ptr = _arr(v.export_ptr, w + 1, np.int64).copy()
+            idx = _arr(v.export_idx, ptr[-1], np.int64).copy()
+            self.exports = [idx[ptr[r]:ptr[r + 1]] for r in range(w)]
+        finally:
+            lib.kifmm_halo_destroy(h)
 
 
 # --------------------------------------------------------------- operators

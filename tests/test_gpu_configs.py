@@ -50,11 +50,11 @@ def test_config_parity_vs_oracle(require_gpu, cid):
     t0 = time.time()
     with fmm.Fmm(pos, cfg) as f:
         t1 = time.time()
-        pot, grad, _ = f.evaluate(q.astype(dt), input_order=False)  # reordered order
-        pot_in, grad_in, _ = f.evaluate(q.astype(dt), input_order=True)
-        backend = f.info()["m2l_backend"]
         tree, ops = f.tree, f.operators
         qr = q[tree.original_index]
+        pot, grad, _ = f.evaluate(qr.astype(dt), input_order=False)  # charges and results in reordered order
+        pot_in, grad_in, _ = f.evaluate(q.astype(dt), input_order=True)
+        backend = f.info()["m2l_backend"]
         # input-order output is the permutation of the reordered one
         assert np.array_equal(pot_in[tree.original_index], pot)
         t2 = time.time()
