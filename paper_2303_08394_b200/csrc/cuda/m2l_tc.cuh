@@ -76,6 +76,18 @@ constexpr int LAUNCH_REGS = KIFMM_TC_LAUNCH_REGS, LOW_REGS = KIFMM_TC_LOW_REGS, 
 static_assert(4 * 32 * LOW_REGS * 2 + 8 * 32 * EPI_REGS <= THREADS * LAUNCH_REGS, "setmaxnreg budget");
 constexpr uint32_t TMEM_COLS = 512;  // NACC 160-column accumulators at 0, 160, 320
 constexpr int NACC = 3;              // accumulator buffers: the MMA runs up to two taps ahead of the epilogue
+// The tensor-core accumulator rounds toward zero after every MMA (1 ulp per K step, measured), a bias that
+// adds up coherently along a chain of GEMMs.  The single-CTA instantiation (the factored solves, M2M and
+// L2L chain -- up to ten GEMMs deep) therefore keeps three accumulators per tap: the A_hi B_hi products of
+// even and odd K steps in two of them (5 truncations each instead of 30 in one) and the 2^-11-smaller
+// A_hi B_lo + A_lo B_hi corrections in the third; the epilogue sums them in fp32 round-to-nearest.  One
+// such set fills 480 TMEM columns, so that variant runs one tap at a time (NSET 1).  The M2L pair keeps
+// one accumulator per tap and three sets in flight (its taps are summed in fp32 per tap anyway).
+template <bool PAIR>
+struct Acc {
+  static constexpr int NSET = PAIR ? NACC : 1;         // accumulator sets in TMEM
+  static constexpr int SET_COLS = PAIR ? NP : 3 * NP;  // columns per set
+};
 
 // ROWB: bytes of one operand row per stage (K block of ROWB/4 fp32): 128 (SWIZZLE_128B) or 64 (SWIZZLE_64B,
 // twice the stages for the same shared memory => deeper latency hiding).
@@ -286,6 +298,25 @@ __device__ __forceinline__ void mma3(uint32_t tmem_d, uint64_t ah, uint64_t al, 
 #undef KIFMM_MMA3
 }
 
+// Split accumulation of one K step (single CTA): main (=/+=) A_hi B_hi; corr (=/+=) A_hi B_lo; corr += A_lo B_hi.
+template <int ES>
+__device__ __forceinline__ void mma3_split(uint32_t d_main, uint32_t d_corr, uint64_t ah, uint64_t al, uint64_t bh,
+                                           uint64_t bl, uint32_t idesc, uint32_t acc_main, uint32_t acc_corr) {
+#define KIFMM_MMA3S(KIND)                                                                        \
+  asm volatile(                                                                                  \
+      "{\n.reg .pred p, q, t;\nsetp.ne.b32 p, %7, 0;\nsetp.ne.b32 q, %8, 0;\nsetp.eq.b32 t, %7, %7;\n" \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], %2, %4, %6, p;\n"                          \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%1], %2, %5, %6, q;\n"                          \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%1], %3, %4, %6, t;\n"                          \
+      "}" ::"r"(d_main), "r"(d_corr), "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc_main),   \
+      "r"(acc_corr))
+  if constexpr (ES == 4)
+    KIFMM_MMA3S("tf32");
+  else
+    KIFMM_MMA3S("f16");
+#undef KIFMM_MMA3S
+}
+
 // tcgen05.commit: arrive on `bar` (in both CTAs of the pair when PAIR) once prior MMAs complete
 template <bool PAIR>
 __device__ __forceinline__ void commit(uint32_t bar) {
@@ -389,7 +420,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
       mbar_init(empty(s), 1);  // one tcgen05.commit per stage (multicast to both CTAs when PAIR)
       mbar_init(afull(s), 128);
     }
-    for (int b = 0; b < NACC; ++b) {
+    for (int b = 0; b < Acc<PAIR>::NSET; ++b) {
       mbar_init(tfull(b), 1);
       mbar_init(tempty(b), C::CTAS * EPI_WARPS);  // one elected lane per epilogue warp per CTA
     }
@@ -456,18 +487,43 @@ __global__ void __maxnreg__(LAUNCH_REGS)
         TC_PROBE(4, warp == EPI_WARP0 && lane == 0 && kk == k_begin && j == 0)
         __syncwarp();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * NP + h * EPI_COLS);
-#pragma unroll
-        for (int cb = 0; cb < (TC_DBG(4) ? 0 : EPI_COLS / 16); ++cb) {
-          uint32_t v[16];
+        const uint32_t taddr =
+            tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * Acc<PAIR>::SET_COLS + h * EPI_COLS);
+        auto ld16 = [&](uint32_t a, uint32_t (&v)[16]) {
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-              : "r"(taddr + uint32_t(cb * 16)));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+              : "r"(a));
+        };
+        if constexpr (PAIR) {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) acc[cb * 16 + k] = fmaf(__uint_as_float(v[k]), f, acc[cb * 16 + k]);
+          for (int cb = 0; cb < (TC_DBG(4) ? 0 : EPI_COLS / 16); ++cb) {
+            uint32_t v[16];
+            ld16(taddr + uint32_t(cb * 16), v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc[cb * 16 + k] = fmaf(__uint_as_float(v[k]), f, acc[cb * 16 + k]);
+          }
+        } else {  // (even + odd) + corrections, fp32 round-to-nearest; 8-column chunks of the three buffers
+          auto ld8 = [&](uint32_t a, uint32_t (&v)[8]) {
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                           "=r"(v[7])
+                         : "r"(a));
+          };
+#pragma unroll
+          for (int cb = 0; cb < EPI_COLS / 8; ++cb) {
+            uint32_t v0[8], v1[8], v2[8];
+            ld8(taddr + uint32_t(cb * 8), v0);
+            ld8(taddr + uint32_t(NP + cb * 8), v1);
+            ld8(taddr + uint32_t(2 * NP + cb * 8), v2);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              acc[cb * 8 + k] = fmaf((__uint_as_float(v0[k]) + __uint_as_float(v1[k])) + __uint_as_float(v2[k]), f,
+                                     acc[cb * 8 + k]);
+          }
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
@@ -477,7 +533,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
           else
             mbar_arrive_local(tempty(b));
         }
-        if (++b == NACC) {
+        if (++b == Acc<PAIR>::NSET) {
           b = 0;
           tph ^= 1u;
         }
@@ -725,7 +781,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
             mbar_wait(tempty(ab), aph ^ 1u);
             if (prof) t_te += clock64() - c0;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t d = tmem_base + uint32_t(ab * NP);
+            const uint32_t d = tmem_base + uint32_t(ab * Acc<PAIR>::SET_COLS);
             for (int kb = 0; kb < NKB; ++kb) {
               c0 = prof ? clock64() : 0;
               mbar_wait(full(s), ph);
@@ -737,7 +793,13 @@ __global__ void __maxnreg__(LAUNCH_REGS)
 #pragma unroll
                 for (int k = 0; k < ROWB / 32; ++k) {  // 32 bytes of K per MMA (8 tf32 / 16 f16)
                   const uint64_t o = so + uint64_t(2 * k);
-                  mma3<PAIR, ES>(d, dah0 + o, dal0 + o, dbh0 + o, dbl0 + o, IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+                  if constexpr (PAIR) {
+                    mma3<PAIR, ES>(d, dah0 + o, dal0 + o, dbh0 + o, dbl0 + o, IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+                  } else {  // K step ks: main buffer ks & 1, corrections in the third buffer
+                    const int ks = kb * (ROWB / 32) + k;
+                    mma3_split<ES>(d + uint32_t((ks & 1) * NP), d + uint32_t(2 * NP), dah0 + o, dal0 + o, dbh0 + o,
+                                   dbl0 + o, IDESC, ks >= 2 ? 1u : 0u, ks >= 1 ? 1u : 0u);
+                  }
                 }
                 if (s % C::EG == C::EG - 1) commit<PAIR>(empty(s));
               }
@@ -749,7 +811,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
               ++nst;
             }
             if (elect_one()) commit<PAIR>(tfull(ab));
-            if (++ab == NACC) {
+            if (++ab == Acc<PAIR>::NSET) {
               ab = 0;
               aph ^= 1u;
             }
