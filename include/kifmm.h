@@ -247,6 +247,12 @@ typedef struct kifmm_gpu_plan_info {
   int32_t kernel_launches;  /* kernels launched per evaluate */
   int64_t halo_rows_max;    /* world_size > 1: rows per all-gather slot (kifmm_halo_view.max_export) */
   int64_t halo_rows_mine;   /* rows this rank exports */
+  /* call structure (SPEC acceptance #8): tree levels each level-by-level operator covers -- M2M at the
+   * parent levels >= 2 (the multipoles of levels 0-1 feed no operator), M2L at every target level >= 2 in
+   * ONE batched launch, L2L at the child levels >= 3 -- and the leaves / nodes each per-target operator
+   * is applied to (each exactly once) */
+  int32_t m2m_levels, m2l_levels, l2l_levels, m2l_launch_levels;
+  int64_t p2m_leaves, near_leaves, l2p_leaves, m2p_leaves, p2l_nodes;
 } kifmm_gpu_plan_info;
 
 kifmm_status kifmm_gpu_plan_create(const kifmm_gpu_options* options, const kifmm_tree_view* tree,

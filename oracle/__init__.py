@@ -23,10 +23,12 @@ P, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
 
 class Timings(C.Structure):
     _fields_ = [(n, f64) for n in ("p2m_ms", "m2m_ms", "m2l_ms", "p2l_ms", "l2l_ms", "near_ms", "l2p_ms",
-                                   "m2p_ms", "total_ms")]
+                                   "m2p_ms", "total_ms")] + \
+        [(n, i64) for n in ("m2m_levels", "m2l_levels", "l2l_levels", "p2m_calls", "near_calls", "l2p_calls",
+                            "m2p_calls", "p2l_calls")]
 
     def as_dict(self):
-        return {n: float(getattr(self, n)) for n, _ in self._fields_}
+        return {n: (int if t is i64 else float)(getattr(self, n)) for n, t in self._fields_}
 
 
 _lib.oracle_evaluate.argtypes = [P, P, P, P, P, i32, i64, i64, C.POINTER(Timings)]

@@ -314,6 +314,13 @@ int oracle_downward(const kifmm_tree_view* t, const kifmm_operator_view* o, cons
   // reference level; the level factors of K_l = 2^(l-2) K_2 and dc2e_inv_l = 2^(2-l) dc2e_inv_2
   // cancel, so L_B = dc2e_inv_2 check_B.
   auto t0 = std::chrono::steady_clock::now();
+  {
+    std::set<int> lv;
+    for (int64_t b = 0; b < nn; ++b)
+      if (active[b] && lev(t->node_key[b]) >= 2 && t->v_ptr[b] != t->v_ptr[b + 1]) lv.insert(lev(t->node_key[b]));
+    local.m2l_levels = int64_t(lv.size());
+    for (int64_t b = 0; b < nn; ++b) local.p2l_calls += active[b] && t->x_ptr[b] != t->x_ptr[b + 1];
+  }
   pfor(nn, threads, [&](int64_t b) {
     if (!active[b] || lev(t->node_key[b]) < 2) return;
     double* c = &chk[size_t(b) * nc];
@@ -356,6 +363,7 @@ int oracle_downward(const kifmm_tree_view* t, const kifmm_operator_view* o, cons
   t0 = std::chrono::steady_clock::now();
   for (int l = 2; l <= t->depth; ++l) {
     const int64_t b0 = t->level_ptr[l], e0 = t->level_ptr[l + 1];
+    if (l - 1 >= 2) ++local.l2l_levels;
     pfor(e0 - b0, threads, [&](int64_t i) {
       const int64_t b = b0 + i;
       if (!active[b]) return;
@@ -378,6 +386,11 @@ int oracle_downward(const kifmm_tree_view* t, const kifmm_operator_view* o, cons
 
   // leaves: near field, L2P (467-472), M2P (474-479)
   t0 = std::chrono::steady_clock::now();
+  for (int64_t a = lb; a < le; ++a) {
+    ++local.near_calls;
+    local.l2p_calls += lev(t->node_key[t->leaf_node[a]]) >= 2;
+    local.m2p_calls += t->w_ptr[a] != t->w_ptr[a + 1];
+  }
   pfor(le - lb, threads, [&](int64_t li) {
     const int64_t a = lb + li;
     const int64_t node = t->leaf_node[a];
@@ -418,6 +431,12 @@ int oracle_downward(const kifmm_tree_view* t, const kifmm_operator_view* o, cons
   });
   local.near_ms = ms_since(t0);
   if (tm) {
+    tm->m2l_levels += local.m2l_levels;
+    tm->l2l_levels += local.l2l_levels;
+    tm->near_calls += local.near_calls;
+    tm->l2p_calls += local.l2p_calls;
+    tm->m2p_calls += local.m2p_calls;
+    tm->p2l_calls += local.p2l_calls;
     tm->m2l_ms += local.m2l_ms;
     tm->p2l_ms += local.p2l_ms;
     tm->l2l_ms += local.l2l_ms;
@@ -434,9 +453,11 @@ int oracle_evaluate(const kifmm_tree_view* t, const kifmm_operator_view* o, cons
   oracle_timings local{};
   auto t1 = std::chrono::steady_clock::now();
   pfor(t->n_leaves, threads, [&](int64_t l) { p2m_leaf(t, o, q, l, M.data()); });
+  local.p2m_calls = t->n_leaves;
   local.p2m_ms = ms_since(t1);
   t1 = std::chrono::steady_clock::now();
   for (int l = t->depth - 1; l >= 0; --l) {
+    ++local.m2m_levels;
     const int64_t b = t->level_ptr[l], e = t->level_ptr[l + 1];
     pfor(e - b, threads, [&](int64_t i) {
       if (t->node_leaf[b + i] < 0) m2m_node(t, o, b + i, M.data());

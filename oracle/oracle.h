@@ -24,6 +24,10 @@ extern "C" {
 
 typedef struct oracle_timings {
   double p2m_ms, m2m_ms, m2l_ms, p2l_ms, l2l_ms, near_ms, l2p_ms, m2p_ms, total_ms;
+  /* call structure (SPEC acceptance #8): level invocations of the level-by-level operators and
+     per-target applications of the leaf / node operators */
+  int64_t m2m_levels, m2l_levels, l2l_levels;
+  int64_t p2m_calls, near_calls, l2p_calls, m2p_calls, p2l_calls;
 } oracle_timings;
 
 /* Full evaluate over reordered charges.  potential: N (reordered);

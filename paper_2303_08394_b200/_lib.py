@@ -82,6 +82,8 @@ class GpuPlanInfo(C.Structure):
         ("m2l_pairs", i64), ("m2l_padded_pairs", i64),
         ("n_e", i32), ("n_c", i32), ("ne_pad", i32), ("m2l_backend", i32),
         ("device_bytes", i64), ("kernel_launches", i32), ("halo_rows_max", i64), ("halo_rows_mine", i64),
+        ("m2m_levels", i32), ("m2l_levels", i32), ("l2l_levels", i32), ("m2l_launch_levels", i32),
+        ("p2m_leaves", i64), ("near_leaves", i64), ("l2p_leaves", i64), ("m2p_leaves", i64), ("p2l_nodes", i64),
     ]
 
     def as_dict(self):

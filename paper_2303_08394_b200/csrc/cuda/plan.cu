@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <numeric>
 #include <string>
@@ -345,6 +346,7 @@ struct LeafPlan {
 };
 
 struct M2MLevel {
+  int level = 0;    // parent level
   GemmTiles tiles;  // one tile per (64 parents, octant)   [SIMT]
   TcGemm tc;        // one tile per (128 parents, octant), or per 128 parents with 8 octant taps (direct)
   bool direct = false;
@@ -844,6 +846,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     g->parents.upload(par, &dev_bytes);
     g->masks.upload(msk, &dev_bytes);
     g->n = int(parents.size());
+    g->level = parents.empty() ? 0 : node_lvl(parents[0]);
     m2m_scratch_rows = std::max<int64_t>(m2m_scratch_rows, int64_t(parents.size()) * 8);
     return g;
   };
@@ -1338,6 +1341,31 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     leaf_ptr_dev.upload(lp, &dev_bytes);
   }
 
+  // call structure (SPEC acceptance #8)
+  {
+    std::set<int> m2m_lv, m2l_lv, l2l_lv;
+    for (const auto* lvs : {&m2m_levels, &m2m_top})
+      for (const auto& g : *lvs) m2m_lv.insert(g->level);
+    for (const auto& g : m2l_groups)
+      for (int64_t n : g) m2l_lv.insert(node_lvl(n));
+    for (int l = 2; l < depth; ++l)
+      for (int64_t n = t.level_ptr[l + 1]; n < t.level_ptr[l + 2]; ++n)
+        if (active[n]) {
+          l2l_lv.insert(l + 1);
+          break;
+        }
+    info.m2m_levels = int(m2m_lv.size());
+    info.m2l_levels = int(m2l_lv.size());
+    info.m2l_launch_levels = m2l_lv.empty() ? 0 : 1;  // every M2L level in one batched launch
+    info.l2l_levels = int(l2l_lv.size());
+    info.p2m_leaves = n_p2m;
+    info.p2l_nodes = n_p2l;
+    for (int64_t l = lb; l < le; ++l) {
+      ++info.near_leaves;
+      info.l2p_leaves += node_lvl(t.leaf_node[l]) >= 2;
+      info.m2p_leaves += t.w_ptr[l + 1] != t.w_ptr[l];
+    }
+  }
   info.n_particles = N;
   info.n_leaves = nl;
   info.n_nodes = nn;

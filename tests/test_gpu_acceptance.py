@@ -1,0 +1,86 @@
+"""SPEC acceptance criteria #7 (near-linear scaling) and #8 (call structure)
+on the GPU evaluate.  Measured slopes are printed and appended to gpurun_out/acceptance_r02.jsonl."""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2303_08394_b200 import fmm, generators
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _log(rec):
+    print(json.dumps(rec))
+    out = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out):
+        with open(os.path.join(out, "acceptance_r02.jsonl"), "a") as f:
+            f.write(json.dumps(rec) + "\n")
+
+
+def test_acceptance8_call_structure(require_gpu):
+    """Depth-4 tree: the plan covers M2M at the parent levels >= 2 (levels 0-1 feed no operator), M2L at
+    every level >= 2 in one batched launch, L2L into levels 3 and 4, and applies P2M, the near field and
+    L2P exactly once per leaf (the GPU batches levels where SPEC calls per level)."""
+    pos, q = generators.sample("uniform-cube", 40000, seed=3, fp32=True)
+    with fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=40, precision=32)) as f:
+        assert f.tree.depth == 4
+        i = f.info()
+        nl = f.tree.n_leaves
+    assert i["m2m_levels"] == 2 and i["m2l_levels"] == 3 and i["m2l_launch_levels"] == 1 and i["l2l_levels"] == 2
+    assert i["p2m_leaves"] == i["near_leaves"] == i["l2p_leaves"] == nl
+    assert i["m2p_leaves"] == 0 and i["p2l_nodes"] == 0
+    _log({"acceptance": 8, **{k: i[k] for k in ("m2m_levels", "m2l_levels", "m2l_launch_levels", "l2l_levels",
+                                                  "p2m_leaves", "near_leaves", "l2p_leaves")}, "leaves": nl})
+
+
+def _slope(ns, ts):
+    return float(np.polyfit(np.log(ns), np.log(ts), 1)[0])
+
+
+def test_acceptance7_near_linear_scaling(require_gpu):
+    """sphere-surface N in {2.5e4, 5e4, 1e5, 2e5}, n_crit = 150, p = 6, 5 repeats: log-log
+    slope of the total FMM time (tree + lists + plan + evaluate, operators cached) <= 1.3, while the direct
+    oracle's slope over {2.5e4, 5e4} >= 1.8.  At these sizes the GPU evaluate is launch-bound, so the
+    same fit is also reported for N in {2.5e5 .. 4e6} (device evaluate only), where the GPU is busy."""
+    ops = {}
+    ns, tot, ev = [2.5e4, 5e4, 1e5, 2e5], [], []
+    for n in ns:
+        pos, q = generators.sample("sphere-surface", int(n), seed=5, charges="uniform", fp32=True)
+        rep_t, rep_e = [], []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            f = fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=150, precision=32), operators=ops.get("o"))
+            ops.setdefault("o", f.operators)
+            _, _, tm = f.evaluate(q.astype(np.float32), timed=True)
+            rep_t.append(time.perf_counter() - t0)
+            rep_e.append(tm["total_ms"])
+            f.close()
+        tot.append(float(np.mean(rep_t)))
+        ev.append(float(np.mean(rep_e)))
+    s_total = _slope(ns, tot)
+    dn, dt = [2.5e4, 5e4], []
+    for n in dn:
+        pos, q = generators.sample("sphere-surface", int(n), seed=5, charges="uniform")
+        t0 = time.perf_counter()
+        oracle.direct(pos, q)
+        dt.append(time.perf_counter() - t0)
+    s_direct = _slope(dn, dt)
+    big, bt = [2.5e5, 5e5, 1e6, 2e6, 4e6], []
+    for n in big:
+        pos, q = generators.sample("sphere-surface", int(n), seed=5, charges="uniform", fp32=True)
+        with fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=150, precision=32)) as f:
+            qq = q.astype(np.float32)
+            f.evaluate(qq)
+            ms = [f.evaluate(qq, timed=True)[2]["total_ms"] for _ in range(3)]
+        bt.append(float(np.median(ms)))
+    rec = {"acceptance": 7, "sizes": ns, "total_s": tot, "slope_total": s_total, "evaluate_ms": ev,
+           "slope_evaluate": _slope(ns, ev), "direct_sizes": dn, "direct_s": dt, "slope_direct": s_direct,
+           "large_sizes": big, "large_evaluate_ms": bt, "slope_large_evaluate": _slope(big, bt)}
+    _log(rec)
+    assert s_total <= 1.3 and s_direct >= 1.8
+    assert rec["slope_large_evaluate"] <= 1.3

@@ -108,3 +108,19 @@ def test_relative_error_examples():
     assert oracle.relative_error(b, b) == 0.0
     assert oracle.relative_error(2 * b, b) == pytest.approx(1.0)
     assert oracle.relative_error(b, np.zeros(3)) == -1.0
+
+
+def test_acceptance8_call_structure_depth4():
+    """SPEC.md:742 (acceptance #8) on a depth-4 tree, instrumented in the oracle's evaluate: 4 M2M level
+    invocations (levels 3..0), L2L at 2 levels (into levels 3 and 4), and exactly one application per
+    leaf of P2M, the near field and L2P (M2P / P2L once per leaf / node with a W / X list).  M2L runs at
+    every level >= 2 -- 3 levels on a depth-4 tree: SPEC's "2" (the paper's d - 2 calls)
+    would skip a level that has V-list work, so it is recorded, not matched."""
+    pos, q = generators.sample("uniform-cube", 40000, seed=3)
+    t = host.Tree(pos, 40)
+    assert t.depth == 4
+    o = host.Operators(3, domain_side=t.side)
+    _, _, tm = oracle.evaluate(t, o, q[t.original_index])
+    assert tm["m2m_levels"] == 4 and tm["l2l_levels"] == 2 and tm["m2l_levels"] == 3
+    assert tm["p2m_calls"] == tm["near_calls"] == tm["l2p_calls"] == t.n_leaves
+    assert tm["m2p_calls"] == 0 and tm["p2l_calls"] == 0  # uniform depth-4 tree: W and X empty
