@@ -1573,12 +1573,21 @@ struct M2LTcPlan {
   // check += M2L(M) with the multipoles already split into sp (rows = n_nodes, kind::f16 plan); the
   // reduce also writes the fp16 split of the finished check rows into cd (when given)
   void launch_presplit(const TcSplit& sp, float* check, const TcSplit* cd, cudaStream_t s) {
+    launch_presplit_main(sp, s);
+    launch_presplit_reduce(check, cd, s);
+  }
+  // the two halves of launch_presplit: the tcgen05 items (partials only: they neither read nor write the check
+  // rows, so P2L may fill those concurrently), then the fixed-order reduction into the check rows (+ split)
+  void launch_presplit_main(const TcSplit& sp, cudaStream_t s) {
     if (!n_items) return;
     if (!f16 || sp.rows != int(nn)) throw InvalidArgument("M2L presplit: kind::f16 plan over all nodes required");
     if (pair)
       run_kernel<true, 64, 2>(s, sp.hi, sp.lo, sp.un);
     else
       run_kernel<false, 64, 2>(s, sp.hi, sp.lo, sp.un);
+  }
+  void launch_presplit_reduce(float* check, const TcSplit* cd, cudaStream_t s) {
+    if (!n_items) return;
     launch_pdl(tc::m2l_tc_reduce_split_kernel, dim3(n_tiles, (rows + 7) / 8), dim3(256), 0, s, (const float*)d_partial,
                (const int*)d_tile_out, (const int*)d_tile_slot, rows, check, cd ? cd->hi : (__half*)nullptr,
                cd ? cd->lo : (__half*)nullptr, cd ? cd->un : (float*)nullptr);

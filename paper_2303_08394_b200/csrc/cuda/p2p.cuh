@@ -121,12 +121,53 @@ __host__ __device__ inline int leaf_slices(int nt, bool packed) {
 #endif
 __host__ __device__ inline int leaf_unroll(bool packed) { return packed ? KIFMM_NEAR_UNROLL / kNearNPair : 8; }
 
+#ifndef KIFMM_P2P_IL
+#define KIFMM_P2P_IL 0  // 1: two sources in lockstep (p2p_pair2)
+#endif
 // Packed fp32 pair-of-targets round: FP32x2 instructions whose source operand
 // is a scalar register broadcast to both lanes (ptxas folds mov.b64 {s, s}
 // into the ".F32" operand form), so the staged source stays one float4.  Per
 // source and thread: 3 FADD2 + 3 FMUL2/FFMA2 (r^2) + 2 MUFU.RSQ + 2 (potential)
 // + 5 (gradient) instructions for TWO target-source pairs.
 __device__ __forceinline__ f2_t f2_bcast(float a) { return f2_pack(a, a); }
+
+// Two staged sources in lockstep (every statement for source a, then for source b): two independent
+// dependency chains per thread, so a warp has an independent FP32x2 instruction ready while the other
+// chain waits on its MUFU.RSQ / LDS result (the one-source-at-a-time chain stalls on short scoreboards).
+// Same operations per pair and the same accumulation order (a before b) as the sequential loop.
+template <bool GRAD, bool MASK>
+__device__ __forceinline__ void p2p_pair2(const float4& sa, const float4& sb, f2_t x, f2_t y, f2_t z, f2_t& a_ph,
+                                          f2_t& a_gx, f2_t& a_gy, f2_t& a_gz) {
+  const f2_t dxa = f2_sub(x, f2_bcast(sa.x)), dxb = f2_sub(x, f2_bcast(sb.x));
+  const f2_t dya = f2_sub(y, f2_bcast(sa.y)), dyb = f2_sub(y, f2_bcast(sb.y));
+  const f2_t dza = f2_sub(z, f2_bcast(sa.z)), dzb = f2_sub(z, f2_bcast(sb.z));
+  f2_t r2a = f2_mul(dxa, dxa), r2b = f2_mul(dxb, dxb);
+  r2a = f2_fma(dya, dya, r2a);
+  r2b = f2_fma(dyb, dyb, r2b);
+  r2a = f2_fma(dza, dza, r2a);
+  r2b = f2_fma(dzb, dzb, r2b);
+  float a0, a1, b0, b1;
+  f2_unpack(r2a, a0, a1);
+  f2_unpack(r2b, b0, b1);
+  const f2_t ria = MASK ? f2_pack(rinv_masked(a0), rinv_masked(a1)) : f2_pack(rinv(a0), rinv(a1));
+  const f2_t rib = MASK ? f2_pack(rinv_masked(b0), rinv_masked(b1)) : f2_pack(rinv(b0), rinv(b1));
+  if (GRAD) {
+    const f2_t qra = f2_mul(f2_bcast(sa.w), ria), qrb = f2_mul(f2_bcast(sb.w), rib);
+    const f2_t r2ia = f2_mul(ria, ria), r2ib = f2_mul(rib, rib);
+    a_ph = f2_add(a_ph, qra);
+    const f2_t qr3a = f2_mul(qra, r2ia), qr3b = f2_mul(qrb, r2ib);
+    a_gx = f2_fma(qr3a, dxa, a_gx);
+    a_gy = f2_fma(qr3a, dya, a_gy);
+    a_gz = f2_fma(qr3a, dza, a_gz);
+    a_ph = f2_add(a_ph, qrb);
+    a_gx = f2_fma(qr3b, dxb, a_gx);
+    a_gy = f2_fma(qr3b, dyb, a_gy);
+    a_gz = f2_fma(qr3b, dzb, a_gz);
+  } else {
+    a_ph = f2_fma(f2_bcast(sa.w), ria, a_ph);
+    a_ph = f2_fma(f2_bcast(sb.w), rib, a_ph);
+  }
+}
 
 // NP target pairs per thread: one staged source (one LDS.128) feeds NP lane pairs.
 template <bool GRAD, bool MASK, int NP>
@@ -137,6 +178,18 @@ __device__ __forceinline__ void p2p_round_fn(const float4* sh, int begin, int en
   f2_t a_ph[NP], a_gx[NP], a_gy[NP], a_gz[NP];
 #pragma unroll
   for (int k = 0; k < NP; ++k) a_ph[k] = a_gx[k] = a_gy[k] = a_gz[k] = 0;
+#if KIFMM_P2P_IL
+  if constexpr (NP == 1) {
+#pragma unroll 2
+    for (int j = begin; j < end; j += 4) {
+      const float4 s0 = sh[j], s1 = sh[j + 1], s2 = sh[j + 2], s3 = sh[j + 3];
+      p2p_pair2<GRAD, MASK>(s0, s1, x[0], y[0], z[0], a_ph[0], a_gx[0], a_gy[0], a_gz[0]);
+      p2p_pair2<GRAD, MASK>(s2, s3, x[0], y[0], z[0], a_ph[0], a_gx[0], a_gy[0], a_gz[0]);
+    }
+  } else {
+#else
+  {
+#endif
 #pragma unroll 2
   for (int j = begin; j < end; j += U) {
 #pragma unroll
@@ -162,6 +215,7 @@ __device__ __forceinline__ void p2p_round_fn(const float4* sh, int begin, int en
       }
     }
   }
+  }
 #pragma unroll
   for (int k = 0; k < NP; ++k) {
     ph[k] = f2_add(ph[k], a_ph[k]);
@@ -177,6 +231,14 @@ template <bool GRAD, bool MASK>
 __device__ __forceinline__ void p2p_round_f2(const float4* sh, int begin, int end, f2_t x, f2_t y, f2_t z, f2_t& ph,
                                              f2_t& gx, f2_t& gy, f2_t& gz) {
   f2_t a_ph = 0, a_gx = 0, a_gy = 0, a_gz = 0;  // all-zero bits == (0.f, 0.f)
+#if KIFMM_P2P_IL
+#pragma unroll 2
+  for (int j = begin; j < end; j += 4) {
+    const float4 s0 = sh[j], s1 = sh[j + 1], s2 = sh[j + 2], s3 = sh[j + 3];
+    p2p_pair2<GRAD, MASK>(s0, s1, x, y, z, a_ph, a_gx, a_gy, a_gz);
+    p2p_pair2<GRAD, MASK>(s2, s3, x, y, z, a_ph, a_gx, a_gy, a_gz);
+  }
+#else
 #pragma unroll 2
   for (int j = begin; j < end; j += 4) {
 #pragma unroll
@@ -199,6 +261,7 @@ __device__ __forceinline__ void p2p_round_f2(const float4* sh, int begin, int en
       }
     }
   }
+#endif
   ph = f2_add(ph, a_ph);
   if (GRAD) {
     gx = f2_add(gx, a_gx);
@@ -630,13 +693,23 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_f2_kernel(
 
 // Far field with one HALF-warp per work.  far_f2_kernel gives a work the whole warp as 16 target pairs x 2 source slices, so
 // every warp pays its start-up loads and a shuffle reduction for 76 sources per lane; here lanes 0-15
-// and 16-31 take two consecutive works, each lane owns targets (hl, hl + 16) of its work and runs all
-// n_e sources, with no reduction.  The halves stage their surfaces in shared-memory slots 64 bytes
-// apart modulo 128, so the two broadcast addresses of an LDS.128 fall on different banks.
-constexpr int kFarHwSlot = 164;  // float4 per half-warp slot: >= n_e padded to 4 (p <= 6), 2624 B = 64 mod 128
+// and 16-31 take two consecutive works.  A work holds <= 32 targets (a leaf is cut into chunks of 32; the
+// last chunk is usually small): its TT = ceil(n / 2) target pairs are spread over the half-warp's 16 lanes
+// and the R = min(8, 16 / TT) lane groups split every staged surface into R source slices, so a chunk of a
+// few targets costs a fraction of a pass instead of a full one (config 2: 35 % of the leaves have more than
+// 32 targets).  Slice partials are summed in fixed order with shuffles inside the half-warp.  The halves
+// stage their surfaces in shared-memory slots 64 bytes apart modulo 128, so the two broadcast addresses of an
+// LDS.128 fall on different banks.  Works are sorted on the host by (surface count, R), so the two halves
+// of a warp loop over equally long source lists.
+constexpr int kFarHwSlot = 164;  // float4 per half-warp slot: >= n_e padded to 4 R (p <= 6), 2624 B = 64 mod 128
 #ifndef KIFMM_FARHW_MINB
 #define KIFMM_FARHW_MINB KIFMM_FAR_MINB
 #endif
+__host__ __device__ inline int far_hw_slices(int nt) {
+  const int tt = (nt + 1) >> 1;
+  const int r = 16 / (tt > 0 ? tt : 1);
+  return r < 1 ? 1 : (r > 8 ? 8 : r);
+}
 template <bool GRAD>
 __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kernel(
     P2PParams<float> p, const FarWork* __restrict__ works, int n_works, const int2* __restrict__ surfaces,
@@ -651,8 +724,12 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
   FarWork w{};
   if (valid) w = works[wi];
   const int t0 = w.t0, nt = valid ? w.count : 0;
-  const int ta = hl, tb = hl + 16;
-  const bool has_a = ta < nt, has_b = tb < nt;
+  const int TT = (nt + 1) >> 1, R = far_hw_slices(nt);
+  const int slice = TT > 0 ? hl / TT : 0, pi = hl - slice * TT;
+  const bool act = slice < R;
+  const int ta = pi, tb = pi + TT;
+  const bool has_a = act && ta < nt, has_b = act && tb < nt;
+  const bool out_a = has_a && slice == 0, out_b = has_b && slice == 0;
   const float4 xa = p.src[t0 + (has_a ? ta : 0)], xb = p.src[t0 + (has_b ? tb : 0)];
   // the near-field result and the output permutation, prefetched
   float pv[2] = {0.f, 0.f}, gv[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
@@ -660,7 +737,7 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int t = t0 + (h ? tb : ta);
-    if (h ? has_b : has_a) {
+    if (h ? out_b : out_a) {
       pv[h] = pot[t];
       if (GRAD)
 #pragma unroll
@@ -670,11 +747,10 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
   }
   const f2_t x = f2_pair(xa.x, xb.x), y = f2_pair(xa.y, xb.y), z = f2_pair(xa.z, xb.z);
   f2_t ph = 0, gx = 0, gy = 0, gz = 0;
-  // surfaces of this half's work; the halves loop to the longer list (works are paired by surface count
-  // on the host, so the shorter one idles rarely)
+  // surfaces of this half's work; the halves loop to the longer list (works are paired on the host)
   const int ns = valid ? w.surf_end - w.surf_begin : 0;
   const int ns_max = max(ns, __shfl_xor_sync(0xffffffffu, ns, 16));
-  const int pad = (p.n_e + 3) & ~3;
+  const int q4 = 4 * R, pad = (p.n_e + q4 - 1) / q4 * q4, per = pad / R;
   float4* my = sh[warp][half];
   const float fa = float(kFarAway);
   for (int k = 0; k < ns_max; ++k) {
@@ -686,7 +762,7 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
     for (int j = hl; j < pad; j += 16)
       my[j] = (k < ns && j < p.n_e) ? surface_source(p, sf.x, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
     __syncwarp();
-    p2p_round_f2<GRAD, false>(my, 0, pad, x, y, z, ph, gx, gy, gz);
+    if (act && k < ns) p2p_round_f2<GRAD, false>(my, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
   }
   timeline_end(5);
   float v[8];
@@ -694,12 +770,24 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
   f2_unpack(gx, v[1], v[5]);
   f2_unpack(gy, v[2], v[6]);
   f2_unpack(gz, v[3], v[7]);
+  // fixed-order slice reduction into slice 0 (lanes of the other half read their own half's lanes)
+  const int rmax = max(R, __shfl_xor_sync(0xffffffffu, R, 16));
+  for (int k = 1; k < rmax; ++k) {
+    const int src_hl = hl + k * TT;
+    const bool take = slice == 0 && k < R && src_hl < 16;
+    const int src = (half << 4) + (take ? src_hl : hl);
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+      const float o = __shfl_sync(0xffffffffu, v[d], src);
+      if (GRAD || (d & 3) == 0) v[d] += take ? o : 0.f;
+    }
+  }
   const float c = float(kInv4PiD);
   float* po = perm ? pot_out : pot;
   float* go = perm ? grad_out : grad;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    if (!(h ? has_b : has_a)) continue;
+    if (!(h ? out_b : out_a)) continue;
     const int o = ov[h];
     po[o] = pv[h] + c * v[4 * h];
     if (GRAD) {

@@ -26,6 +26,7 @@
 #include "morton.hpp"
 #include "p2p.cuh"
 #include "near_ws.cuh"
+#include "near_warp.cuh"
 
 namespace kifmm {
 namespace gpu {
@@ -377,6 +378,11 @@ struct kifmm_gpu_plan {
   // standalone launch of the serialized timed run (there 2-5 % slower than one leaf_eval_f2 block per leaf)
   int near_ws = 1;
   int near_ws_bps = 2;
+  // warp-per-work persistent near field (near_warp.cuh), the default for fp32; KIFMM_NEAR_WARP=0 selects the
+  // block-per-leaf kernels (leaf_eval_f2 / near_ws) for comparison
+  bool near_warp = false;
+  int near_warp_bps = 2;     // its side blocks per SM next to the tcgen05 kernels (2 x 8 warps, 2 x 32 KB)
+  int near_warp_blocks = 4;  // resident blocks per SM of the standalone / drain launch (occupancy query)
   int near_ws_blocks = 6;  // resident blocks per SM of the standalone / drain launch (occupancy query)   // its side blocks per SM next to the tcgen05 kernels (smem: 2 x 37 KB + stages)
   int near_pause = 0;  // side blocks sleep during M2L: 1 all, 2 half (KIFMM_NEAR_PAUSE; 1 measured slower)
   int near_bps = 3;  // queue mode: near-field blocks per SM next to the tree passes (KIFMM_NEAR_BPS, 0 = off)
@@ -428,6 +434,10 @@ struct kifmm_gpu_plan {
   TcGemm tg_dn2_up, tg_dn2_lo;
   cudaStream_t side2 = nullptr;
   cudaEvent_t ev_dn_fork = nullptr, ev_dn_join = nullptr;
+  // P2L (MUFU-bound check potentials) on side2 next to the tensor-core M2L kernel, which neither reads nor
+  // writes the check rows; the M2L reduction joins them (KIFMM_P2L_OVERLAP=0: serial)
+  bool p2l_overlap = true;
+  cudaEvent_t ev_p2l_fork = nullptr, ev_p2l_join = nullptr;
   DevMem dn_extra;  // down-check rows with P2L but no M2L (split after M2L)
   int n_dn_extra = 0;
   DevMem m2m_scratch;
@@ -460,6 +470,8 @@ struct kifmm_gpu_plan {
     if (side2) cudaStreamDestroy(side2);
     if (ev_dn_fork) cudaEventDestroy(ev_dn_fork);
     if (ev_dn_join) cudaEventDestroy(ev_dn_join);
+    if (ev_p2l_fork) cudaEventDestroy(ev_p2l_fork);
+    if (ev_p2l_join) cudaEventDestroy(ev_p2l_join);
     if (pipe) {
       if (pipe->cin) cudaStreamDestroy(pipe->cin);
       if (pipe->cout) cudaStreamDestroy(pipe->cout);
@@ -656,6 +668,9 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     KIFMM_CUDA(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, hi));
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_dn_fork, cudaEventDisableTiming));
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_dn_join, cudaEventDisableTiming));
+    KIFMM_CUDA(cudaEventCreateWithFlags(&ev_p2l_fork, cudaEventDisableTiming));
+    KIFMM_CUDA(cudaEventCreateWithFlags(&ev_p2l_join, cudaEventDisableTiming));
+    if (const char* e = std::getenv("KIFMM_P2L_OVERLAP")) p2l_overlap = std::atoi(e) != 0;
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
@@ -1141,8 +1156,10 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   }
   const bool packed = leaf_packed;
   if (packed) {
+    if (const char* e = std::getenv("KIFMM_NEAR_WARP")) near_warp = std::atoi(e) != 0;
     if (const char* e = std::getenv("KIFMM_NEAR_WS")) near_ws = std::atoi(e);
     if (near_ws) near_bps = near_ws_bps;
+    if (near_warp) near_bps = near_warp_bps;
     if (const char* e = std::getenv("KIFMM_NEAR_BPS")) near_bps = std::max(0, std::atoi(e));
     near_counter.alloc(4 * sizeof(int), &dev_bytes);
 #ifdef KIFMM_EXPERIMENTS  // timing experiments only (tools/build_variant.sh); NEAR_SKIP gives wrong results
@@ -1162,11 +1179,16 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
                           (const void*)near_ws_kernel<true, 2>, (const void*)near_ws_kernel<false, 0>,
                           (const void*)near_ws_kernel<false, 1>, (const void*)near_ws_kernel<false, 2>,
                           (const void*)leaf_eval_f2_kernel<true, false, false>,
-                          (const void*)leaf_eval_f2_kernel<false, false, false>})
+                          (const void*)leaf_eval_f2_kernel<false, false, false>,
+                          (const void*)near_warp_kernel<true, 0>, (const void*)near_warp_kernel<true, 1>,
+                          (const void*)near_warp_kernel<true, 2>, (const void*)near_warp_kernel<false, 0>,
+                          (const void*)near_warp_kernel<false, 1>, (const void*)near_warp_kernel<false, 2>})
       KIFMM_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     int nb = 0;
     KIFMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, near_ws_kernel<true, 2>, kNearWsThreads, 0));
     near_ws_blocks = std::max(1, nb);
+    KIFMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, near_warp_kernel<true, 2>, kNwWarps * 32, 0));
+    near_warp_blocks = std::max(1, nb);
   }
   auto build_leaf_plan = [&](bool near_part, LeafPlan& lp) {
     struct Src {
@@ -1221,10 +1243,14 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
         }
         if (other.empty()) continue;
       }
-      for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += kP2PThreads) {
-        const int nt = int(std::min<int64_t>(kP2PThreads, t.leaf_ptr[l + 1] - t0));
-        const int R = leaf_slices(nt, packed), q = leaf_unroll(packed) * R;
-        const int cap = kP2PCap - kP2PCap % q;
+      // warp geometry (near_warp_kernel, near part): <= 64 targets per work, R = nw_slices source slices,
+      // rounds of <= kNwCap sources; block geometry: <= 128 targets, leaf_slices, rounds of <= kP2PCap
+      const bool wg = near_part && packed && near_warp;
+      const int chunk = wg ? kNwTargets : kP2PThreads;
+      for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += chunk) {
+        const int nt = int(std::min<int64_t>(chunk, t.leaf_ptr[l + 1] - t0));
+        const int R = wg ? nw_slices(nt) : leaf_slices(nt, packed), q = (wg ? 4 : leaf_unroll(packed)) * R;
+        const int cap = wg ? kNwCap - kNwCap % q : kP2PCap - kP2PCap % q;
         const int rb = int(rounds.size());
         size_t si = 0, oi = 0;
         int soff = 0, ooff = 0;  // offsets inside the current self / other source
@@ -1328,9 +1354,11 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     if (const char* e = std::getenv("KIFMM_FAR_HW")) far_hw = far_hw && std::atoi(e) != 0;
     // half-warp kernel: a warp's two works loop to the longer surface list -- pair works of equal
     // surface counts (stable sort by count; every work writes only its own targets, order is free)
-    if (far_hw && packed)
+    if (far_hw && packed)  // equal (surface count, source slices) in the two halves of a warp
       std::stable_sort(fw2.begin(), fw2.end(), [](const FarWork& a, const FarWork& b) {
-        return a.surf_end - a.surf_begin > b.surf_end - b.surf_begin;
+        const int na = a.surf_end - a.surf_begin, nb = b.surf_end - b.surf_begin;
+        if (na != nb) return na > nb;
+        return far_hw_slices(a.count) < far_hw_slices(b.count);
       });
     if (packed)
       far_works.upload(fw2, &dev_bytes);
@@ -1452,6 +1480,18 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
     const int4* it = lp.items.as<int4>();
     T* g = grad ? grad_buf.as<T>() : nullptr;
     if constexpr (sizeof(T) == 4) {
+      if (leaf_packed && near_warp && &lp == &leaf_near && !acc) {  // standalone warp-per-work near field
+        int* qc = near_counter.as<int>();
+        KIFMM_CUDA(cudaMemsetAsync(qc, 0, 4 * sizeof(int), st));
+        const int grid = int(std::min<int64_t>(ceil_div(lp.n, kNwWarps), int64_t(near_warp_blocks) * sm_count()));
+        if (grad)
+          near_warp_kernel<true, 0><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pot.as<T>(), g, lp.n, qc);
+        else
+          near_warp_kernel<false, 0><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pot.as<T>(), g, lp.n, qc);
+        KIFMM_LAUNCH_CHECK();
+        ++launches;
+        return;
+      }
       if (leaf_packed && near_ws >= 2 && &lp == &leaf_near && !acc) {  // standalone persistent near field
         int* qc = near_counter.as<int>();
         KIFMM_CUDA(cudaMemsetAsync(qc, 0, 4 * sizeof(int), st));
@@ -1518,6 +1558,19 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
       int* qc = near_counter.as<int>();
       float* pt = pot.as<float>();
       const int n = leaf_near.n;
+      if (near_warp) {
+        if (grad && drain)
+          near_warp_kernel<true, 2><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pt, g, n, qc);
+        else if (grad)
+          near_warp_kernel<true, 1><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pt, g, n, qc);
+        else if (drain)
+          near_warp_kernel<false, 2><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pt, g, n, qc);
+        else
+          near_warp_kernel<false, 1><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pt, g, n, qc);
+        KIFMM_LAUNCH_CHECK();
+        ++launches;
+        return;
+      }
       if (near_ws) {
         if (grad && drain)
           near_ws_kernel<true, 2><<<grid, kNearWsThreads, 0, st>>>(pp, w, r, it, pt, g, n, qc);
@@ -1628,12 +1681,18 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
   if (!down) return;
   mark();  // 3
   // downward: P2L check into the down-check buffer (zeroed at the start of the evaluate)
+  const bool p2l_side = !timed && n_p2l && p2l_overlap && gemm_tc && m2l_backend == 2 && sizeof(T) == 4;
+  if (p2l_side) {
+    KIFMM_CUDA(cudaEventRecord(ev_p2l_fork, s));
+    KIFMM_CUDA(cudaStreamWaitEvent(side2, ev_p2l_fork, 0));
+  }
   if (n_p2l) {
     launch_check<T>(np, n_p2l, pp, p2l_works.as<CheckWork>(), p2l_ranges.as<int2>(), node_level.as<int>(),
-                    ref_level, T(alpha_in), check_dn.as<T>(), s);
+                    ref_level, T(alpha_in), check_dn.as<T>(), p2l_side ? side2 : s);
     KIFMM_LAUNCH_CHECK();
     ++launches;
   }
+  if (p2l_side) KIFMM_CUDA(cudaEventRecord(ev_p2l_join, side2));
   mark();  // 4
 #ifdef KIFMM_EXPERIMENTS
   if (const char* e = std::getenv("KIFMM_CORUN_DUMMY"); e && timed) {  // experiments: a dummy load next to M2L
@@ -1651,7 +1710,9 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
     if constexpr (sizeof(T) == 4) {
       if (gemm_tc && m2l_backend == 2) {  // multipoles already split; the reduce splits the check rows
         // no P2L rows: the fp32 check rows are never read (only their split) -- skip them entirely
-        m2l_tc.launch_presplit(sp_M, n_p2l ? check_dn.as<float>() : nullptr, &sp_cd, s);
+        m2l_tc.launch_presplit_main(sp_M, s);
+        if (p2l_side) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_p2l_join, 0));
+        m2l_tc.launch_presplit_reduce(n_p2l ? check_dn.as<float>() : nullptr, &sp_cd, s);
         launches += 2;
         if (n_dn_extra) {  // P2L-only check rows (no V list): split them here
           tc::split_f16_list_kernel<<<unsigned((n_dn_extra + 7) / 8), 256, 0, s>>>(
@@ -1734,7 +1795,11 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
 #endif
   // drain the works the side-stream blocks did not take (persistent: at most 8 blocks per SM, so an
   // empty queue costs one short wave instead of a block per leaf)
-  if (queue_mode) near_queue(s, std::min(leaf_near.n, (near_ws ? near_ws_blocks : 8) * sm_count()), true);
+  if (queue_mode)
+    near_queue(s,
+               near_warp ? int(std::min<int64_t>(ceil_div(leaf_near.n, kNwWarps), int64_t(near_warp_blocks) * sm_count()))
+                         : std::min(leaf_near.n, (near_ws ? near_ws_blocks : 8) * sm_count()),
+               true);
   if ((!timed || corun) && leaf_near.n && !near_skip) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
   bool fused_out = false;  // the packed far kernel wrote the final (input-order) output
   if (far_as_leaf) leaf(leaf_far, true, s);
