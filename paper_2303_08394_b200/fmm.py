@@ -84,8 +84,11 @@ def load_or_precompute(cfg: FmmConfig, domain_side: float) -> host.Operators:
 class Fmm:
     """Plan: tree + lists + operators on the host, evaluate on the GPU."""
 
-    def __init__(self, positions, config: FmmConfig | None = None, operators: host.Operators | None = None,
-                 tree: host.Tree | None = None):
+    def __init__(self, positions, config: FmmConfig | None = None,
+                 operators: host.Operators | dict | None = None, tree: host.Tree | None = None):
+        """`operators`: a precomputed operator set (its domain side must equal the tree's), or a dict used as
+        an in-memory operator cache keyed by fingerprint (load on fingerprint match, else
+        precompute and insert) -- point clouds whose bounding cubes differ get their own entries."""
         cfg = config or FmmConfig()
         cfg.validate()
         self.config = cfg
@@ -93,7 +96,13 @@ class Fmm:
         t0 = time.perf_counter()
         self.tree = tree if tree is not None else host.Tree(positions, cfg.n_crit, threads=cfg.threads)
         t1 = time.perf_counter()
-        self.operators = operators if operators is not None else load_or_precompute(cfg, self.tree.side)
+        if isinstance(operators, dict):
+            fp = operator_fingerprint(cfg.p, cfg.alpha_inner, cfg.alpha_outer, cfg.svd_cutoff, self.tree.side)
+            if fp not in operators:
+                operators[fp] = load_or_precompute(cfg, self.tree.side)
+            self.operators = operators[fp]
+        else:
+            self.operators = operators if operators is not None else load_or_precompute(cfg, self.tree.side)
         t2 = time.perf_counter()
         self.timings.update(tree_s=t1 - t0, precompute_s=t2 - t1)
         self.dtype = np.float32 if cfg.precision == 32 else np.float64
