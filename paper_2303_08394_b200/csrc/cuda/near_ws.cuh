@@ -23,7 +23,6 @@
 namespace kifmm {
 namespace gpu {
 
-static_assert(kNearNPair == 1, "near_ws_kernel mirrors the one-pair-per-thread geometry");
 constexpr int kNearStages = 2;
 constexpr int kNearWsThreads = 160;  // warps 0-3 consumers, warp 4 producer
 
@@ -143,11 +142,12 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
   }
 
   // ---------------- consumers (warps 0-3): geometry and arithmetic of leaf_eval_f2_kernel
+  constexpr int NPR = kNearNPair;  // target pairs per thread: targets t0 + m TT, m < 2 NPR
   int stage = 0;
   uint32_t phase = 0;
   int nt = 0, TT = 1, R = 1, slice = 0, t0 = 0, mul_r = 0;
   bool active = false;
-  f2_t x[1], y[1], z[1], ph[1], gx[1], gy[1], gz[1];
+  f2_t x[NPR], y[NPR], z[NPR], ph[NPR], gx[NPR], gy[NPR], gz[NPR];
   for (;;) {
     tc::mbar_wait(tc::smem_u32(&sm.full[stage]), phase);
     NearStage& S = sm.st[stage];
@@ -161,24 +161,27 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
       slice = div_mul(tid, S.mul_tt);
       t0 = tid - slice * TT;
       active = slice < R;
-      const int ta = t0, tb = t0 + TT;
       // targets straight from global (L2-resident; staging them too would cost the sixth block per SM)
-      const float4 xa = p.src[S.t_begin + (active && ta < nt ? ta : 0)];
-      const float4 xb = p.src[S.t_begin + (active && tb < nt ? tb : 0)];
-      x[0] = f2_pair(xa.x, xb.x);
-      y[0] = f2_pair(xa.y, xb.y);
-      z[0] = f2_pair(xa.z, xb.z);
-      ph[0] = gx[0] = gy[0] = gz[0] = 0;
+#pragma unroll
+      for (int k = 0; k < NPR; ++k) {
+        const int ta = t0 + (2 * k) * TT, tb = t0 + (2 * k + 1) * TT;
+        const float4 xa = p.src[S.t_begin + (active && ta < nt ? ta : 0)];
+        const float4 xb = p.src[S.t_begin + (active && tb < nt ? tb : 0)];
+        x[k] = f2_pair(xa.x, xb.x);
+        y[k] = f2_pair(xa.y, xb.y);
+        z[k] = f2_pair(xa.z, xb.z);
+        ph[k] = gx[k] = gy[k] = gz[k] = 0;
+      }
     }
     const int Ssz = S.S, Osz = S.O;
     if (active) {
       if (Ssz) {
         const int per = div_mul(Ssz, mul_r);
-        p2p_round_fn<GRAD, true, 1>(S.src, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
+        p2p_round_fn<GRAD, true, NPR>(S.src, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
       }
       if (Osz) {
         const int per = div_mul(Osz, mul_r);
-        p2p_round_fn<GRAD, false, 1>(S.src, Ssz + slice * per, Ssz + slice * per + per, x, y, z, ph, gx, gy, gz);
+        p2p_round_fn<GRAD, false, NPR>(S.src, Ssz + slice * per, Ssz + slice * per + per, x, y, z, ph, gx, gy, gz);
       }
     }
     if (flags & 2) {  // last round: fixed-order slice reduction through this stage's source buffer
@@ -187,16 +190,19 @@ __global__ void __launch_bounds__(kNearWsThreads, KIFMM_NEAR_WS_MINB) near_ws_ke
       float* red = reinterpret_cast<float*>(S.src);  // [slice][component][n_t]
       constexpr int NC = GRAD ? 4 : 1;
       if (active) {
-        float a[4], b[4];
-        f2_unpack(ph[0], a[0], b[0]);
-        f2_unpack(gx[0], a[1], b[1]);
-        f2_unpack(gy[0], a[2], b[2]);
-        f2_unpack(gz[0], a[3], b[3]);
-        const int ta = t0, tb = t0 + TT;
 #pragma unroll
-        for (int d = 0; d < NC; ++d) {
-          if (ta < nt) red[(slice * NC + d) * nt + ta] = a[d];
-          if (tb < nt) red[(slice * NC + d) * nt + tb] = b[d];
+        for (int k = 0; k < NPR; ++k) {
+          float a[4], b[4];
+          f2_unpack(ph[k], a[0], b[0]);
+          f2_unpack(gx[k], a[1], b[1]);
+          f2_unpack(gy[k], a[2], b[2]);
+          f2_unpack(gz[k], a[3], b[3]);
+          const int ta = t0 + (2 * k) * TT, tb = t0 + (2 * k + 1) * TT;
+#pragma unroll
+          for (int d = 0; d < NC; ++d) {
+            if (ta < nt) red[(slice * NC + d) * nt + ta] = a[d];
+            if (tb < nt) red[(slice * NC + d) * nt + tb] = b[d];
+          }
         }
       }
       near_consumer_sync();

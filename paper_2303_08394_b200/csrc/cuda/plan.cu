@@ -389,7 +389,7 @@ struct kifmm_gpu_plan {
   bool m2m_parent_tiles = false;  // KIFMM_M2M=parent: 8-tap parent tiles, direct (measured slower)
   DevMem near_counter;  // queue mode work counter [, counter at the drain launch (KIFMM_NEAR_DEBUG)]
   bool near_debug = false, near_skip = false, far_as_leaf = false, near_corun = false;
-  int near_fork_at = 0;  // 0: at the start of the evaluate, 1: just before M2L
+  int near_fork_at = 0;  // 0: at the start of the evaluate, 1: just before M2L, 2: after the P2M check, 3: after M2M
   bool grad = false;
   int64_t N = 0, nl = 0, nn = 0;
   int depth = 0, ne = 0, nc = 0, np = 0, ref_level = 2;
@@ -1166,7 +1166,10 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     if (const char* e = std::getenv("KIFMM_NEAR_PAUSE")) near_pause = std::atoi(e);
     near_debug = std::getenv("KIFMM_NEAR_DEBUG") != nullptr;
     near_skip = std::getenv("KIFMM_NEAR_SKIP") != nullptr;
-    if (const char* e = std::getenv("KIFMM_NEAR_FORK")) near_fork_at = std::string(e) == "m2l" ? 1 : 0;
+    if (const char* e = std::getenv("KIFMM_NEAR_FORK")) {
+      const std::string v(e);
+      near_fork_at = v == "m2l" ? 1 : v == "check" ? 2 : v == "m2m" ? 3 : 0;
+    }
     near_corun = std::getenv("KIFMM_NEAR_CORUN") != nullptr;
 #endif
     // full shared-memory carveout, so an SM running near-field blocks need not drain before a tcgen05
@@ -1616,6 +1619,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
     KIFMM_LAUNCH_CHECK();
     ++launches;
   }
+  if (up && near_fork_at == 2 && !corun) fork_near();
   // tcgen05 GEMM: split the fp32 source rows, then dst (=/+=) A . B^T
   // tcgen05 GEMMs: the A rows arrive already split by their producer (check kernel, previous GEMM's
   // epilogue, M2M / M2L reductions); the epilogue writes the fp32 rows (Y, may be null) and their split
@@ -1661,6 +1665,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
     for (auto& lv : m2m_levels) m2m_level(*lv);
     mark();  // 2
   }
+  if (up && near_fork_at == 3 && !corun) fork_near();
   // multipole exchange (multi-GPU): export rows -> all-gather -> import rows (+ their fp16 split), then the
   // nodes spanning ranks, recomputed by every rank
   if (world > 1) {

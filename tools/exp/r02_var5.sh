@@ -1,0 +1,7 @@
+KIFMM_LIB=variants/base.so python tools/exp/cmp_lib.py 2 save /tmp/ref2.npz
+for v in np2 np2u4 np2w5; do
+  KIFMM_LIB=variants/$v.so python tools/exp/cmp_lib.py 2 check /tmp/ref2.npz 2>&1 | tail -1
+  KIFMM_LIB=variants/$v.so timeout 300 python tools/near_time.py 2 30 2>&1 | tail -1 | cut -c1-100
+  KIFMM_NEAR_BPS=0 KIFMM_LIB=variants/$v.so timeout 300 python tools/near_time.py 2 10 2>&1 | tail -1 | grep -o '"leaf_ms": [0-9.]*'
+done
+KIFMM_LIB=variants/base.so timeout 300 python tools/near_time.py 2 30 2>&1 | tail -1 | cut -c1-100
