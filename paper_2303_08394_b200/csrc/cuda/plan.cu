@@ -26,6 +26,7 @@
 #include "morton.hpp"
 #include "p2p.cuh"
 #include "near_ws.cuh"
+#include "m2l_oz.cuh"
 #include "near_warp.cuh"
 
 namespace kifmm {
@@ -445,6 +446,7 @@ struct kifmm_gpu_plan {
   int m2l_red_tiles = 0;
   int64_t m2m_scratch_rows = 0;
   M2LTcPlan m2l_tc;
+  M2LOzPlan m2l_oz;  // fp64 M2L on the int8 tensor cores (m2l_backend 4)
   // exchange
   void* comm = nullptr;
   DevMem x_send, x_recv, x_rows, x_rank /* source slot of each received row */, x_my_rows;
@@ -982,6 +984,16 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     m2l_tc.build(t, m2l_groups, np, ops, &dev_bytes);
     m2l_backend = m2l_tc.f16 ? 2 : 3;  // 2: kind::f16 3-term split, 3: kind::tf32 3xTF32
     info.m2l_padded_pairs = m2l_tc.slots;
+  }
+  if (o.m2l_backend == 4 && precision != 64) throw InvalidArgument("gpu: the int8 (Ozaki) M2L is an fp64 path");
+  if (precision == 64 &&
+      (o.m2l_backend == 4 || (o.m2l_backend == 0 && M2LOzPlan::supported(np) && m2l_tc_available()))) {
+    if (!M2LOzPlan::supported(np)) throw InvalidArgument("gpu: the int8 (Ozaki) M2L needs n_e padded to 160 or 224");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    m2l_oz.build(t, m2l_groups, np, ops, nn, node_lvl, depth, sms, &dev_bytes);
+    m2l_backend = 4;
+    info.m2l_padded_pairs = m2l_oz.slots;
   }
   if (m2l_backend == 1) {
     std::vector<TileSpec> tiles;
@@ -1711,7 +1723,12 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
   if (queue_mode && near_pause)  // side near-field blocks sleep while M2L runs
     KIFMM_CUDA(cudaMemsetAsync(near_counter.as<int>() + 3, near_pause, 1, s));
   // M2L over all levels at once, accumulated as reference-level check potentials
-  if (m2l_backend >= 2) {
+  if (m2l_backend == 4) {
+    if constexpr (sizeof(T) == 8) {
+      m2l_oz.run(Mp, node_level.as<int>(), check_dn.as<T>(), s);
+      launches += m2l_oz.launches();
+    }
+  } else if (m2l_backend >= 2) {
     if constexpr (sizeof(T) == 4) {
       if (gemm_tc && m2l_backend == 2) {  // multipoles already split; the reduce splits the check rows
         // no P2L rows: the fp32 check rows are never read (only their split) -- skip them entirely

@@ -6,6 +6,7 @@ Tolerances (north star, BASELINE.json): relative L2 <= 1e-12 for fp64 and
 1e-11 (fp64) and 5e-5 (fp32).  Both oracle and GPU consume the same fp64
 operator matrices and factored pseudo-inverses (SURVEY 8c parity protocol).
 """
+import json
 import os
 
 import numpy as np
@@ -323,3 +324,35 @@ def test_schedule_switches_bit_identical(require_gpu, monkeypatch):
     for name in ("nosplit", "nopdl"):
         assert np.array_equal(out[name][0], out["ref"][0]) and np.array_equal(out[name][1], out["ref"][1]), name
     assert fmm.relative_error(out["noface"][0], out["ref"][0]) <= 1e-6
+
+
+@pytest.mark.parametrize("dist,n,ncrit,p", [("uniform-cube", 20000, 40, 7), ("sphere-surface", 20000, 30, 6),
+                                            ("two-cluster", 12000, 20, 7)])
+def test_fp64_int8_ozaki_m2l(require_gpu, dist, n, ncrit, p):
+    """fp64 M2L on the int8 tensor cores (m2l_backend 4, the fp64 default for p = 6, 7) against the DMMA
+    kernel (backend 1) and the fp64 oracle: the digit-sliced products are exact in int32, so the two
+    backends agree to fp64 rounding and both meet the 1e-12 parity gate."""
+    pos, q = generators.sample(dist, n, seed=17, charges="signed")
+    out = {}
+    for b in (4, 1):
+        with fmm.Fmm(pos, fmm.FmmConfig(p=p, n_crit=ncrit, precision=64, gradient=True, m2l_backend=b)) as f:
+            assert f.info()["m2l_backend"] == b
+            out[b] = f.evaluate(q)[:2]
+            if b == 4:
+                ref, gref = _ref(f, q, True)
+    e41 = fmm.relative_error(out[4][0], out[1][0])
+    e4 = fmm.relative_error(out[4][0], ref)
+    eg4 = fmm.relative_error(out[4][1], gref)
+    print(f"ozaki {dist} p={p}: vs DMMA {e41:.2e}, vs oracle {e4:.2e} (gradient {eg4:.2e})")
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(os.path.join("gpurun_out", "ozaki_r02.jsonl"), "a") as fh:
+        fh.write(json.dumps({"dist": dist, "n": n, "n_crit": ncrit, "p": p, "charges": "signed",
+                             "rel_l2_vs_dmma": e41, "rel_l2_vs_oracle": e4, "rel_l2_gradient_vs_oracle": eg4,
+                             "lib": os.environ.get("KIFMM_LIB", "default")}) + "\n")
+    assert e41 <= 1e-12 and e4 <= 1e-12 and eg4 <= 1e-11
+
+
+def test_int8_m2l_is_fp64_only(require_gpu):
+    pos, q = generators.sample("uniform-cube", 3000, seed=1, charges="signed", fp32=True)
+    with pytest.raises(InvalidArgument):
+        fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=40, precision=32, m2l_backend=4))

@@ -18,7 +18,8 @@ c = generators.CONFIGS[cfg_id]
 pos, q = generators.config_sample(cfg_id)
 ndt = np.float32 if c["precision"] == 32 else np.float64
 tdt = torch.float32 if c["precision"] == 32 else torch.float64
-f = fmm.Fmm(pos, fmm.FmmConfig(p=c["p"], n_crit=c["n_crit"], precision=c["precision"], gradient=c["gradient"]))
+f = fmm.Fmm(pos, fmm.FmmConfig(p=c["p"], n_crit=c["n_crit"], precision=c["precision"], gradient=c["gradient"],
+                               m2l_backend=int(os.environ.get("KIFMM_M2L_BACKEND", "0"))))
 n = len(q)
 dq = torch.from_numpy(q.astype(ndt)).cuda()
 dpot = torch.empty(n, dtype=tdt, device="cuda")
