@@ -409,6 +409,12 @@ def main():
         tf32 = peaks.get("bf16_tflops", 1590.0) / 2.0
         peak, bound, src = tf32 / 3.0, "tensor", ("measured bf16/2 (TF32) / 3 (3xTF32 issues 3 MMAs per "
                                                   "useful MAC), " + ("of measured" if peaks else "of fallback"))
+    elif info["m2l_backend"] == 4:
+        # int8 Ozaki scheme: 36 digit-slice products per useful fp64 MAC at 2x the bf16 MMA rate
+        i8 = 2.0 * peaks.get("bf16_tflops", 1590.0)
+        peak, bound, src = i8 / 36.0, "tensor", ("measured dense bf16 x 2 (kind::i8 rate) / 36: the 8-slice Ozaki "
+                                                 "scheme issues 36 int8 MMAs per useful fp64 MAC; " +
+                                                 ("of measured" if peaks else "of fallback"))
     else:
         fp32 = fmm.fma_peak(32, local) / 1e12
         peak, bound, src = fp32, "tensor", ("FP32 SIMT kernel: peak = FFMA throughput measured in this run "
@@ -416,7 +422,8 @@ def main():
                                             "compute roof, not tensor cores")
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak if peak else None, "traffic": ncu_traffic("m2l"),
-            "kernel": "M2L (gather_gemm_kernel)" if info["m2l_backend"] == 1 else "M2L (m2l_tc_kernel)",
+            "kernel": {1: "M2L (gather_gemm_kernel / gather_dmma_kernel)", 4: "M2L (m2l_oz_kernel)"}.get(
+                info["m2l_backend"], "M2L (m2l_tc_kernel)"),
             "peak_source": src,
             "work": f"2*n_e*n_c flop per V pair x {info['m2l_pairs']} V pairs per launch",
             "m2l_ms": ph["m2l_ms"]}
@@ -453,7 +460,8 @@ def main():
                                f"{f.tree.n_leaves} leaves",
                    "parallelism": f"morton-range x{world}" if world > 1 else "single-gpu",
                    "l2": "flushed (256 MiB write) between timed steps",
-                   "m2l_backend": {1: "simt", 2: "tcgen05-f16x3", 3: "tcgen05-3xtf32"}.get(info["m2l_backend"])},
+                   "m2l_backend": {1: "simt/dmma", 2: "tcgen05-f16x3", 3: "tcgen05-3xtf32",
+                                   4: "tcgen05-i8-ozaki"}.get(info["m2l_backend"])},
         "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "Fmm.evaluate_many_ptr (kifmm_gpu_evaluate_many): K steps = K charge vectors from pinned "
                        "host buffers, H2D / evaluate / D2H pipelined on three streams; wall clock",
