@@ -236,12 +236,19 @@ __global__ void __launch_bounds__(THREADS, 1) m2l_oz_kernel(const __grid_constan
       }
     }
   } else if (warp >= PROD_WARP0) {
-    // ---------------- A producers: thread = tile row r; per stage the two 16-byte chunks of each needed
-    //                  digit slice of its gathered source row, cp.async into the SWIZZLE_32B atom
-    const int r = threadIdx.x - 32 * PROD_WARP0;
-    const int sw = (r >> 2) & 1;
-    const uint32_t so0 = uint32_t((r >> 3) * 256 + (r & 7) * 32 + ((0 ^ sw) << 4));
-    const uint32_t so1 = uint32_t((r >> 3) * 256 + (r & 7) * 32 + ((1 ^ sw) << 4));
+    // ---------------- A producers: threads 2r', 2r' + 1 copy the two 16-byte halves of the 32-byte K block of
+    //                  rows r' and r' + 64, for every needed digit slice, by cp.async into the SWIZZLE_32B
+    //                  atoms -- a warp instruction covers 16 rows x 32 B, i.e. whole 32-byte sectors (a
+    //                  thread per row issued two half-sector requests per sector: L1TEX 94 % busy)
+    const int t = threadIdx.x - 32 * PROD_WARP0;
+    const int half = t & 1;
+    int rr[2], so[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int r = (t >> 1) + 64 * k;
+      rr[k] = r;
+      so[k] = (r >> 3) * 256 + (r & 7) * 32 + ((half ^ ((r >> 2) & 1)) << 4);
+    }
     int s = 0;
     uint32_t ph = 0;
     for (int kk = k_begin; kk < k_end; ++kk) {
@@ -249,22 +256,32 @@ __global__ void __launch_bounds__(THREADS, 1) m2l_oz_kernel(const __grid_constan
       const int sg0 = a.seg_ptr[tile], sg1 = a.seg_ptr[tile + 1];
       for (int p = 0; p < 2; ++p) {
         const int ns = n_slices(p);
-        int nxt = sg0 < sg1 ? a.seg_in[size_t(sg0) * BM + r] : -1;
+        int nxt[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) nxt[k] = sg0 < sg1 ? a.seg_in[size_t(sg0) * BM + rr[k]] : -1;
         for (int sg = sg0; sg < sg1; ++sg) {
-          const int src = nxt;
-          if (sg + 1 < sg1) nxt = a.seg_in[size_t(sg + 1) * BM + r];  // one tap ahead
-          const bool ok = src >= 0;
-          const int8_t* row = a.a8 + size_t(ok ? src : a.zero_row) * (S * NP);
-          const int sz = ok ? 16 : 0;
+          const int8_t* row[2];
+          int sz[2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const bool ok = nxt[k] >= 0;
+            row[k] = a.a8 + size_t(ok ? nxt[k] : a.zero_row) * (S * NP) + half * 16;
+            sz[k] = ok ? 16 : 0;
+          }
+          if (sg + 1 < sg1) {  // one tap ahead
+#pragma unroll
+            for (int k = 0; k < 2; ++k) nxt[k] = a.seg_in[size_t(sg + 1) * BM + rr[k]];
+          }
           for (int kb = 0; kb < C::NKB; ++kb) {
             mbar_wait(empty(s), ph ^ 1u);
             const uint32_t base = a_sl(s);
             for (int i = 0; i < ns; ++i) {
-              const int8_t* g = row + i * NP + kb * 32;
               const uint32_t d = base + uint32_t(i * C::A_SL);
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d + so0), "l"(g), "r"(sz) : "memory");
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d + so1), "l"(g + 16), "r"(sz)
-                           : "memory");
+#pragma unroll
+              for (int k = 0; k < 2; ++k)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d + uint32_t(so[k])),
+                             "l"(row[k] + i * NP + kb * 32), "r"(sz[k])
+                             : "memory");
             }
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
             if (++s == STAGES) {
