@@ -27,7 +27,6 @@
 #include "p2p.cuh"
 #include "near_ws.cuh"
 #include "m2l_oz.cuh"
-#include "near_warp.cuh"
 
 namespace kifmm {
 namespace gpu {
@@ -379,11 +378,6 @@ struct kifmm_gpu_plan {
   // standalone launch of the serialized timed run (there 2-5 % slower than one leaf_eval_f2 block per leaf)
   int near_ws = 1;
   int near_ws_bps = 2;
-  // warp-per-work persistent near field (near_warp.cuh), the default for fp32; KIFMM_NEAR_WARP=0 selects the
-  // block-per-leaf kernels (leaf_eval_f2 / near_ws) for comparison
-  bool near_warp = false;
-  int near_warp_bps = 2;     // its side blocks per SM next to the tcgen05 kernels (2 x 8 warps, 2 x 32 KB)
-  int near_warp_blocks = 4;  // resident blocks per SM of the standalone / drain launch (occupancy query)
   int near_ws_blocks = 6;  // resident blocks per SM of the standalone / drain launch (occupancy query)   // its side blocks per SM next to the tcgen05 kernels (smem: 2 x 37 KB + stages)
   int near_pause = 0;  // side blocks sleep during M2L: 1 all, 2 half (KIFMM_NEAR_PAUSE; 1 measured slower)
   int near_bps = 3;  // queue mode: near-field blocks per SM next to the tree passes (KIFMM_NEAR_BPS, 0 = off)
@@ -391,6 +385,8 @@ struct kifmm_gpu_plan {
   DevMem near_counter;  // queue mode work counter [, counter at the drain launch (KIFMM_NEAR_DEBUG)]
   bool near_debug = false, near_skip = false, far_as_leaf = false, near_corun = false;
   int near_fork_at = 0;  // 0: at the start of the evaluate, 1: just before M2L, 2: after the P2M check, 3: after M2M
+  bool near_serial = false;  // near field on the plan stream after L2L instead of a side stream (KIFMM_NEAR_SERIAL;
+                             // default for fp64)
   bool grad = false;
   int64_t N = 0, nl = 0, nn = 0;
   int depth = 0, ne = 0, nc = 0, np = 0, ref_level = 2;
@@ -1167,11 +1163,13 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     leaf_packed = precision == 32 && !(e && std::string(e) == "scalar");
   }
   const bool packed = leaf_packed;
+  // fp64: the scalar near field slows the int8 M2L more than it gains next to it (config 4: 101 ms serial,
+  // 105 ms on the side stream); fp32 keeps its queue-mode side blocks (config 2: 1.20 vs 1.46 ms serial)
+  near_serial = precision == 64;
+  if (const char* e = std::getenv("KIFMM_NEAR_SERIAL")) near_serial = std::atoi(e) != 0;
   if (packed) {
-    if (const char* e = std::getenv("KIFMM_NEAR_WARP")) near_warp = std::atoi(e) != 0;
     if (const char* e = std::getenv("KIFMM_NEAR_WS")) near_ws = std::atoi(e);
     if (near_ws) near_bps = near_ws_bps;
-    if (near_warp) near_bps = near_warp_bps;
     if (const char* e = std::getenv("KIFMM_NEAR_BPS")) near_bps = std::max(0, std::atoi(e));
     near_counter.alloc(4 * sizeof(int), &dev_bytes);
 #ifdef KIFMM_EXPERIMENTS  // timing experiments only (tools/build_variant.sh); NEAR_SKIP gives wrong results
@@ -1194,16 +1192,11 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
                           (const void*)near_ws_kernel<true, 2>, (const void*)near_ws_kernel<false, 0>,
                           (const void*)near_ws_kernel<false, 1>, (const void*)near_ws_kernel<false, 2>,
                           (const void*)leaf_eval_f2_kernel<true, false, false>,
-                          (const void*)leaf_eval_f2_kernel<false, false, false>,
-                          (const void*)near_warp_kernel<true, 0>, (const void*)near_warp_kernel<true, 1>,
-                          (const void*)near_warp_kernel<true, 2>, (const void*)near_warp_kernel<false, 0>,
-                          (const void*)near_warp_kernel<false, 1>, (const void*)near_warp_kernel<false, 2>})
+                          (const void*)leaf_eval_f2_kernel<false, false, false>})
       KIFMM_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     int nb = 0;
     KIFMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, near_ws_kernel<true, 2>, kNearWsThreads, 0));
     near_ws_blocks = std::max(1, nb);
-    KIFMM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, near_warp_kernel<true, 2>, kNwWarps * 32, 0));
-    near_warp_blocks = std::max(1, nb);
   }
   auto build_leaf_plan = [&](bool near_part, LeafPlan& lp) {
     struct Src {
@@ -1258,14 +1251,12 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
         }
         if (other.empty()) continue;
       }
-      // warp geometry (near_warp_kernel, near part): <= 64 targets per work, R = nw_slices source slices,
-      // rounds of <= kNwCap sources; block geometry: <= 128 targets, leaf_slices, rounds of <= kP2PCap
-      const bool wg = near_part && packed && near_warp;
-      const int chunk = wg ? kNwTargets : kP2PThreads;
+      // block geometry: <= 128 targets, leaf_slices source slices, rounds of <= kP2PCap sources
+      const int chunk = kP2PThreads;
       for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += chunk) {
         const int nt = int(std::min<int64_t>(chunk, t.leaf_ptr[l + 1] - t0));
-        const int R = wg ? nw_slices(nt) : leaf_slices(nt, packed), q = (wg ? 4 : leaf_unroll(packed)) * R;
-        const int cap = wg ? kNwCap - kNwCap % q : kP2PCap - kP2PCap % q;
+        const int R = leaf_slices(nt, packed), q = leaf_unroll(packed) * R;
+        const int cap = kP2PCap - kP2PCap % q;
         const int rb = int(rounds.size());
         size_t si = 0, oi = 0;
         int soff = 0, ooff = 0;  // offsets inside the current self / other source
@@ -1495,18 +1486,6 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
     const int4* it = lp.items.as<int4>();
     T* g = grad ? grad_buf.as<T>() : nullptr;
     if constexpr (sizeof(T) == 4) {
-      if (leaf_packed && near_warp && &lp == &leaf_near && !acc) {  // standalone warp-per-work near field
-        int* qc = near_counter.as<int>();
-        KIFMM_CUDA(cudaMemsetAsync(qc, 0, 4 * sizeof(int), st));
-        const int grid = int(std::min<int64_t>(ceil_div(lp.n, kNwWarps), int64_t(near_warp_blocks) * sm_count()));
-        if (grad)
-          near_warp_kernel<true, 0><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pot.as<T>(), g, lp.n, qc);
-        else
-          near_warp_kernel<false, 0><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pot.as<T>(), g, lp.n, qc);
-        KIFMM_LAUNCH_CHECK();
-        ++launches;
-        return;
-      }
       if (leaf_packed && near_ws >= 2 && &lp == &leaf_near && !acc) {  // standalone persistent near field
         int* qc = near_counter.as<int>();
         KIFMM_CUDA(cudaMemsetAsync(qc, 0, 4 * sizeof(int), st));
@@ -1563,7 +1542,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
   // kernels and take works from a shared counter, drained by a full launch after L2L
   // (KIFMM_NEAR_CORUN: experiments -- the timed run co-runs the near field with M2L to time M2L under load)
   const bool corun = timed && near_corun && leaf_packed;
-  const bool queue_mode = (!timed || corun) && leaf_packed && near_bps > 0 && leaf_near.n && !near_skip;
+  const bool queue_mode = (!timed || corun) && !near_serial && leaf_packed && near_bps > 0 && leaf_near.n && !near_skip;
   auto near_queue = [&](cudaStream_t st, int grid, bool drain) {
     if constexpr (sizeof(T) == 4) {
       const LeafWork* w = leaf_near.works.as<LeafWork>();
@@ -1573,19 +1552,6 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
       int* qc = near_counter.as<int>();
       float* pt = pot.as<float>();
       const int n = leaf_near.n;
-      if (near_warp) {
-        if (grad && drain)
-          near_warp_kernel<true, 2><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pt, g, n, qc);
-        else if (grad)
-          near_warp_kernel<true, 1><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pt, g, n, qc);
-        else if (drain)
-          near_warp_kernel<false, 2><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pt, g, n, qc);
-        else
-          near_warp_kernel<false, 1><<<grid, kNwWarps * 32, 0, st>>>(pp, w, r, it, pt, g, n, qc);
-        KIFMM_LAUNCH_CHECK();
-        ++launches;
-        return;
-      }
       if (near_ws) {
         if (grad && drain)
           near_ws_kernel<true, 2><<<grid, kNearWsThreads, 0, st>>>(pp, w, r, it, pt, g, n, qc);
@@ -1611,8 +1577,9 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
       ++launches;
     }
   };
+  const bool near_fork = (!timed || corun) && !near_serial;  // near field on the side stream
   auto fork_near = [&]() {
-    if ((!timed || corun) && leaf_near.n && !near_skip) {
+    if (near_fork && leaf_near.n && !near_skip) {
       if (queue_mode) KIFMM_CUDA(cudaMemsetAsync(near_counter.p, 0, 4 * sizeof(int), s));
       KIFMM_CUDA(cudaEventRecord(ev_fork, s));
       KIFMM_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
@@ -1809,7 +1776,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
     mark();  // 7
   }
   // leaves: near field (side stream, or here when timed) then L2P + M2P
-  if (timed && !corun) leaf(leaf_near, false, s);
+  if (!near_fork) leaf(leaf_near, false, s);
 #ifdef KIFMM_EXPERIMENTS
   if (queue_mode && near_debug && !std::getenv("KIFMM_NEAR_DEBUG_M2L"))  // experiments: works taken by now
     KIFMM_CUDA(cudaMemcpyAsync(near_counter.as<int>() + 2, near_counter.as<int>(), sizeof(int),
@@ -1819,10 +1786,9 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
   // empty queue costs one short wave instead of a block per leaf)
   if (queue_mode)
     near_queue(s,
-               near_warp ? int(std::min<int64_t>(ceil_div(leaf_near.n, kNwWarps), int64_t(near_warp_blocks) * sm_count()))
-                         : std::min(leaf_near.n, (near_ws ? near_ws_blocks : 8) * sm_count()),
+               std::min(leaf_near.n, (near_ws ? near_ws_blocks : 8) * sm_count()),
                true);
-  if ((!timed || corun) && leaf_near.n && !near_skip) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+  if (near_fork && leaf_near.n && !near_skip) KIFMM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
   bool fused_out = false;  // the packed far kernel wrote the final (input-order) output
   if (far_as_leaf) leaf(leaf_far, true, s);
   if constexpr (sizeof(T) == 4) {

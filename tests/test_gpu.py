@@ -182,30 +182,23 @@ def test_run_api(require_gpu):  # run(particles, config) -> potenti
 
 def test_near_queue_mode_bit_identical(require_gpu, monkeypatch):
     """Queue mode (near field taken by side-stream blocks from a counter, drained after L2L) computes
-    every leaf work in exactly one warp / block: results equal the standalone launch bit for bit, for the
-    warp-per-work kernel (default, KIFMM_NEAR_WARP=1) and for the block-per-leaf family (KIFMM_NEAR_WARP=0:
-    KIFMM_NEAR_WS=0 one leaf_eval_f2 block per work, 1 the warp-specialised kernel in queue mode, 2 also
-    standalone).  The two families slice the sources differently, so they agree to fp32 rounding."""
+    every leaf work in exactly one block: results equal the standalone launch bit for bit
+    (KIFMM_NEAR_WS=0 one leaf_eval_f2 block per work, 1 the warp-specialised kernel in queue mode, 2 also
+    standalone; KIFMM_NEAR_BPS = side blocks per SM, 0 = no queue)."""
     pos, q = generators.sample("two-cluster", 60000, seed=21, charges="signed", fp32=True)
     cfg = fmm.FmmConfig(p=6, n_crit=40, precision=32, gradient=True)
-    fam = {}
-    for warp, wss in (("1", ("1",)), ("0", ("0", "1", "2"))):
-        out = {}
-        for ws in wss:
-            for bps in ("0", "1", "2"):
-                monkeypatch.setenv("KIFMM_NEAR_WARP", warp)
-                monkeypatch.setenv("KIFMM_NEAR_WS", ws)
-                monkeypatch.setenv("KIFMM_NEAR_BPS", bps)
-                with fmm.Fmm(pos, cfg) as f:
-                    out[ws, bps] = f.evaluate(q)[:2]
-                    if bps == "0":
-                        out[ws, "timed"] = f.evaluate(q, timed=True)[:2]
-        ref = out[wss[0], "0"]
-        for k, v in out.items():
-            assert np.array_equal(v[0], ref[0]) and np.array_equal(v[1], ref[1]), (warp, k)
-        fam[warp] = ref
-    assert fmm.relative_error(fam["1"][0], fam["0"][0]) <= 1e-6
-    assert fmm.relative_error(fam["1"][1], fam["0"][1]) <= 1e-5
+    out = {}
+    for ws in ("0", "1", "2"):
+        for bps in ("0", "1", "2"):
+            monkeypatch.setenv("KIFMM_NEAR_WS", ws)
+            monkeypatch.setenv("KIFMM_NEAR_BPS", bps)
+            with fmm.Fmm(pos, cfg) as f:
+                out[ws, bps] = f.evaluate(q)[:2]
+                if bps == "0":
+                    out[ws, "timed"] = f.evaluate(q, timed=True)[:2]
+    ref = out["0", "0"]
+    for k, v in out.items():
+        assert np.array_equal(v[0], ref[0]) and np.array_equal(v[1], ref[1]), k
 
 
 def test_simt_gemms_with_tcgen05_m2l(require_gpu, monkeypatch):
@@ -356,3 +349,15 @@ def test_int8_m2l_is_fp64_only(require_gpu):
     pos, q = generators.sample("uniform-cube", 3000, seed=1, charges="signed", fp32=True)
     with pytest.raises(InvalidArgument):
         fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=40, precision=32, m2l_backend=4))
+
+
+def test_fp64_near_serial_bit_identical(require_gpu, monkeypatch):
+    """fp64 runs the near field on the plan stream after L2L (KIFMM_NEAR_SERIAL, the fp64 default) or on
+    the side stream next to the tree passes: the same kernels and accumulation order, bit-identical."""
+    pos, q = generators.sample("uniform-cube", 20000, seed=31, charges="signed")
+    out = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("KIFMM_NEAR_SERIAL", v)
+        with fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=40, precision=64, gradient=True)) as f:
+            out[v] = f.evaluate(q)[:2]
+    assert np.array_equal(out["1"][0], out["0"][0]) and np.array_equal(out["1"][1], out["0"][1])
