@@ -345,6 +345,23 @@ def test_fp64_int8_ozaki_m2l(require_gpu, dist, n, ncrit, p):
     assert e41 <= 1e-12 and e4 <= 1e-12 and eg4 <= 1e-11
 
 
+def test_fp64_int8_ozaki_dynamic_range(require_gpu):
+    """The int8 digits are relative to each LEVEL's largest multipole, so rows far below it keep fewer
+    bits.  Charges spanning six decades (log-uniform, random signs) on a clustered cloud still meet the
+    fp64 gate against the DMMA kernel and the oracle."""
+    pos, _ = generators.sample("two-cluster", 12000, seed=41)
+    rng = np.random.default_rng(41)
+    q = rng.choice([-1.0, 1.0], size=len(pos)) * 10.0 ** rng.uniform(-6, 0, size=len(pos))
+    out = {}
+    for b in (4, 1):
+        with fmm.Fmm(pos, fmm.FmmConfig(p=7, n_crit=20, precision=64, m2l_backend=b)) as f:
+            out[b] = f.evaluate(q)[0]
+            if b == 4:
+                ref, _ = _ref(f, q, False)
+    assert fmm.relative_error(out[4], out[1]) <= 1e-12
+    assert fmm.relative_error(out[4], ref) <= 1e-12
+
+
 def test_int8_m2l_is_fp64_only(require_gpu):
     pos, q = generators.sample("uniform-cube", 3000, seed=1, charges="signed", fp32=True)
     with pytest.raises(InvalidArgument):

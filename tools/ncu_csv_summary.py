@@ -12,6 +12,7 @@ COLS = [
     ("duration", "gpu__time_duration.sum"),
     ("SM clock", "sm__cycles_elapsed.avg.per_second"),
     ("FMA pipe %", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+    ("FP64 pipe %", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
     ("XU (MUFU) inst %", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
     ("issue active %", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
     ("warps active %", "sm__warps_active.avg.pct_of_peak_sustained_active"),
