@@ -714,8 +714,9 @@ template <bool GRAD>
 __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kernel(
     P2PParams<float> p, const FarWork* __restrict__ works, int n_works, const int2* __restrict__ surfaces,
     const float* __restrict__ M, const float* __restrict__ L, float* pot, float* grad, const int* __restrict__ perm,
-    float* pot_out, float* grad_out) {
+    float* pot_out, float* grad_out, float4* __restrict__ part = nullptr) {
   __shared__ float4 sh[kFarWarps][2][kFarHwSlot];
+  __shared__ float dens_next[kFarWarps][2][kFarHwSlot];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
   const int wi = (blockIdx.x * kFarWarps + warp) * 2 + half;
   timeline_begin(5);
@@ -747,22 +748,58 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
   }
   const f2_t x = f2_pair(xa.x, xb.x), y = f2_pair(xa.y, xb.y), z = f2_pair(xa.z, xb.z);
   f2_t ph = 0, gx = 0, gy = 0, gz = 0;
-  // surfaces of this half's work; the halves loop to the longer list (works are paired on the host)
+  // surfaces of this half's work; the halves loop to the longer list (works are paired on the host).
+  // Surface k + 1 is fetched while surface k is computed: its equivalent densities by cp.async into a
+  // per-half buffer, its node geometry into registers, and the descriptor of k + 2 -- so a work with
+  // many (M2P) surfaces no longer waits on two dependent global loads before every surface.
   const int ns = valid ? w.surf_end - w.surf_begin : 0;
   const int ns_max = max(ns, __shfl_xor_sync(0xffffffffu, ns, 16));
   const int q4 = 4 * R, pad = (p.n_e + q4 - 1) / q4 * q4, per = pad / R;
   float4* my = sh[warp][half];
+  float* dn = dens_next[warp][half];
   const float fa = float(kFarAway);
-  for (int k = 0; k < ns_max; ++k) {
-    const int2 sf = k == 0 ? make_int2(w.node0, w.kind0) : k < ns ? surfaces[w.surf_begin + k] : make_int2(0, 0);
+  auto surf = [&](int k) {
+    return k == 0 ? make_int2(w.node0, w.kind0) : k < ns ? surfaces[w.surf_begin + k] : make_int2(-1, 0);
+  };
+  // surface 0: staged directly
+  {
+    const int2 sf = surf(0);
     const bool l2p = sf.y == kSrcL2P;
     const float alpha = l2p ? p.alpha_outer : p.alpha_inner;
     const float* dens = l2p ? L : M;
-    __syncwarp();
     for (int j = hl; j < pad; j += 16)
-      my[j] = (k < ns && j < p.n_e) ? surface_source(p, sf.x, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
+      my[j] = (0 < ns && j < p.n_e) ? surface_source(p, sf.x, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
+  }
+  int2 sf_n = surf(1);  // descriptor of the next surface
+  for (int k = 0; k < ns_max; ++k) {
     __syncwarp();
+    // issue surface k + 1: densities -> dn (cp.async), node geometry -> registers
+    const bool nlive = k + 1 < ns;
+    float4 gn = make_float4(0.f, 0.f, 0.f, 0.f);
+    float an = 0.f;
+    if (nlive) {
+      const bool l2p = sf_n.y == kSrcL2P;
+      an = l2p ? p.alpha_outer : p.alpha_inner;
+      const float* dens = (l2p ? L : M) + size_t(sf_n.x) * p.ld;
+      gn = p.node_geom[sf_n.x];
+      for (int j = hl; j < p.n_e; j += 16)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(uint32_t(__cvta_generic_to_shared(dn + j))),
+                     "l"(dens + j)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const int2 sf_nn = surf(k + 2);
     if (act && k < ns) p2p_round_f2<GRAD, false>(my, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
+    if (k + 1 < ns_max) {
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncwarp();  // every lane is done reading surface k and sees surface k + 1's densities
+      const float sc = an * gn.w;
+      for (int j = hl; j < pad; j += 16)
+        my[j] = (nlive && j < p.n_e) ? make_float4(gn.x + sc * p.surface[3 * j], gn.y + sc * p.surface[3 * j + 1],
+                                                   gn.z + sc * p.surface[3 * j + 2], dn[j])
+                                     : make_float4(fa, fa, fa, 0.f);
+    }
+    sf_n = sf_nn;
   }
   timeline_end(5);
   float v[8];
@@ -783,6 +820,14 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
     }
   }
   const float c = float(kInv4PiD);
+  if (w.pad0 > 0) {  // a chunk of a long work: partial sums only (far_combine_kernel finishes the targets)
+    float4* pp = part + size_t(w.pad0 - 1) * 32;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (h ? out_b : out_a)
+        pp[h ? tb : ta] = make_float4(c * v[4 * h], c * v[4 * h + 1], c * v[4 * h + 2], c * v[4 * h + 3]);
+    return;
+  }
   float* po = perm ? pot_out : pot;
   float* go = perm ? grad_out : grad;
 #pragma unroll
@@ -795,6 +840,39 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
       go[3 * size_t(o) + 1] = gv[h][1] - c * v[4 * h + 2];
       go[3 * size_t(o) + 2] = gv[h][2] - c * v[4 * h + 3];
     }
+  }
+}
+
+// Targets of a far work cut into surface chunks: near field + the chunks' partial sums in chunk order,
+// written like far_hw_kernel writes (input order through perm, or back into pot / grad).
+// group = {t0, count, first slot, chunks}; one thread per (group, target).
+template <bool GRAD>
+__global__ void far_combine_kernel(const int4* __restrict__ groups, int n_groups, const float4* __restrict__ part,
+                                   float* pot, float* grad, const int* __restrict__ perm, float* pot_out,
+                                   float* grad_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gi = i >> 5, ti = i & 31;
+  if (gi >= n_groups) return;
+  const int4 g = groups[gi];
+  if (ti >= g.y) return;
+  const int t = g.x + ti;
+  float a = 0.f, bx = 0.f, by = 0.f, bz = 0.f;
+  for (int c = 0; c < g.w; ++c) {
+    const float4 p = part[size_t(g.z + c) * 32 + ti];
+    a += p.x;
+    bx += p.y;
+    by += p.z;
+    bz += p.w;
+  }
+  const int o = perm ? perm[t] : t;
+  float* po = perm ? pot_out : pot;
+  po[o] = pot[t] + a;
+  if (GRAD) {
+    float* go = perm ? grad_out : grad;
+    const float g0 = grad[3 * size_t(t)], g1 = grad[3 * size_t(t) + 1], g2 = grad[3 * size_t(t) + 2];
+    go[3 * size_t(o)] = g0 - bx;
+    go[3 * size_t(o) + 1] = g1 - by;
+    go[3 * size_t(o) + 2] = g2 - bz;
   }
 }
 

@@ -413,6 +413,8 @@ struct kifmm_gpu_plan {
   LeafPlan leaf_near, leaf_far;
   DevMem far_works, far_surfaces, leaf_ptr_dev;  // far_works: int4 (scalar kernel) or FarWork (packed)
   int n_far = 0;
+  int far_chunk = 0, n_far_groups = 0;  // surface chunking of long half-warp far works (see build)
+  DevMem far_part, far_groups;
   bool far_hw = false;  // half-warp far kernel (every work has at most one surface; KIFMM_FAR_HW=0: off)
   int n_p2m = 0, n_p2l = 0;
   GemmTiles solve_up1, solve_up2, solve_dn1, solve_dn2, m2l;
@@ -1355,9 +1357,46 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
           fw.push_back(make_int4(int(t0), b, e, cnt));
       }
     }
-    n_far = int(packed ? fw2.size() : fw.size());
     far_hw = packed && ne <= 4 * (kFarHwSlot / 4);
     if (const char* e = std::getenv("KIFMM_FAR_HW")) far_hw = far_hw && std::atoi(e) != 0;
+    // Long works (many M2P surfaces, adaptive trees) are cut into chunks of <= far_chunk surfaces: a
+    // half-warp walks one work's surfaces in sequence, so the longest work bounds the kernel (config 3:
+    // 41 surfaces, against 19 per resident half-warp on average).  Chunks write partial sums to far_part
+    // slots (FarWork.pad0 = slot + 1); far_combine_kernel adds them in chunk order to the near field
+    // and writes the output.
+    // Measured (config 3): 1.312 ms unchunked, 1.217 / 1.210 / 1.213 ms with chunks of 6 / 8 / 12, 1.231 with
+    // the mean surfaces per resident half-warp (19); config 5 is unchanged (118 ms).  KIFMM_FAR_CHUNK=0: off.
+    far_chunk = 0;
+    if (far_hw) {
+      far_chunk = 12;
+      if (const char* e = std::getenv("KIFMM_FAR_CHUNK")) far_chunk = std::atoi(e);
+    }
+    std::vector<int4> groups;  // {t0, count, first slot, n chunks}
+    if (far_chunk > 0) {
+      std::vector<FarWork> out;
+      int slots = 0;
+      for (const FarWork& w : fw2) {
+        const int nsf = w.surf_end - w.surf_begin;
+        if (nsf <= far_chunk) {
+          out.push_back(w);
+          continue;
+        }
+        const int nch = (nsf + far_chunk - 1) / far_chunk;
+        groups.push_back(make_int4(w.t0, w.count, slots, nch));
+        for (int c = 0; c < nch; ++c) {
+          const int b = w.surf_begin + c * far_chunk, e = std::min(w.surf_end, b + far_chunk);
+          out.push_back({w.t0, w.count, b, e, sf[b].x, sf[b].y, slots + c + 1, 0});
+        }
+        slots += nch;
+      }
+      fw2.swap(out);
+      n_far_groups = int(groups.size());
+      if (slots) {
+        far_part.alloc(size_t(slots) * 32 * sizeof(float4), &dev_bytes);
+        far_groups.upload(groups, &dev_bytes);
+      }
+    }
+    n_far = int(packed ? fw2.size() : fw.size());
     // half-warp kernel: a warp's two works loop to the longer surface list -- pair works of equal
     // surface counts (stable sort by count; every work writes only its own targets, order is free)
     if (far_hw && packed)  // equal (surface count, source slices) in the two halves of a warp
@@ -1802,14 +1841,15 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
       const int* pm = input_order ? perm.as<int>() : nullptr;
       float* go = grad ? grad_out.as<float>() : nullptr;
       const int hw_blocks = int(ceil_div(n_far, 2 * kFarWarps));
+      float4* part = n_far_groups ? far_part.as<float4>() : nullptr;
       if (far_hw && grad)
         far_hw_kernel<true><<<hw_blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far,
                                                                  far_surfaces.as<int2>(), Mp, Lp, pot.as<float>(), g,
-                                                                 pm, pot_out.as<float>(), go);
+                                                                 pm, pot_out.as<float>(), go, part);
       else if (far_hw)
         far_hw_kernel<false><<<hw_blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far,
                                                                   far_surfaces.as<int2>(), Mp, Lp, pot.as<float>(), g,
-                                                                  pm, pot_out.as<float>(), go);
+                                                                  pm, pot_out.as<float>(), go, part);
       else if (grad)
         far_f2_kernel<true><<<blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far, far_surfaces.as<int2>(),
                                                               Mp, Lp, pot.as<float>(), g, pm, pot_out.as<float>(), go);
@@ -1817,6 +1857,16 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
         far_f2_kernel<false><<<blocks, kFarWarps * 32, 0, s>>>(pp, far_works.as<FarWork>(), n_far,
                                                                far_surfaces.as<int2>(), Mp, Lp, pot.as<float>(), g, pm,
                                                                pot_out.as<float>(), go);
+      if (far_hw && n_far_groups) {  // targets of the long works cut into surface chunks
+        KIFMM_LAUNCH_CHECK();
+        ++launches;
+        if (grad)
+          far_combine_kernel<true><<<unsigned(ceil_div(int64_t(n_far_groups) * 32, 256)), 256, 0, s>>>(
+              far_groups.as<int4>(), n_far_groups, part, pot.as<float>(), g, pm, pot_out.as<float>(), go);
+        else
+          far_combine_kernel<false><<<unsigned(ceil_div(int64_t(n_far_groups) * 32, 256)), 256, 0, s>>>(
+              far_groups.as<int4>(), n_far_groups, part, pot.as<float>(), g, pm, pot_out.as<float>(), go);
+      }
       KIFMM_LAUNCH_CHECK();
       ++launches;
       fused_out = true;

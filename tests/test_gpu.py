@@ -378,3 +378,28 @@ def test_fp64_near_serial_bit_identical(require_gpu, monkeypatch):
         with fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=40, precision=64, gradient=True)) as f:
             out[v] = f.evaluate(q)[:2]
     assert np.array_equal(out["1"][0], out["0"][0]) and np.array_equal(out["1"][1], out["0"][1])
+
+
+@pytest.mark.parametrize("gradient,input_order", [(False, True), (True, True), (True, False)])
+def test_far_surface_chunks(require_gpu, monkeypatch, gradient, input_order):
+    """Far works with many (M2P) surfaces are cut into chunks whose partial sums far_combine_kernel adds in
+    chunk order: the result equals the unchunked far kernel (KIFMM_FAR_CHUNK=0) to fp32 summation order,
+    in input order and in reordered order, with and without gradient, and meets the oracle gate."""
+    pos, q = generators.sample("sphere-surface", 60000, seed=29, charges="signed", fp32=True)
+    cfg = fmm.FmmConfig(p=6, n_crit=40, precision=32, gradient=gradient)
+    out = {}
+    for ch in ("0", "3"):
+        monkeypatch.setenv("KIFMM_FAR_CHUNK", ch)
+        with fmm.Fmm(pos, cfg) as f:
+            qq = q if input_order else q[f.tree.original_index]
+            out[ch] = f.evaluate(qq, input_order=input_order)[:2]
+            if ch == "3":
+                ref, gref = _ref(f, q, gradient)
+                if not input_order:
+                    ref = ref[f.tree.original_index]
+                    gref = gref[f.tree.original_index] if gradient else None
+    assert fmm.relative_error(out["3"][0], out["0"][0]) <= 1e-6
+    assert fmm.relative_error(out["3"][0], ref) <= 1e-5
+    if gradient:
+        assert fmm.relative_error(out["3"][1], out["0"][1]) <= 1e-6
+        assert fmm.relative_error(out["3"][1], gref) <= 5e-5
