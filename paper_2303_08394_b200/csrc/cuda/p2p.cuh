@@ -101,6 +101,41 @@ __device__ __forceinline__ void p2p_round(const v4_t<T>* sh, int begin, int end,
   gz += a_gz;
 }
 
+// Two targets per thread (the fp64 near field): one staged source feeds two independent chains (ILP),
+// same per-target arithmetic and accumulation order as p2p_round.
+template <class T, bool GRAD, bool MASK>
+__device__ __forceinline__ void p2p_round2(const v4_t<T>* sh, int begin, int end, const v4_t<T>& xa,
+                                           const v4_t<T>& xb, T (&acc)[2][4]) {
+  T pa[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+  for (int j = begin; j < end; j += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const v4_t<T> s = sh[j + u];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const v4_t<T>& x = h ? xb : xa;
+        const T dx = x.x - s.x, dy = x.y - s.y, dz = x.z - s.z;
+        const T r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        const T ri = MASK ? rinv_masked(r2) : rinv(r2);
+        if (GRAD) {
+          const T qr = s.w * ri;
+          pa[h][0] += qr;
+          const T qr3 = qr * (ri * ri);
+          pa[h][1] = fma(qr3, dx, pa[h][1]);
+          pa[h][2] = fma(qr3, dy, pa[h][2]);
+          pa[h][3] = fma(qr3, dz, pa[h][3]);
+        } else {
+          pa[h][0] = fma(s.w, ri, pa[h][0]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int d = 0; d < 4; ++d) acc[h][d] += pa[h][d];
+}
+
 // Thread geometry of a leaf work: the scalar kernel (fp64) gives every thread
 // one target and unrolls sources by 8; the packed fp32 kernel gives every
 // thread two targets (one FP32x2 lane pair) and unrolls by 4.  Sections are
@@ -521,6 +556,75 @@ __global__ void __launch_bounds__(kP2PThreads) leaf_eval_kernel(P2PParams<T> p, 
     for (int sl = 0; sl < R; ++sl)
 #pragma unroll
       for (int d = 0; d < NC; ++d) a[d] += red[(sl * NC + d) * kP2PThreads + tid];
+    const int t = w.t_begin + tid;
+    pot[t] = (ACC ? pot[t] : T(0)) + c * a[0];
+    if (GRAD) {
+      T* gp = grad + 3 * size_t(t);
+      gp[0] = (ACC ? gp[0] : T(0)) - c * a[NC > 1 ? 1 : 0];
+      gp[1] = (ACC ? gp[1] : T(0)) - c * a[NC > 2 ? 2 : 0];
+      gp[2] = (ACC ? gp[2] : T(0)) - c * a[NC > 3 ? 3 : 0];
+    }
+  }
+}
+
+// fp64 near field with two targets per thread (geometry of the packed fp32 kernel: TT = ceil(n_t / 2)
+// target pairs x R = leaf_slices(n_t, true) source slices, targets t0 and t0 + TT), scalar arithmetic.
+template <class T, bool GRAD, bool ACC>
+__global__ void __launch_bounds__(kP2PThreads) leaf_eval_pair_kernel(P2PParams<T> p, const LeafWork* __restrict__ works,
+                                                                      const int4* __restrict__ rounds,
+                                                                      const int4* __restrict__ items,
+                                                                      T* __restrict__ pot, T* __restrict__ grad) {
+  __shared__ v4_t<T> sh[kP2PCap];
+  const LeafWork w = works[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nt = w.t_count, TT = w.geom >> 8, R = w.geom & 0xFF;
+  const int slice = div_mul(tid, w.mul_tt), t0 = tid - slice * TT;
+  const bool active = slice < R;
+  const int ta = t0, tb = t0 + TT;
+  const v4_t<T> xa = p.src[w.t_begin + (active && ta < nt ? ta : 0)];
+  const v4_t<T> xb = p.src[w.t_begin + (active && tb < nt ? tb : 0)];
+  T acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+  const v4_t<T> far = make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
+  for (int r = w.round_begin; r < w.round_end; ++r) {
+    const int4 rd = rounds[r];
+    const int S = rd.z & 0xFFFF, ns = rd.z >> 16, O = rd.w & 0xFFFF, no = rd.w >> 16;
+    for (int k = rd.x + warp; k < rd.y; k += 4) {  // near plan: particle items only
+      const int4 item = items[k];
+      for (int i = lane; i < item.z; i += 32) sh[item.w + i] = p.src[item.y + i];
+    }
+    for (int i = ns + tid; i < S; i += kP2PThreads) sh[i] = far;
+    for (int i = S + no + tid; i < S + O; i += kP2PThreads) sh[i] = far;
+    __syncthreads();
+    if (active) {
+      if (S) {
+        const int per = div_mul(S, w.mul_r);
+        p2p_round2<T, GRAD, true>(sh, slice * per, slice * per + per, xa, xb, acc);
+      }
+      if (O) {
+        const int per = div_mul(O, w.mul_r);
+        p2p_round2<T, GRAD, false>(sh, S + slice * per, S + slice * per + per, xa, xb, acc);
+      }
+    }
+    __syncthreads();
+  }
+  T* red = reinterpret_cast<T*>(sh);  // [slice][component][n_t]: R * n_t <= 256
+  constexpr int NC = GRAD ? 4 : 1;
+  if (active) {
+#pragma unroll
+    for (int d = 0; d < NC; ++d) {
+      if (ta < nt) red[(slice * NC + d) * nt + ta] = acc[0][d];
+      if (tb < nt) red[(slice * NC + d) * nt + tb] = acc[1][d];
+    }
+  }
+  __syncthreads();
+  if (tid < nt) {
+    const T c = T(kInv4PiD);
+    T a[NC];
+#pragma unroll
+    for (int d = 0; d < NC; ++d) a[d] = 0;
+    for (int sl = 0; sl < R; ++sl)
+#pragma unroll
+      for (int d = 0; d < NC; ++d) a[d] += red[(sl * NC + d) * nt + tid];
     const int t = w.t_begin + tid;
     pot[t] = (ACC ? pot[t] : T(0)) + c * a[0];
     if (GRAD) {

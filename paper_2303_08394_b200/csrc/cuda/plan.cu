@@ -385,6 +385,7 @@ struct kifmm_gpu_plan {
   DevMem near_counter;  // queue mode work counter [, counter at the drain launch (KIFMM_NEAR_DEBUG)]
   bool near_debug = false, near_skip = false, far_as_leaf = false, near_corun = false;
   int near_fork_at = 0;  // 0: at the start of the evaluate, 1: just before M2L, 2: after the P2M check, 3: after M2M
+  bool near_pair64 = false;  // fp64 near field: two targets per thread (leaf_eval_pair_kernel; KIFMM_NEAR_PAIR64)
   bool near_serial = false;  // near field on the plan stream after L2L instead of a side stream (KIFMM_NEAR_SERIAL;
                              // default for fp64)
   bool grad = false;
@@ -1168,6 +1169,8 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   // fp64: the scalar near field slows the int8 M2L more than it gains next to it (config 4: 101 ms serial,
   // 105 ms on the side stream); fp32 keeps its queue-mode side blocks (config 2: 1.20 vs 1.46 ms serial)
   near_serial = precision == 64;
+  near_pair64 = precision == 64;
+  if (const char* e = std::getenv("KIFMM_NEAR_PAIR64")) near_pair64 = precision == 64 && std::atoi(e) != 0;
   if (const char* e = std::getenv("KIFMM_NEAR_SERIAL")) near_serial = std::atoi(e) != 0;
   if (packed) {
     if (const char* e = std::getenv("KIFMM_NEAR_WS")) near_ws = std::atoi(e);
@@ -1253,11 +1256,13 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
         }
         if (other.empty()) continue;
       }
-      // block geometry: <= 128 targets, leaf_slices source slices, rounds of <= kP2PCap sources
+      // block geometry: <= 128 targets, leaf_slices source slices, rounds of <= kP2PCap sources; two
+      // targets per thread for the packed fp32 kernels and the fp64 pair kernel (near field)
       const int chunk = kP2PThreads;
+      const bool pairs = packed || (near_part && near_pair64);
       for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += chunk) {
         const int nt = int(std::min<int64_t>(chunk, t.leaf_ptr[l + 1] - t0));
-        const int R = leaf_slices(nt, packed), q = leaf_unroll(packed) * R;
+        const int R = leaf_slices(nt, pairs), q = leaf_unroll(pairs) * R;
         const int cap = kP2PCap - kP2PCap % q;
         const int rb = int(rounds.size());
         size_t si = 0, oi = 0;
@@ -1294,7 +1299,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
           const int O = (no + q - 1) / q * q;
           rounds.push_back(make_int4(ib, int(items.size()), S | (ns << 16), O | (no << 16)));
         }
-        const int TT = packed ? (nt + 2 * kNearNPair - 1) / (2 * kNearNPair) : nt;
+        const int TT = packed ? (nt + 2 * kNearNPair - 1) / (2 * kNearNPair) : pairs ? (nt + 1) / 2 : nt;
         w.push_back({int(l), int(t0), nt, rb, int(rounds.size()), R | (TT << 8), (65536 + TT - 1) / TT,
                      (65536 + R - 1) / R});
       }
@@ -1550,6 +1555,15 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
         ++launches;
         return;
       }
+    }
+    if (near_pair64 && &lp == &leaf_near && !acc) {  // fp64 near field, two targets per thread
+      if (grad)
+        leaf_eval_pair_kernel<T, true, false><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, pot.as<T>(), g);
+      else
+        leaf_eval_pair_kernel<T, false, false><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, pot.as<T>(), g);
+      KIFMM_LAUNCH_CHECK();
+      ++launches;
+      return;
     }
     if (grad && acc)
       leaf_eval_kernel<T, true, true><<<lp.n, kP2PThreads, 0, st>>>(pp, w, r, it, Mp, Lp, pot.as<T>(), g);
