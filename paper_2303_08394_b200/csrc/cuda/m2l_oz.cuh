@@ -486,10 +486,12 @@ struct M2LOzPlan {
     // ---- operator digit slices: rows (t S + j) np + n, K-major (np bytes), one exponent F for all
     const int nt = ops.n_m2l, nc = ops.n_c, ne = ops.n_e;
     double kmax = 0.0;
-    for (size_t i = 0; i < size_t(nt) * nc * ne; ++i) kmax = std::max(kmax, std::fabs(ops.m2l[i]));
+#pragma omp parallel for reduction(max : kmax) schedule(static)
+    for (int64_t i = 0; i < int64_t(nt) * nc * ne; ++i) kmax = std::max(kmax, std::fabs(ops.m2l[i]));
     const int F = kmax > 0.0 ? std::ilogb(kmax) + 2 : 0;
     fscale = std::ldexp(1.0, F);
     std::vector<int8_t> b8(size_t(nt) * S * np * np, 0);
+#pragma omp parallel for schedule(static)
     for (int tv = 0; tv < nt; ++tv)
       for (int n = 0; n < nc; ++n)
         for (int k = 0; k < ne; ++k) {
