@@ -1145,6 +1145,118 @@ __global__ void __launch_bounds__(kCheckWarps * 32, KIFMM_CHECK_MINB) check_f2_k
   if (sp_hi) split_row_warp<32 * KMAX>(row, lane, size_t(w.out_row), sp_hi, sp_lo, sp_un);
 }
 
+// Check potentials with HALF a warp per work (p = 6: 16 lanes x 5 FP32x2 pairs = 160 check points, no
+// scalar remainder).  check_f2_kernel gives a work the whole warp (5 points per lane, the fifth scalar
+// -- half the FP32 rate) and exposes each work's start-up loads to one warp; here the two halves take
+// two works (the host sorts works by source count, so the halves loop equally long) and stream their
+// sources in chunks of 16 (one per lane).  Per check point the arithmetic and source order are those of
+// check_f2_kernel: bit-identical results.
+template <int NPP>
+__global__ void __launch_bounds__(kCheckWarps * 32, KIFMM_CHECK_MINB) check_hw_kernel(
+    P2PParams<float> p, const CheckWork* __restrict__ works, int n_works, const int2* __restrict__ ranges,
+    int ref_level, float alpha, float* __restrict__ out, int ld_out, __half* __restrict__ sp_hi = nullptr,
+    __half* __restrict__ sp_lo = nullptr, float* __restrict__ sp_un = nullptr) {
+  __shared__ float4 sh[kCheckWarps][2][16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+  const int wp = blockIdx.x * kCheckWarps + warp;
+  if (2 * wp >= n_works) return;
+  const int wi = 2 * wp + half;
+  const bool valid = wi < n_works;
+  CheckWork w{};
+  if (valid) w = works[wi];
+  const float fa = float(kFarAway);
+  const float4 g = p.node_geom[valid ? w.node : 0];
+  const float s = alpha * g.w;
+  auto coord = [&](int j, int d) {
+    const int jj = j < p.n_e ? j : 0;
+    return (d == 0 ? g.x : d == 1 ? g.y : g.z) + s * p.surface[3 * jj + d];
+  };
+  // pair q holds check points hl + 32 q and hl + 32 q + 16
+  f2_t yx[NPP], yy[NPP], yz[NPP], acc[NPP];
+#pragma unroll
+  for (int q = 0; q < NPP; ++q) {
+    const int ja = hl + 32 * q, jb = ja + 16;
+    yx[q] = f2_pair(coord(ja, 0), coord(jb, 0));
+    yy[q] = f2_pair(coord(ja, 1), coord(jb, 1));
+    yz[q] = f2_pair(coord(ja, 2), coord(jb, 2));
+    acc[q] = 0;
+  }
+  float4* my = sh[warp][half];
+  int r = valid ? w.range_begin : 0, b = 0;
+  const int r_end = valid ? w.range_end : 0;
+  int2 rg = valid ? make_int2(w.first, w.count) : make_int2(0, 0);
+  for (;;) {
+    const bool more = r < r_end;
+    if (!__any_sync(0xffffffffu, more)) break;
+    const int cnt = more ? min(16, rg.y - b) : 0;
+    __syncwarp();
+    my[hl] = hl < cnt ? p.src[rg.x + b + hl] : make_float4(fa, fa, fa, 0.f);
+    __syncwarp();
+    const int cnt4 = (cnt + 3) & ~3;
+    const int cmax = max(cnt4, __shfl_xor_sync(0xffffffffu, cnt4, 16));
+    for (int k = 0; k < cmax; k += 4) {
+      if (k >= cnt4) continue;  // the other half still has sources in this chunk
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 sv = my[k + u];
+        const f2_t sx = f2_pack(sv.x, sv.x), sy = f2_pack(sv.y, sv.y), sz = f2_pack(sv.z, sv.z);
+        const f2_t sq = f2_pack(sv.w, sv.w);
+#pragma unroll
+        for (int q = 0; q < NPP; ++q) {
+          const f2_t dx = f2_sub(yx[q], sx), dy = f2_sub(yy[q], sy), dz = f2_sub(yz[q], sz);
+          const f2_t r2 = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+          float ra, rb;
+          f2_unpack(r2, ra, rb);
+          acc[q] = f2_fma(sq, f2_pack(rinv(ra), rinv(rb)), acc[q]);
+        }
+      }
+    }
+    if (more) {  // advance this half's cursor
+      b += cnt;
+      if (b >= rg.y) {
+        ++r;
+        b = 0;
+        if (r < r_end) rg = ranges[r];
+      }
+    }
+  }
+  if (!valid) return;
+  const int e = ref_level - w.level;  // |e| <= 15: exact power of two
+  const float scale = float(kInv4PiD) * (e >= 0 ? float(1 << e) : 1.f / float(1 << (-e)));
+  float* o = out + size_t(w.out_row) * ld_out;
+  float row[2 * NPP];
+  float mx = 0.f;
+#pragma unroll
+  for (int q = 0; q < NPP; ++q) {
+    float a0, a1;
+    f2_unpack(acc[q], a0, a1);
+    const int ja = hl + 32 * q, jb = ja + 16;
+    row[2 * q] = ja < p.n_e ? a0 * scale : 0.f;
+    row[2 * q + 1] = jb < p.n_e ? a1 * scale : 0.f;
+    if (ja < ld_out) o[ja] = row[2 * q];
+    if (jb < ld_out) o[jb] = row[2 * q + 1];
+    mx = fmaxf(mx, fmaxf(fabsf(row[2 * q]), fabsf(row[2 * q + 1])));
+  }
+  if (sp_hi) {  // the fp16 split of the check row (split_row_warp over the half-warp's 160 values)
+#pragma unroll
+    for (int o2 = 8; o2 > 0; o2 >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
+    const int ex = f16_row_exponent(mx);
+    const float sc = ldexpf(1.f, ex);
+    const size_t row0 = size_t(w.out_row) * (32 * NPP);
+#pragma unroll
+    for (int q = 0; q < NPP; ++q)
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int j = hl + 32 * q + 16 * t;
+        const float x = row[2 * q + t] * sc;
+        const __half h = __float2half_rn(x);
+        sp_hi[row0 + j] = h;
+        sp_lo[row0 + j] = __float2half_rn(x - __half2float(h));
+      }
+    if (hl == 0) sp_un[w.out_row] = ldexpf(1.f, -ex);
+  }
+}
+
 // Direct sum at `m` targets from all `n` sources (verification).
 template <class T, bool GRAD>
 __global__ void __launch_bounds__(kP2PThreads) direct_kernel(const v4_t<T>* __restrict__ src, int64_t n,

@@ -227,9 +227,16 @@ __global__ void scatter_rows_split_kernel(const float* __restrict__ src, const i
 
 template <class T>
 void launch_check(int np, int n, const P2PParams<T>& pp, const CheckWork* works, const int2* ranges, const int* lvl,
-                  int ref, T alpha, T* out, cudaStream_t s, const TcSplit* split = nullptr) {
+                  int ref, T alpha, T* out, cudaStream_t s, const TcSplit* split = nullptr, bool half_warp = false) {
   const int blocks = int(ceil_div(n, kCheckWarps));
   if constexpr (sizeof(T) == 4) {
+    if (np == 160 && half_warp) {  // p = 6: packed fp32 kernel, half a warp per work
+      check_hw_kernel<5><<<int(ceil_div(n, 2 * kCheckWarps)), kCheckWarps * 32, 0, s>>>(
+          pp, works, n, ranges, ref, alpha, out, np, split ? split->hi : nullptr, split ? split->lo : nullptr,
+          split ? split->un : nullptr);
+      KIFMM_LAUNCH_CHECK();
+      return;
+    }
     if (np == 160) {  // p = 6: packed fp32 kernel
       check_f2_kernel<5><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, ref, alpha, out, np,
                                                              split ? split->hi : nullptr, split ? split->lo : nullptr,
@@ -385,6 +392,7 @@ struct kifmm_gpu_plan {
   DevMem near_counter;  // queue mode work counter [, counter at the drain launch (KIFMM_NEAR_DEBUG)]
   bool near_debug = false, near_skip = false, far_as_leaf = false, near_corun = false;
   int near_fork_at = 0;  // 0: at the start of the evaluate, 1: just before M2L, 2: after the P2M check, 3: after M2M
+  bool check_hw = true;     // fp32 p = 6 check potentials: half-warp kernel (KIFMM_CHECK_HW=0: warp per work)
   bool near_pair64 = false;  // fp64 near field: two targets per thread (leaf_eval_pair_kernel; KIFMM_NEAR_PAIR64)
   bool near_serial = false;  // near field on the plan stream after L2L instead of a side stream (KIFMM_NEAR_SERIAL;
                              // default for fp64)
@@ -677,6 +685,8 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
   }
   for (auto& e : ev) KIFMM_CUDA(cudaEventCreate(&e));
+  check_hw = precision == 32 && np == 160;
+  if (const char* e = std::getenv("KIFMM_CHECK_HW")) check_hw = check_hw && std::atoi(e) != 0;
 
   ptick("setup");
   // ---- partition, owners, halo export tables (csrc/host/halo.cpp)
@@ -755,6 +765,19 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       info.p2m_pairs += (t.leaf_ptr[l + 1] - t.leaf_ptr[l]) * ne;
     }
     n_p2m = int(w.size());
+    if (check_hw) {  // half-warp check kernel: pair works of similar source counts in a warp
+      auto srcs = [&](const CheckWork& c) {
+        int64_t n = 0;
+        for (int r = c.range_begin; r < c.range_end; ++r) n += rg[r].y;
+        return n;
+      };
+      std::vector<std::pair<int64_t, int>> key(w.size());
+      for (size_t i = 0; i < w.size(); ++i) key[i] = {-srcs(w[i]), int(i)};
+      std::stable_sort(key.begin(), key.end());
+      std::vector<CheckWork> sorted(w.size());
+      for (size_t i = 0; i < w.size(); ++i) sorted[i] = w[key[i].second];
+      w.swap(sorted);
+    }
     p2m_works.upload(w, &dev_bytes);
     p2m_ranges.upload(rg, &dev_bytes);
     check_up.alloc(size_t(std::max<int64_t>(1, le - lb)) * np * es, &dev_bytes);
@@ -936,6 +959,19 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       w.push_back({int(n), int(n), r0, int(rg.size()), rg[r0].x, rg[r0].y, node_lvl(n), 0});
     }
     n_p2l = int(w.size());
+    if (check_hw) {  // half-warp check kernel: pair works of similar source counts in a warp
+      auto srcs = [&](const CheckWork& c) {
+        int64_t n = 0;
+        for (int r = c.range_begin; r < c.range_end; ++r) n += rg[r].y;
+        return n;
+      };
+      std::vector<std::pair<int64_t, int>> key(w.size());
+      for (size_t i = 0; i < w.size(); ++i) key[i] = {-srcs(w[i]), int(i)};
+      std::stable_sort(key.begin(), key.end());
+      std::vector<CheckWork> sorted(w.size());
+      for (size_t i = 0; i < w.size(); ++i) sorted[i] = w[key[i].second];
+      w.swap(sorted);
+    }
     p2l_works.upload(w, &dev_bytes);
     p2l_ranges.upload(rg, &dev_bytes);
   }
@@ -1647,7 +1683,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
   // upward: P2M check -> factored solve
   if (up && n_p2m) {
     launch_check<T>(np, n_p2m, pp, p2m_works.as<CheckWork>(), p2m_ranges.as<int2>(), node_level.as<int>(),
-                    ref_level, T(alpha_out), check_up.as<T>(), s, gemm_tc ? &sp_cu : nullptr);
+                    ref_level, T(alpha_out), check_up.as<T>(), s, gemm_tc ? &sp_cu : nullptr, check_hw);
     KIFMM_LAUNCH_CHECK();
     ++launches;
   }
@@ -1725,7 +1761,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
   }
   if (n_p2l) {
     launch_check<T>(np, n_p2l, pp, p2l_works.as<CheckWork>(), p2l_ranges.as<int2>(), node_level.as<int>(),
-                    ref_level, T(alpha_in), check_dn.as<T>(), p2l_side ? side2 : s);
+                    ref_level, T(alpha_in), check_dn.as<T>(), p2l_side ? side2 : s, nullptr, check_hw);
     KIFMM_LAUNCH_CHECK();
     ++launches;
   }
