@@ -47,6 +47,7 @@
 #include <set>
 #include <array>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -56,13 +57,14 @@ namespace gpu {
 namespace tc {
 
 constexpr int BM = 128;  // target rows per CTA
-constexpr int NP = 160;  // check points / equivalent points, padded (p = 6)
+// NP (template parameter of everything below): check / equivalent points per row, padded to a multiple of
+// 32 -- 64 (p = 4), 128 (p = 5), 160 (p = 6); see tc_np_supported() / tc_dispatch_np().
 // Warpgroups: 0 = {TMA + TMEM alloc, MMA issuer, A-arrival forwarder (pair), idle}, 1 = A producers,
 // 2-3 = epilogue.  The kernel launches with 80 registers per thread (__maxnreg__) and rebalances with
 // setmaxnreg (warpgroups 0-1 down to 48, epilogue up to 112): a CTA holds 40 K registers, leaving
 // room on the SM for three near-field blocks next to it (measured fastest end to end, despite a few
 // hundred bytes of epilogue spills; 96/56/136 with two near blocks: +2.5 %).
-constexpr int EPI_WARPS = 8, EPI_COLS = NP / 2;   // 2 warps per TMEM lane quarter, 80 columns each
+constexpr int EPI_WARPS = 8;                      // 2 warps per TMEM lane quarter, NP / 2 columns each
 constexpr int EPI_WARP0 = 8;                      // epilogue warps 8..15
 constexpr int PROD_WARP0 = 4;                     // A producer warps 4..7
 constexpr int FWD_WARP = 2;                       // A-arrival forwarder (pair)
@@ -83,7 +85,7 @@ constexpr int NACC = 3;              // accumulator buffers: the MMA runs up to 
 // A_hi B_lo + A_lo B_hi corrections in the third; the epilogue sums them in fp32 round-to-nearest.  One
 // such set fills 480 TMEM columns, so that variant runs one tap at a time (NSET 1).  The M2L pair keeps
 // one accumulator per tap and three sets in flight (its taps are summed in fp32 per tap anyway).
-template <bool PAIR>
+template <int NP, bool PAIR>
 struct Acc {
   static constexpr int NSET = PAIR ? NACC : 1;         // accumulator sets in TMEM
   static constexpr int SET_COLS = PAIR ? NP : 3 * NP;  // columns per set
@@ -102,7 +104,7 @@ constexpr int kStageBudgetKB = KIFMM_TC_STAGE_KB;
 #define KIFMM_TC_EG 1
 #endif
 
-template <bool PAIR, int ROWB, int ES = 4>
+template <int NP, bool PAIR, int ROWB, int ES = 4>
 struct Cfg {
   static constexpr int KB = ROWB / ES;           // operand elements per K block (tf32: 4 B, f16: 2 B)
   static constexpr int NKB = NP / KB;            // K blocks per tap
@@ -243,30 +245,6 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
   return d;
 }
 
-template <bool PAIR, int ES = 4>
-__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
-  constexpr uint32_t idesc = Cfg<PAIR, 128, ES>::IDESC;
-  if constexpr (PAIR && ES == 4)
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-  else if constexpr (ES == 4)
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-  else if constexpr (PAIR)
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-  else
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
 // The three MMAs of one K step of the 3-term split: D (+)= A_hi B_hi, += A_hi B_lo, += A_lo B_hi.
 #ifndef KIFMM_MMA3_BFIRST
 #define KIFMM_MMA3_ORDER(GROUP, KIND)                                            \
@@ -361,14 +339,17 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
-template <bool PAIR, int ROWB, int ES>
+template <int NP, bool PAIR, int ROWB, int ES>
 __global__ void __maxnreg__(LAUNCH_REGS)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tm_khi, const __grid_constant__ CUtensorMap tm_klo,
                   const void* __restrict__ m_hi, const void* __restrict__ m_lo, const Item* __restrict__ items,
                   const int* __restrict__ sched, const int* __restrict__ seg_mat, const int* __restrict__ seg_in, int zero_row,
                   const float* __restrict__ row_unscale, float k_unscale, Epi epi) {
-  using C = Cfg<PAIR, ROWB, ES>;
+  using C = Cfg<NP, PAIR, ROWB, ES>;
+  using AccT = Acc<NP, PAIR>;
   constexpr int KB = C::KB, NKB = C::NKB;
+  constexpr int EPI_COLS = NP / 2;
+  static_assert(NP % 32 == 0 && AccT::NSET * AccT::SET_COLS <= int(TMEM_COLS), "row width / TMEM budget");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -420,7 +401,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
       mbar_init(empty(s), 1);  // one tcgen05.commit per stage (multicast to both CTAs when PAIR)
       mbar_init(afull(s), 128);
     }
-    for (int b = 0; b < Acc<PAIR>::NSET; ++b) {
+    for (int b = 0; b < AccT::NSET; ++b) {
       mbar_init(tfull(b), 1);
       mbar_init(tempty(b), C::CTAS * EPI_WARPS);  // one elected lane per epilogue warp per CTA
     }
@@ -488,7 +469,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
         __syncwarp();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t taddr =
-            tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * Acc<PAIR>::SET_COLS + h * EPI_COLS);
+            tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * AccT::SET_COLS + h * EPI_COLS);
         auto ld16 = [&](uint32_t a, uint32_t (&v)[16]) {
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -533,7 +514,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
           else
             mbar_arrive_local(tempty(b));
         }
-        if (++b == Acc<PAIR>::NSET) {
+        if (++b == AccT::NSET) {
           b = 0;
           tph ^= 1u;
         }
@@ -781,7 +762,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
             mbar_wait(tempty(ab), aph ^ 1u);
             if (prof) t_te += clock64() - c0;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t d = tmem_base + uint32_t(ab * Acc<PAIR>::SET_COLS);
+            const uint32_t d = tmem_base + uint32_t(ab * AccT::SET_COLS);
             for (int kb = 0; kb < NKB; ++kb) {
               c0 = prof ? clock64() : 0;
               mbar_wait(full(s), ph);
@@ -811,7 +792,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
               ++nst;
             }
             if (elect_one()) commit<PAIR>(tfull(ab));
-            if (++ab == Acc<PAIR>::NSET) {
+            if (++ab == AccT::NSET) {
               ab = 0;
               aph ^= 1u;
             }
@@ -970,6 +951,7 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, size_t n, float* 
 // Per operand row r in [r0, r1): scale by 2^e so max|row| lands in [2^9, 2^10) (far inside the fp16
 // range), split x*2^e = hi + lo in fp16 (round to nearest), and record 2^-e.  Rows >= nn are zero rows
 // (the appended gather target of absent sources).  One warp per row.
+template <int NP>
 __global__ void split_f16_rows_kernel(const float* __restrict__ M, int r0, int r1, int nn, __half* __restrict__ hi,
                                       __half* __restrict__ lo, float* __restrict__ unscale) {
   const int row = r0 + blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -1001,6 +983,7 @@ __global__ void split_f16_rows_kernel(const float* __restrict__ M, int r0, int r
 }
 
 // Split the listed rows (warp per row).
+template <int NP>
 __global__ void split_f16_list_kernel(const float* __restrict__ X, const int* __restrict__ list, int n,
                                       __half* __restrict__ hi, __half* __restrict__ lo, float* __restrict__ un) {
   pdl_trigger();
@@ -1016,6 +999,7 @@ __global__ void split_f16_list_kernel(const float* __restrict__ X, const int* __
 
 // check[out(r)] += sum over the tile's items (fixed order) of partial[slot][r], warp per row (grid
 // (tiles, rows / 8), 256 threads); with hi set, also the fp16 split of the finished row.
+template <int NP>
 __global__ void m2l_tc_reduce_split_kernel(const float* __restrict__ partial, const int* __restrict__ tile_out,
                                            const int* __restrict__ tile_slot, int rows, float* __restrict__ check,
                                            __half* __restrict__ hi, __half* __restrict__ lo,
@@ -1046,6 +1030,7 @@ __global__ void m2l_tc_reduce_split_kernel(const float* __restrict__ partial, co
 
 // check[out(r)] += sum over the tile's items (fixed order) of partial[slot][r]
 // grid (tiles, rows / 16); thread = (row, float4 column group), 640 threads
+template <int NP>
 __global__ void m2l_tc_reduce_kernel(const float* __restrict__ partial, const int* __restrict__ tile_out,
                                      const int* __restrict__ tile_slot, int rows, float* __restrict__ check) {
   const int tile = blockIdx.x;
@@ -1145,12 +1130,24 @@ inline bool m2l_tc_available() {
   return major == 10 && minor == 0;
 }
 
+// Row widths (n_e padded to a multiple of 32) the tcgen05 kernels are instantiated for: p = 4, 5, 6.
+inline bool tc_np_supported(int np) { return np == 64 || np == 128 || np == 160; }
+template <class F>
+inline void tc_dispatch_np(int np, F&& f) {
+  switch (np) {
+    case 64: f(std::integral_constant<int, 64>{}); break;
+    case 128: f(std::integral_constant<int, 128>{}); break;
+    case 160: f(std::integral_constant<int, 160>{}); break;
+    default: throw InvalidArgument("tcgen05 path: row width (n_e padded to 32) must be 64, 128 or 160 (p = 4, 5, 6)");
+  }
+}
+
 // fp32 operand rows split for the kind::f16 GEMMs: rows+1 rows (the last one zero) of hi / lo fp16 and
 // the per-row power-of-two unscale.
 struct TcSplit {
   __half *hi = nullptr, *lo = nullptr;
   float* un = nullptr;
-  int rows = 0;
+  int rows = 0, np = 0;
   TcSplit() = default;
   TcSplit(const TcSplit&) = delete;
   TcSplit& operator=(const TcSplit&) = delete;
@@ -1158,9 +1155,11 @@ struct TcSplit {
     for (void* p : {(void*)hi, (void*)lo, (void*)un})
       if (p) cudaFree(p);
   }
-  void alloc(int r, size_t* total) {
+  void alloc(int r, int width, size_t* total) {
+    if (!tc_np_supported(width)) throw InvalidArgument("TcSplit: unsupported row width");
     rows = r;
-    const size_t n = size_t(r + 1) * tc::NP;
+    np = width;
+    const size_t n = size_t(r + 1) * np;
     KIFMM_CUDA(cudaMalloc(&hi, n * sizeof(__half)));
     KIFMM_CUDA(cudaMalloc(&lo, n * sizeof(__half)));
     KIFMM_CUDA(cudaMalloc(&un, size_t(r + 1) * sizeof(float)));
@@ -1173,7 +1172,9 @@ struct TcSplit {
   // split rows [r0, r1) of the fp32 buffer X (row stride NP)
   void split(const float* X, int r0, int r1, cudaStream_t s) const {
     if (r1 <= r0) return;
-    tc::split_f16_rows_kernel<<<unsigned((r1 - r0 + 7) / 8), 256, 0, s>>>(X, r0, r1, rows, hi, lo, un);
+    tc_dispatch_np(np, [&](auto w) {
+      tc::split_f16_rows_kernel<decltype(w)::value><<<unsigned((r1 - r0 + 7) / 8), 256, 0, s>>>(X, r0, r1, rows, hi, lo, un);
+    });
     KIFMM_LAUNCH_CHECK();
   }
 };
@@ -1182,6 +1183,7 @@ struct TcSplit {
 struct M2LTcPlan {
   bool pair = false;  // 2-CTA (cta_group::2) kernel on large trees; KIFMM_TC_PAIR=0/1 forces the choice
   int rows = 256;    // output rows per tile
+  int np = 0;        // row width (n_e padded to 32): 64, 128 or 160
   int rowb = 128;    // bytes per operand row per stage (128: SWIZZLE_128B, 64: SWIZZLE_64B)
   bool f16 = true;  // 3-term fp16 split (kind::f16) with power-of-two row scaling; KIFMM_TC_KIND=tf32 for 3xTF32
   static constexpr float kKScale = 256.f;
@@ -1226,10 +1228,10 @@ struct M2LTcPlan {
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-  static void encode(EncodeFn fn, CUtensorMap* m, void* base, uint64_t rows_total, uint32_t box_rows, int rowb,
+  static void encode(EncodeFn fn, CUtensorMap* m, void* base, int np, uint64_t rows_total, uint32_t box_rows, int rowb,
                      int es = 4) {
-    const cuuint64_t dims[2] = {cuuint64_t(tc::NP), cuuint64_t(rows_total)};
-    const cuuint64_t strides[1] = {cuuint64_t(tc::NP) * es};
+    const cuuint64_t dims[2] = {cuuint64_t(np), cuuint64_t(rows_total)};
+    const cuuint64_t strides[1] = {cuuint64_t(np) * es};
     const cuuint32_t box[2] = {cuuint32_t(rowb / es), box_rows};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = fn(m, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base,
@@ -1323,9 +1325,13 @@ struct M2LTcPlan {
   }
 
   template <class TreeView, class OpsView>
-  void build(const TreeView& t, const std::vector<std::vector<int64_t>>& groups, int np, const OpsView& ops,
+  void build(const TreeView& t, const std::vector<std::vector<int64_t>>& groups, int width, const OpsView& ops,
              size_t* total) {
-    if (np != tc::NP) throw InvalidArgument("tcgen05 M2L: only p = 6 (n_e padded to 160) is instantiated");
+    if (!tc_np_supported(width))
+      throw InvalidArgument("tcgen05 M2L: instantiated for p = 4, 5, 6 (n_e padded to 64, 128, 160)");
+    np = width;
+    // KIFMM_TC_KIND=tf32: the kind::tf32 variant (reported as m2l_backend 3), instantiated for p = 6 only
+    if (const char* e = std::getenv("KIFMM_TC_KIND")) f16 = std::string(e) != "tf32" || np != 160;
     nn = size_t(t.n_nodes);
     pair = nn >= 20000;  // 2-CTA pays off once there are enough 256-row tiles (measured at 1e5 / 1e6 points)
     if (const char* e = std::getenv("KIFMM_TC_PAIR")) pair = std::atoi(e) != 0;
@@ -1471,42 +1477,43 @@ struct M2LTcPlan {
     up(&d_sched, sched, total);
     // ---- K_t split into tf32 hi / lo, padded to 160 x 160 per transfer vector
     const int ne = ops.n_e, nc = ops.n_c, nt = ops.n_m2l;
-    std::vector<float> khi(size_t(nt) * tc::NP * tc::NP, 0.f), klo(khi.size(), 0.f);
+    std::vector<float> khi(size_t(nt) * np * np, 0.f), klo(khi.size(), 0.f);
 #pragma omp parallel for schedule(static)
     for (int v = 0; v < nt; ++v)
       for (int c = 0; c < nc; ++c)
         for (int e = 0; e < ne; ++e) {
           const float x = float(ops.m2l[(size_t(v) * nc + c) * ne + e]);
           const float h = tf32_rna(x);
-          const size_t idx = (size_t(v) * tc::NP + c) * tc::NP + e;
+          const size_t idx = (size_t(v) * np + c) * np + e;
           khi[idx] = h;
           klo[idx] = x - h;
         }
     up(&d_khi, khi, total);
     up(&d_klo, klo, total);
     // multipole hi/lo with one appended zero row (gather target of absent sources)
-    KIFMM_CUDA(cudaMalloc(&d_mhi, (nn + 1) * tc::NP * sizeof(float)));
-    KIFMM_CUDA(cudaMalloc(&d_mlo, (nn + 1) * tc::NP * sizeof(float)));
-    KIFMM_CUDA(cudaMemset(d_mhi + nn * tc::NP, 0, tc::NP * sizeof(float)));
-    KIFMM_CUDA(cudaMemset(d_mlo + nn * tc::NP, 0, tc::NP * sizeof(float)));
-    KIFMM_CUDA(cudaMalloc(&d_partial, std::max(1, n_items) * size_t(rows) * tc::NP * sizeof(float)));
-    *total += 2 * (nn + 1) * tc::NP * sizeof(float) + size_t(n_items) * rows * tc::NP * sizeof(float);
+    KIFMM_CUDA(cudaMalloc(&d_mhi, (nn + 1) * np * sizeof(float)));
+    KIFMM_CUDA(cudaMalloc(&d_mlo, (nn + 1) * np * sizeof(float)));
+    KIFMM_CUDA(cudaMemset(d_mhi + nn * np, 0, np * sizeof(float)));
+    KIFMM_CUDA(cudaMemset(d_mlo + nn * np, 0, np * sizeof(float)));
+    KIFMM_CUDA(cudaMalloc(&d_partial, std::max(1, n_items) * size_t(rows) * np * sizeof(float)));
+    *total += 2 * (nn + 1) * np * sizeof(float) + size_t(n_items) * rows * np * sizeof(float);
     // ---- TMA descriptors (SWIZZLE_128B, 32-float boxes): K_t tiles of this CTA's rows, gather4 rows of M
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     KIFMM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
     if (!fn) throw DeviceError(KIFMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     if (const char* e = std::getenv("KIFMM_TC_ROWB")) rowb = std::atoi(e) == 64 ? 64 : 128;
-    const uint32_t brow = uint32_t(pair ? tc::NP / 2 : tc::NP);
-    encode(reinterpret_cast<EncodeFn>(fn), &tm_khi, d_khi, uint64_t(nt) * tc::NP, brow, rowb);
-    encode(reinterpret_cast<EncodeFn>(fn), &tm_klo, d_klo, uint64_t(nt) * tc::NP, brow, rowb);
-    set_smem<false, 128>();
-    set_smem<true, 128>();
-    set_smem<false, 64>();
-    set_smem<true, 64>();
+    const uint32_t brow = uint32_t(pair ? np / 2 : np);
+    encode(reinterpret_cast<EncodeFn>(fn), &tm_khi, d_khi, np, uint64_t(nt) * np, brow, rowb);
+    encode(reinterpret_cast<EncodeFn>(fn), &tm_klo, d_klo, np, uint64_t(nt) * np, brow, rowb);
+    if (np == 160) {  // kind::tf32 variants (m2l_backend 3): p = 6 only
+      set_smem<false, 128>();
+      set_smem<true, 128>();
+      set_smem<false, 64>();
+      set_smem<true, 64>();
+    }
 
     // ---- f16 kind: K_t * 2^8 split into fp16 hi/lo; multipoles split per row with a power-of-two scale
-    if (const char* e = std::getenv("KIFMM_TC_KIND")) f16 = std::string(e) != "tf32";
     if (f16) {
       std::vector<__half> h16(khi.size()), l16(khi.size());
 #pragma omp parallel for schedule(static)
@@ -1518,25 +1525,28 @@ struct M2LTcPlan {
       }
       up(&d_khi16, h16, total);
       up(&d_klo16, l16, total);
-      KIFMM_CUDA(cudaMalloc(&d_mhi16, (nn + 1) * tc::NP * sizeof(__half)));
-      KIFMM_CUDA(cudaMalloc(&d_mlo16, (nn + 1) * tc::NP * sizeof(__half)));
+      KIFMM_CUDA(cudaMalloc(&d_mhi16, (nn + 1) * np * sizeof(__half)));
+      KIFMM_CUDA(cudaMalloc(&d_mlo16, (nn + 1) * np * sizeof(__half)));
       KIFMM_CUDA(cudaMalloc(&d_unscale, (nn + 1) * sizeof(float)));
-      *total += 2 * (nn + 1) * tc::NP * sizeof(__half) + (nn + 1) * sizeof(float);
-      encode(reinterpret_cast<EncodeFn>(fn), &tm_khi16, d_khi16, uint64_t(nt) * tc::NP, brow, 64, 2);
-      encode(reinterpret_cast<EncodeFn>(fn), &tm_klo16, d_klo16, uint64_t(nt) * tc::NP, brow, 64, 2);
-      KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<false, 64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      tc::Cfg<false, 64, 2>::SMEM_BYTES));
-      KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<true, 64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      tc::Cfg<true, 64, 2>::SMEM_BYTES));
+      *total += 2 * (nn + 1) * np * sizeof(__half) + (nn + 1) * sizeof(float);
+      encode(reinterpret_cast<EncodeFn>(fn), &tm_khi16, d_khi16, np, uint64_t(nt) * np, brow, 64, 2);
+      encode(reinterpret_cast<EncodeFn>(fn), &tm_klo16, d_klo16, np, uint64_t(nt) * np, brow, 64, 2);
+      tc_dispatch_np(np, [&](auto w) {
+        constexpr int W = decltype(w)::value;
+        KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<W, false, 64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        tc::Cfg<W, false, 64, 2>::SMEM_BYTES));
+        KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<W, true, 64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        tc::Cfg<W, true, 64, 2>::SMEM_BYTES));
+      });
     }
   }
 
   template <bool P, int R>
   static void set_smem() {
-    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<P, R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::Cfg<P, R, 4>::SMEM_BYTES));
+    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<160, P, R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::Cfg<160, P, R, 4>::SMEM_BYTES));
   }
-  template <bool P, int R, int ES = 4>
+  template <int W, bool P, int R, int ES = 4>
   void run_kernel(cudaStream_t s, const void* ah_ext = nullptr, const void* al_ext = nullptr,
                   const float* un_ext = nullptr) {
     const CUtensorMap& mh = ES == 4 ? tm_khi : tm_khi16;
@@ -1555,15 +1565,15 @@ struct M2LTcPlan {
       attr[1] = pdl_attr();
       cfg.gridDim = dim3(2 * sched_g);
       cfg.blockDim = dim3(tc::THREADS);
-      cfg.dynamicSmemBytes = tc::Cfg<P, R, ES>::SMEM_BYTES;
+      cfg.dynamicSmemBytes = tc::Cfg<W, P, R, ES>::SMEM_BYTES;
       cfg.stream = s;
       cfg.attrs = attr;
       cfg.numAttrs = 2;
-      KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<P, R, ES>, mh, ml, ah, al, (const tc::Item*)d_items, (const int*)d_sched,
+      KIFMM_CUDA(cudaLaunchKernelEx(&cfg, tc::m2l_tc_kernel<W, P, R, ES>, mh, ml, ah, al, (const tc::Item*)d_items, (const int*)d_sched,
                                     (const int*)d_seg_mat, (const int*)d_seg_in, int(nn), un, ku,
                                     tc::Epi{d_partial, nullptr, nullptr, nullptr, 0, tc_debug(), nullptr, nullptr, nullptr}));
     } else {
-      launch_pdl(tc::m2l_tc_kernel<P, R, ES>, dim3(sched_g), dim3(tc::THREADS), tc::Cfg<P, R, ES>::SMEM_BYTES, s, mh, ml,
+      launch_pdl(tc::m2l_tc_kernel<W, P, R, ES>, dim3(sched_g), dim3(tc::THREADS), tc::Cfg<W, P, R, ES>::SMEM_BYTES, s, mh, ml,
                  ah, al, (const tc::Item*)d_items, (const int*)d_sched, (const int*)d_seg_mat, (const int*)d_seg_in,
                  int(nn), un, ku, tc::Epi{d_partial, nullptr, nullptr, nullptr, 0, tc_debug(), nullptr, nullptr, nullptr});
     }
@@ -1581,42 +1591,53 @@ struct M2LTcPlan {
   void launch_presplit_main(const TcSplit& sp, cudaStream_t s) {
     if (!n_items) return;
     if (!f16 || sp.rows != int(nn)) throw InvalidArgument("M2L presplit: kind::f16 plan over all nodes required");
-    if (pair)
-      run_kernel<true, 64, 2>(s, sp.hi, sp.lo, sp.un);
-    else
-      run_kernel<false, 64, 2>(s, sp.hi, sp.lo, sp.un);
+    if (sp.np != np) throw InvalidArgument("M2L presplit: row width mismatch");
+    tc_dispatch_np(np, [&](auto w) {
+      if (pair)
+        run_kernel<decltype(w)::value, true, 64, 2>(s, sp.hi, sp.lo, sp.un);
+      else
+        run_kernel<decltype(w)::value, false, 64, 2>(s, sp.hi, sp.lo, sp.un);
+    });
   }
   void launch_presplit_reduce(float* check, const TcSplit* cd, cudaStream_t s) {
     if (!n_items) return;
-    launch_pdl(tc::m2l_tc_reduce_split_kernel, dim3(n_tiles, (rows + 7) / 8), dim3(256), 0, s, (const float*)d_partial,
-               (const int*)d_tile_out, (const int*)d_tile_slot, rows, check, cd ? cd->hi : (__half*)nullptr,
-               cd ? cd->lo : (__half*)nullptr, cd ? cd->un : (float*)nullptr);
+    tc_dispatch_np(np, [&](auto w) {
+      launch_pdl(tc::m2l_tc_reduce_split_kernel<decltype(w)::value>, dim3(n_tiles, (rows + 7) / 8), dim3(256), 0, s,
+                 (const float*)d_partial, (const int*)d_tile_out, (const int*)d_tile_slot, rows, check,
+                 cd ? cd->hi : (__half*)nullptr, cd ? cd->lo : (__half*)nullptr, cd ? cd->un : (float*)nullptr);
+    });
     KIFMM_LAUNCH_CHECK();
   }
 
   // check += M2L(M): run the tcgen05 items, reduce partials.
-  void launch(const float* M, float* check, int np, cudaStream_t s) {
+  void launch(const float* M, float* check, int width, cudaStream_t s) {
     if (!n_items) return;
+    if (width != np) throw InvalidArgument("M2L launch: row width mismatch");
     if (f16) {
-      tc::split_f16_rows_kernel<<<unsigned((nn + 8) / 8), 256, 0, s>>>(M, 0, int(nn) + 1, int(nn), d_mhi16, d_mlo16,
-                                                                      d_unscale);
-      KIFMM_LAUNCH_CHECK();
-      if (pair)
-        run_kernel<true, 64, 2>(s);
-      else
-        run_kernel<false, 64, 2>(s);
-      tc::m2l_tc_reduce_kernel<<<dim3(n_tiles, rows / 16), 16 * (tc::NP / 4), 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
+      tc_dispatch_np(np, [&](auto w) {
+        constexpr int W = decltype(w)::value;
+        tc::split_f16_rows_kernel<W><<<unsigned((nn + 8) / 8), 256, 0, s>>>(M, 0, int(nn) + 1, int(nn), d_mhi16, d_mlo16,
+                                                                            d_unscale);
+        KIFMM_LAUNCH_CHECK();
+        if (pair)
+          run_kernel<W, true, 64, 2>(s);
+        else
+          run_kernel<W, false, 64, 2>(s);
+        tc::m2l_tc_reduce_kernel<W><<<dim3(n_tiles, rows / 16), 16 * (W / 4), 0, s>>>(d_partial, d_tile_out, d_tile_slot,
+                                                                                    rows, check);
+      });
       KIFMM_LAUNCH_CHECK();
       return;
     }
+    // kind::tf32 (3xTF32, m2l_backend 3): p = 6 only (checked in build)
     const size_t n = nn * size_t(np);
     tc::split_tf32_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(M, n, d_mhi, d_mlo);
     KIFMM_LAUNCH_CHECK();
-    if (pair && rowb == 64) run_kernel<true, 64>(s);
-    else if (pair) run_kernel<true, 128>(s);
-    else if (rowb == 64) run_kernel<false, 64>(s);
-    else run_kernel<false, 128>(s);
-    tc::m2l_tc_reduce_kernel<<<dim3(n_tiles, rows / 16), 16 * (tc::NP / 4), 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
+    if (pair && rowb == 64) run_kernel<160, true, 64>(s);
+    else if (pair) run_kernel<160, true, 128>(s);
+    else if (rowb == 64) run_kernel<160, false, 64>(s);
+    else run_kernel<160, false, 128>(s);
+    tc::m2l_tc_reduce_kernel<160><<<dim3(n_tiles, rows / 16), 16 * (160 / 4), 0, s>>>(d_partial, d_tile_out, d_tile_slot, rows, check);
     KIFMM_LAUNCH_CHECK();
   }
 };
@@ -1629,7 +1650,7 @@ struct M2LTcPlan {
 // scale per output column common to all matrices (so 1/sigma factors of the pseudo-inverse stay in
 // range); the epilogue multiplies the column unscale back.
 struct TcGemm {
-  int n_tiles = 0, sched_g = 0;
+  int n_tiles = 0, sched_g = 0, np = 0;
   int *d_out = nullptr, *d_seg_mat = nullptr, *d_seg_in = nullptr, *d_sched = nullptr;
   tc::Item* d_items = nullptr;
   __half *d_bhi = nullptr, *d_blo = nullptr;
@@ -1646,9 +1667,11 @@ struct TcGemm {
 
   // tiles: out (128 rows, -1 pad) + segs (matrix, 128 input rows or -1)
   template <class Tile>
-  void build(const std::vector<Tile>& tiles, const std::vector<double>& B, int n_mats, size_t* total,
+  void build(const std::vector<Tile>& tiles, const std::vector<double>& B, int n_mats, int width, size_t* total,
              int max_ctas = 0) {
-    constexpr int NP = tc::NP;
+    if (!tc_np_supported(width)) throw InvalidArgument("TcGemm: unsupported row width");
+    np = width;
+    const int NP = np;
     if (B.size() != size_t(n_mats) * NP * NP) throw InvalidArgument("TcGemm: B size");
     std::vector<int> out, seg_mat, seg_in;
     std::vector<tc::Item> items;
@@ -1699,10 +1722,12 @@ struct TcGemm {
     KIFMM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
     if (!fn) throw DeviceError(KIFMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     auto enc = reinterpret_cast<M2LTcPlan::EncodeFn>(fn);
-    M2LTcPlan::encode(enc, &tm_hi, d_bhi, uint64_t(n_mats) * NP, NP, 64, 2);
-    M2LTcPlan::encode(enc, &tm_lo, d_blo, uint64_t(n_mats) * NP, NP, 64, 2);
-    KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<false, 64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::Cfg<false, 64, 2>::SMEM_BYTES));
+    M2LTcPlan::encode(enc, &tm_hi, d_bhi, NP, uint64_t(n_mats) * NP, NP, 64, 2);
+    M2LTcPlan::encode(enc, &tm_lo, d_blo, NP, uint64_t(n_mats) * NP, NP, 64, 2);
+    tc_dispatch_np(np, [&](auto w) {
+      KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<decltype(w)::value, false, 64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      tc::Cfg<decltype(w)::value, false, 64, 2>::SMEM_BYTES));
+    });
   }
 
   // dst[out rows] (=, or += when accumulate) A(split rows) . B^T; with out_split, the fp16 split of the
@@ -1714,11 +1739,15 @@ struct TcGemm {
   }
   void run(const TcSplit& a, float* dst, bool accumulate, cudaStream_t s, const TcSplit* out_split = nullptr) const {
     if (!n_tiles) return;
-    launch_pdl(tc::m2l_tc_kernel<false, 64, 2>, dim3(sched_g), dim3(tc::THREADS), tc::Cfg<false, 64, 2>::SMEM_BYTES, s,
-               tm_hi, tm_lo, (const void*)a.hi, (const void*)a.lo, (const tc::Item*)d_items, (const int*)d_sched,
-               (const int*)d_seg_mat, (const int*)d_seg_in, a.rows, (const float*)a.un, 1.f,
-               tc::Epi{nullptr, d_out, d_cu, dst, accumulate ? 1 : 0, 0, out_split ? out_split->hi : nullptr,
-                       out_split ? out_split->lo : nullptr, out_split ? out_split->un : nullptr});
+    if (a.np != np || (out_split && out_split->np != np)) throw InvalidArgument("TcGemm: row width mismatch");
+    tc_dispatch_np(np, [&](auto w) {
+      launch_pdl(tc::m2l_tc_kernel<decltype(w)::value, false, 64, 2>, dim3(sched_g), dim3(tc::THREADS),
+                 tc::Cfg<decltype(w)::value, false, 64, 2>::SMEM_BYTES, s, tm_hi, tm_lo, (const void*)a.hi, (const void*)a.lo,
+                 (const tc::Item*)d_items, (const int*)d_sched, (const int*)d_seg_mat, (const int*)d_seg_in, a.rows,
+                 (const float*)a.un, 1.f,
+                 tc::Epi{nullptr, d_out, d_cu, dst, accumulate ? 1 : 0, 0, out_split ? out_split->hi : nullptr,
+                         out_split ? out_split->lo : nullptr, out_split ? out_split->un : nullptr});
+    });
     KIFMM_LAUNCH_CHECK();
   }
 };

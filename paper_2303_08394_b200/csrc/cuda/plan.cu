@@ -207,11 +207,11 @@ __global__ void scatter_rows_kernel(const T* __restrict__ src, int ld, const int
   T* b = dst + size_t(rows[k]) * ld;
   for (int j = threadIdx.x; j < ld; j += blockDim.x) b[j] = a[j];
 }
-// fp32 / p = 6 (tcgen05 path): warp per received row, also writes the row's fp16 split (M2L A operand)
+// fp32 tcgen05 path: warp per received row, also writes the row's fp16 split (M2L A operand)
+template <int W>
 __global__ void scatter_rows_split_kernel(const float* __restrict__ src, const int* __restrict__ rows,
                                           const int* __restrict__ slot, int n, float* __restrict__ dst,
                                           __half* __restrict__ hi, __half* __restrict__ lo, float* __restrict__ un) {
-  constexpr int W = tc::NP;
   const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (k >= n) return;
   const float* a = src + size_t(slot[k]) * W;
@@ -230,17 +230,21 @@ void launch_check(int np, int n, const P2PParams<T>& pp, const CheckWork* works,
                   int ref, T alpha, T* out, cudaStream_t s, const TcSplit* split = nullptr, bool half_warp = false) {
   const int blocks = int(ceil_div(n, kCheckWarps));
   if constexpr (sizeof(T) == 4) {
-    if (np == 160 && half_warp) {  // p = 6: packed fp32 kernel, half a warp per work
-      check_hw_kernel<5><<<int(ceil_div(n, 2 * kCheckWarps)), kCheckWarps * 32, 0, s>>>(
-          pp, works, n, ranges, ref, alpha, out, np, split ? split->hi : nullptr, split ? split->lo : nullptr,
-          split ? split->un : nullptr);
-      KIFMM_LAUNCH_CHECK();
-      return;
-    }
-    if (np == 160) {  // p = 6: packed fp32 kernel
-      check_f2_kernel<5><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, ref, alpha, out, np,
-                                                             split ? split->hi : nullptr, split ? split->lo : nullptr,
-                                                             split ? split->un : nullptr);
+    // p = 4, 5, 6 (np = 64, 128, 160): packed fp32 kernels, which also write the fp16 split of the check row
+    // for the tcgen05 solve -- half a warp per work (works sorted by source count), or a warp per work
+    if (tc_np_supported(np)) {
+      tc_dispatch_np(np, [&](auto w) {
+        constexpr int K = decltype(w)::value / 32;
+        if (half_warp)
+          check_hw_kernel<K><<<int(ceil_div(n, 2 * kCheckWarps)), kCheckWarps * 32, 0, s>>>(
+              pp, works, n, ranges, ref, alpha, out, np, split ? split->hi : nullptr, split ? split->lo : nullptr,
+              split ? split->un : nullptr);
+        else
+          check_f2_kernel<K><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, ref, alpha, out, np,
+                                                                 split ? split->hi : nullptr,
+                                                                 split ? split->lo : nullptr,
+                                                                 split ? split->un : nullptr);
+      });
       KIFMM_LAUNCH_CHECK();
       return;
     }
@@ -306,12 +310,12 @@ __global__ void m2m_reduce_kernel(const T* __restrict__ scratch, const int* __re
   }
 }
 
-// fp32 / p = 6 variant (warp per parent, same fixed octant order) that also writes the fp16 split of the
+// fp32 tcgen05 variant (warp per parent, same fixed octant order) that also writes the fp16 split of the
 // parent row for the next tcgen05 GEMM (M2M of the level above, M2L)
+template <int W>
 __global__ void m2m_reduce_split_kernel(const float* __restrict__ scratch, const int* __restrict__ parents,
                                         const int* __restrict__ masks, int n, float* __restrict__ M,
                                         __half* __restrict__ hi, __half* __restrict__ lo, float* __restrict__ un) {
-  constexpr int W = tc::NP;
   pdl_trigger();
   pdl_wait();
   const int s = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -685,7 +689,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
   }
   for (auto& e : ev) KIFMM_CUDA(cudaEventCreate(&e));
-  check_hw = precision == 32 && np == 160;
+  check_hw = precision == 32 && tc_np_supported(np);
   if (const char* e = std::getenv("KIFMM_CHECK_HW")) check_hw = check_hw && std::atoi(e) != 0;
 
   ptick("setup");
@@ -729,7 +733,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   const int bm_m2l = 64;
   {
     const char* e = std::getenv("KIFMM_TC_GEMM");
-    gemm_tc = precision == 32 && np == tc::NP && o.m2l_backend != 1 && m2l_tc_available() &&
+    gemm_tc = precision == 32 && tc_np_supported(np) && o.m2l_backend != 1 && m2l_tc_available() &&
               !(e && std::string(e) == "0");
   }
   // solves / L2L: 64-row tiles on the SIMT path (2 CTAs per SM; K = 160 only), 128 on tcgen05
@@ -799,9 +803,9 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     if (gemm_tc) {
       std::vector<double> b1, b2;
       factored_b(ops.uc2e_u, ops.uc2e_s, ops.uc2e_v, ops.uc2e_rank, b1, b2);
-      tg_up1.build(a, b1, 1, &dev_bytes);
-      tg_up2.build(b, b2, 1, &dev_bytes);
-      sp_cu.alloc(int(std::max<int64_t>(1, le - lb)), &dev_bytes);
+      tg_up1.build(a, b1, 1, np, &dev_bytes);
+      tg_up2.build(b, b2, 1, np, &dev_bytes);
+      sp_cu.alloc(int(std::max<int64_t>(1, le - lb)), np, &dev_bytes);
     } else {
       solve_up1.build(a, ld_tiles, &dev_bytes);
       solve_up2.build(b, ld_tiles, &dev_bytes);
@@ -864,10 +868,10 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
         }
         pt.push_back(std::move(ts));
       }
-      g->tc.build(pt, b_m2m, 8, &dev_bytes);
+      g->tc.build(pt, b_m2m, 8, np, &dev_bytes);
       g->direct = true;
     } else if (gemm_tc) {
-      g->tc.build(tiles, b_m2m, 8, &dev_bytes);
+      g->tc.build(tiles, b_m2m, 8, np, &dev_bytes);
       int64_t lo = INT64_MAX, hi = -1;  // child rows (one level: contiguous node range)
       for (int64_t pn : parents)
         for (int o = 0; o < 8; ++o) {
@@ -1014,7 +1018,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     for (auto& kv : groups) m2l_groups.push_back(kv.second);
   }
   m2l_backend = 1;
-  if (o.m2l_backend == 2 || (o.m2l_backend == 0 && precision == 32 && np == tc::NP && m2l_tc_available())) {
+  if (o.m2l_backend == 2 || (o.m2l_backend == 0 && precision == 32 && tc_np_supported(np) && m2l_tc_available())) {
     if (precision != 32) throw InvalidArgument("gpu: tcgen05 3xTF32 M2L is an fp32 path");
     m2l_tc.build(t, m2l_groups, np, ops, &dev_bytes);
     m2l_backend = m2l_tc.f16 ? 2 : 3;  // 2: kind::f16 3-term split, 3: kind::tf32 3xTF32
@@ -1116,7 +1120,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     if (gemm_tc) {
       std::vector<double> b1, b2;
       factored_b(ops.dc2e_u, ops.dc2e_s, ops.dc2e_v, ops.dc2e_rank, b1, b2);
-      tg_dn1.build(a, b1, 1, &dev_bytes);
+      tg_dn1.build(a, b1, 1, np, &dev_bytes);
       // rows of the deepest level start at dn_nodes[k] (level-major order); tiles of the second solve are
       // cut there so the upper levels' rows finish first
       size_t k = 0;
@@ -1139,10 +1143,10 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
           (s0 < k ? bu : bl).push_back(std::move(y));
           s0 = e0;
         }
-        tg_dn2_up.build(bu, b2, 1, &dev_bytes);
-        tg_dn2_lo.build(bl, b2, 1, &dev_bytes, TcGemm::min_ctas(int(bl.size())));
+        tg_dn2_up.build(bu, b2, 1, np, &dev_bytes);
+        tg_dn2_lo.build(bl, b2, 1, np, &dev_bytes, TcGemm::min_ctas(int(bl.size())));
       } else {
-        tg_dn2.build(b, b2, 1, &dev_bytes);
+        tg_dn2.build(b, b2, 1, np, &dev_bytes);
       }
     } else {
       solve_dn1.build(a, ld_tiles, &dev_bytes);
@@ -1152,10 +1156,10 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   const int64_t tmp_rows = std::max<int64_t>({int64_t(1), le - lb, int64_t(dn_nodes.size())});
   tmp.alloc(size_t(tmp_rows) * np * es, &dev_bytes);
   if (gemm_tc) {
-    sp_tmp.alloc(int(tmp_rows), &dev_bytes);
-    sp_M.alloc(int(nn), &dev_bytes);
-    sp_cd.alloc(int(nn), &dev_bytes);
-    sp_L.alloc(int(nn), &dev_bytes);
+    sp_tmp.alloc(int(tmp_rows), np, &dev_bytes);
+    sp_M.alloc(int(nn), np, &dev_bytes);
+    sp_cd.alloc(int(nn), np, &dev_bytes);
+    sp_L.alloc(int(nn), np, &dev_bytes);
   }
   const std::vector<double> b_l2l = gemm_tc ? octant_b(ops.l2l) : std::vector<double>();
 
@@ -1182,7 +1186,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     if (!tiles.empty()) {
       auto g = std::make_unique<L2LLevel>();
       if (gemm_tc) {
-        g->tc.build(tiles, b_l2l, 8, &dev_bytes);
+        g->tc.build(tiles, b_l2l, 8, np, &dev_bytes);
         g->r0 = int(t.level_ptr[l]);
         g->r1 = int(t.level_ptr[l + 1]);
       } else {
@@ -1518,8 +1522,10 @@ void kifmm_gpu_plan::allgather(cudaStream_t s) {
 void kifmm_gpu_plan::scatter_imports(cudaStream_t s) {
   if (x_total <= 0) return;
   if (precision == 32 && gemm_tc) {
-    scatter_rows_split_kernel<<<unsigned((x_total + 7) / 8), 256, 0, s>>>(
-        x_recv.as<float>(), x_rows.as<int>(), x_rank.as<int>(), x_total, M.as<float>(), sp_M.hi, sp_M.lo, sp_M.un);
+    tc_dispatch_np(np, [&](auto w) {
+      scatter_rows_split_kernel<decltype(w)::value><<<unsigned((x_total + 7) / 8), 256, 0, s>>>(
+          x_recv.as<float>(), x_rows.as<int>(), x_rank.as<int>(), x_total, M.as<float>(), sp_M.hi, sp_M.lo, sp_M.un);
+    });
   } else if (precision == 32) {
     scatter_rows_kernel<float><<<x_total, 128, 0, s>>>(x_recv.as<float>(), np, x_rows.as<int>(), x_rank.as<int>(),
                                                        x_total, M.as<float>());
@@ -1717,9 +1723,11 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
     if (gemm_tc) {
       if constexpr (sizeof(T) == 4) {
         tgemm(lv.tc, sp_M, m2m_scratch.as<T>(), false, nullptr);
-        launch_pdl(m2m_reduce_split_kernel, dim3(unsigned((lv.n + 7) / 8)), dim3(256), 0, s,
-                   (const float*)m2m_scratch.as<float>(), (const int*)lv.parents.as<int>(),
-                   (const int*)lv.masks.as<int>(), lv.n, Mp, sp_M.hi, sp_M.lo, sp_M.un);
+        tc_dispatch_np(np, [&](auto w) {
+          launch_pdl(m2m_reduce_split_kernel<decltype(w)::value>, dim3(unsigned((lv.n + 7) / 8)), dim3(256), 0, s,
+                     (const float*)m2m_scratch.as<float>(), (const int*)lv.parents.as<int>(),
+                     (const int*)lv.masks.as<int>(), lv.n, Mp, sp_M.hi, sp_M.lo, sp_M.un);
+        });
       }
     } else {
       gemm(lv.tiles, Mp, w_m2m.as<T>(), m2m_scratch.as<T>(), false, true);
@@ -1793,8 +1801,10 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
         m2l_tc.launch_presplit_reduce(n_p2l ? check_dn.as<float>() : nullptr, &sp_cd, s);
         launches += 2;
         if (n_dn_extra) {  // P2L-only check rows (no V list): split them here
-          tc::split_f16_list_kernel<<<unsigned((n_dn_extra + 7) / 8), 256, 0, s>>>(
-              check_dn.as<float>(), dn_extra.as<int>(), n_dn_extra, sp_cd.hi, sp_cd.lo, sp_cd.un);
+          tc_dispatch_np(np, [&](auto w) {
+            tc::split_f16_list_kernel<decltype(w)::value><<<unsigned((n_dn_extra + 7) / 8), 256, 0, s>>>(
+                check_dn.as<float>(), dn_extra.as<int>(), n_dn_extra, sp_cd.hi, sp_cd.lo, sp_cd.un);
+          });
           KIFMM_LAUNCH_CHECK();
           ++launches;
         }

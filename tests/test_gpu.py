@@ -41,7 +41,7 @@ CASES = [("uniform-cube", 6000, 40, 4), ("uniform-cube", 5000, 50, 6), ("sphere-
 @pytest.mark.parametrize("precision,backend", [(64, 0), (32, 1), (32, 0)],
                          ids=["fp64", "fp32-simt", "fp32-auto"])
 def test_parity_vs_oracle(require_gpu, kind, n, n_crit, p, precision, backend):
-    """backend 0 = the production choice (tcgen05 M2L and GEMMs for fp32 p = 6, DMMA for fp64),
+    """backend 0 = the production choice (tcgen05 M2L and GEMMs for fp32 p = 4, 5, 6; int8 tcgen05 or DMMA for fp64),
     1 = the SIMT M2L / GEMM kernels."""
     if precision == 32 and p >= 7:
         pytest.skip("fp32 at p=7: kept spectrum cond ~1e11, see test_fp32_p7_accuracy_bound")
@@ -199,6 +199,23 @@ def test_near_queue_mode_bit_identical(require_gpu, monkeypatch):
     ref = out["0", "0"]
     for k, v in out.items():
         assert np.array_equal(v[0], ref[0]) and np.array_equal(v[1], ref[1]), k
+
+
+@pytest.mark.parametrize("pair", ["0", "1"], ids=["1cta", "2cta"])
+@pytest.mark.parametrize("p,kind,n,n_crit", [(4, "uniform-cube", 40000, 40), (5, "uniform-cube", 40000, 64),
+                                             (5, "sphere-surface", 30000, 50), (4, "two-cluster", 20000, 30)])
+def test_tcgen05_path_other_orders(require_gpu, monkeypatch, p, kind, n, n_crit, pair):
+    """The tcgen05 M2L and GEMM chain are instantiated per row width (n_e padded to 32): 64 (p = 4),
+    128 (p = 5) and 160 (p = 6).  fp32 plans at p = 4, 5 take that path by default (m2l_backend 2), in the
+    single-CTA and the 2-CTA pair kernels, and meet the fp32 parity gates against the oracle."""
+    monkeypatch.setenv("KIFMM_TC_PAIR", pair)
+    pos, q = generators.sample(kind, n, seed=31, charges="signed", fp32=True)
+    with fmm.Fmm(pos, fmm.FmmConfig(p=p, n_crit=n_crit, precision=32, gradient=True)) as f:
+        assert f.info()["m2l_backend"] == 2
+        pot, grad, _ = f.evaluate(q)
+        ref, gref = _ref(f, q, True)
+    assert fmm.relative_error(pot, ref) <= 1e-5
+    assert fmm.relative_error(grad, gref) <= 5e-5
 
 
 def test_simt_gemms_with_tcgen05_m2l(require_gpu, monkeypatch):
