@@ -27,7 +27,7 @@ class FmmConfig:
     n_crit: int = 150
     alpha_inner: float = 1.05
     alpha_outer: float = 2.95
-    svd_cutoff: float = 1e-12
+    svd_cutoff: float = 1e-12        # SPEC default (an fp64 setting); fp32 plans at p = 7 need ~1e-8 (tests/test_gpu.py)
     threads: int = 0                 # host threads for tree/lists/precompute (0 = all)
     precision: int = 32              # 32 or 64
     gradient: bool = False
