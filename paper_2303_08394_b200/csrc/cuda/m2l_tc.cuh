@@ -1326,7 +1326,7 @@ struct M2LTcPlan {
 
   template <class TreeView, class OpsView>
   void build(const TreeView& t, const std::vector<std::vector<int64_t>>& groups, int width, const OpsView& ops,
-             size_t* total) {
+             size_t* total, bool own_split = true) {
     if (!tc_np_supported(width))
       throw InvalidArgument("tcgen05 M2L: instantiated for p = 4, 5, 6 (n_e padded to 64, 128, 160)");
     np = width;
@@ -1475,68 +1475,81 @@ struct M2LTcPlan {
     up(&d_seg_in, seg_in, total);
     up(&d_items, items, total);
     up(&d_sched, sched, total);
-    // ---- K_t split into tf32 hi / lo, padded to 160 x 160 per transfer vector
+    // ---- operators and A-operand buffers of the chosen kind only (the other kind's 2 x 32 MB of K_t and
+    //      2 x n_nodes rows are neither built nor allocated)
     const int ne = ops.n_e, nc = ops.n_c, nt = ops.n_m2l;
-    std::vector<float> khi(size_t(nt) * np * np, 0.f), klo(khi.size(), 0.f);
-#pragma omp parallel for schedule(static)
-    for (int v = 0; v < nt; ++v)
-      for (int c = 0; c < nc; ++c)
-        for (int e = 0; e < ne; ++e) {
-          const float x = float(ops.m2l[(size_t(v) * nc + c) * ne + e]);
-          const float h = tf32_rna(x);
-          const size_t idx = (size_t(v) * np + c) * np + e;
-          khi[idx] = h;
-          klo[idx] = x - h;
-        }
-    up(&d_khi, khi, total);
-    up(&d_klo, klo, total);
-    // multipole hi/lo with one appended zero row (gather target of absent sources)
-    KIFMM_CUDA(cudaMalloc(&d_mhi, (nn + 1) * np * sizeof(float)));
-    KIFMM_CUDA(cudaMalloc(&d_mlo, (nn + 1) * np * sizeof(float)));
-    KIFMM_CUDA(cudaMemset(d_mhi + nn * np, 0, np * sizeof(float)));
-    KIFMM_CUDA(cudaMemset(d_mlo + nn * np, 0, np * sizeof(float)));
     KIFMM_CUDA(cudaMalloc(&d_partial, std::max(1, n_items) * size_t(rows) * np * sizeof(float)));
-    *total += 2 * (nn + 1) * np * sizeof(float) + size_t(n_items) * rows * np * sizeof(float);
-    // ---- TMA descriptors (SWIZZLE_128B, 32-float boxes): K_t tiles of this CTA's rows, gather4 rows of M
+    *total += size_t(n_items) * rows * np * sizeof(float);
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     KIFMM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
     if (!fn) throw DeviceError(KIFMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     if (const char* e = std::getenv("KIFMM_TC_ROWB")) rowb = std::atoi(e) == 64 ? 64 : 128;
     const uint32_t brow = uint32_t(pair ? np / 2 : np);
-    encode(reinterpret_cast<EncodeFn>(fn), &tm_khi, d_khi, np, uint64_t(nt) * np, brow, rowb);
-    encode(reinterpret_cast<EncodeFn>(fn), &tm_klo, d_klo, np, uint64_t(nt) * np, brow, rowb);
-    if (np == 160) {  // kind::tf32 variants (m2l_backend 3): p = 6 only
+    const size_t kn = size_t(nt) * np * np;
+    if (!f16) {
+      // kind::tf32 (m2l_backend 3, p = 6 only): K_t split into tf32 hi / lo, padded to np x np per
+      // transfer vector; multipole hi / lo with one appended zero row (gather target of absent sources)
+      std::vector<float> khi(kn, 0.f), klo(kn, 0.f);
+#pragma omp parallel for schedule(static)
+      for (int v = 0; v < nt; ++v)
+        for (int c = 0; c < nc; ++c)
+          for (int e = 0; e < ne; ++e) {
+            const float x = float(ops.m2l[(size_t(v) * nc + c) * ne + e]);
+            const float h = tf32_rna(x);
+            const size_t idx = (size_t(v) * np + c) * np + e;
+            khi[idx] = h;
+            klo[idx] = x - h;
+          }
+      up(&d_khi, khi, total);
+      up(&d_klo, klo, total);
+      KIFMM_CUDA(cudaMalloc(&d_mhi, (nn + 1) * np * sizeof(float)));
+      KIFMM_CUDA(cudaMalloc(&d_mlo, (nn + 1) * np * sizeof(float)));
+      KIFMM_CUDA(cudaMemset(d_mhi + nn * np, 0, np * sizeof(float)));
+      KIFMM_CUDA(cudaMemset(d_mlo + nn * np, 0, np * sizeof(float)));
+      *total += 2 * (nn + 1) * np * sizeof(float);
+      // TMA descriptors (SWIZZLE_128B / 64B, 32- / 16-float boxes): K_t tiles of this CTA's rows
+      encode(reinterpret_cast<EncodeFn>(fn), &tm_khi, d_khi, np, uint64_t(nt) * np, brow, rowb);
+      encode(reinterpret_cast<EncodeFn>(fn), &tm_klo, d_klo, np, uint64_t(nt) * np, brow, rowb);
       set_smem<false, 128>();
       set_smem<true, 128>();
       set_smem<false, 64>();
       set_smem<true, 64>();
-    }
-
-    // ---- f16 kind: K_t * 2^8 split into fp16 hi/lo; multipoles split per row with a power-of-two scale
-    if (f16) {
-      std::vector<__half> h16(khi.size()), l16(khi.size());
+    } else {
+      // kind::f16: K_t * 2^8 split into fp16 hi / lo (padded to np x np); multipoles are split per row
+      // with a power-of-two scale -- by the caller (launch_presplit) or, with own_split, into this
+      // plan's own buffers (launch)
+      std::vector<__half> h16(kn, __float2half_rn(0.f)), l16(kn, __float2half_rn(0.f));
 #pragma omp parallel for schedule(static)
-      for (int64_t i = 0; i < int64_t(khi.size()); ++i) {
-        const float x = (khi[i] + klo[i]) * kKScale;  // (hi + lo) == the fp32 K_t value exactly
-        const __half h = __float2half_rn(x);
-        h16[i] = h;
-        l16[i] = __float2half_rn(x - __half2float(h));
-      }
+      for (int v = 0; v < nt; ++v)
+        for (int c = 0; c < nc; ++c)
+          for (int e = 0; e < ne; ++e) {
+            const float x = float(ops.m2l[(size_t(v) * nc + c) * ne + e]) * kKScale;
+            const __half h = __float2half_rn(x);
+            const size_t idx = (size_t(v) * np + c) * np + e;
+            h16[idx] = h;
+            l16[idx] = __float2half_rn(x - __half2float(h));
+          }
       up(&d_khi16, h16, total);
       up(&d_klo16, l16, total);
-      KIFMM_CUDA(cudaMalloc(&d_mhi16, (nn + 1) * np * sizeof(__half)));
-      KIFMM_CUDA(cudaMalloc(&d_mlo16, (nn + 1) * np * sizeof(__half)));
-      KIFMM_CUDA(cudaMalloc(&d_unscale, (nn + 1) * sizeof(float)));
-      *total += 2 * (nn + 1) * np * sizeof(__half) + (nn + 1) * sizeof(float);
+      if (own_split) {
+        KIFMM_CUDA(cudaMalloc(&d_mhi16, (nn + 1) * np * sizeof(__half)));
+        KIFMM_CUDA(cudaMalloc(&d_mlo16, (nn + 1) * np * sizeof(__half)));
+        KIFMM_CUDA(cudaMalloc(&d_unscale, (nn + 1) * sizeof(float)));
+        *total += 2 * (nn + 1) * np * sizeof(__half) + (nn + 1) * sizeof(float);
+      }
       encode(reinterpret_cast<EncodeFn>(fn), &tm_khi16, d_khi16, np, uint64_t(nt) * np, brow, 64, 2);
       encode(reinterpret_cast<EncodeFn>(fn), &tm_klo16, d_klo16, np, uint64_t(nt) * np, brow, 64, 2);
       tc_dispatch_np(np, [&](auto w) {
         constexpr int W = decltype(w)::value;
-        KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<W, false, 64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        tc::Cfg<W, false, 64, 2>::SMEM_BYTES));
-        KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<W, true, 64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        tc::Cfg<W, true, 64, 2>::SMEM_BYTES));
+        if (pair)
+          KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<W, true, 64, 2>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          tc::Cfg<W, true, 64, 2>::SMEM_BYTES));
+        else
+          KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<W, false, 64, 2>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          tc::Cfg<W, false, 64, 2>::SMEM_BYTES));
       });
     }
   }
@@ -1613,6 +1626,7 @@ struct M2LTcPlan {
   void launch(const float* M, float* check, int width, cudaStream_t s) {
     if (!n_items) return;
     if (width != np) throw InvalidArgument("M2L launch: row width mismatch");
+    if (f16 && !d_mhi16) throw InvalidArgument("M2L launch: plan was built without its own split buffers");
     if (f16) {
       tc_dispatch_np(np, [&](auto w) {
         constexpr int W = decltype(w)::value;
