@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <exception>
 #include <cstdio>
 #include <cstring>
 #include <tuple>
@@ -199,8 +200,40 @@ void precompute(Operators& ops, int p, double ai, double ao, double cutoff, doub
   std::vector<double> kup(size_t(nc) * ne), kdn(size_t(nc) * ne);
   kernel_matrix(ue.data(), ne, uc.data(), nc, kup.data());
   kernel_matrix(de.data(), ne, dc.data(), nc, kdn.data());
-  factor_pinv(kup, nc, ne, cutoff, ops.uc2e_rank, ops.uc2e_u, ops.uc2e_s, ops.uc2e_v, "uc2e");
-  factor_pinv(kdn, nc, ne, cutoff, ops.dc2e_rank, ops.dc2e_u, ops.dc2e_s, ops.dc2e_v, "dc2e");
+  // The two truncated SVDs (serial Jacobi sweeps, ~45 ms each at p = 6) and the 316 M2L kernel matrices
+  // are independent: one dynamic loop runs them side by side (jobs 0, 1 = the SVDs).  Each job owns its
+  // outputs, so the result does not depend on the thread count.
+  // M2L kernel matrices K_t: source up-equivalent (alpha_in) at offset t * (2 h2) ->
+  // target down-check (alpha_in), both at the reference level (SPEC.md:414, 504).
+  const auto& tvs = transfer_vector_table();
+  ops.m2l.assign(tvs.size() * size_t(nc) * ne, 0.0);
+  std::exception_ptr svd_err[2];
+  auto first_job = [&](size_t job) {
+    if (job < 2) {
+      try {
+        if (job == 0)
+          factor_pinv(kup, nc, ne, cutoff, ops.uc2e_rank, ops.uc2e_u, ops.uc2e_s, ops.uc2e_v, "uc2e");
+        else
+          factor_pinv(kdn, nc, ne, cutoff, ops.dc2e_rank, ops.dc2e_u, ops.dc2e_s, ops.dc2e_v, "dc2e");
+      } catch (...) {
+        svd_err[job] = std::current_exception();
+      }
+      return;
+    }
+    const size_t t = job - 2;
+    const double sc[3] = {2.0 * h2 * tvs[t][0], 2.0 * h2 * tvs[t][1], 2.0 * h2 * tvs[t][2]};
+    const auto sue = scaled(ops.surface, sc, ai * h2);
+    kernel_matrix(sue.data(), ne, dc.data(), nc, &ops.m2l[t * size_t(nc) * ne]);
+  };
+  const long long n_first = 2 + static_cast<long long>(tvs.size());
+  if (threads <= 1) {
+    for (long long j = 0; j < n_first; ++j) first_job(size_t(j));
+  } else {
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
+    for (long long j = 0; j < n_first; ++j) first_job(size_t(j));
+  }
+  for (auto& e : svd_err)
+    if (e) std::rethrow_exception(e);
 
   // M2M_o = uc2e_inv(l) K(child ue(l+1) -> parent uc(l)); L2L_o = dc2e_inv(l+1) K(parent de(l) -> child dc(l+1)).
   // Both level-invariant; built with parent at level 2, child at 3.
@@ -225,15 +258,6 @@ void precompute(Operators& ops, int p, double ai, double ao, double cutoff, doub
     }
   });
 
-  // M2L kernel matrices K_t: source up-equivalent (alpha_in) at offset t * (2 h2) ->
-  // target down-check (alpha_in), both at the reference level (SPEC.md:414, 504).
-  const auto& tvs = transfer_vector_table();
-  ops.m2l.assign(tvs.size() * size_t(nc) * ne, 0.0);
-  parallel_for(tvs.size(), threads, [&](size_t t) {
-    const double sc[3] = {2.0 * h2 * tvs[t][0], 2.0 * h2 * tvs[t][1], 2.0 * h2 * tvs[t][2]};
-    const auto sue = scaled(ops.surface, sc, ai * h2);
-    kernel_matrix(sue.data(), ne, dc.data(), nc, &ops.m2l[t * size_t(nc) * ne]);
-  });
   for (double x : ops.m2m)
     if (!std::isfinite(x)) throw NumericalError("precompute: non-finite m2m");
   for (double x : ops.l2l)
