@@ -234,6 +234,8 @@ typedef struct kifmm_gpu_timings {
   float l2l_ms;
   float leaf_ms;       /* near field + L2P + M2P */
   float download_ms;   /* D2H potentials (+ permutation) */
+  float upward_ms;     /* device time of the last kifmm_gpu_evaluate_upward (without its host copies) */
+  float downward_ms;   /* device time of the last kifmm_gpu_evaluate_downward (without its host copies) */
 } kifmm_gpu_timings;
 
 typedef struct kifmm_gpu_plan_info {

@@ -67,7 +67,7 @@ class GpuOptions(C.Structure):
 class GpuTimings(C.Structure):
     _fields_ = [(n, f32) for n in (
         "total_ms", "upload_ms", "p2m_ms", "m2m_ms", "exchange_ms", "p2l_ms", "m2l_ms",
-        "down_solve_ms", "l2l_ms", "leaf_ms", "download_ms")]
+        "down_solve_ms", "l2l_ms", "leaf_ms", "download_ms", "upward_ms", "downward_ms")]
 
     def as_dict(self):
         return {n: float(getattr(self, n)) for n, _ in self._fields_}

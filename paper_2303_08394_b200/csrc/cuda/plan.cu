@@ -411,6 +411,7 @@ struct kifmm_gpu_plan {
   cudaStream_t stream = nullptr, side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_done = nullptr;  // end of the last evaluate (any entry point, any stream)
+  cudaEvent_t ev_half[2] = {nullptr, nullptr};  // device span of an upward / downward half (exchange = 1)
   std::array<cudaEvent_t, 16> ev{};
   kifmm_gpu_plan_info info{};
   kifmm_gpu_timings last{};
@@ -495,6 +496,8 @@ struct kifmm_gpu_plan {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (ev_done) cudaEventDestroy(ev_done);
+    for (auto& e : ev_half)
+      if (e) cudaEventDestroy(e);
     if (comm) Nccl::get().commDestroy(static_cast<ncclComm_t>(comm));
   }
 
@@ -687,6 +690,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     KIFMM_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+    for (auto& e : ev_half) KIFMM_CUDA(cudaEventCreate(&e));
   }
   for (auto& e : ev) KIFMM_CUDA(cudaEventCreate(&e));
   check_hw = precision == 32 && tc_np_supported(np);
@@ -2255,14 +2259,17 @@ kifmm_status kifmm_gpu_evaluate_upward(kifmm_gpu_plan* p, const void* charges, i
     p->begin(s);
     KIFMM_CUDA(cudaMemcpyAsync(p->q_in.p, charges, size_t(p->N) * es, cudaMemcpyDefault, s));
     p->host_phase_input_order = input_order != 0;
+    KIFMM_CUDA(cudaEventRecord(p->ev_half[0], s));
     if (p->precision == 32)
       p->run<float>(s, input_order != 0, false, 1);
     else
       p->run<double>(s, input_order != 0, false, 1);
+    KIFMM_CUDA(cudaEventRecord(p->ev_half[1], s));
     if (p->x_mine > 0)
       KIFMM_CUDA(cudaMemcpyAsync(export_rows, p->x_send.p, size_t(p->x_mine) * p->np * es, cudaMemcpyDefault, s));
     p->finish(s);
     KIFMM_CUDA(cudaStreamSynchronize(s));
+    KIFMM_CUDA(cudaEventElapsedTime(&p->last.upward_ms, p->ev_half[0], p->ev_half[1]));
   });
 }
 
@@ -2280,13 +2287,16 @@ kifmm_status kifmm_gpu_evaluate_downward(kifmm_gpu_plan* p, const void* gathered
     if (p->x_max > 0)
       KIFMM_CUDA(cudaMemcpyAsync(p->x_recv.p, gathered, size_t(p->world) * p->x_max * p->np * es, cudaMemcpyDefault,
                                  s));
+    KIFMM_CUDA(cudaEventRecord(p->ev_half[0], s));
     if (p->precision == 32)
       p->run<float>(s, io, false, 2);
     else
       p->run<double>(s, io, false, 2);
+    KIFMM_CUDA(cudaEventRecord(p->ev_half[1], s));
     p->copy_out(potential, gradient, io, s);
     p->finish(s);
     KIFMM_CUDA(cudaStreamSynchronize(s));
+    KIFMM_CUDA(cudaEventElapsedTime(&p->last.downward_ms, p->ev_half[0], p->ev_half[1]));
   });
 }
 

@@ -215,6 +215,13 @@ class Fmm:
               "gpu_evaluate_downward")
         return pot, grad
 
+    def last_timings(self) -> dict:
+        """Device times of the last timed evaluate and of the last upward / downward halves
+        (kifmm_gpu_last_timings)."""
+        tm = _lib.GpuTimings()
+        check(lib.kifmm_gpu_last_timings(self._h, C.byref(tm)), "gpu_last_timings")
+        return tm.as_dict()
+
     def info(self) -> dict:
         inf = _lib.GpuPlanInfo()
         check(lib.kifmm_gpu_plan_get_info(self._h, C.byref(inf)), "plan_info")

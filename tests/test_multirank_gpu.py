@@ -35,6 +35,9 @@ def _emulated(pos, q, cfg_kw, world, input_order=True):
         for r, s in enumerate(sends):
             gathered[r, :s.shape[0]] = s
         outs = [p.evaluate_downward(gathered) for p in plans]
+        for p in plans:  # device spans of the two halves (kifmm_gpu_last_timings; tools/scale_projection.py)
+            tm = p.last_timings()
+            assert tm["upward_ms"] > 0 and tm["downward_ms"] > 0
         return outs, info, plans[0].tree
     finally:
         for p in plans:
