@@ -19,7 +19,7 @@ fi
 if [[ -z "$ARGS" || " $ARGS " == *" ncu "* ]]; then
   for c in ${NCU_CFGS:-2 3 5}; do
     KIFMM_NEAR_BPS=0 KIFMM_CFG=$c KIFMM_ITERS=1 timeout 1200 ncu -f --set full --clock-control none --import-source on \
-      -k regex:"leaf_eval|far_hw|far_f2|check_f2|m2l_tc_kernel<1|near_ws|gather_dmma" -c ${NCU_COUNT:-8} -o /tmp/r02_cfg$c \
+      -k regex:"leaf_eval|far_hw|far_f2|check_f2|m2l_tc_kernel<160, 1|near_ws|gather_dmma" -c ${NCU_COUNT:-8} -o /tmp/r02_cfg$c \
       python tools/profile_run.py > gpurun_out/ncu$c.log 2>&1
     echo cfg$c rc=$?
     ncu -i /tmp/r02_cfg$c.ncu-rep --page raw --csv > gpurun_out/r02_cfg${c}_raw.csv 2>&1
