@@ -27,7 +27,8 @@ struct GemmArgs {
   const int* seg_in;    // n_segs * BM   (-1 = zero row)
   const T* X;
   int ldx;
-  const T* W;           // [mats][K][N]
+  const T* W;           // [mats][K][ldw]; a CTA of column block blockIdx.y computes columns [y N, y N + N)
+  int ldw;              // row stride of W (= N for the widths instantiated directly; 2 N or 4 N for p = 8, 9, 10)
   int K;                // multiple of KC
   T* Y;
   int ldy;
@@ -102,9 +103,12 @@ __global__ void __launch_bounds__(GemmShape<T, N, BM, TM, TN, KC, STAGES>::NT, 1
       const T* g = a.X + size_t(src < 0 ? 0 : src) * a.ldx + kc + col * S::VEC;
       cp_async16(As + row * (KC + S::APAD) + col * S::VEC, g, src >= 0);
     }
-    const T* wm = a.W + size_t(a.seg_mat[seg]) * a.K * N + size_t(kc) * N;
-    constexpr int WCH = KC * N / S::VEC;
-    for (int c = tid; c < WCH; c += S::NT) cp_async16(Ws + c * S::VEC, wm + c * S::VEC, true);
+    const T* wm = a.W + (size_t(a.seg_mat[seg]) * a.K + size_t(kc)) * a.ldw + size_t(blockIdx.y) * N;
+    constexpr int WCH = KC * N / S::VEC, WROW = N / S::VEC;
+    for (int c = tid; c < WCH; c += S::NT) {
+      const int k = c / WROW, col = c % WROW;
+      cp_async16(Ws + c * S::VEC, wm + size_t(k) * a.ldw + col * S::VEC, true);
+    }
   };
 
   T acc[TM][TN];
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(GemmShape<T, N, BM, TM, TN, KC, STAGES>::NT, 1
     const int row = tr + i * S::TR;
     const int out = a.tile_out[size_t(tile) * BM + row];
     if (out < 0) continue;
-    T* y = a.Y + size_t(out) * a.ldy;
+    T* y = a.Y + size_t(out) * a.ldy + size_t(blockIdx.y) * N;
 #pragma unroll
     for (int g = 0; g < S::G; ++g) {
       const int col = g * S::GSTRIDE + tc * S::VEC;
@@ -222,11 +226,11 @@ __global__ void __launch_bounds__(256, 1) gather_dmma_kernel(GemmArgs<double> a)
       const double* g = a.X + size_t(src < 0 ? 0 : src) * a.ldx + kc + col * 2;
       cp_async16(As + row * S::AST + col * 2, g, src >= 0);
     }
-    const double* wm_ = a.W + size_t(a.seg_mat[seg]) * a.K * N + size_t(kc) * N;
+    const double* wm_ = a.W + (size_t(a.seg_mat[seg]) * a.K + size_t(kc)) * a.ldw + size_t(blockIdx.y) * N;
     constexpr int WCH = KC * N / 2;
     for (int c = tid; c < WCH; c += S::NT) {
       const int k = c / (N / 2), col = c % (N / 2);
-      cp_async16(Ws + k * S::BST + col * 2, wm_ + size_t(k) * N + col * 2, true);
+      cp_async16(Ws + k * S::BST + col * 2, wm_ + size_t(k) * a.ldw + col * 2, true);
     }
   };
 
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(256, 1) gather_dmma_kernel(GemmArgs<double> a)
     const int row = wm * 32 + 8 * i + (lane >> 2);
     const int out = a.tile_out[size_t(tile) * BM + row];
     if (out < 0) continue;
-    double* y = a.Y + size_t(out) * a.ldy;
+    double* y = a.Y + size_t(out) * a.ldy + size_t(blockIdx.y) * N;
 #pragma unroll
     for (int j = 0; j < S::NB; ++j) {
       const int col = wn * (N / 4) + 8 * j + 2 * (lane & 3);

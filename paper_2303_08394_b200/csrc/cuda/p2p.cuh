@@ -663,7 +663,6 @@ __global__ void __launch_bounds__(kFarWarps * 32) far_kernel(P2PParams<T> p, con
   if (wi >= n_works) return;
   const int4 w = works[wi];
   const int t0 = w.x, t1 = w.x + w.w;
-  const int ne8 = (p.n_e + 7) & ~7;
   v4_t<T>* my = sh[warp];
   {
     const int t = t0 + lane;
@@ -675,12 +674,16 @@ __global__ void __launch_bounds__(kFarWarps * 32) far_kernel(P2PParams<T> p, con
       const bool l2p = sf.y == kSrcL2P;
       const T alpha = l2p ? p.alpha_outer : p.alpha_inner;
       const T* dens = l2p ? L : M;
-      __syncwarp();
-      for (int j = lane; j < ne8; j += 32)
-        my[j] = j < p.n_e ? surface_source(p, sf.x, alpha, dens, j)
-                          : make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
-      __syncwarp();
-      p2p_round<T, GRAD, false>(my, 0, ne8, x.x, x.y, x.z, ph, gx, gy, gz);
+      // surfaces above kFarMaxNe points (p >= 8) are staged in chunks; one chunk otherwise
+      for (int j0 = 0; j0 < p.n_e; j0 += kFarMaxNe) {
+        const int cn = min(kFarMaxNe, p.n_e - j0), cn8 = (cn + 7) & ~7;
+        __syncwarp();
+        for (int j = lane; j < cn8; j += 32)
+          my[j] = j < cn ? surface_source(p, sf.x, alpha, dens, j0 + j)
+                         : make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
+        __syncwarp();
+        p2p_round<T, GRAD, false>(my, 0, cn8, x.x, x.y, x.z, ph, gx, gy, gz);
+      }
     }
     if (act) {
       const T c = T(kInv4PiD);

@@ -108,7 +108,7 @@ inline bool use_dmma() {  // read per launch (a captured graph keeps the choice 
 }
 
 template <class T, int N, int BM, int TM>
-void launch_gemm_n(const GemmTiles& t, const GemmArgs<T>& a, cudaStream_t s) {
+void launch_gemm_n(const GemmTiles& t, const GemmArgs<T>& a, cudaStream_t s, int col_blocks = 1) {
   if constexpr (sizeof(T) == 8 && BM == 64 && N % 32 == 0) {
     if (use_dmma()) {
       auto kern = gather_dmma_kernel<N>;
@@ -117,7 +117,7 @@ void launch_gemm_n(const GemmTiles& t, const GemmArgs<T>& a, cudaStream_t s) {
         KIFMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(DmmaShape<N>::SMEM)));
         attr = true;
       }
-      kern<<<t.n_tiles, DmmaShape<N>::NT, DmmaShape<N>::SMEM, s>>>(a);
+      kern<<<dim3(t.n_tiles, col_blocks), DmmaShape<N>::NT, DmmaShape<N>::SMEM, s>>>(a);
       KIFMM_LAUNCH_CHECK();
       return;
     }
@@ -130,7 +130,7 @@ void launch_gemm_n(const GemmTiles& t, const GemmArgs<T>& a, cudaStream_t s) {
     KIFMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM)));
     attr = true;
   }
-  kern<<<t.n_tiles, S::NT, S::SMEM, s>>>(a);
+  kern<<<dim3(t.n_tiles, col_blocks), S::NT, S::SMEM, s>>>(a);
   KIFMM_LAUNCH_CHECK();
 }
 
@@ -147,6 +147,10 @@ void launch_gemm(int np, const GemmTiles& t, GemmArgs<T> a, cudaStream_t s) {
     case 128: return launch_gemm_n<T, 128, BM, TM>(t, a, s);
     case 160: return launch_gemm_n<T, 160, BM, TM>(t, a, s);
     case 224: return launch_gemm_n<T, 224, BM, TM>(t, a, s);
+    // p = 8, 9, 10: column blocks of an instantiated width (blockIdx.y; W row stride a.ldw = np)
+    case 320: return launch_gemm_n<T, 160, BM, TM>(t, a, s, 2);
+    case 448: return launch_gemm_n<T, 224, BM, TM>(t, a, s, 2);
+    case 512: return launch_gemm_n<T, 128, BM, TM>(t, a, s, 4);
     default: throw InvalidArgument("gemm: unsupported padded width " + std::to_string(np));
   }
 }
@@ -255,6 +259,9 @@ void launch_check(int np, int n, const P2PParams<T>& pp, const CheckWork* works,
     case 4: check_kernel<T, 4><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
     case 5: check_kernel<T, 5><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
     case 7: check_kernel<T, 7><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
+    case 10: check_kernel<T, 10><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
+    case 14: check_kernel<T, 14><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
+    case 16: check_kernel<T, 16><<<blocks, kCheckWarps * 32, 0, s>>>(pp, works, n, ranges, lvl, ref, alpha, out, np); break;
     default: throw InvalidArgument("check kernel: unsupported width");
   }
   KIFMM_LAUNCH_CHECK();
@@ -429,6 +436,7 @@ struct kifmm_gpu_plan {
   int n_far = 0;
   int far_chunk = 0, n_far_groups = 0;  // surface chunking of long half-warp far works (see build)
   DevMem far_part, far_groups;
+  bool far_packed = false;  // fp32 packed far kernels (fused output write); else the scalar chunked far_kernel
   bool far_hw = false;  // half-warp far kernel (every work has at most one surface; KIFMM_FAR_HW=0: off)
   int n_p2m = 0, n_p2l = 0;
   GemmTiles solve_up1, solve_up2, solve_dn1, solve_dn2, m2l;
@@ -658,7 +666,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   if (precision != 32 && precision != 64) throw InvalidArgument("gpu: precision must be 32 or 64");
   if (rank < 0 || rank >= world) throw InvalidArgument("gpu: rank out of range");
   if (ops.n_e != ops.n_c) throw InvalidArgument("gpu: n_c != n_e is not supported");
-  if (ops.n_e > 224) throw InvalidArgument("gpu: expansion order above p=7 (n_e > 224) is not supported");
+  if (ops.n_e > 512) throw InvalidArgument("gpu: expansion order above p=10 (n_e > 512) is not supported");
   if (t.n_particles >= (int64_t(1) << 31)) throw InvalidArgument("gpu: N >= 2^31");
   if (ops.n_m2l != 316) throw InvalidArgument("gpu: operator cache must hold 316 M2L matrices");
   KIFMM_CUDA(cudaSetDevice(device));
@@ -670,6 +678,9 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   nc = ops.n_c;
   np = round_up(ne, 32);
   if (np == 96 || np == 192) np += 32;  // instantiated widths: 32, 64, 128, 160, 224
+  // p = 8, 9, 10 (n_e = 296, 386, 488 -> 320, 448, 512): column blocks of the 160 / 224 / 128-wide GEMM
+  // kernels, chunked far-field staging
+  if (np == 416) np = 448;
   ref_level = ops.reference_level;
   alpha_in = ops.alpha_inner;
   alpha_out = ops.alpha_outer;
@@ -1378,6 +1389,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
   if (const char* e = std::getenv("KIFMM_FAR")) far_as_leaf = packed && std::string(e) == "leaf";
   if (far_as_leaf) build_leaf_plan(false, leaf_far);  // experiments: far field on the block kernel
   // far field: one warp-work per owned leaf with any L2P / M2P surface
+  far_packed = packed && ne <= kFarMaxNe;  // the packed fp32 kernels stage whole surfaces (p <= 7)
   {
     std::vector<int4> fw;
     std::vector<FarWork> fw2;
@@ -1400,13 +1412,13 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
       const int e = int(sf.size());
       for (int64_t t0 = t.leaf_ptr[l]; t0 < t.leaf_ptr[l + 1]; t0 += chunk) {
         const int cnt = int(std::min<int64_t>(chunk, t.leaf_ptr[l + 1] - t0));
-        if (packed)
+        if (far_packed)
           fw2.push_back({int(t0), cnt, b, e, e > b ? sf[b].x : 0, e > b ? sf[b].y : 0, 0, 0});
         else if (e > b)
           fw.push_back(make_int4(int(t0), b, e, cnt));
       }
     }
-    far_hw = packed && ne <= 4 * (kFarHwSlot / 4);
+    far_hw = far_packed && ne <= 4 * (kFarHwSlot / 4);
     if (const char* e = std::getenv("KIFMM_FAR_HW")) far_hw = far_hw && std::atoi(e) != 0;
     // Long works (many M2P surfaces, adaptive trees) are cut into chunks of <= far_chunk surfaces: a
     // half-warp walks one work's surfaces in sequence, so the longest work bounds the kernel (config 3:
@@ -1445,16 +1457,16 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
         far_groups.upload(groups, &dev_bytes);
       }
     }
-    n_far = int(packed ? fw2.size() : fw.size());
+    n_far = int(far_packed ? fw2.size() : fw.size());
     // half-warp kernel: a warp's two works loop to the longer surface list -- pair works of equal
     // surface counts (stable sort by count; every work writes only its own targets, order is free)
-    if (far_hw && packed)  // equal (surface count, source slices) in the two halves of a warp
+    if (far_hw && far_packed)  // equal (surface count, source slices) in the two halves of a warp
       std::stable_sort(fw2.begin(), fw2.end(), [](const FarWork& a, const FarWork& b) {
         const int na = a.surf_end - a.surf_begin, nb = b.surf_end - b.surf_begin;
         if (na != nb) return na > nb;
         return far_hw_slices(a.count) < far_hw_slices(b.count);
       });
-    if (packed)
+    if (far_packed)
       far_works.upload(fw2, &dev_bytes);
     else
       far_works.upload(fw, &dev_bytes);
@@ -1557,6 +1569,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
     a.X = X;
     a.ldx = np;
     a.W = W;
+    a.ldw = np;
     a.K = np;
     a.Y = Y;
     a.ldy = np;
@@ -1895,7 +1908,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
   bool fused_out = false;  // the packed far kernel wrote the final (input-order) output
   if (far_as_leaf) leaf(leaf_far, true, s);
   if constexpr (sizeof(T) == 4) {
-    if (leaf_packed && n_far && !far_as_leaf) {
+    if (far_packed && n_far && !far_as_leaf) {
       if (input_order && world > 1) {
         KIFMM_CUDA(cudaMemsetAsync(pot_out.p, 0, pot_out.bytes, s));
         if (grad) KIFMM_CUDA(cudaMemsetAsync(grad_out.p, 0, grad_out.bytes, s));

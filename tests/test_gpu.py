@@ -66,6 +66,25 @@ def test_fp32_p7_accuracy_bound(require_gpu):
     assert fmm.relative_error(pot, ref) <= 5e-4
 
 
+@pytest.mark.parametrize("kind,n,n_crit,p,precision,cutoff", [
+    ("two-cluster", 3000, 30, 8, 64, 1e-12), ("sphere-surface", 4000, 60, 10, 64, 1e-12),
+    ("uniform-cube", 4000, 60, 9, 32, 1e-8)])
+def test_high_orders(require_gpu, kind, n, n_crit, p, precision, cutoff):
+    """p = 8, 9, 10 (row widths 320, 448, 512; the paper's L2P experiment uses p = 10) on the any-width
+    kernels: parity gates against the oracle, and the graph launch equals the eager timed run."""
+    pos, q = generators.sample(kind, n, seed=5, charges="signed", fp32=precision == 32)
+    cfg = fmm.FmmConfig(p=p, n_crit=n_crit, precision=precision, svd_cutoff=cutoff, gradient=True)
+    with fmm.Fmm(pos, cfg) as f:
+        assert f.info()["m2l_backend"] == 1
+        pot, grad, _ = f.evaluate(q)
+        pot2, grad2, _ = f.evaluate(q, timed=True)
+        ref, gref = _ref(f, q, True)
+    assert np.array_equal(pot, pot2) and np.array_equal(grad, grad2)
+    tp, tg = TOL[precision]
+    assert fmm.relative_error(pot, ref) <= tp
+    assert fmm.relative_error(grad, gref) <= tg
+
+
 @pytest.mark.parametrize("kind,n,n_crit", [("two-cluster", 4000, 8), ("uniform-cube", 20000, 60)])
 def test_fp32_p7_with_fp32_cutoff(require_gpu, kind, n, n_crit):
     """fp32 at p = 7 meets the fp32 gate once the pseudo-inverse cutoff suits fp32: the SPEC default
@@ -185,7 +204,7 @@ def test_invalid_arguments(require_gpu):
         with pytest.raises(InvalidArgument):
             f.evaluate(q[:10])
     with pytest.raises(InvalidArgument):
-        fmm.Fmm(pos, fmm.FmmConfig(p=9, n_crit=20))  # n_e > 224 unsupported on the GPU
+        fmm.Fmm(pos, fmm.FmmConfig(p=11, n_crit=20))  # n_e > 512 (p > 10) unsupported on the GPU
     with pytest.raises(InvalidArgument):
         fmm.Fmm(pos, fmm.FmmConfig(precision=16))
 
