@@ -303,7 +303,7 @@ kifmm_status kifmm_operators_load(const char* path, uint64_t expected_fingerprin
 }
 
 kifmm_status kifmm_svd(const double* a, int32_t m, int32_t n, double* u, double* s, double* v) {
-  return guard([&] { jacobi_svd(a, m, n, u, s, v); });
+  return guard([&] { jacobi_svd(a, m, n, u, s, v, resolve_threads(0)); });
 }
 
 }  // extern "C"

@@ -47,62 +47,147 @@ void kernel_matrix(const double* src, int64_t m, const double* tgt, int64_t k, d
                                tgt[3 * j + 2]);
 }
 
-void jacobi_svd(const double* a, int m, int n, double* u, double* s, double* v) {
-  if (m < n || n < 1) throw InvalidArgument("jacobi_svd: need m >= n >= 1");
-  std::vector<double> w(size_t(m) * n), vv(size_t(n) * n, 0.0);  // column-major
-  for (int i = 0; i < m; ++i)
-    for (int j = 0; j < n; ++j) w[size_t(j) * m + i] = a[size_t(i) * n + j];
-  for (int j = 0; j < n; ++j) vv[size_t(j) * n + j] = 1.0;
-  const double tol = DBL_EPSILON;
-  for (int sweep = 0; sweep < 80; ++sweep) {
-    int rot = 0;
-    for (int p = 0; p < n - 1; ++p) {
-      double* wp = &w[size_t(p) * m];
-      double* vp = &vv[size_t(p) * n];
-      for (int q = p + 1; q < n; ++q) {
-        double* wq = &w[size_t(q) * m];
-        double* vq = &vv[size_t(q) * n];
-        double alpha = 0, beta = 0, gamma = 0;
-        for (int i = 0; i < m; ++i) {
-          alpha += wp[i] * wp[i];
-          beta += wq[i] * wq[i];
-          gamma += wp[i] * wq[i];
-        }
-        if (gamma == 0.0 || std::fabs(gamma) <= tol * std::sqrt(alpha * beta)) continue;
-        ++rot;
-        const double zeta = (beta - alpha) / (2.0 * gamma);
-        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
-        for (int i = 0; i < m; ++i) {
-          const double x = wp[i], y = wq[i];
-          wp[i] = c * x - sn * y;
-          wq[i] = sn * x + c * y;
-        }
-        for (int i = 0; i < n; ++i) {
-          const double x = vp[i], y = vq[i];
-          vp[i] = c * x - sn * y;
-          vq[i] = sn * x + c * y;
-        }
-      }
+namespace {
+// Below this column count a matrix is swept serially in cyclic order (the two precompute SVDs then run side by
+// side with the M2L matrices); from it on, in parallel rounds of disjoint pairs.  The order depends on n only,
+// never on the thread count, so the operators are reproducible on any host.
+constexpr int kJacobiParallelMin = 256;
+// One-sided Jacobi state of one matrix (columns of w are rotated until mutually orthogonal; vv accumulates V).
+struct JacobiState {
+  int m = 0, n = 0;
+  std::vector<double> w, vv;  // column-major
+  bool done = false;
+  JacobiState(const double* a, int m_, int n_) : m(m_), n(n_), w(size_t(m_) * n_), vv(size_t(n_) * n_, 0.0) {
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < n; ++j) w[size_t(j) * m + i] = a[size_t(i) * n + j];
+    for (int j = 0; j < n; ++j) vv[size_t(j) * n + j] = 1.0;
+  }
+  int rotate(int p, int q) {
+    const double tol = DBL_EPSILON;
+    double* wp = &w[size_t(p) * m];
+    double* wq = &w[size_t(q) * m];
+    double alpha = 0, beta = 0, gamma = 0;
+    for (int i = 0; i < m; ++i) {
+      alpha += wp[i] * wp[i];
+      beta += wq[i] * wq[i];
+      gamma += wp[i] * wq[i];
     }
-    if (rot == 0) break;
+    if (gamma == 0.0 || std::fabs(gamma) <= tol * std::sqrt(alpha * beta)) return 0;
+    const double zeta = (beta - alpha) / (2.0 * gamma);
+    const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+    const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+    for (int i = 0; i < m; ++i) {
+      const double x = wp[i], y = wq[i];
+      wp[i] = c * x - sn * y;
+      wq[i] = sn * x + c * y;
+    }
+    double* vp = &vv[size_t(p) * n];
+    double* vq = &vv[size_t(q) * n];
+    for (int i = 0; i < n; ++i) {
+      const double x = vp[i], y = vq[i];
+      vp[i] = c * x - sn * y;
+      vq[i] = sn * x + c * y;
+    }
+    return 1;
   }
-  std::vector<double> sig(n);
-  for (int j = 0; j < n; ++j) {
-    double acc = 0;
-    for (int i = 0; i < m; ++i) acc += w[size_t(j) * m + i] * w[size_t(j) * m + i];
-    sig[j] = std::sqrt(acc);
+  // serial cyclic-by-rows sweeps (all pairs p < q in order) until a sweep makes no rotation
+  void cyclic_sweeps() {
+    for (int sweep = 0; sweep < 80; ++sweep) {
+      int rot = 0;
+      for (int p = 0; p < n - 1; ++p)
+        for (int q = p + 1; q < n; ++q) rot += rotate(p, q);
+      if (rot == 0) break;
+    }
+    done = true;
   }
-  std::vector<int> order(n);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return sig[x] > sig[y]; });
-  for (int jj = 0; jj < n; ++jj) {
-    const int j = order[jj];
-    s[jj] = sig[j];
-    const double inv = sig[j] > 0 ? 1.0 / sig[j] : 0.0;
-    for (int i = 0; i < m; ++i) u[size_t(i) * n + jj] = w[size_t(j) * m + i] * inv;
-    for (int i = 0; i < n; ++i) v[size_t(i) * n + jj] = vv[size_t(j) * n + i];
+  void finish(double* u, double* s, double* v) const {
+    std::vector<double> sig(n);
+    for (int j = 0; j < n; ++j) {
+      double acc = 0;
+      for (int i = 0; i < m; ++i) acc += w[size_t(j) * m + i] * w[size_t(j) * m + i];
+      sig[j] = std::sqrt(acc);
+    }
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return sig[x] > sig[y]; });
+    for (int jj = 0; jj < n; ++jj) {
+      const int j = order[jj];
+      s[jj] = sig[j];
+      const double inv = sig[j] > 0 ? 1.0 / sig[j] : 0.0;
+      for (int i = 0; i < m; ++i) u[size_t(i) * n + jj] = w[size_t(j) * m + i] * inv;
+      for (int i = 0; i < n; ++i) v[size_t(i) * n + jj] = vv[size_t(j) * n + i];
+    }
   }
+};
+
+// Round-robin ("tournament") pair order: a sweep is np - 1 rounds of np / 2 disjoint column pairs (np = n
+// rounded up to even; the extra column is a bye).  The pairs of a round -- of every matrix of the batch, all
+// of the same n -- rotate independently, so one parallel loop per round covers them all and the result does
+// not depend on the thread count.  A matrix leaves the batch after its first sweep without a rotation.
+void jacobi_sweeps(std::vector<JacobiState*>& mats, int threads) {
+  if (mats.empty()) return;
+  const int n = mats[0]->n, np = n + (n & 1), half = np / 2, nm = int(mats.size());
+  std::vector<int> seat(np);
+  std::iota(seat.begin(), seat.end(), 0);
+  std::vector<long long> rot(nm);
+  for (int sweep = 0; sweep < 80 && n > 1; ++sweep) {
+    std::fill(rot.begin(), rot.end(), 0);
+    for (int round = 0; round < np - 1; ++round) {
+      // seats i and np - 1 - i meet; seat 0 stays, the others move one place per round
+      auto meet = [&](int job) -> int {
+        JacobiState& st = *mats[job / half];
+        if (st.done) return 0;
+        const int i = job % half;
+        int p = seat[i], q = seat[np - 1 - i];
+        if (p >= n || q >= n) return 0;  // bye
+        if (p > q) std::swap(p, q);
+        return st.rotate(p, q);
+      };
+      const int jobs = nm * half;
+      if (threads > 1 && jobs >= 16) {
+#pragma omp parallel for schedule(static) num_threads(threads)
+        for (int job = 0; job < jobs; ++job) {
+          if (meet(job)) {
+#pragma omp atomic
+            rot[job / half] += 1;
+          }
+        }
+      } else {
+        for (int job = 0; job < jobs; ++job) rot[job / half] += meet(job);
+      }
+      std::rotate(seat.begin() + 1, seat.end() - 1, seat.end());
+    }
+    bool all = true;
+    for (int k = 0; k < nm; ++k) {
+      if (rot[k] == 0) mats[k]->done = true;
+      all = all && mats[k]->done;
+    }
+    if (all) break;
+  }
+}
+}  // namespace
+
+void jacobi_svd(const double* a, int m, int n, double* u, double* s, double* v, int threads) {
+  if (m < n || n < 1) throw InvalidArgument("jacobi_svd: need m >= n >= 1");
+  JacobiState st(a, m, n);
+  if (n < kJacobiParallelMin) {
+    st.cyclic_sweeps();
+  } else {
+    std::vector<JacobiState*> mats{&st};
+    jacobi_sweeps(mats, threads);
+  }
+  st.finish(u, s, v);
+}
+
+// The SVDs of two matrices of the same shape in one batch (half as many synchronisations per rotation).
+void jacobi_svd_pair(const double* a0, const double* a1, int m, int n, double* u0, double* s0, double* v0, double* u1,
+                     double* s1, double* v1, int threads) {
+  if (m < n || n < 1) throw InvalidArgument("jacobi_svd: need m >= n >= 1");
+  JacobiState x(a0, m, n), y(a1, m, n);
+  std::vector<JacobiState*> mats{&x, &y};
+  jacobi_sweeps(mats, threads);
+  x.finish(u0, s0, v0);
+  y.finish(u1, s1, v1);
 }
 
 uint64_t operator_fingerprint(int p, double ai, double ao, double cutoff, double side) {
@@ -127,11 +212,9 @@ uint64_t operator_fingerprint(int p, double ai, double ao, double cutoff, double
 namespace {
 
 // Truncated SVD of the check<-equivalent kernel matrix; keeps sigma_i >= cutoff*sigma_max.
-void factor_pinv(const std::vector<double>& k, int nc, int ne, double cutoff, int& rank,
-                 std::vector<double>& uk, std::vector<double>& sk, std::vector<double>& vk,
-                 const char* name) {
-  std::vector<double> u(size_t(nc) * ne), s(ne), v(size_t(ne) * ne);
-  jacobi_svd(k.data(), nc, ne, u.data(), s.data(), v.data());
+void truncate_svd(const std::vector<double>& u, const std::vector<double>& s, const std::vector<double>& v, int nc,
+                  int ne, double cutoff, int& rank, std::vector<double>& uk, std::vector<double>& sk,
+                  std::vector<double>& vk, const char* name) {
   if (!(s[0] > 0.0) || !std::isfinite(s[0]))
     throw NumericalError(std::string("precompute: singular/non-finite ") + name);
   int r = 0;
@@ -200,40 +283,49 @@ void precompute(Operators& ops, int p, double ai, double ao, double cutoff, doub
   std::vector<double> kup(size_t(nc) * ne), kdn(size_t(nc) * ne);
   kernel_matrix(ue.data(), ne, uc.data(), nc, kup.data());
   kernel_matrix(de.data(), ne, dc.data(), nc, kdn.data());
-  // The two truncated SVDs (serial Jacobi sweeps, ~45 ms each at p = 6) and the 316 M2L kernel matrices
-  // are independent: one dynamic loop runs them side by side (jobs 0, 1 = the SVDs).  Each job owns its
-  // outputs, so the result does not depend on the thread count.
   // M2L kernel matrices K_t: source up-equivalent (alpha_in) at offset t * (2 h2) ->
   // target down-check (alpha_in), both at the reference level.
   const auto& tvs = transfer_vector_table();
   ops.m2l.assign(tvs.size() * size_t(nc) * ne, 0.0);
-  std::exception_ptr svd_err[2];
-  auto first_job = [&](size_t job) {
-    if (job < 2) {
-      try {
-        if (job == 0)
-          factor_pinv(kup, nc, ne, cutoff, ops.uc2e_rank, ops.uc2e_u, ops.uc2e_s, ops.uc2e_v, "uc2e");
-        else
-          factor_pinv(kdn, nc, ne, cutoff, ops.dc2e_rank, ops.dc2e_u, ops.dc2e_s, ops.dc2e_v, "dc2e");
-      } catch (...) {
-        svd_err[job] = std::current_exception();
-      }
-      return;
-    }
-    const size_t t = job - 2;
+  auto m2l_matrix = [&](size_t t) {
     const double sc[3] = {2.0 * h2 * tvs[t][0], 2.0 * h2 * tvs[t][1], 2.0 * h2 * tvs[t][2]};
     const auto sue = scaled(ops.surface, sc, ai * h2);
     kernel_matrix(sue.data(), ne, dc.data(), nc, &ops.m2l[t * size_t(nc) * ne]);
   };
-  const long long n_first = 2 + static_cast<long long>(tvs.size());
-  if (threads <= 1) {
-    for (long long j = 0; j < n_first; ++j) first_job(size_t(j));
-  } else {
+  std::vector<double> u0(size_t(nc) * ne), s0(ne), v0(size_t(ne) * ne), u1(u0.size()), s1(ne), v1(v0.size());
+  if (ne < kJacobiParallelMin) {
+    // small systems (p <= 7): the two serial SVDs (~45 ms each at p = 6) and the 316 M2L matrices are
+    // independent jobs of one dynamic loop (jobs 0, 1 = the SVDs); each job owns its outputs
+    std::exception_ptr svd_err[2];
+    auto first_job = [&](size_t job) {
+      if (job >= 2) return m2l_matrix(job - 2);
+      try {
+        if (job == 0)
+          jacobi_svd(kup.data(), nc, ne, u0.data(), s0.data(), v0.data(), 1);
+        else
+          jacobi_svd(kdn.data(), nc, ne, u1.data(), s1.data(), v1.data(), 1);
+      } catch (...) {
+        svd_err[job] = std::current_exception();
+      }
+    };
+    const long long n_first = 2 + static_cast<long long>(tvs.size());
+    if (threads <= 1) {
+      for (long long j = 0; j < n_first; ++j) first_job(size_t(j));
+    } else {
 #pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
-    for (long long j = 0; j < n_first; ++j) first_job(size_t(j));
+      for (long long j = 0; j < n_first; ++j) first_job(size_t(j));
+    }
+    for (auto& e : svd_err)
+      if (e) std::rethrow_exception(e);
+  } else {
+    // large systems (p >= 8): one Jacobi batch of both matrices, parallel over the disjoint column pairs of
+    // each round-robin round; then the M2L matrices
+    jacobi_svd_pair(kup.data(), kdn.data(), nc, ne, u0.data(), s0.data(), v0.data(), u1.data(), s1.data(), v1.data(),
+                    threads);
+    parallel_for(tvs.size(), threads, m2l_matrix);
   }
-  for (auto& e : svd_err)
-    if (e) std::rethrow_exception(e);
+  truncate_svd(u0, s0, v0, nc, ne, cutoff, ops.uc2e_rank, ops.uc2e_u, ops.uc2e_s, ops.uc2e_v, "uc2e");
+  truncate_svd(u1, s1, v1, nc, ne, cutoff, ops.dc2e_rank, ops.dc2e_u, ops.dc2e_s, ops.dc2e_v, "dc2e");
 
   // M2M_o = uc2e_inv(l) K(child ue(l+1) -> parent uc(l)); L2L_o = dc2e_inv(l+1) K(parent de(l) -> child dc(l+1)).
   // Both level-invariant; built with parent at level 2, child at 3.

@@ -26,7 +26,8 @@ int surface_count(int p);
 std::vector<double> surface_grid(int p);
 void kernel_matrix(const double* src, int64_t m, const double* tgt, int64_t k, double* out);
 // One-sided Jacobi SVD, a: m x n row-major (m >= n). Singular values descending.
-void jacobi_svd(const double* a, int m, int n, double* u, double* s, double* v);
+// threads > 1: the disjoint column pairs of each round-robin round rotate in parallel (same result for any count)
+void jacobi_svd(const double* a, int m, int n, double* u, double* s, double* v, int threads = 1);
 uint64_t operator_fingerprint(int p, double ai, double ao, double cutoff, double side);
 void precompute(Operators& ops, int p, double alpha_inner, double alpha_outer, double svd_cutoff,
                 double domain_side, int threads);

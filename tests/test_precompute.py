@@ -18,13 +18,24 @@ def ops6():
 
 def test_jacobi_svd_matches_lapack():
     rng = np.random.default_rng(0)
-    for shape in ((40, 40), (60, 30)):
+    # (300, 280) and the odd (270, 257) take the parallel round-robin order (n >= 256; a bye column when odd)
+    for shape in ((40, 40), (60, 30), (300, 280), (270, 257)):
         a = rng.standard_normal(shape)
         u, s, v = host.svd(a)
         s_np = np.linalg.svd(a, compute_uv=False)
         assert np.allclose(s, s_np, rtol=1e-13, atol=1e-13 * s_np[0])
         assert np.allclose(u @ np.diag(s) @ v.T, a, atol=1e-12)
         assert np.allclose(v.T @ v, np.eye(shape[1]), atol=1e-12)
+
+
+def test_precompute_independent_of_thread_count():
+    """Operators do not depend on the host thread count: p = 6 (serial cyclic SVDs next to the M2L
+    matrices) and p = 8 (parallel round-robin Jacobi batch)."""
+    for p in (6, 8):
+        a = host.Operators(p=p, domain_side=1.0, threads=1)
+        b = host.Operators(p=p, domain_side=1.0, threads=3)
+        for x, y in zip(a.uc2e + a.dc2e + (a.m2m, a.l2l, a.m2l), b.uc2e + b.dc2e + (b.m2m, b.l2l, b.m2l)):
+            assert np.array_equal(x, y), p
 
 
 def test_svd_of_check_matrix(ops6):
