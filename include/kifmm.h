@@ -211,7 +211,8 @@ typedef struct kifmm_gpu_options {
   int32_t cut_level;      /* partition alignment level for world_size > 1 (0 = auto, kifmm_halo_plan) */
   const void* nccl_unique_id; /* 128 bytes from kifmm_gpu_nccl_unique_id() on rank 0 */
   int32_t m2l_backend;    /* 0 auto, 1 SIMT (fp32) / DMMA (fp64), 2 tcgen05 (fp32 only; n_e padded to 64,
-                             128 or 160, i.e. p = 4, 5, 6 -- the fp32 default there): kind::f16
+                             128, 160 or 224, i.e. p = 4..7 -- the fp32 default there; at p = 7 the M2L
+                             alone, solves / M2M / L2L stay on the SIMT GEMM): kind::f16
                              3-term fp16 split by default -- reported as 2 -- or kind::tf32 3xTF32 with
                              KIFMM_TC_KIND=tf32 (p = 6 only) -- reported as 3; 4 tcgen05 kind::i8 (fp64 only, n_e
                              padded to 160 or 224, i.e. p = 6, 7): Ozaki scheme, 8 int8 digit slices per

@@ -74,8 +74,15 @@ constexpr int THREADS = 512;
 #define KIFMM_TC_LOW_REGS 48
 #define KIFMM_TC_EPI_REGS 112
 #endif
-constexpr int LAUNCH_REGS = KIFMM_TC_LAUNCH_REGS, LOW_REGS = KIFMM_TC_LOW_REGS, EPI_REGS = KIFMM_TC_EPI_REGS;
-static_assert(4 * 32 * LOW_REGS * 2 + 8 * 32 * EPI_REGS <= THREADS * LAUNCH_REGS, "setmaxnreg budget");
+// Row width 224 (p = 7, M2L pair kernel only): an epilogue thread keeps 112 fp32 sums, so that instantiation
+// launches with 104 registers per thread and rebalances to 40 / 168 (one near-field side block fits next to it).
+template <int NP>
+struct Regs {
+  static constexpr int LAUNCH = NP > 160 ? 104 : KIFMM_TC_LAUNCH_REGS;
+  static constexpr int LOW = NP > 160 ? 40 : KIFMM_TC_LOW_REGS;
+  static constexpr int EPI = NP > 160 ? 168 : KIFMM_TC_EPI_REGS;
+  static_assert(4 * 32 * LOW * 2 + 8 * 32 * EPI <= THREADS * LAUNCH, "setmaxnreg budget");
+};
 constexpr uint32_t TMEM_COLS = 512;  // NACC 160-column accumulators at 0, 160, 320
 constexpr int NACC = 3;              // accumulator buffers: the MMA runs up to two taps ahead of the epilogue
 // The tensor-core accumulator rounds toward zero after every MMA (1 ulp per K step, measured), a bias that
@@ -87,7 +94,7 @@ constexpr int NACC = 3;              // accumulator buffers: the MMA runs up to 
 // one accumulator per tap and three sets in flight (its taps are summed in fp32 per tap anyway).
 template <int NP, bool PAIR>
 struct Acc {
-  static constexpr int NSET = PAIR ? NACC : 1;         // accumulator sets in TMEM
+  static constexpr int NSET = PAIR ? (NACC * NP <= int(TMEM_COLS) ? NACC : 2) : 1;  // accumulator sets in TMEM
   static constexpr int SET_COLS = PAIR ? NP : 3 * NP;  // columns per set
 };
 
@@ -340,7 +347,7 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map
 }
 
 template <int NP, bool PAIR, int ROWB, int ES>
-__global__ void __maxnreg__(LAUNCH_REGS)
+__global__ void __maxnreg__(Regs<NP>::LAUNCH)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tm_khi, const __grid_constant__ CUtensorMap tm_klo,
                   const void* __restrict__ m_hi, const void* __restrict__ m_lo, const Item* __restrict__ items,
                   const int* __restrict__ sched, const int* __restrict__ seg_mat, const int* __restrict__ seg_in, int zero_row,
@@ -438,7 +445,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
   }
 #endif
   if (warp >= EPI_WARP0) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Regs<NP>::EPI));
 
     // ---------------- epilogue: per-tap promotion; warp w reads TMEM lanes 32*(w%4).. (its rows)
     //                  and columns [h*80, h*80+80), h = (w-6)/4
@@ -705,7 +712,7 @@ __global__ void __maxnreg__(LAUNCH_REGS)
       }
     }
   } else {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(LOW_REGS));
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Regs<NP>::LOW));
     if (warp == 0) {
       // ---------------- B producer: this CTA's rows of K_t hi/lo (TMA tile, swizzled); the whole warp
       //                  walks the loop (uniform values), one elected lane issues
@@ -1130,8 +1137,21 @@ inline bool m2l_tc_available() {
   return major == 10 && minor == 0;
 }
 
-// Row widths (n_e padded to a multiple of 32) the tcgen05 kernels are instantiated for: p = 4, 5, 6.
+// Row widths (n_e padded to a multiple of 32) the tcgen05 kernels are instantiated for: p = 4, 5, 6 (M2L and
+// the GEMM chain), and p = 7 (224) for the M2L 2-CTA pair kernel alone -- three 224-column accumulators of the
+// single-CTA GEMM exceed the 512 TMEM columns.
 inline bool tc_np_supported(int np) { return np == 64 || np == 128 || np == 160; }
+inline bool tc_m2l_np_supported(int np) { return tc_np_supported(np) || np == 224; }
+template <class F>
+inline void tc_dispatch_m2l_np(int np, F&& f) {
+  switch (np) {
+    case 64: f(std::integral_constant<int, 64>{}); break;
+    case 128: f(std::integral_constant<int, 128>{}); break;
+    case 160: f(std::integral_constant<int, 160>{}); break;
+    case 224: f(std::integral_constant<int, 224>{}); break;
+    default: throw InvalidArgument("tcgen05 M2L: row width (n_e padded to 32) must be 64, 128, 160 or 224 (p = 4..7)");
+  }
+}
 template <class F>
 inline void tc_dispatch_np(int np, F&& f) {
   switch (np) {
@@ -1327,14 +1347,15 @@ struct M2LTcPlan {
   template <class TreeView, class OpsView>
   void build(const TreeView& t, const std::vector<std::vector<int64_t>>& groups, int width, const OpsView& ops,
              size_t* total, bool own_split = true) {
-    if (!tc_np_supported(width))
-      throw InvalidArgument("tcgen05 M2L: instantiated for p = 4, 5, 6 (n_e padded to 64, 128, 160)");
+    if (!tc_m2l_np_supported(width))
+      throw InvalidArgument("tcgen05 M2L: instantiated for p = 4, 5, 6, 7 (n_e padded to 64, 128, 160, 224)");
     np = width;
     // KIFMM_TC_KIND=tf32: the kind::tf32 variant (reported as m2l_backend 3), instantiated for p = 6 only
     if (const char* e = std::getenv("KIFMM_TC_KIND")) f16 = std::string(e) != "tf32" || np != 160;
     nn = size_t(t.n_nodes);
     pair = nn >= 20000;  // 2-CTA pays off once there are enough 256-row tiles (measured at 1e5 / 1e6 points)
     if (const char* e = std::getenv("KIFMM_TC_PAIR")) pair = std::atoi(e) != 0;
+    if (width > 160) pair = true;  // row width 224: only the 2-CTA pair kernel is instantiated
     rows = pair ? 2 * tc::BM : tc::BM;
     // ---- tiles (rows same-class targets) and their tap segments
     std::vector<int> tile_out, seg_mat, seg_in, tile_seg{0};
@@ -1540,16 +1561,17 @@ struct M2LTcPlan {
       }
       encode(reinterpret_cast<EncodeFn>(fn), &tm_khi16, d_khi16, np, uint64_t(nt) * np, brow, 64, 2);
       encode(reinterpret_cast<EncodeFn>(fn), &tm_klo16, d_klo16, np, uint64_t(nt) * np, brow, 64, 2);
-      tc_dispatch_np(np, [&](auto w) {
+      tc_dispatch_m2l_np(np, [&](auto w) {
         constexpr int W = decltype(w)::value;
-        if (pair)
+        if (pair) {
           KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<W, true, 64, 2>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           tc::Cfg<W, true, 64, 2>::SMEM_BYTES));
-        else
+        } else if constexpr (W <= 160) {
           KIFMM_CUDA(cudaFuncSetAttribute(tc::m2l_tc_kernel<W, false, 64, 2>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           tc::Cfg<W, false, 64, 2>::SMEM_BYTES));
+        }
       });
     }
   }
@@ -1605,7 +1627,7 @@ struct M2LTcPlan {
     if (!n_items) return;
     if (!f16 || sp.rows != int(nn)) throw InvalidArgument("M2L presplit: kind::f16 plan over all nodes required");
     if (sp.np != np) throw InvalidArgument("M2L presplit: row width mismatch");
-    tc_dispatch_np(np, [&](auto w) {
+    tc_dispatch_np(np, [&](auto w) {  // presplit operands come from the GEMM chain: widths <= 160
       if (pair)
         run_kernel<decltype(w)::value, true, 64, 2>(s, sp.hi, sp.lo, sp.un);
       else
@@ -1628,15 +1650,14 @@ struct M2LTcPlan {
     if (width != np) throw InvalidArgument("M2L launch: row width mismatch");
     if (f16 && !d_mhi16) throw InvalidArgument("M2L launch: plan was built without its own split buffers");
     if (f16) {
-      tc_dispatch_np(np, [&](auto w) {
+      tc_dispatch_m2l_np(np, [&](auto w) {
         constexpr int W = decltype(w)::value;
         tc::split_f16_rows_kernel<W><<<unsigned((nn + 8) / 8), 256, 0, s>>>(M, 0, int(nn) + 1, int(nn), d_mhi16, d_mlo16,
                                                                             d_unscale);
         KIFMM_LAUNCH_CHECK();
-        if (pair)
-          run_kernel<W, true, 64, 2>(s);
-        else
-          run_kernel<W, false, 64, 2>(s);
+        if (pair) run_kernel<W, true, 64, 2>(s);
+        if constexpr (W <= 160)
+          if (!pair) run_kernel<W, false, 64, 2>(s);
         tc::m2l_tc_reduce_kernel<W><<<dim3(n_tiles, rows / 16), 16 * (W / 4), 0, s>>>(d_partial, d_tile_out, d_tile_slot,
                                                                                     rows, check);
       });

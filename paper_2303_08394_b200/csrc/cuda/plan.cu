@@ -1033,7 +1033,7 @@ void kifmm_gpu_plan::build(const kifmm_gpu_options& o, const kifmm_tree_view& t,
     for (auto& kv : groups) m2l_groups.push_back(kv.second);
   }
   m2l_backend = 1;
-  if (o.m2l_backend == 2 || (o.m2l_backend == 0 && precision == 32 && tc_np_supported(np) && m2l_tc_available())) {
+  if (o.m2l_backend == 2 || (o.m2l_backend == 0 && precision == 32 && tc_m2l_np_supported(np) && m2l_tc_available())) {
     if (precision != 32) throw InvalidArgument("gpu: tcgen05 3xTF32 M2L is an fp32 path");
     m2l_tc.build(t, m2l_groups, np, ops, &dev_bytes, /*own_split=*/!gemm_tc);
     m2l_backend = m2l_tc.f16 ? 2 : 3;  // 2: kind::f16 3-term split, 3: kind::tf32 3xTF32

@@ -32,7 +32,7 @@ class FmmConfig:
     precision: int = 32              # 32 or 64
     gradient: bool = False
     device: int = 0
-    m2l_backend: int = 0             # 0 auto, 1 SIMT / fp64 DMMA, 2 tcgen05 (fp32, p = 4, 5, 6: fp16 3-term split; tf32 via KIFMM_TC_KIND),
+    m2l_backend: int = 0             # 0 auto, 1 SIMT / fp64 DMMA, 2 tcgen05 (fp32, p = 4..7: fp16 3-term split; tf32 via KIFMM_TC_KIND),
     #                                  4 tcgen05 int8 Ozaki scheme (fp64, p = 6, 7; the fp64 default there)
     use_graph: bool = True
     rank: int = 0

@@ -91,9 +91,11 @@ def test_fp32_p7_with_fp32_cutoff(require_gpu, kind, n, n_crit):
     (svd_cutoff 1e-12, an fp64 setting) keeps singular values down to 1e-11 of the largest, and the
     fp32 rounding of the resulting densities costs 1e-4; with svd_cutoff = 1e-8 the same plan agrees
     with the oracle (same operators) to < 1e-6 and is closer to direct summation than p = 6
-    (tools/exp/r02_p7cut.py: 3.7e-7 / 6.6e-7 against 1.3e-6 / 2.9e-6)."""
+    (tools/exp/r02_p7cut.py: 3.7e-7 / 6.6e-7 against 1.3e-6 / 2.9e-6 with the SIMT M2L; 1.1e-6 / 7.6e-7
+    with the tcgen05 M2L, tools/exp/r02_p7tc.py)."""
     pos, q = generators.sample(kind, n, seed=7, charges="signed", fp32=True)
     with fmm.Fmm(pos, fmm.FmmConfig(p=7, n_crit=n_crit, precision=32, svd_cutoff=1e-8, gradient=True)) as f:
+        assert f.info()["m2l_backend"] == 2  # tcgen05 M2L, row width 224 (2-CTA pair kernel); SIMT solves / M2M / L2L
         pot, grad, _ = f.evaluate(q)
         ref, gref = _ref(f, q, True)
     assert fmm.relative_error(pot, ref) <= 2e-6
