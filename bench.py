@@ -63,6 +63,13 @@ def parse():
     return ap.parse_args()
 
 
+def metric_name(config):
+    """BASELINE.json's metric for the configuration it is quoted on (config 2); other configs say which."""
+    if config == CONFIG:
+        return "FMM evaluate points/sec at N=1M p=6"
+    return f"FMM evaluate points/sec (BASELINE config {config})"
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -209,7 +216,7 @@ def run_reference(args):
             f"({tree.n_leaves} leaves) per step, {threads} OpenMP threads; mean of {steps} steps after {warm} "
             f"warm-up (std {float(np.std(times)) * 1e3:.1f} ms); tree/lists/operators built in a child process")
     line = {
-        "impl": "reference", "metric": "FMM evaluate points/sec at N=1M p=6", "value": value, "unit": "points/s",
+        "impl": "reference", "metric": metric_name(args.config), "value": value, "unit": "points/s",
         "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"BASELINE config {args.config}: N={tree.n} {c['kind']}, p={c['p']}, "
@@ -452,7 +459,7 @@ def main():
                          f"mean of 3 (std {float(np.std(ts)) * 1e3:.1f} ms)", **cpu_info(), "omp_max_threads": th}
 
     line = {
-        "metric": "FMM evaluate points/sec at N=1M p=6", "value": value, "unit": "points/s", "n_gpus": world,
+        "metric": metric_name(args.config), "value": value, "unit": "points/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if prec == 32 else "f64", "data": "synthetic",
         "config": {"workload": f"BASELINE config {args.config}: N={n} {c['kind']} (seed 0), p={c['p']}, "
