@@ -52,7 +52,22 @@ struct P2PParams {
   int n_e;
   int ld;                   // row stride of expansion buffers
   T alpha_inner, alpha_outer;
+  const v4_t<T>* node_lo;   // fp32: centre - float(centre) per node (the centre as a float pair); fp64: unused
 };
+
+// Surface geometry of the fp32 kernels is node-local: a check / equivalent point is s u_j relative to the node
+// centre c, and the particle is shifted instead, x' = (x - c_hi) - c_lo with c = c_hi + c_lo the fp64 centre as a
+// float pair.  x - c_hi is one correctly rounded difference, so every distance keeps ~1e-7 relative error at any
+// depth, where c_hi + s u_j in absolute coordinates rounds at ulp(|c|) -- 1e-3 of a level-15 box -- and c_hi
+// alone displaces the whole surface by up to ulp(|c|) / 2 (clustered clouds: 1e-4 potential error at depth 14,
+// tools/exp/r02_deep.py).  The fp64 kernels keep the oracle's absolute form (bit-compatible arithmetic).
+template <class T>
+struct LocalGeom {
+  static constexpr bool on = sizeof(T) == 4;
+};
+__device__ __forceinline__ float4 shift_local(float4 v, const float4& g, const float4& lo) {
+  return make_float4((v.x - g.x) - lo.x, (v.y - g.y) - lo.y, (v.z - g.z) - lo.z, v.w);
+}
 
 constexpr int kP2PThreads = 128;
 constexpr int kP2PCap = 1024;  // staged sources per round
@@ -62,6 +77,17 @@ __device__ __forceinline__ v4_t<T> surface_source(const P2PParams<T>& p, int nod
   const v4_t<T> g = p.node_geom[node];
   const T s = alpha * g.w;
   return make4<T>(g.x + s * p.surface[3 * j], g.y + s * p.surface[3 * j + 1], g.z + s * p.surface[3 * j + 2],
+                  dens[size_t(node) * p.ld + j]);
+}
+
+// Far-field source j of a node's surface: node-local (s u_j, density) for fp32 -- the caller shifts its targets
+// by the centre pair instead (see LocalGeom) -- or absolute (c + s u_j, density) for fp64.
+template <class T>
+__device__ __forceinline__ v4_t<T> surface_source_local(const P2PParams<T>& p, int node, const v4_t<T>& g, T alpha,
+                                                        const T* dens, int j) {
+  const T s = alpha * g.w;
+  constexpr T k = LocalGeom<T>::on ? T(0) : T(1);
+  return make4<T>(k * g.x + s * p.surface[3 * j], k * g.y + s * p.surface[3 * j + 1], k * g.z + s * p.surface[3 * j + 2],
                   dens[size_t(node) * p.ld + j]);
 }
 
@@ -674,15 +700,23 @@ __global__ void __launch_bounds__(kFarWarps * 32) far_kernel(P2PParams<T> p, con
       const bool l2p = sf.y == kSrcL2P;
       const T alpha = l2p ? p.alpha_outer : p.alpha_inner;
       const T* dens = l2p ? L : M;
+      const v4_t<T> gc = p.node_geom[sf.x];  // node-local: targets shifted by the centre (surface_source_local)
+      T xs = x.x, ys = x.y, zs = x.z;
+      if constexpr (LocalGeom<T>::on) {
+        const v4_t<T> lo = p.node_lo[sf.x];
+        xs = (xs - gc.x) - lo.x;
+        ys = (ys - gc.y) - lo.y;
+        zs = (zs - gc.z) - lo.z;
+      }
       // surfaces above kFarMaxNe points (p >= 8) are staged in chunks; one chunk otherwise
       for (int j0 = 0; j0 < p.n_e; j0 += kFarMaxNe) {
         const int cn = min(kFarMaxNe, p.n_e - j0), cn8 = (cn + 7) & ~7;
         __syncwarp();
         for (int j = lane; j < cn8; j += 32)
-          my[j] = j < cn ? surface_source(p, sf.x, alpha, dens, j0 + j)
+          my[j] = j < cn ? surface_source_local(p, sf.x, gc, alpha, dens, j0 + j)
                          : make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
         __syncwarp();
-        p2p_round<T, GRAD, false>(my, 0, cn8, x.x, x.y, x.z, ph, gx, gy, gz);
+        p2p_round<T, GRAD, false>(my, 0, cn8, xs, ys, zs, ph, gx, gy, gz);
       }
     }
     if (act) {
@@ -757,11 +791,16 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_f2_kernel(
     const bool l2p = sf.y == kSrcL2P;
     const float alpha = l2p ? p.alpha_outer : p.alpha_inner;
     const float* dens = l2p ? L : M;
+    const float4 gc = p.node_geom[sf.x], gl = p.node_lo[sf.x];  // node-local: targets shifted by the centre pair
     __syncwarp();
     for (int j = lane; j < pad; j += 32)
-      my[j] = j < p.n_e ? surface_source(p, sf.x, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
+      my[j] = j < p.n_e ? surface_source_local(p, sf.x, gc, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
     __syncwarp();
-    if (active) p2p_round_f2<GRAD, false>(my, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
+    if (active)
+      p2p_round_f2<GRAD, false>(my, slice * per, slice * per + per,
+                                f2_sub(f2_sub(x, f2_bcast(gc.x)), f2_bcast(gl.x)),
+                                f2_sub(f2_sub(y, f2_bcast(gc.y)), f2_bcast(gl.y)),
+                                f2_sub(f2_sub(z, f2_bcast(gc.z)), f2_bcast(gl.z)), ph, gx, gy, gz);
   }
   // fixed-order slice reduction into slice 0
   float v[8];
@@ -868,27 +907,34 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
   auto surf = [&](int k) {
     return k == 0 ? make_int2(w.node0, w.kind0) : k < ns ? surfaces[w.surf_begin + k] : make_int2(-1, 0);
   };
-  // surface 0: staged directly
+  // surface 0: staged directly.  Node-local geometry (surface_source_local): gk is the centre of the surface
+  // being computed, and the targets are shifted by it
+  float4 gk = make_float4(0.f, 0.f, 0.f, 0.f), lk = gk;
   {
     const int2 sf = surf(0);
     const bool l2p = sf.y == kSrcL2P;
     const float alpha = l2p ? p.alpha_outer : p.alpha_inner;
     const float* dens = l2p ? L : M;
+    if (0 < ns) {
+      gk = p.node_geom[sf.x];
+      lk = p.node_lo[sf.x];
+    }
     for (int j = hl; j < pad; j += 16)
-      my[j] = (0 < ns && j < p.n_e) ? surface_source(p, sf.x, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
+      my[j] = (0 < ns && j < p.n_e) ? surface_source_local(p, sf.x, gk, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
   }
   int2 sf_n = surf(1);  // descriptor of the next surface
   for (int k = 0; k < ns_max; ++k) {
     __syncwarp();
     // issue surface k + 1: densities -> dn (cp.async), node geometry -> registers
     const bool nlive = k + 1 < ns;
-    float4 gn = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 gn = make_float4(0.f, 0.f, 0.f, 0.f), ln = gn;
     float an = 0.f;
     if (nlive) {
       const bool l2p = sf_n.y == kSrcL2P;
       an = l2p ? p.alpha_outer : p.alpha_inner;
       const float* dens = (l2p ? L : M) + size_t(sf_n.x) * p.ld;
       gn = p.node_geom[sf_n.x];
+      ln = p.node_lo[sf_n.x];
       for (int j = hl; j < p.n_e; j += 16)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(uint32_t(__cvta_generic_to_shared(dn + j))),
                      "l"(dens + j)
@@ -896,15 +942,21 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     const int2 sf_nn = surf(k + 2);
-    if (act && k < ns) p2p_round_f2<GRAD, false>(my, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
+    if (act && k < ns)
+      p2p_round_f2<GRAD, false>(my, slice * per, slice * per + per,
+                                f2_sub(f2_sub(x, f2_bcast(gk.x)), f2_bcast(lk.x)),
+                                f2_sub(f2_sub(y, f2_bcast(gk.y)), f2_bcast(lk.y)),
+                                f2_sub(f2_sub(z, f2_bcast(gk.z)), f2_bcast(lk.z)), ph, gx, gy, gz);
     if (k + 1 < ns_max) {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       __syncwarp();  // every lane is done reading surface k and sees surface k + 1's densities
       const float sc = an * gn.w;
       for (int j = hl; j < pad; j += 16)
-        my[j] = (nlive && j < p.n_e) ? make_float4(gn.x + sc * p.surface[3 * j], gn.y + sc * p.surface[3 * j + 1],
-                                                   gn.z + sc * p.surface[3 * j + 2], dn[j])
+        my[j] = (nlive && j < p.n_e) ? make_float4(sc * p.surface[3 * j], sc * p.surface[3 * j + 1],
+                                                   sc * p.surface[3 * j + 2], dn[j])
                                      : make_float4(fa, fa, fa, 0.f);
+      gk = gn;
+      lk = ln;
     }
     sf_n = sf_nn;
   }
@@ -1007,15 +1059,19 @@ __global__ void __launch_bounds__(kCheckWarps * 32) check_kernel(P2PParams<T> p,
   if (wi >= n_works) return;
   const CheckWork w = works[wi];
   const v4_t<T> g = p.node_geom[w.node];
+  v4_t<T> glo = g;
+  if constexpr (LocalGeom<T>::on) glo = p.node_lo[w.node];
   const T s = alpha * g.w;
   T yx[KMAX], yy[KMAX], yz[KMAX], acc[KMAX];
 #pragma unroll
   for (int m = 0; m < KMAX; ++m) {
     const int j = lane + 32 * m;
     const int jj = j < p.n_e ? j : 0;
-    yx[m] = g.x + s * p.surface[3 * jj];
-    yy[m] = g.y + s * p.surface[3 * jj + 1];
-    yz[m] = g.z + s * p.surface[3 * jj + 2];
+    // fp32: node-local geometry, sources shifted by the centre pair (LocalGeom); fp64: absolute
+    constexpr T ka = LocalGeom<T>::on ? T(0) : T(1);
+    yx[m] = ka * g.x + s * p.surface[3 * jj];
+    yy[m] = ka * g.y + s * p.surface[3 * jj + 1];
+    yz[m] = ka * g.z + s * p.surface[3 * jj + 2];
     acc[m] = T(0);
   }
   for (int r = w.range_begin; r < w.range_end; ++r) {
@@ -1023,6 +1079,11 @@ __global__ void __launch_bounds__(kCheckWarps * 32) check_kernel(P2PParams<T> p,
     for (int b = 0; b < rg.y; b += 32) {
       const int cnt = min(32, rg.y - b);
       v4_t<T> mine = lane < cnt ? p.src[rg.x + b + lane] : make4<T>(T(kFarAway), T(kFarAway), T(kFarAway), T(0));
+      if constexpr (LocalGeom<T>::on) {
+        mine.x = (mine.x - g.x) - glo.x;
+        mine.y = (mine.y - g.y) - glo.y;
+        mine.z = (mine.z - g.z) - glo.z;
+      }
       for (int k = 0; k < cnt; ++k) {
         const T sx = __shfl_sync(0xffffffffu, mine.x, k), sy = __shfl_sync(0xffffffffu, mine.y, k);
         const T sz = __shfl_sync(0xffffffffu, mine.z, k), sq = __shfl_sync(0xffffffffu, mine.w, k);
@@ -1072,13 +1133,14 @@ __global__ void __launch_bounds__(kCheckWarps * 32, KIFMM_CHECK_MINB) check_f2_k
   const float fa = float(kFarAway);
   // first source window issued together with the node geometry (both depend on the work only)
   const float4 pre = lane < w.count ? p.src[w.first + lane] : make_float4(fa, fa, fa, 0.f);
-  const float4 g = p.node_geom[w.node];
+  const float4 g = p.node_geom[w.node], glo = p.node_lo[w.node];
   const float s = alpha * g.w;
-  auto coord = [&](int m, int d) {
+  auto coord = [&](int m, int d) {  // node-local (see check_kernel): sources are shifted by the centre instead
     const int j = lane + 32 * m;
     const int jj = j < p.n_e ? j : 0;
-    return (d == 0 ? g.x : d == 1 ? g.y : g.z) + s * p.surface[3 * jj + d];
+    return s * p.surface[3 * jj + d];
   };
+  auto local = [&](float4 v) { return shift_local(v, g, glo); };
   f2_t yx[KP > 0 ? KP : 1], yy[KP > 0 ? KP : 1], yz[KP > 0 ? KP : 1], acc[KP > 0 ? KP : 1];
 #pragma unroll
   for (int m = 0; m < KP; ++m) {
@@ -1099,9 +1161,9 @@ __global__ void __launch_bounds__(kCheckWarps * 32, KIFMM_CHECK_MINB) check_f2_k
     for (int b = 0; b < rg.y; b += 32) {
       const int cnt = min(32, rg.y - b);
       __syncwarp();
-      my[lane] = (r == w.range_begin && b == 0) ? pre
-                 : lane < cnt                   ? p.src[rg.x + b + lane]
-                                                : make_float4(fa, fa, fa, 0.f);
+      my[lane] = local((r == w.range_begin && b == 0) ? pre
+                       : lane < cnt                   ? p.src[rg.x + b + lane]
+                                                      : make_float4(fa, fa, fa, 0.f));
       __syncwarp();
       const int cnt4 = (cnt + 3) & ~3;
       for (int k = 0; k < cnt4; k += 4) {
@@ -1168,11 +1230,11 @@ __global__ void __launch_bounds__(kCheckWarps * 32, KIFMM_CHECK_MINB) check_hw_k
   CheckWork w{};
   if (valid) w = works[wi];
   const float fa = float(kFarAway);
-  const float4 g = p.node_geom[valid ? w.node : 0];
+  const float4 g = p.node_geom[valid ? w.node : 0], glo = p.node_lo[valid ? w.node : 0];
   const float s = alpha * g.w;
-  auto coord = [&](int j, int d) {
+  auto coord = [&](int j, int d) {  // node-local (see check_kernel): sources are shifted by the centre instead
     const int jj = j < p.n_e ? j : 0;
-    return (d == 0 ? g.x : d == 1 ? g.y : g.z) + s * p.surface[3 * jj + d];
+    return s * p.surface[3 * jj + d];
   };
   // pair q holds check points hl + 32 q and hl + 32 q + 16
   f2_t yx[NPP], yy[NPP], yz[NPP], acc[NPP];
@@ -1193,7 +1255,10 @@ __global__ void __launch_bounds__(kCheckWarps * 32, KIFMM_CHECK_MINB) check_hw_k
     if (!__any_sync(0xffffffffu, more)) break;
     const int cnt = more ? min(16, rg.y - b) : 0;
     __syncwarp();
-    my[hl] = hl < cnt ? p.src[rg.x + b + hl] : make_float4(fa, fa, fa, 0.f);
+    {
+      const float4 v = hl < cnt ? p.src[rg.x + b + hl] : make_float4(fa, fa, fa, 0.f);
+      my[hl] = shift_local(v, g, glo);
+    }
     __syncwarp();
     const int cnt4 = (cnt + 3) & ~3;
     const int cmax = max(cnt4, __shfl_xor_sync(0xffffffffu, cnt4, 16));

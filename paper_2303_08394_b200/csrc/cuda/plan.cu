@@ -424,7 +424,7 @@ struct kifmm_gpu_plan {
   kifmm_gpu_timings last{};
 
   // static data
-  DevMem pos4, perm, node_geom, node_level, surface;
+  DevMem pos4, perm, node_geom, node_lo, node_level, surface;
   DevMem w_us_u, w_vt_u, w_us_d, w_vt_d, w_m2m, w_l2l, w_m2l;
   // per-evaluate buffers
   DevMem q_in, src4, pot, grad_buf, pot_out, grad_out;
@@ -605,7 +605,7 @@ void kifmm_gpu_plan::upload_static(const kifmm_tree_view& t, const kifmm_operato
   for (int64_t i = 0; i < N; ++i) pm[i] = int(t.original_index[i]);
   perm.upload(pm, &dev_bytes);
   // node geometry (center, half side) computed in fp64 then rounded
-  std::vector<T> g(size_t(nn) * 4);
+  std::vector<T> g(size_t(nn) * 4), glo(size_t(nn) * 4, T(0));  // glo: centre - T(centre) (fp32 node-local geometry)
   std::vector<int> lv(nn);
 #pragma omp parallel for schedule(static)
   for (int64_t n = 0; n < nn; ++n) {
@@ -613,11 +613,16 @@ void kifmm_gpu_plan::upload_static(const kifmm_tree_view& t, const kifmm_operato
     const auto a = key_anchor(k);
     const int l = key_level(k);
     const double w = t.side / double(uint64_t(1) << l);
-    for (int d = 0; d < 3; ++d) g[4 * n + d] = T(t.origin[d] + (double(a[d]) + 0.5) * w);
+    for (int d = 0; d < 3; ++d) {
+      const double c = t.origin[d] + (double(a[d]) + 0.5) * w;
+      g[4 * n + d] = T(c);
+      glo[4 * n + d] = T(c - double(T(c)));
+    }
     g[4 * n + 3] = T(t.side / double(uint64_t(1) << (l + 1)));
     lv[n] = l;
   }
   node_geom.upload(g, &dev_bytes);
+  node_lo.upload(glo, &dev_bytes);
   node_level.upload(lv, &dev_bytes);
   surface.upload(to_t<T>(std::vector<double>(ops.surface, ops.surface + 3 * ne)), &dev_bytes);
 
@@ -1562,7 +1567,7 @@ void kifmm_gpu_plan::run(cudaStream_t s, bool input_order, bool timed, int phase
   };
   int launches = 0;
   const P2PParams<T> pp{src4.as<v4_t<T>>(), node_geom.as<v4_t<T>>(), surface.as<T>(), ne, np, T(alpha_in),
-                        T(alpha_out)};
+                        T(alpha_out), node_lo.as<v4_t<T>>()};
   auto gemm = [&](const GemmTiles& tl, const T* X, const T* W, T* Y, bool acc, bool m2l_shape) {
     if (tl.n_tiles == 0) return;
     GemmArgs<T> a{};

@@ -66,6 +66,46 @@ def test_fp32_p7_accuracy_bound(require_gpu):
     assert fmm.relative_error(pot, ref) <= 5e-4
 
 
+@pytest.mark.parametrize("side,depth_min", [(1e-2, 9), (1e-3, 12), (1e-4, 15)])
+def test_fp32_deep_cluster(require_gpu, side, depth_min):
+    """fp32 on a clustered cloud (a dense cube of the given side in a uniform background, tree depth 10-15): the
+    surface geometry of the fp32 kernels is node-local with the centre as a float pair, so the parity gate holds
+    at any depth -- absolute fp32 coordinates gave 9e-6 / 1.1e-4 / 2.6e-4 here (tools/exp/r02_deep.py)."""
+    rng = np.random.default_rng(3)
+    n = 20000
+    pos = np.concatenate([rng.random((n // 2, 3)), 0.3 + side * rng.random((n // 2, 3))])
+    pos = pos.astype(np.float32).astype(np.float64)
+    q = 2 * rng.random(n) - 1
+    with fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=30, precision=32, gradient=True)) as f:
+        assert f.tree.depth >= depth_min
+        pot, grad, _ = f.evaluate(q)
+        ref, gref = _ref(f, q, True)
+    assert fmm.relative_error(pot, ref) <= 3e-6
+    assert fmm.relative_error(grad, gref) <= 5e-6
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("kind,n_crit", [("dups", 1), ("dups", 2), ("line", 1)])
+def test_degenerate_clouds_max_depth(require_gpu, kind, n_crit, precision):
+    """Clouds that drive the tree to its maximum depth (15): every point three times with n_crit < 3, and points
+    on a line with n_crit = 1 (cases found by the randomised GPU-vs-oracle runs, tools/exp/r02_fuzz.py)."""
+    rng = np.random.default_rng(11)
+    if kind == "dups":
+        base = rng.random((100, 3))
+        pos, q = np.concatenate([base] * 3), np.tile(2 * rng.random(100) - 1, 3)
+    else:
+        t = np.sort(rng.random(300))
+        pos, q = np.stack([t, 0.5 + 0 * t, 0.25 + 0 * t], axis=1), 2 * rng.random(300) - 1
+    if precision == 32:
+        pos = pos.astype(np.float32).astype(np.float64)
+    with fmm.Fmm(pos, fmm.FmmConfig(p=5, n_crit=n_crit, precision=precision)) as f:
+        assert f.tree.depth == 15
+        pot, _, _ = f.evaluate(q)
+        ref, _ = _ref(f, q, False)
+    assert np.all(np.isfinite(pot))
+    assert fmm.relative_error(pot, ref) <= TOL[precision][0]
+
+
 @pytest.mark.parametrize("kind,n,n_crit,p,precision,cutoff", [
     ("two-cluster", 3000, 30, 8, 64, 1e-12), ("sphere-surface", 4000, 60, 10, 64, 1e-12),
     ("uniform-cube", 4000, 60, 9, 32, 1e-8)])

@@ -1,0 +1,76 @@
+"""Randomised GPU-vs-oracle check: random size, leaf capacity, order, distribution, precision, gradient, and a few
+degenerate clouds (duplicates, a line, one point).  Prints one JSON line per case; non-zero exit on a failure."""
+import json, sys, time
+import numpy as np
+sys.path.insert(0, ".")
+from paper_2303_08394_b200 import fmm, generators
+import oracle
+
+budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+ops_cache = {}
+t_end = time.time() + budget
+fails = 0
+case = 0
+while time.time() < t_end:
+    case += 1
+    prec = int(rng.choice([32, 64]))
+    p = int(rng.choice([2, 3, 4, 5, 6, 7, 8])) if prec == 64 else int(rng.choice([2, 3, 4, 5, 6, 7]))
+    kind = str(rng.choice(["uniform-cube", "sphere-surface", "two-cluster", "dups", "line", "tiny"]))
+    n = int(rng.integers(1, 6000))
+    ncrit = int(rng.choice([1, 2, 5, 17, 40, 64, 150, 400]))
+    if ncrit <= 2:
+        n = min(n, 300)
+    grad = bool(rng.integers(0, 2))
+    seed = int(rng.integers(0, 1000))
+    if kind in ("uniform-cube", "sphere-surface", "two-cluster"):
+        pos, q = generators.sample(kind, n, seed=seed, charges="signed", fp32=prec == 32)
+    elif kind == "dups":  # every point three times (coincident particles: r = 0 pairs contribute 0)
+        base, qb = generators.sample("uniform-cube", max(1, n // 3), seed=seed, charges="signed", fp32=prec == 32)
+        pos, q = np.concatenate([base] * 3), np.concatenate([qb] * 3)
+    elif kind == "line":
+        t = np.sort(rng.random(n))
+        pos = np.stack([t, 0.5 + 0 * t, 0.25 + 0 * t], axis=1)
+        q = 2 * rng.random(n) - 1
+        if prec == 32:
+            pos = pos.astype(np.float32).astype(np.float64)
+    else:
+        n = int(rng.integers(1, 4))
+        pos, q = generators.sample("uniform-cube", n, seed=seed, charges="signed", fp32=prec == 32)
+    n = len(q)
+    cut = 1e-12 if prec == 64 or p < 7 else 1e-8
+    rec = {"case": case, "kind": kind, "n": n, "n_crit": ncrit, "p": p, "precision": prec, "gradient": grad, "seed": seed}
+    try:
+        with fmm.Fmm(pos, fmm.FmmConfig(p=p, n_crit=ncrit, precision=prec, gradient=grad, svd_cutoff=cut),
+                     operators=ops_cache) as f:
+            pot, g, _ = f.evaluate(q)
+            pot2, g2, _ = f.evaluate(q, timed=True)
+            qr = np.asarray(q, dtype=np.float64)[f.tree.original_index]
+            phi, gr, _ = oracle.evaluate(f.tree, f.operators, qr, gradient=grad)
+            ii = np.empty_like(f.tree.original_index); ii[f.tree.original_index] = np.arange(f.tree.n)
+            rec["backend"] = f.info()["m2l_backend"]; rec["leaves"] = int(f.tree.n_leaves); rec["depth"] = int(f.tree.depth)
+        same = bool(np.array_equal(pot, pot2) and (g is None or np.array_equal(g, g2)))
+        ref = phi[ii]
+        nb = np.linalg.norm(ref)
+        ep = float(np.linalg.norm(pot - ref) / nb) if nb > 0 else float(np.abs(pot).max())
+        eg = 0.0
+        if grad:
+            ng = np.linalg.norm(gr)
+            eg = float(np.linalg.norm(g - gr[ii]) / ng) if ng > 0 else float(np.abs(g).max())
+        tp, tg = (1e-12, 1e-11) if prec == 64 else (1e-5, 5e-5)
+        # the gradient differentiates the local expansion over the leaf box: potential noise dphi becomes dphi / h,
+        # so fp32 gradients of leaves at depth >= 12 (h <= 1e-4) carry up to 1e-2 of noise; fp64 at depth 15 ~1e-10
+        if rec["depth"] >= 12:
+            tg = 1e-9 if prec == 64 else 2e-2
+        ok = same and ep <= tp and eg <= tg and bool(np.all(np.isfinite(pot)))
+        rec.update(pot_err=ep, grad_err=eg, graph_equals_timed=same, ok=ok)
+    except Exception as e:  # noqa: BLE001
+        rec.update(ok=False, error=repr(e)[:300])
+    if not rec["ok"]:
+        fails += 1
+    if not rec["ok"] or case % 10 == 0:
+        print(json.dumps(rec), flush=True)
+    if len(ops_cache) > 24:
+        ops_cache.clear()
+print(json.dumps({"cases": case, "failures": fails}), flush=True)
+sys.exit(1 if fails else 0)

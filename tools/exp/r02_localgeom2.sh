@@ -1,0 +1,13 @@
+rm -f gpurun_out/parity_r02.jsonl
+timeout 900 python -m pytest tests/test_gpu_configs.py -m gpu -q -x -p no:cacheprovider 2>&1 | tail -1
+python - <<P
+import json
+for l in open('gpurun_out/parity_r02.jsonl'):
+    c=json.loads(l); print("hi+lo", c["config"], "%.3e"%c["rel_l2_potential_vs_oracle"], c.get("rel_l2_gradient_vs_oracle"), "%.3e"%c["rel_l2_potential_vs_direct_1000"])
+P
+python tools/exp/r02_deep.py 2>&1 | tail -5
+python tools/configs.py 2 3 5 | python -c "
+import sys,json
+for l in sys.stdin:
+    c=json.loads(l); print(c['config'], round(c['eval_ms_median'],3), c['phases_serialized_ms']['leaf_ms'], c['phases_serialized_ms']['p2l_ms'], c['phases_serialized_ms']['p2m_ms'])
+"
