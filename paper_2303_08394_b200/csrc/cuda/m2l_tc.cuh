@@ -1206,7 +1206,7 @@ struct M2LTcPlan {
   int np = 0;        // row width (n_e padded to 32): 64, 128 or 160
   int rowb = 128;    // bytes per operand row per stage (128: SWIZZLE_128B, 64: SWIZZLE_64B)
   bool f16 = true;  // 3-term fp16 split (kind::f16) with power-of-two row scaling; KIFMM_TC_KIND=tf32 for 3xTF32
-  static constexpr float kKScale = 256.f;
+  float k_scale = 256.f;  // power of two that puts max |K_t| in [2^6, 2^7) before the fp16 split (256 for a unit domain)
   __half *d_khi16 = nullptr, *d_klo16 = nullptr, *d_mhi16 = nullptr, *d_mlo16 = nullptr;
   float* d_unscale = nullptr;
   CUtensorMap tm_khi16{}, tm_klo16{};
@@ -1540,6 +1540,16 @@ struct M2LTcPlan {
       // kind::f16: K_t * 2^8 split into fp16 hi / lo (padded to np x np); multipoles are split per row
       // with a power-of-two scale -- by the caller (launch_presplit) or, with own_split, into this
       // plan's own buffers (launch)
+      // K_t scales with 1 / (domain side): the power-of-two scale follows its largest entry, so the split keeps
+      // its 22 bits for any domain (a fixed 2^8 overflowed fp16 for a domain of side 1e-4 and lost 5 bits at 1e4)
+      double kmax = 0.0;
+      for (size_t i = 0; i < size_t(nt) * nc * ne; ++i) kmax = std::max(kmax, std::fabs(double(ops.m2l[i])));
+      if (kmax > 0.0 && std::isfinite(kmax)) {
+        int ex = 0;
+        std::frexp(kmax, &ex);  // kmax in [2^(ex-1), 2^ex)
+        k_scale = float(std::ldexp(1.0, 7 - ex));
+      }
+      const float kKScale = k_scale;
       std::vector<__half> h16(kn, __float2half_rn(0.f)), l16(kn, __float2half_rn(0.f));
 #pragma omp parallel for schedule(static)
       for (int v = 0; v < nt; ++v)
@@ -1589,7 +1599,7 @@ struct M2LTcPlan {
     const void* ah = ah_ext ? ah_ext : ES == 4 ? static_cast<const void*>(d_mhi) : static_cast<const void*>(d_mhi16);
     const void* al = al_ext ? al_ext : ES == 4 ? static_cast<const void*>(d_mlo) : static_cast<const void*>(d_mlo16);
     const float* un = un_ext ? un_ext : ES == 4 ? nullptr : d_unscale;
-    const float ku = ES == 4 ? 1.f : 1.f / kKScale;
+    const float ku = ES == 4 ? 1.f : 1.f / k_scale;
     if (P) {
       cudaLaunchConfig_t cfg{};
       cudaLaunchAttribute attr[2];

@@ -66,6 +66,24 @@ def test_fp32_p7_accuracy_bound(require_gpu):
     assert fmm.relative_error(pot, ref) <= 5e-4
 
 
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("scale,shift", [(1e-4, 0.0), (1e4, 0.0), (1.0, -1000.0), (1e3, 5e4), (1e-3, 1.0)])
+def test_scaled_and_shifted_domains(require_gpu, scale, shift, precision):
+    """Clouds away from the unit cube.  K_t scales with 1 / side: the fp16 split of the tcgen05 M2L takes its
+    power-of-two scale from the largest operator entry (a fixed 2^8 gave NaN for a domain of side 1e-4 and 1.1e-5
+    at side 1e4, tools/exp/r02_scaleshift.py)."""
+    pos, q = generators.sample("two-cluster", 20000, seed=4, charges="signed")
+    pos = pos * scale + shift
+    if precision == 32:
+        pos = pos.astype(np.float32).astype(np.float64)
+    with fmm.Fmm(pos, fmm.FmmConfig(p=6, n_crit=40, precision=precision, gradient=True)) as f:
+        pot, grad, _ = f.evaluate(q)
+        ref, gref = _ref(f, q, True)
+    tp, tg = (1e-12, 1e-11) if precision == 64 else (2e-6, 2e-6)
+    assert fmm.relative_error(pot, ref) <= tp
+    assert fmm.relative_error(grad, gref) <= tg
+
+
 @pytest.mark.parametrize("side,depth_min", [(1e-2, 9), (1e-3, 12), (1e-4, 15)])
 def test_fp32_deep_cluster(require_gpu, side, depth_min):
     """fp32 on a clustered cloud (a dense cube of the given side in a uniform background, tree depth 10-15): the

@@ -37,9 +37,14 @@ while time.time() < t_end:
     else:
         n = int(rng.integers(1, 4))
         pos, q = generators.sample("uniform-cube", n, seed=seed, charges="signed", fp32=prec == 32)
+    scale = float(rng.choice([1.0, 1.0, 1e-5, 1e-2, 37.0, 1e5]))
+    shift = float(rng.choice([0.0, 0.0, -3.0, 250.0])) * scale
+    pos = pos * scale + shift
+    if prec == 32:
+        pos = pos.astype(np.float32).astype(np.float64)
     n = len(q)
     cut = 1e-12 if prec == 64 or p < 7 else 1e-8
-    rec = {"case": case, "kind": kind, "n": n, "n_crit": ncrit, "p": p, "precision": prec, "gradient": grad, "seed": seed}
+    rec = {"case": case, "kind": kind, "n": n, "n_crit": ncrit, "p": p, "precision": prec, "gradient": grad, "seed": seed, "scale": scale, "shift": shift}
     try:
         with fmm.Fmm(pos, fmm.FmmConfig(p=p, n_crit=ncrit, precision=prec, gradient=grad, svd_cutoff=cut),
                      operators=ops_cache) as f:
@@ -60,8 +65,9 @@ while time.time() < t_end:
         tp, tg = (1e-12, 1e-11) if prec == 64 else (1e-5, 5e-5)
         # the gradient differentiates the local expansion over the leaf box: potential noise dphi becomes dphi / h,
         # so fp32 gradients of leaves at depth >= 12 (h <= 1e-4) carry up to 1e-2 of noise; fp64 at depth 15 ~1e-10
+        # (1e-9 when the cloud sits 250 domain sides away from the origin)
         if rec["depth"] >= 12:
-            tg = 1e-9 if prec == 64 else 2e-2
+            tg = 1e-8 if prec == 64 else 2e-2  # fp64: absolute geometry rounds at ulp(|c|) in the oracle and on the GPU
         ok = same and ep <= tp and eg <= tg and bool(np.all(np.isfinite(pot)))
         rec.update(pot_err=ep, grad_err=eg, graph_equals_timed=same, ok=ok)
     except Exception as e:  # noqa: BLE001
