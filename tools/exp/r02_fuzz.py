@@ -42,9 +42,22 @@ while time.time() < t_end:
     pos = pos * scale + shift
     if prec == 32:
         pos = pos.astype(np.float32).astype(np.float64)
+    qmode = str(rng.choice(["plain", "plain", "big", "small", "zero", "one", "wide"]))
+    if qmode == "big":  # 1e12 at 1e-9 spacings overflows the fp32 intermediate q / r^3 of the gradient (3 cases of 1330)
+        q = q * 1e6
+    elif qmode == "small":
+        q = q * 1e-12
+    elif qmode == "zero":
+        q = np.zeros_like(q)
+    elif qmode == "one":
+        q = np.zeros_like(q); q[int(rng.integers(0, len(q)))] = 1.0
+    elif qmode == "wide":
+        q = q * 10.0 ** rng.uniform(-6, 6, size=len(q))
+    if rng.random() < 0.1:
+        ncrit = 100000  # one leaf
     n = len(q)
     cut = 1e-12 if prec == 64 or p < 7 else 1e-8
-    rec = {"case": case, "kind": kind, "n": n, "n_crit": ncrit, "p": p, "precision": prec, "gradient": grad, "seed": seed, "scale": scale, "shift": shift}
+    rec = {"case": case, "kind": kind, "n": n, "n_crit": ncrit, "p": p, "precision": prec, "gradient": grad, "seed": seed, "scale": scale, "shift": shift, "qmode": qmode}
     try:
         with fmm.Fmm(pos, fmm.FmmConfig(p=p, n_crit=ncrit, precision=prec, gradient=grad, svd_cutoff=cut),
                      operators=ops_cache) as f:
