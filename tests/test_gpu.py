@@ -84,6 +84,32 @@ def test_scaled_and_shifted_domains(require_gpu, scale, shift, precision):
     assert fmm.relative_error(grad, gref) <= tg
 
 
+@pytest.mark.parametrize("kind,n,n_crit,p,precision", [
+    ("uniform-cube", 60000, 60, 6, 32), ("two-cluster", 40000, 30, 6, 32), ("sphere-surface", 30000, 40, 5, 32),
+    ("two-cluster", 20000, 30, 7, 64), ("uniform-cube", 20000, 60, 5, 64), ("two-cluster", 6000, 30, 8, 64)])
+def test_no_state_carries_between_evaluates(require_gpu, kind, n, n_crit, p, precision):
+    """A plan keeps no state from one evaluate to the next: charges A, then B (sparse and 1e6 times larger), then
+    zeros, then A again reproduce A bit for bit; B equals a fresh plan's B; zeros give zeros.  Covers the fp32
+    tcgen05 path (split buffers, partial rows, near-field queue), the fp64 int8 path (per-level exponents
+    recomputed every evaluate) and the column-blocked GEMMs of p = 8, through the graph and the eager launch."""
+    pos, qa = generators.sample(kind, n, seed=41, charges="signed", fp32=precision == 32)
+    rng = np.random.default_rng(5)
+    qb = np.where(rng.random(n) < 0.01, 1e6 * (2 * rng.random(n) - 1), 0.0)
+    cfg = fmm.FmmConfig(p=p, n_crit=n_crit, precision=precision, gradient=True)
+    with fmm.Fmm(pos, cfg) as f:
+        a1 = f.evaluate(qa)[:2]
+        b1 = f.evaluate(qb)[:2]
+        z = f.evaluate(np.zeros(n))[:2]
+        a2 = f.evaluate(qa)[:2]
+        a3 = f.evaluate(qa, timed=True)[:2]
+        tree, ops = f.tree, f.operators
+    with fmm.Fmm(pos, cfg, operators=ops, tree=tree) as g:
+        b2 = g.evaluate(qb)[:2]
+    for x, y in ((a1, a2), (a1, a3), (b1, b2)):
+        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
+    assert not np.any(z[0]) and not np.any(z[1])
+
+
 @pytest.mark.parametrize("side,depth_min", [(1e-2, 9), (1e-3, 12), (1e-4, 15)])
 def test_fp32_deep_cluster(require_gpu, side, depth_min):
     """fp32 on a clustered cloud (a dense cube of the given side in a uniform background, tree depth 10-15): the
