@@ -783,24 +783,38 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FAR_MINB) far_f2_kernel(
 #ifndef KIFMM_FAR_LATE_OUT
   load_out();  // prefetch the near-field result and the output permutation
 #endif
-  const f2_t x = f2_pair(xa.x, xb.x), y = f2_pair(xa.y, xb.y), z = f2_pair(xa.z, xb.z);
+  f2_t x = f2_pair(xa.x, xb.x), y = f2_pair(xa.y, xb.y), z = f2_pair(xa.z, xb.z);
   f2_t ph = 0, gx = 0, gy = 0, gz = 0;
   const float fa = float(kFarAway);
+  // work-local geometry (see LocalGeom and far_hw_kernel): anchor = centre of the first surface
+  float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), l0 = g0;
+  if (w.surf_begin < w.surf_end) {
+    g0 = p.node_geom[w.node0];
+    l0 = p.node_lo[w.node0];
+    x = f2_sub(f2_sub(x, f2_bcast(g0.x)), f2_bcast(l0.x));
+    y = f2_sub(f2_sub(y, f2_bcast(g0.y)), f2_bcast(l0.y));
+    z = f2_sub(f2_sub(z, f2_bcast(g0.z)), f2_bcast(l0.z));
+  }
   for (int si = w.surf_begin; si < w.surf_end; ++si) {
     const int2 sf = si == w.surf_begin ? make_int2(w.node0, w.kind0) : surfaces[si];
     const bool l2p = sf.y == kSrcL2P;
     const float alpha = l2p ? p.alpha_outer : p.alpha_inner;
     const float* dens = l2p ? L : M;
-    const float4 gc = p.node_geom[sf.x], gl = p.node_lo[sf.x];  // node-local: targets shifted by the centre pair
+    const float4 gc = p.node_geom[sf.x], gl = p.node_lo[sf.x];
+    const float ox = (gc.x - g0.x) + (gl.x - l0.x), oy = (gc.y - g0.y) + (gl.y - l0.y), oz = (gc.z - g0.z) + (gl.z - l0.z);
     __syncwarp();
-    for (int j = lane; j < pad; j += 32)
-      my[j] = j < p.n_e ? surface_source_local(p, sf.x, gc, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
+    for (int j = lane; j < pad; j += 32) {
+      float4 v = make_float4(fa, fa, fa, 0.f);
+      if (j < p.n_e) {
+        v = surface_source_local(p, sf.x, gc, alpha, dens, j);
+        v.x += ox;
+        v.y += oy;
+        v.z += oz;
+      }
+      my[j] = v;
+    }
     __syncwarp();
-    if (active)
-      p2p_round_f2<GRAD, false>(my, slice * per, slice * per + per,
-                                f2_sub(f2_sub(x, f2_bcast(gc.x)), f2_bcast(gl.x)),
-                                f2_sub(f2_sub(y, f2_bcast(gc.y)), f2_bcast(gl.y)),
-                                f2_sub(f2_sub(z, f2_bcast(gc.z)), f2_bcast(gl.z)), ph, gx, gy, gz);
+    if (active) p2p_round_f2<GRAD, false>(my, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
   }
   // fixed-order slice reduction into slice 0
   float v[8];
@@ -892,7 +906,7 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
       ov[h] = perm ? perm[t] : t;
     }
   }
-  const f2_t x = f2_pair(xa.x, xb.x), y = f2_pair(xa.y, xb.y), z = f2_pair(xa.z, xb.z);
+  f2_t x = f2_pair(xa.x, xb.x), y = f2_pair(xa.y, xb.y), z = f2_pair(xa.z, xb.z);
   f2_t ph = 0, gx = 0, gy = 0, gz = 0;
   // surfaces of this half's work; the halves loop to the longer list (works are paired on the host).
   // Surface k + 1 is fetched while surface k is computed: its equivalent densities by cp.async into a
@@ -907,20 +921,24 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
   auto surf = [&](int k) {
     return k == 0 ? make_int2(w.node0, w.kind0) : k < ns ? surfaces[w.surf_begin + k] : make_int2(-1, 0);
   };
-  // surface 0: staged directly.  Node-local geometry (surface_source_local): gk is the centre of the surface
-  // being computed, and the targets are shifted by it
-  float4 gk = make_float4(0.f, 0.f, 0.f, 0.f), lk = gk;
+  // surface 0: staged directly.  Work-local geometry (see LocalGeom): the anchor is the centre of the work's
+  // first surface, as a float pair (g0, l0); the targets are shifted by it once, and every later surface is
+  // staged at (c_k - c_0) + s u_j -- a short lattice vector plus the node-local point
+  float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), l0 = g0;
   {
     const int2 sf = surf(0);
     const bool l2p = sf.y == kSrcL2P;
     const float alpha = l2p ? p.alpha_outer : p.alpha_inner;
     const float* dens = l2p ? L : M;
     if (0 < ns) {
-      gk = p.node_geom[sf.x];
-      lk = p.node_lo[sf.x];
+      g0 = p.node_geom[sf.x];
+      l0 = p.node_lo[sf.x];
     }
     for (int j = hl; j < pad; j += 16)
-      my[j] = (0 < ns && j < p.n_e) ? surface_source_local(p, sf.x, gk, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
+      my[j] = (0 < ns && j < p.n_e) ? surface_source_local(p, sf.x, g0, alpha, dens, j) : make_float4(fa, fa, fa, 0.f);
+    x = f2_sub(f2_sub(x, f2_bcast(g0.x)), f2_bcast(l0.x));
+    y = f2_sub(f2_sub(y, f2_bcast(g0.y)), f2_bcast(l0.y));
+    z = f2_sub(f2_sub(z, f2_bcast(g0.z)), f2_bcast(l0.z));
   }
   int2 sf_n = surf(1);  // descriptor of the next surface
   for (int k = 0; k < ns_max; ++k) {
@@ -942,21 +960,16 @@ __global__ void __launch_bounds__(kFarWarps * 32, KIFMM_FARHW_MINB) far_hw_kerne
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     const int2 sf_nn = surf(k + 2);
-    if (act && k < ns)
-      p2p_round_f2<GRAD, false>(my, slice * per, slice * per + per,
-                                f2_sub(f2_sub(x, f2_bcast(gk.x)), f2_bcast(lk.x)),
-                                f2_sub(f2_sub(y, f2_bcast(gk.y)), f2_bcast(lk.y)),
-                                f2_sub(f2_sub(z, f2_bcast(gk.z)), f2_bcast(lk.z)), ph, gx, gy, gz);
+    if (act && k < ns) p2p_round_f2<GRAD, false>(my, slice * per, slice * per + per, x, y, z, ph, gx, gy, gz);
     if (k + 1 < ns_max) {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       __syncwarp();  // every lane is done reading surface k and sees surface k + 1's densities
       const float sc = an * gn.w;
+      const float ox = (gn.x - g0.x) + (ln.x - l0.x), oy = (gn.y - g0.y) + (ln.y - l0.y), oz = (gn.z - g0.z) + (ln.z - l0.z);
       for (int j = hl; j < pad; j += 16)
-        my[j] = (nlive && j < p.n_e) ? make_float4(sc * p.surface[3 * j], sc * p.surface[3 * j + 1],
-                                                   sc * p.surface[3 * j + 2], dn[j])
+        my[j] = (nlive && j < p.n_e) ? make_float4(ox + sc * p.surface[3 * j], oy + sc * p.surface[3 * j + 1],
+                                                   oz + sc * p.surface[3 * j + 2], dn[j])
                                      : make_float4(fa, fa, fa, 0.f);
-      gk = gn;
-      lk = ln;
     }
     sf_n = sf_nn;
   }
