@@ -1,8 +1,8 @@
 """Randomised GPU-vs-oracle check: random size, leaf capacity, order, distribution, precision, gradient, and a few
 degenerate clouds (duplicates, a line, one point).  Prints one JSON line per case; non-zero exit on a failure."""
-import json, sys, time
+import json, os, sys, time
 import numpy as np
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2303_08394_b200 import fmm, generators
 import oracle
 

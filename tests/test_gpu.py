@@ -66,6 +66,17 @@ def test_fp32_p7_accuracy_bound(require_gpu):
     assert fmm.relative_error(pot, ref) <= 5e-4
 
 
+def test_randomised_clouds_short(require_gpu):
+    """A short run of the randomised GPU-vs-oracle tool (random size, leaf capacity, order 2-8, distribution,
+    degenerate clouds, scale / shift, charge range, precision, gradient): every case inside the parity gates."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "randomised_gpu.py"), "20", "5"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("precision", [32, 64])
 @pytest.mark.parametrize("scale,shift", [(1e-4, 0.0), (1e4, 0.0), (1.0, -1000.0), (1e3, 5e4), (1e-3, 1.0)])
 def test_scaled_and_shifted_domains(require_gpu, scale, shift, precision):
@@ -132,7 +143,7 @@ def test_fp32_deep_cluster(require_gpu, side, depth_min):
 @pytest.mark.parametrize("kind,n_crit", [("dups", 1), ("dups", 2), ("line", 1)])
 def test_degenerate_clouds_max_depth(require_gpu, kind, n_crit, precision):
     """Clouds that drive the tree to its maximum depth (15): every point three times with n_crit < 3, and points
-    on a line with n_crit = 1 (cases found by the randomised GPU-vs-oracle runs, tools/exp/r02_fuzz.py)."""
+    on a line with n_crit = 1 (cases found by the randomised GPU-vs-oracle runs, tests/randomised_gpu.py)."""
     rng = np.random.default_rng(11)
     if kind == "dups":
         base = rng.random((100, 3))
