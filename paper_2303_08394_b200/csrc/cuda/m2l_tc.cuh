@@ -1,7 +1,7 @@
 // M2L on the 5th-generation tensor cores (SURVEY 7.3 "M2L batching").
 //
 // Work: for a tile of same-class target nodes and one transfer vector t,
-//   D[rows x 160] += A_t[rows x 160] . K_t^T,  A_t rows = multipoles of the
+//   D[rows x NP] += A_t[rows x NP] . K_t^T (NP = n_e padded: 64, 128, 160, 224 for p = 4..7),  A_t rows = multipoles of the
 // V-list sources at offset t (a zero row where absent), K_t = reference-level
 // kernel matrix (n_c x n_e, K-major).  Two error-compensated operand formats
 // (template ES):
@@ -17,7 +17,7 @@
 // block) pairs.
 //
 // Two variants (template PAIR):
-//   PAIR = false: one CTA, M = 128 targets, 3 stages of 72 KB.
+//   PAIR = false: one CTA, M = 128 targets (stage counts below are for NP = 160, 128-byte rows).
 //   PAIR = true : a 2-CTA cluster (cta_group::2), M = 256; each CTA gathers its
 //                 own 128 A rows and half of K_t (80 check rows), 4 stages of
 //                 52 KB; only the leader issues tcgen05.mma, and stage / TMEM
@@ -83,7 +83,7 @@ struct Regs {
   static constexpr int EPI = NP > 160 ? 168 : KIFMM_TC_EPI_REGS;
   static_assert(4 * 32 * LOW * 2 + 8 * 32 * EPI <= THREADS * LAUNCH, "setmaxnreg budget");
 };
-constexpr uint32_t TMEM_COLS = 512;  // NACC 160-column accumulators at 0, 160, 320
+constexpr uint32_t TMEM_COLS = 512;  // accumulator sets of NP columns at 0, NP, 2 NP (two sets at NP = 224)
 constexpr int NACC = 3;              // accumulator buffers: the MMA runs up to two taps ahead of the epilogue
 // The tensor-core accumulator rounds toward zero after every MMA (1 ulp per K step, measured), a bias that
 // adds up coherently along a chain of GEMMs.  The single-CTA instantiation (the factored solves, M2M and
