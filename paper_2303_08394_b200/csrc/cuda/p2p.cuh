@@ -72,12 +72,18 @@ __device__ __forceinline__ float4 shift_local(float4 v, const float4& g, const f
 constexpr int kP2PThreads = 128;
 constexpr int kP2PCap = 1024;  // staged sources per round
 
+// Absolute surface coordinate c + s u.  fp64: product and sum rounded separately, as the oracle's (uncontracted)
+// c + alpha h u does -- a fused multiply-add differs by up to one ulp of |c|, which is 1e-11 of a level-15 box and
+// showed up as 1e-12 parity outliers on depth-15 clouds in the randomised runs.
+__device__ __forceinline__ double surf_abs(double c, double s, double u) { return __dadd_rn(c, __dmul_rn(s, u)); }
+__device__ __forceinline__ float surf_abs(float c, float s, float u) { return c + s * u; }
+
 template <class T>
 __device__ __forceinline__ v4_t<T> surface_source(const P2PParams<T>& p, int node, T alpha, const T* dens, int j) {
   const v4_t<T> g = p.node_geom[node];
   const T s = alpha * g.w;
-  return make4<T>(g.x + s * p.surface[3 * j], g.y + s * p.surface[3 * j + 1], g.z + s * p.surface[3 * j + 2],
-                  dens[size_t(node) * p.ld + j]);
+  return make4<T>(surf_abs(g.x, s, p.surface[3 * j]), surf_abs(g.y, s, p.surface[3 * j + 1]),
+                  surf_abs(g.z, s, p.surface[3 * j + 2]), dens[size_t(node) * p.ld + j]);
 }
 
 // Far-field source j of a node's surface: node-local (s u_j, density) for fp32 -- the caller shifts its targets
@@ -86,9 +92,12 @@ template <class T>
 __device__ __forceinline__ v4_t<T> surface_source_local(const P2PParams<T>& p, int node, const v4_t<T>& g, T alpha,
                                                         const T* dens, int j) {
   const T s = alpha * g.w;
-  constexpr T k = LocalGeom<T>::on ? T(0) : T(1);
-  return make4<T>(k * g.x + s * p.surface[3 * j], k * g.y + s * p.surface[3 * j + 1], k * g.z + s * p.surface[3 * j + 2],
-                  dens[size_t(node) * p.ld + j]);
+  if constexpr (LocalGeom<T>::on)
+    return make4<T>(s * p.surface[3 * j], s * p.surface[3 * j + 1], s * p.surface[3 * j + 2],
+                    dens[size_t(node) * p.ld + j]);
+  else
+    return make4<T>(surf_abs(g.x, s, p.surface[3 * j]), surf_abs(g.y, s, p.surface[3 * j + 1]),
+                    surf_abs(g.z, s, p.surface[3 * j + 2]), dens[size_t(node) * p.ld + j]);
 }
 
 // One block per work item (leaf, <= 128 targets).  The block's 128 threads are
@@ -1081,10 +1090,15 @@ __global__ void __launch_bounds__(kCheckWarps * 32) check_kernel(P2PParams<T> p,
     const int j = lane + 32 * m;
     const int jj = j < p.n_e ? j : 0;
     // fp32: node-local geometry, sources shifted by the centre pair (LocalGeom); fp64: absolute
-    constexpr T ka = LocalGeom<T>::on ? T(0) : T(1);
-    yx[m] = ka * g.x + s * p.surface[3 * jj];
-    yy[m] = ka * g.y + s * p.surface[3 * jj + 1];
-    yz[m] = ka * g.z + s * p.surface[3 * jj + 2];
+    if constexpr (LocalGeom<T>::on) {
+      yx[m] = s * p.surface[3 * jj];
+      yy[m] = s * p.surface[3 * jj + 1];
+      yz[m] = s * p.surface[3 * jj + 2];
+    } else {
+      yx[m] = surf_abs(g.x, s, p.surface[3 * jj]);
+      yy[m] = surf_abs(g.y, s, p.surface[3 * jj + 1]);
+      yz[m] = surf_abs(g.z, s, p.surface[3 * jj + 2]);
+    }
     acc[m] = T(0);
   }
   for (int r = w.range_begin; r < w.range_end; ++r) {

@@ -38,6 +38,8 @@ while time.time() < t_end:
         n = int(rng.integers(1, 4))
         pos, q = generators.sample("uniform-cube", n, seed=seed, charges="signed", fp32=prec == 32)
     scale = float(rng.choice([1.0, 1.0, 1e-5, 1e-2, 37.0, 1e5]))
+    if kind == "line" and grad and prec == 32 and scale < 1e-2:
+        scale = 1e-2  # thousands of points on a 1e-5 line: spacings down to 1e-12, and |q| / r^3 of the gradient leaves the fp32 range
     shift = float(rng.choice([0.0, 0.0, -3.0, 250.0])) * scale
     pos = pos * scale + shift
     if prec == 32:
