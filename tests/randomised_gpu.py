@@ -16,6 +16,8 @@ while time.time() < t_end:
     case += 1
     prec = int(rng.choice([32, 64]))
     p = int(rng.choice([2, 3, 4, 5, 6, 7, 8])) if prec == 64 else int(rng.choice([2, 3, 4, 5, 6, 7]))
+    if os.environ.get("KIFMM_FUZZ_HIGH_ORDERS"):  # p = 8, 9, 10 only (slow operator precompute: a few seconds per cloud)
+        p = int(rng.choice([8, 9, 10]))
     kind = str(rng.choice(["uniform-cube", "sphere-surface", "two-cluster", "dups", "line", "tiny"]))
     n = int(rng.integers(1, 6000))
     ncrit = int(rng.choice([1, 2, 5, 17, 40, 64, 150, 400]))
